@@ -1,0 +1,218 @@
+/*
+ * tofr_gpu.h -- C ABI of the B200 ToF ReSTIR renderer (libtofr_b200.so).
+ *
+ * Drop-in boundary for the CPU reference library `tofr`
+ * (/root/reference/proj/include/tofr).  The reference has no FFI; its public
+ * surface is the C++ API below, and each entry point here replaces one of
+ * those functions with plain pointers/sizes (no C++ or torch types):
+ *
+ *   tofr_scene_create / tofr_scene_parse / tofr_scene_load
+ *       <- SceneDef construction, parse_scene, load_scene
+ *          (scene.hpp:417-429, scene_io.hpp:136-313)
+ *   tofr_gpu_render_gated       <- render_gated           (pipeline.hpp:323-392)
+ *   tofr_gpu_render_doppler     <- render_doppler         (pipeline.hpp:574-578)  [not built: returns TOFR_ERR_UNSUPPORTED]
+ *   tofr_gpu_render_transient   <- render_transient       (pipeline.hpp:396-528)
+ *   tofr_gpu_render_transient_plain <- render_transient_plain (pipeline.hpp:531-571)
+ *   tofr_gpu_reference          <- reference_render       (harness.hpp:16-30)
+ *   tofr_render_config          <- RenderConfig           (pipeline.hpp:18-61)
+ *   tofr_frame_stats            <- FrameStats/StageStats/ShiftCounts
+ *                                  (pipeline.hpp:63-72, shiftmap.hpp:398-417)
+ *
+ * Errors: every call returns 0 (TOFR_OK) or a TOFR_ERR_* code and never
+ * throws; the message of the last failure is tofr_gpu_last_error(ctx) (or the
+ * err buffer of the scene calls).  The reference's exceptions map as:
+ * ParseError(line,col) -> TOFR_ERR_PARSE with "line:col: msg";
+ * runtime_error("bvh: empty mesh"/"bvh: degenerate triangle") -> TOFR_ERR_SCENE.
+ *
+ * Threading: one context per process/device; a context is not re-entrant.
+ * Outputs are caller-allocated host buffers filled by the call (the reference
+ * returns RenderOutput by value).
+ */
+#ifndef TOFR_GPU_H
+#define TOFR_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOFR_OK 0
+#define TOFR_ERR_INVALID 1
+#define TOFR_ERR_PARSE 2
+#define TOFR_ERR_SCENE 3
+#define TOFR_ERR_CUDA 4
+#define TOFR_ERR_OOM 5
+#define TOFR_ERR_UNSUPPORTED 6
+
+/* enums keep the reference's enumerator order */
+enum { TOFR_MAT_DIFFUSE = 0, TOFR_MAT_GLOSSY = 1, TOFR_MAT_MIRROR = 2 };     /* MatKind */
+enum { TOFR_LIGHT_COLLIMATED = 0, TOFR_LIGHT_WIDE = 1 };                     /* LightRegime */
+enum { TOFR_MODE_GATED = 0, TOFR_MODE_TRANSIENT = 1, TOFR_MODE_DOPPLER = 2 }; /* RenderMode */
+enum { TOFR_INIT_DIRECT = 0, TOFR_INIT_ELLIPSOIDAL = 1, TOFR_INIT_SHRINK = 2 }; /* InitMode */
+enum { TOFR_GAUGE_FIXED = 0, TOFR_GAUGE_RAW = 1, TOFR_GAUGE_AVG = 2 };        /* GaugeKind */
+enum { TOFR_GATE_LENGTH = 0, TOFR_GATE_VELOCITY = 1 };                       /* GateSpec::Kind */
+
+typedef struct tofr_material {
+    int32_t kind;
+    double albedo[3];
+    double roughness;
+} tofr_material;
+
+typedef struct tofr_light {
+    int32_t regime;
+    double position[3];
+    double direction[3]; /* unit */
+    double cone_half_angle;
+    double intensity[3];
+} tofr_light;
+
+typedef struct tofr_camera_key {
+    double frame;
+    double position[3], forward[3], up[3];
+} tofr_camera_key;
+
+typedef struct tofr_pose_key {
+    double frame;
+    double q[4]; /* w, x, y, z */
+    double t[3];
+} tofr_pose_key;
+
+typedef struct tofr_object_desc {
+    const char* name;
+    int32_t n_tris;
+    const double* verts;       /* n_tris * 9: object-space v0, v1, v2 (make_triangle) */
+    const int32_t* materials;  /* n_tris */
+    int32_t n_keys;
+    const tofr_pose_key* keys; /* rigid motion track, sorted by frame */
+} tofr_object_desc;
+
+typedef struct tofr_scene_desc {
+    double cam_position[3], cam_forward[3], cam_up[3];
+    double fov_y; /* radians */
+    int32_t width, height;
+    int32_t n_cam_keys;
+    const tofr_camera_key* cam_keys;
+    int32_t n_materials;
+    const tofr_material* materials;
+    tofr_light light;
+    int32_t n_objects;
+    const tofr_object_desc* objects;
+    double dt_frame;
+} tofr_scene_desc;
+
+typedef struct tofr_render_config {
+    int32_t mode;
+    int32_t gate_kind;
+    double gate_center, gate_width, gate_f0;
+    double gate_step;
+    int32_t bins;
+    double hist_t0, hist_bin_width;
+    int32_t m_init;
+    int32_t init_mode;
+    double shrink_k, shrink_r;
+    int32_t spatial_passes, spatial_neighbors;
+    double spatial_radius;
+    int32_t temporal, bin_reuse;
+    double m_cap;
+    int32_t gauge;
+    int32_t newton;
+    uint64_t seed;
+    int32_t frames;
+    double frame0;
+    int32_t max_depth;
+    int32_t use_rr, accumulate, normalize_gate;
+} tofr_render_config;
+
+typedef struct tofr_shift_counts {
+    uint64_t attempts, newton_ok, newton_failed, occluded, jac_clamped, replay_failed, iterations,
+        solves, success;
+} tofr_shift_counts;
+
+typedef struct tofr_stage_stats {
+    tofr_shift_counts shift;
+    double seconds;
+} tofr_stage_stats;
+
+typedef struct tofr_frame_stats {
+    int32_t frame;
+    tofr_stage_stats temporal, spatial, binwise;
+    double t_init, t_shade;
+} tofr_frame_stats;
+
+/* RenderOutput: image W*H*3 (row-major, rgb), histogram W*H*B(*3) in the
+ * reference index order (y*W + x)*B + b.  Any pointer may be NULL. */
+typedef struct tofr_output {
+    double* image;
+    double* hist_rgb;
+    int64_t* hist_count;
+    tofr_frame_stats* stats;
+    int32_t stats_capacity;
+} tofr_output;
+
+typedef struct tofr_gpu tofr_gpu;
+typedef struct tofr_scene tofr_scene;
+typedef struct tofr_session tofr_session;
+
+/* RenderConfig{} defaults (pipeline.hpp:18-61) */
+void tofr_render_config_default(tofr_render_config* cfg);
+
+/* context */
+int tofr_gpu_create(const int* devices, int n_devices, tofr_gpu** out);
+void tofr_gpu_destroy(tofr_gpu* ctx);
+const char* tofr_gpu_last_error(const tofr_gpu* ctx);
+const char* tofr_gpu_version(void);
+
+/* scenes (host objects; frames are built and uploaded per render) */
+int tofr_scene_create(const tofr_scene_desc* desc, tofr_scene** out, char* err, size_t errlen);
+int tofr_scene_parse(const char* text, const char* base_dir, tofr_scene** out, char* err, size_t errlen);
+int tofr_scene_load(const char* path, tofr_scene** out, char* err, size_t errlen);
+void tofr_scene_destroy(tofr_scene* s);
+int tofr_scene_set_resolution(tofr_scene* s, int32_t width, int32_t height);
+/* info: width, height, n_triangles (frame 0), BVH nodes (frame 0); diag = scene_scale() */
+int tofr_scene_info(const tofr_scene* s, int32_t* width, int32_t* height, int32_t* n_tris, int32_t* n_nodes,
+                    double* diag, char* err, size_t errlen);
+
+/* render drivers (RenderOutput is written into caller buffers) */
+int tofr_gpu_render_gated(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, tofr_output* out);
+int tofr_gpu_render_doppler(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, tofr_output* out);
+int tofr_gpu_render_transient(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                              tofr_output* out);
+int tofr_gpu_render_transient_plain(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                                    tofr_output* out);
+/* reference_render(build_frame(def, frame), gate, spp, seed, max_depth): mean, se are W*H*3 */
+int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* s, double frame, double gate_center, double gate_width,
+                       int32_t spp, uint64_t seed, int32_t max_depth, double* mean, double* se);
+
+/* interactive sessions: the frame loop of render_gated / render_transient
+ * one frame per call, reservoirs kept on the device between calls */
+int tofr_gpu_session_create(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                            tofr_session** out);
+int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats);
+/* last frame's image (gated) or bin-summed frame estimate (transient) */
+int tofr_gpu_session_read_image(tofr_session* ss, double* image);
+int tofr_gpu_session_sync(tofr_session* ss);
+/* device timing of the last step's kernels (ms) and the stage split */
+int tofr_gpu_session_last_ms(tofr_session* ss, double* total_ms, double* stage_ms /* [6] */);
+void tofr_gpu_session_destroy(tofr_session* ss);
+
+/* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit
+ * (Bvh::intersect_min) -> t, tri; mode 1 = occluded(a = o, b = d) -> tri = 0/1 */
+int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* s, double frame, const double* rays, int32_t n,
+                        int32_t mode, double* out_t, int32_t* out_tri);
+/* same probe through the host build of the traversal code (no GPU needed) */
+int tofr_scene_probe_rays_host(const tofr_scene* s, double frame, const double* rays, int32_t n, int32_t mode,
+                               double* out_t, int32_t* out_tri, char* err, size_t errlen);
+/* host BVH of one frame in the reference layout (for build parity):
+ * nodes: n_nodes * 11 doubles {lo.xyz, hi.xyz, tri_area, left, right, first, count}, parent in
+ * node_parent; tri_order n_tris */
+int tofr_scene_dump_bvh(const tofr_scene* s, double frame, int32_t cap_nodes, double* nodes,
+                        int32_t* node_parent, int32_t* n_nodes, int32_t cap_tris, int32_t* tri_order,
+                        int32_t* n_tris, double* diag, char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOFR_GPU_H */

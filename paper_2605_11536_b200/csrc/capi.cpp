@@ -1,0 +1,815 @@
+// capi.cpp -- host runtime behind include/tofr_gpu.h: contexts, scenes,
+// frame upload, the per-frame stage sequence of render_gated /
+// render_transient / render_transient_plain, and the parity probes.
+//
+// Frame loop (pipeline.hpp:323-392, 396-528), per frame f:
+//   host : build_frame(def, frame0 + f)  -> SAH BVH, camera, beam   (µs for
+//          the bundled scenes) -> one packed blob -> one H2D copy
+//   GPU  : k_gbuffer -> k_init_* -> [k_temporal] -> [k_binreuse] ->
+//          k_spatial x P -> k_shade_*   (one stream, no host sync inside)
+// Reservoir grids rotate between three device buffers (cur / prev / spare);
+// the spatial snapshot of the reference (a full copy, pipeline.hpp:363) is a
+// pointer swap here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tofr_gpu.h"
+#include "host_scene.h"
+#include "tofr_kernels.h"
+
+using namespace tofr_b200;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ScopeError : std::runtime_error {
+    int code;
+    ScopeError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation)
+            throw ScopeError(TOFR_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t bytes) {
+        if (bytes <= n) return;
+        release();
+        ck(cudaMalloc(&p, bytes), "cudaMalloc");
+        n = bytes;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// 32-point Gauss-Legendre rule, built the way ellipsoid.hpp:88-121 does
+// (Newton on P_32 from the Chebyshev-like guess) so nodes are bit-identical.
+void gauss_rule32(double* x, double* w) {
+    constexpr int n = 32;
+    for (int i = 0; i < n / 2; ++i) {
+        double t = std::cos(kPi * (i + 0.75) / (n + 0.5));
+        double p0 = 0, p1 = 0;
+        for (int it = 0; it < 100; ++it) {
+            p0 = 1.0;
+            p1 = 0.0;
+            for (int j = 0; j < n; ++j) {
+                double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * j + 1.0) * t * p1 - j * p2) / (j + 1);
+            }
+            double dp = n * (t * p0 - p1) / (t * t - 1.0);
+            double dt = p0 / dp;
+            t -= dt;
+            if (std::abs(dt) < 1e-15) break;
+        }
+        p0 = 1.0;
+        p1 = 0.0;
+        for (int j = 0; j < n; ++j) {
+            double p2 = p1;
+            p1 = p0;
+            p0 = ((2.0 * j + 1.0) * t * p1 - j * p2) / (j + 1);
+        }
+        double dp = n * (t * p0 - p1) / (t * t - 1.0);
+        x[i] = -t;
+        x[n - 1 - i] = t;
+        w[i] = w[n - 1 - i] = 2.0 / ((1.0 - t * t) * dp * dp);
+    }
+}
+
+void set_err(char* err, size_t errlen, const std::string& m) {
+    if (err && errlen) {
+        std::snprintf(err, errlen, "%s", m.c_str());
+    }
+}
+
+}  // namespace
+
+struct tofr_gpu {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+};
+
+struct tofr_scene {
+    HScene s;
+};
+
+// one uploaded frame snapshot
+struct FrameSlot {
+    DevBuf blob;
+    PackedFrame pk;
+    FrameView view;
+    DevBuf gbuf;
+};
+
+struct tofr_session {
+    tofr_gpu* ctx = nullptr;
+    HScene scene;
+    tofr_render_config cfg;
+    int W = 0, H = 0, B = 1;
+    bool transient = false, plain = false;
+    FrameSlot slot[2];
+    DevBuf res[3];
+    int cur = 0, prev = 1, spare = 2;
+    DevBuf image, accum, hist, hist_count;
+    DevBuf ctr;  // [3 stages][SC_COUNT] u64
+    cudaEvent_t ev[7] = {};
+    int f = 0;
+    double prev_center = 0, prev_width = 0;
+    double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+    int has_temporal = 0, has_bin = 0, has_spatial = 0;
+
+    ~tofr_session() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+ResStore store_of(const DevBuf& b, size_t items) { return ResStore{b.as<double2>(), items}; }
+
+PathCfg path_cfg(const tofr_render_config& c, double center, double width) {
+    PathCfg p;
+    std::memset(&p, 0, sizeof(p));
+    p.max_depth = c.max_depth;
+    p.use_rr = c.use_rr;
+    p.ellipsoidal = (c.init_mode == TOFR_INIT_ELLIPSOIDAL && c.gate_kind == TOFR_GATE_LENGTH) ? 1 : 0;
+    p.ell_center = center;
+    p.ell_width = width;
+    p.gauge = c.gauge;
+    p.newton = c.newton;
+    p.jac_min = 1.0 / 50.0;
+    p.jac_max = 50.0;
+    p.m_cap = c.m_cap;
+    p.seed = c.seed;
+    return p;
+}
+
+void upload_frame(tofr_session* s, int which, double frame, int frame_id) {
+    FrameSlot& sl = s->slot[which];
+    HFrame hf = build_frame(s->scene, frame);
+    if (hf.max_depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
+    sl.pk = pack_frame(s->scene, hf, frame_id);
+    sl.blob.ensure(sl.pk.blob.size());
+    ck(cudaMemcpyAsync(sl.blob.p, sl.pk.blob.data(), sl.pk.blob.size(), cudaMemcpyHostToDevice,
+                       s->ctx->stream),
+       "frame upload");
+    sl.view = rebase_view(sl.pk, static_cast<const unsigned char*>(sl.blob.p));
+    sl.gbuf.ensure(size_t(s->W) * s->H * sizeof(GHit));
+}
+
+void check_config(const tofr_render_config* c) {
+    if (!c) throw ScopeError(TOFR_ERR_INVALID, "null config");
+    if (c->max_depth < 1 || c->max_depth > 64) throw ScopeError(TOFR_ERR_INVALID, "max_depth out of range");
+    if (c->frames < 0) throw ScopeError(TOFR_ERR_INVALID, "frames < 0");
+    if (c->gate_kind != TOFR_GATE_LENGTH)
+        throw ScopeError(TOFR_ERR_UNSUPPORTED, "velocity (Doppler) gates are not built yet");
+}
+
+enum SessionKind { KIND_RESTIR = 0, KIND_PLAIN = 1, KIND_BARE = 2 };
+
+tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, int kind) {
+    check_config(cfg);
+    auto s = std::make_unique<tofr_session>();
+    s->ctx = ctx;
+    s->scene = sc->s;
+    s->cfg = *cfg;
+    s->W = sc->s.camera.width;
+    s->H = sc->s.camera.height;
+    if (s->W <= 0 || s->H <= 0) throw ScopeError(TOFR_ERR_INVALID, "empty image");
+    if (kind == KIND_BARE) return s.release();
+    bool plain = kind == KIND_PLAIN;
+    s->plain = plain;
+    s->transient = plain || cfg->mode == TOFR_MODE_TRANSIENT;
+    s->B = s->transient ? cfg->bins : 1;
+    if (s->transient && (cfg->bins < 1 || !(cfg->hist_bin_width > 0)))
+        throw ScopeError(TOFR_ERR_INVALID, "transient needs bins >= 1 and hist_bin_width > 0");
+    if (!s->transient && cfg->m_init < 0) throw ScopeError(TOFR_ERR_INVALID, "m_init < 0");
+    size_t npix = size_t(s->W) * s->H;
+    size_t items = npix * s->B;
+    if (plain) {
+        s->hist.ensure(items * 3 * sizeof(double));
+        s->hist_count.ensure(items * sizeof(uint32_t));
+        ck(cudaMemsetAsync(s->hist.p, 0, items * 3 * sizeof(double), ctx->stream), "memset");
+        ck(cudaMemsetAsync(s->hist_count.p, 0, items * sizeof(uint32_t), ctx->stream), "memset");
+    } else {
+        s->has_temporal = cfg->temporal ? 1 : 0;
+        s->has_bin = (s->transient && cfg->bin_reuse) ? 1 : 0;
+        s->has_spatial = cfg->spatial_passes > 0 ? 1 : 0;
+        size_t rb = items * kResChunks * 16;
+        s->res[0].ensure(rb);
+        s->res[1].ensure(rb);
+        if (s->has_bin || s->has_spatial) s->res[2].ensure(rb);
+        // a never-written grid must read as empty (M = 0) for temporal reuse
+        ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
+        ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
+        if (s->transient) {
+            s->hist.ensure(items * 3 * sizeof(double));
+            ck(cudaMemsetAsync(s->hist.p, 0, items * 3 * sizeof(double), ctx->stream), "memset");
+        } else {
+            s->image.ensure(npix * 3 * sizeof(double));
+            s->accum.ensure(npix * 3 * sizeof(double));
+            ck(cudaMemsetAsync(s->accum.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
+            ck(cudaMemsetAsync(s->image.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
+        }
+    }
+    s->ctr.ensure(3 * SC_COUNT * sizeof(unsigned long long));
+    for (auto& e : s->ev) ck(cudaEventCreate(&e), "event");
+    return s.release();
+}
+
+void fill_counts(tofr_shift_counts& o, const unsigned long long* c) {
+    o.attempts = c[SC_ATTEMPTS];
+    o.newton_ok = c[SC_NEWTON_OK];
+    o.newton_failed = c[SC_NEWTON_FAILED];
+    o.occluded = c[SC_OCCLUDED];
+    o.jac_clamped = c[SC_JAC_CLAMPED];
+    o.replay_failed = c[SC_REPLAY_FAILED];
+    o.iterations = c[SC_ITERATIONS];
+    o.solves = c[SC_SOLVES];
+    o.success = c[SC_SUCCESS];
+}
+
+// One frame of the pipeline (body of the frame loops).
+void session_step(tofr_session* s, tofr_frame_stats* st) {
+    cudaStream_t stream = s->ctx->stream;
+    const tofr_render_config& c = s->cfg;
+    int f = s->f;
+    int sl = f & 1, psl = sl ^ 1;
+    upload_frame(s, sl, c.frame0 + f, f);
+    const FrameView& F = s->slot[sl].view;
+    GHit* g = s->slot[sl].gbuf.as<GHit>();
+    double center = c.gate_center + c.gate_step * f;
+    double width = c.gate_width;
+    PathCfg pc = path_cfg(c, center, width);
+    size_t npix = size_t(s->W) * s->H;
+    size_t items = npix * s->B;
+    HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
+    unsigned long long* ctr = s->ctr.as<unsigned long long>();
+    ck(cudaMemsetAsync(ctr, 0, 3 * SC_COUNT * sizeof(unsigned long long), stream), "memset");
+
+    cudaEventRecord(s->ev[0], stream);
+    launch_gbuffer(F, g, stream);
+    if (s->plain) {
+        launch_hist_plain(F, g, pc, h, c.m_init, f, s->hist.as<double>(), s->hist_count.as<uint32_t>(), stream);
+        for (int i = 1; i < 7; ++i) cudaEventRecord(s->ev[i], stream);
+    } else {
+        InitParams ip{c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
+        ResStore cur = store_of(s->res[s->cur], items);
+        if (s->transient)
+            launch_init_transient(F, g, pc, ip, h, f, cur, stream);
+        else
+            launch_init_gated(F, g, pc, ip, f, cur, stream);
+        cudaEventRecord(s->ev[1], stream);
+        GateGrid cg{s->transient ? 1 : 0, center, width, h};
+        if (c.temporal && f > 0) {
+            GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
+            launch_temporal(F, g, s->slot[psl].view, s->slot[psl].gbuf.as<GHit>(), pc, cg, pg, f, cur,
+                            store_of(s->res[s->prev], items), ctr + 0 * SC_COUNT, stream);
+        }
+        cudaEventRecord(s->ev[2], stream);
+        if (s->transient && c.bin_reuse) {
+            launch_binreuse(F, g, pc, h, f, cur, store_of(s->res[s->spare], items), ctr + 2 * SC_COUNT, stream);
+            std::swap(s->cur, s->spare);
+            cur = store_of(s->res[s->cur], items);
+        }
+        cudaEventRecord(s->ev[3], stream);
+        SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
+        for (int pass = 0; pass < c.spatial_passes; ++pass) {
+            launch_spatial(F, g, pc, cg, sp, pass, f, cur, store_of(s->res[s->spare], items), ctr + 1 * SC_COUNT,
+                           stream);
+            std::swap(s->cur, s->spare);
+            cur = store_of(s->res[s->cur], items);
+        }
+        cudaEventRecord(s->ev[4], stream);
+        if (s->transient)
+            launch_shade_transient(cur, items, h, s->hist.as<double>(), stream);
+        else
+            launch_shade_gated(cur, int(npix), center, width, s->image.as<double>(), s->accum.as<double>(), stream);
+        cudaEventRecord(s->ev[5], stream);
+        cudaEventRecord(s->ev[6], stream);
+        std::swap(s->cur, s->prev);  // bufs.flip()
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    ck(cudaEventSynchronize(s->ev[6]), "frame");
+    float ms[6];
+    for (int i = 0; i < 6; ++i) {
+        ms[i] = 0;
+        cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]);
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, s->ev[0], s->ev[6]);
+    // stage split: init(incl. camera), temporal, bin, spatial, shade, total
+    s->stage_ms[0] = ms[0];
+    s->stage_ms[1] = ms[1];
+    s->stage_ms[2] = ms[2];
+    s->stage_ms[3] = ms[3];
+    s->stage_ms[4] = ms[4];
+    s->stage_ms[5] = tot;
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->frame = f;
+        unsigned long long hc[3 * SC_COUNT];
+        ck(cudaMemcpy(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost), "counters");
+        fill_counts(st->temporal.shift, hc + 0 * SC_COUNT);
+        fill_counts(st->spatial.shift, hc + 1 * SC_COUNT);
+        fill_counts(st->binwise.shift, hc + 2 * SC_COUNT);
+        st->t_init = ms[0] * 1e-3;
+        st->temporal.seconds = (c.temporal && f > 0) ? ms[1] * 1e-3 : 0;
+        st->binwise.seconds = (s->transient && c.bin_reuse) ? ms[2] * 1e-3 : 0;
+        st->spatial.seconds = ms[3] * 1e-3;
+        st->t_shade = ms[4] * 1e-3;
+    }
+    s->prev_center = center;
+    s->prev_width = width;
+    s->f++;
+}
+
+template <class F>
+int guard(tofr_gpu* ctx, F&& fn) {
+    try {
+        fn();
+        if (ctx) ctx->err.clear();
+        return TOFR_OK;
+    } catch (const ScopeError& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const CudaError& e) {
+        if (ctx) ctx->err = e.what();
+        return TOFR_ERR_CUDA;
+    } catch (const std::bad_alloc& e) {
+        if (ctx) ctx->err = "host allocation failed";
+        return TOFR_ERR_OOM;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return TOFR_ERR_SCENE;
+    }
+}
+
+void render_loop(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, tofr_output* out,
+                 bool plain) {
+    if (!ctx || !sc) throw ScopeError(TOFR_ERR_INVALID, "null handle");
+    std::unique_ptr<tofr_session> s(make_session(ctx, sc, cfg, plain ? KIND_PLAIN : KIND_RESTIR));
+    int frames = cfg->frames;
+    for (int f = 0; f < frames; ++f) {
+        tofr_frame_stats st;
+        session_step(s.get(), &st);
+        if (out && out->stats && f < out->stats_capacity) out->stats[f] = st;
+    }
+    if (!out) return;
+    size_t npix = size_t(s->W) * s->H;
+    if (!s->transient) {
+        std::vector<double> img(npix * 3);
+        if (cfg->accumulate && frames > 0) {
+            ck(cudaMemcpy(img.data(), s->accum.p, img.size() * 8, cudaMemcpyDeviceToHost), "image");
+            double k = 1.0 / frames;
+            for (double& v : img) v *= k;
+        } else {
+            ck(cudaMemcpy(img.data(), s->image.p, img.size() * 8, cudaMemcpyDeviceToHost), "image");
+        }
+        if (cfg->normalize_gate && cfg->gate_width > 0) {
+            double k = 1.0 / cfg->gate_width;
+            for (double& v : img) v *= k;
+        }
+        if (out->image) std::memcpy(out->image, img.data(), img.size() * 8);
+        return;
+    }
+    size_t items = npix * s->B;
+    std::vector<double> rgb(items * 3);
+    ck(cudaMemcpy(rgb.data(), s->hist.p, rgb.size() * 8, cudaMemcpyDeviceToHost), "histogram");
+    double k = plain ? 1.0 / std::max(1, frames) : (frames > 0 ? 1.0 / double(frames) : 1.0);
+    if (plain || frames > 0)
+        for (double& v : rgb) v *= k;
+    if (out->hist_rgb) std::memcpy(out->hist_rgb, rgb.data(), rgb.size() * 8);
+    if (out->hist_count) {
+        if (plain) {
+            std::vector<uint32_t> cnt(items);
+            ck(cudaMemcpy(cnt.data(), s->hist_count.p, items * 4, cudaMemcpyDeviceToHost), "counts");
+            for (size_t i = 0; i < items; ++i) out->hist_count[i] = cnt[i];
+        } else {
+            for (size_t i = 0; i < items; ++i) out->hist_count[i] = frames;
+        }
+    }
+    if (out->image) {
+        for (size_t p = 0; p < npix; ++p) {
+            double sx = 0, sy = 0, sz = 0;
+            for (int b = 0; b < s->B; ++b) {
+                const double* v = &rgb[3 * (p * s->B + b)];
+                sx += v[0];
+                sy += v[1];
+                sz += v[2];
+            }
+            out->image[3 * p + 0] = sx;
+            out->image[3 * p + 1] = sy;
+            out->image[3 * p + 2] = sz;
+        }
+    }
+}
+
+HScene scene_from_desc(const tofr_scene_desc* d) {
+    if (!d) throw ScopeError(TOFR_ERR_INVALID, "null scene desc");
+    HScene s;
+    s.camera.base.position = {d->cam_position[0], d->cam_position[1], d->cam_position[2]};
+    s.camera.base.forward = {d->cam_forward[0], d->cam_forward[1], d->cam_forward[2]};
+    s.camera.base.up = {d->cam_up[0], d->cam_up[1], d->cam_up[2]};
+    s.camera.fov_y = d->fov_y;
+    s.camera.width = d->width;
+    s.camera.height = d->height;
+    for (int i = 0; i < d->n_cam_keys; ++i) {
+        const tofr_camera_key& k = d->cam_keys[i];
+        HCamPose p;
+        p.position = {k.position[0], k.position[1], k.position[2]};
+        p.forward = {k.forward[0], k.forward[1], k.forward[2]};
+        p.up = {k.up[0], k.up[1], k.up[2]};
+        s.camera.track.emplace_back(k.frame, p);
+    }
+    for (int i = 0; i < d->n_materials; ++i) {
+        HMaterial m;
+        m.kind = d->materials[i].kind;
+        m.albedo = {d->materials[i].albedo[0], d->materials[i].albedo[1], d->materials[i].albedo[2]};
+        m.roughness = d->materials[i].roughness;
+        s.materials.push_back(m);
+    }
+    if (s.materials.empty()) s.materials.push_back(HMaterial{});
+    const tofr_light& l = d->light;
+    s.light.regime = l.regime;
+    s.light.position = {l.position[0], l.position[1], l.position[2]};
+    s.light.direction = {l.direction[0], l.direction[1], l.direction[2]};
+    s.light.cone_half_angle = l.cone_half_angle;
+    s.light.intensity = {l.intensity[0], l.intensity[1], l.intensity[2]};
+    for (int i = 0; i < d->n_objects; ++i) {
+        const tofr_object_desc& od = d->objects[i];
+        HObject o;
+        o.name = od.name ? od.name : "";
+        for (int t = 0; t < od.n_tris; ++t) {
+            const double* v = od.verts + 9 * size_t(t);
+            int mat = od.materials ? od.materials[t] : 0;
+            if (mat < 0 || mat >= int(s.materials.size())) throw ScopeError(TOFR_ERR_INVALID, "material index");
+            o.local.push_back(make_tri({v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}, mat));
+        }
+        for (int k = 0; k < od.n_keys; ++k) {
+            HPoseKey pk;
+            pk.frame = od.keys[k].frame;
+            pk.pose.q = {od.keys[k].q[0], od.keys[k].q[1], od.keys[k].q[2], od.keys[k].q[3]};
+            pk.pose.t = {od.keys[k].t[0], od.keys[k].t[1], od.keys[k].t[2]};
+            o.track.keys.push_back(pk);
+        }
+        s.objects.push_back(std::move(o));
+    }
+    s.dt_frame = d->dt_frame;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tofr_render_config_default(tofr_render_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->mode = TOFR_MODE_GATED;
+    c->gate_kind = TOFR_GATE_LENGTH;
+    c->gate_center = 0;
+    c->gate_width = 1;
+    c->gate_f0 = 1;
+    c->gate_step = 0;
+    c->bins = 1;
+    c->hist_t0 = 0;
+    c->hist_bin_width = 0;
+    c->m_init = 8;
+    c->init_mode = TOFR_INIT_DIRECT;
+    c->shrink_k = 10;
+    c->shrink_r = 1.0;
+    c->spatial_passes = 0;
+    c->spatial_neighbors = 5;
+    c->spatial_radius = 10;
+    c->temporal = 0;
+    c->bin_reuse = 0;
+    c->m_cap = 20;
+    c->gauge = TOFR_GAUGE_AVG;
+    c->newton = 1;
+    c->seed = 1;
+    c->frames = 1;
+    c->frame0 = 0;
+    c->max_depth = 6;
+    c->use_rr = 1;
+    c->accumulate = 0;
+    c->normalize_gate = 0;
+}
+
+const char* tofr_gpu_version(void) { return "tofr_b200 0.1 sm_100a"; }
+
+int tofr_gpu_create(const int* devices, int n_devices, tofr_gpu** out) {
+    if (!out) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    auto ctx = std::make_unique<tofr_gpu>();
+    int rc = guard(ctx.get(), [&] {
+        ctx->device = (devices && n_devices > 0) ? devices[0] : 0;
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        double x[32], w[32];
+        gauss_rule32(x, w);
+        set_gauss_rule(x, w, ctx->stream);
+        ck(cudaStreamSynchronize(ctx->stream), "init");
+    });
+    if (rc != TOFR_OK) {
+        static thread_local std::string last;
+        last = ctx->err;
+        std::fprintf(stderr, "tofr_gpu_create: %s\n", last.c_str());
+        return rc;
+    }
+    *out = ctx.release();
+    return TOFR_OK;
+}
+
+void tofr_gpu_destroy(tofr_gpu* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* tofr_gpu_last_error(const tofr_gpu* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+static int scene_guard(char* err, size_t errlen, const std::function<void()>& fn);
+
+int tofr_scene_create(const tofr_scene_desc* desc, tofr_scene** out, char* err, size_t errlen) {
+    if (!out) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    return scene_guard(err, errlen, [&] {
+        auto s = std::make_unique<tofr_scene>();
+        s->s = scene_from_desc(desc);
+        if (s->s.objects.empty()) throw ScopeError(TOFR_ERR_INVALID, "scene has no objects");
+        *out = s.release();
+    });
+}
+
+int tofr_scene_parse(const char* text, const char* base_dir, tofr_scene** out, char* err, size_t errlen) {
+    if (!out || !text) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    return scene_guard(err, errlen, [&] {
+        auto s = std::make_unique<tofr_scene>();
+        s->s = parse_scene_text(text, base_dir ? base_dir : ".");
+        *out = s.release();
+    });
+}
+
+int tofr_scene_load(const char* path, tofr_scene** out, char* err, size_t errlen) {
+    if (!out || !path) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    return scene_guard(err, errlen, [&] {
+        auto s = std::make_unique<tofr_scene>();
+        s->s = load_scene_file(path);
+        *out = s.release();
+    });
+}
+
+void tofr_scene_destroy(tofr_scene* s) { delete s; }
+
+int tofr_scene_set_resolution(tofr_scene* s, int32_t width, int32_t height) {
+    if (!s || width <= 0 || height <= 0) return TOFR_ERR_INVALID;
+    s->s.camera.width = width;
+    s->s.camera.height = height;
+    return TOFR_OK;
+}
+
+int tofr_scene_info(const tofr_scene* s, int32_t* width, int32_t* height, int32_t* n_tris, int32_t* n_nodes,
+                    double* diag, char* err, size_t errlen) {
+    if (!s) return TOFR_ERR_INVALID;
+    return scene_guard(err, errlen, [&] {
+        HFrame f = build_frame(s->s, 0);
+        if (width) *width = s->s.camera.width;
+        if (height) *height = s->s.camera.height;
+        if (n_tris) *n_tris = int32_t(f.tris.size());
+        if (n_nodes) *n_nodes = int32_t(f.nodes.size());
+        if (diag) *diag = f.diag;
+    });
+}
+
+int tofr_scene_probe_rays_host(const tofr_scene* s, double frame, const double* rays, int32_t n, int32_t mode,
+                               double* out_t, int32_t* out_tri, char* err, size_t errlen) {
+    if (!s || n < 0) return TOFR_ERR_INVALID;
+    return scene_guard(err, errlen, [&] {
+        HFrame hf = build_frame(s->s, frame);
+        PackedFrame pk = pack_frame(s->s, hf, 0);
+        FrameView v = rebase_view(pk, pk.blob.data());
+        for (int i = 0; i < n; ++i) {
+            const double* r = rays + 8 * size_t(i);
+            V3 o{r[0], r[1], r[2]}, d{r[3], r[4], r[5]};
+            if (mode == 0) {
+                Hit h;
+                bool ok = trace_closest(v, o, d, r[6], r[7], h);
+                out_t[i] = ok ? h.t : kInf;
+                out_tri[i] = ok ? h.tri : -1;
+            } else {
+                out_tri[i] = occluded(v, o, d) ? 1 : 0;
+                out_t[i] = 0;
+            }
+        }
+    });
+}
+
+int tofr_scene_dump_bvh(const tofr_scene* s, double frame, int32_t cap_nodes, double* nodes, int32_t* node_parent,
+                        int32_t* n_nodes, int32_t cap_tris, int32_t* tri_order, int32_t* n_tris, double* diag,
+                        char* err, size_t errlen) {
+    if (!s) return TOFR_ERR_INVALID;
+    return scene_guard(err, errlen, [&] {
+        HFrame f = build_frame(s->s, frame);
+        if (n_nodes) *n_nodes = int32_t(f.nodes.size());
+        if (n_tris) *n_tris = int32_t(f.tris.size());
+        if (diag) *diag = f.diag;
+        if (nodes && int(f.nodes.size()) <= cap_nodes) {
+            for (size_t i = 0; i < f.nodes.size(); ++i) {
+                const HNode& h = f.nodes[i];
+                double* o = nodes + 11 * i;
+                o[0] = h.lo.x;
+                o[1] = h.lo.y;
+                o[2] = h.lo.z;
+                o[3] = h.hi.x;
+                o[4] = h.hi.y;
+                o[5] = h.hi.z;
+                o[6] = h.tri_area;
+                o[7] = h.left;
+                o[8] = h.right;
+                o[9] = h.first;
+                o[10] = h.count;
+                if (node_parent) node_parent[i] = h.parent;
+            }
+        }
+        if (tri_order && int(f.tri_order.size()) <= cap_tris)
+            for (size_t i = 0; i < f.tri_order.size(); ++i) tri_order[i] = f.tri_order[i];
+    });
+}
+
+int tofr_gpu_render_gated(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, tofr_output* out) {
+    return guard(ctx, [&] {
+        if (cfg && cfg->mode == TOFR_MODE_TRANSIENT)
+            throw ScopeError(TOFR_ERR_INVALID, "render_gated called with a transient config");
+        render_loop(ctx, s, cfg, out, false);
+    });
+}
+
+int tofr_gpu_render_doppler(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, tofr_output* out) {
+    (void)s;
+    (void)cfg;
+    (void)out;
+    return guard(ctx, [&] {
+        throw ScopeError(TOFR_ERR_UNSUPPORTED, "render_doppler (velocity gates) is not built yet");
+    });
+}
+
+int tofr_gpu_render_transient(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                              tofr_output* out) {
+    return guard(ctx, [&] {
+        if (!cfg) throw ScopeError(TOFR_ERR_INVALID, "null config");
+        tofr_render_config c = *cfg;
+        c.mode = TOFR_MODE_TRANSIENT;
+        render_loop(ctx, s, &c, out, false);
+    });
+}
+
+int tofr_gpu_render_transient_plain(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                                    tofr_output* out) {
+    return guard(ctx, [&] { render_loop(ctx, s, cfg, out, true); });
+}
+
+int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double gate_center, double gate_width,
+                       int32_t spp, uint64_t seed, int32_t max_depth, double* mean, double* se) {
+    return guard(ctx, [&] {
+        if (!ctx || !sc || spp < 1) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");
+        tofr_render_config c;
+        tofr_render_config_default(&c);
+        c.max_depth = max_depth;
+        c.seed = seed;
+        std::unique_ptr<tofr_session> s(make_session(ctx, sc, &c, KIND_BARE));
+        upload_frame(s.get(), 0, frame, 0);
+        size_t npix = size_t(s->W) * s->H;
+        DevBuf dm, ds;
+        dm.ensure(npix * 3 * 8);
+        ds.ensure(npix * 3 * 8);
+        const FrameView& F = s->slot[0].view;
+        GHit* g = s->slot[0].gbuf.as<GHit>();
+        launch_gbuffer(F, g, ctx->stream);
+        PathCfg pc = path_cfg(c, gate_center, gate_width);
+        pc.ellipsoidal = 0;
+        launch_reference(F, g, pc, gate_center, gate_width, spp, uint64_t(frame), dm.as<double>(), ds.as<double>(),
+                         ctx->stream);
+        ck(cudaGetLastError(), "reference launch");
+        if (mean) ck(cudaMemcpyAsync(mean, dm.p, npix * 24, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        if (se) ck(cudaMemcpyAsync(se, ds.p, npix * 24, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        ck(cudaStreamSynchronize(ctx->stream), "reference");
+    });
+}
+
+int tofr_gpu_session_create(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
+                            tofr_session** out) {
+    if (!out) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        if (!ctx || !s) throw ScopeError(TOFR_ERR_INVALID, "null handle");
+        *out = make_session(ctx, s, cfg, KIND_RESTIR);
+    });
+}
+
+int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats) {
+    if (!ss) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] { session_step(ss, stats); });
+}
+
+int tofr_gpu_session_read_image(tofr_session* ss, double* image) {
+    if (!ss || !image) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        size_t npix = size_t(ss->W) * ss->H;
+        if (!ss->transient) {
+            ck(cudaMemcpyAsync(image, ss->image.p, npix * 24, cudaMemcpyDeviceToHost, ss->ctx->stream), "d2h");
+            ck(cudaStreamSynchronize(ss->ctx->stream), "d2h");
+        } else {
+            throw ScopeError(TOFR_ERR_UNSUPPORTED, "read_image on a transient session");
+        }
+    });
+}
+
+int tofr_gpu_session_sync(tofr_session* ss) {
+    if (!ss) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] { ck(cudaStreamSynchronize(ss->ctx->stream), "sync"); });
+}
+
+int tofr_gpu_session_last_ms(tofr_session* ss, double* total_ms, double* stage_ms) {
+    if (!ss) return TOFR_ERR_INVALID;
+    if (total_ms) *total_ms = ss->stage_ms[5];
+    if (stage_ms)
+        for (int i = 0; i < 6; ++i) stage_ms[i] = ss->stage_ms[i];
+    return TOFR_OK;
+}
+
+void tofr_gpu_session_destroy(tofr_session* ss) { delete ss; }
+
+int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const double* rays, int32_t n,
+                        int32_t mode, double* out_t, int32_t* out_tri) {
+    return guard(ctx, [&] {
+        if (!ctx || !sc || n < 0) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");
+        tofr_render_config c;
+        tofr_render_config_default(&c);
+        std::unique_ptr<tofr_session> s(make_session(ctx, sc, &c, KIND_BARE));
+        upload_frame(s.get(), 0, frame, 0);
+        if (n == 0) return;
+        DevBuf dr, dt, di;
+        dr.ensure(size_t(n) * 64);
+        dt.ensure(size_t(n) * 8);
+        di.ensure(size_t(n) * 4);
+        ck(cudaMemcpyAsync(dr.p, rays, size_t(n) * 64, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+        launch_probe_rays(s->slot[0].view, dr.as<double>(), n, mode, dt.as<double>(), di.as<int>(), ctx->stream);
+        ck(cudaGetLastError(), "probe launch");
+        ck(cudaMemcpyAsync(out_t, dt.p, size_t(n) * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        ck(cudaMemcpyAsync(out_tri, di.p, size_t(n) * 4, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        ck(cudaStreamSynchronize(ctx->stream), "probe");
+    });
+}
+
+}  // extern "C"
+
+static int scene_guard(char* err, size_t errlen, const std::function<void()>& fn) {
+    try {
+        fn();
+        set_err(err, errlen, "");
+        return TOFR_OK;
+    } catch (const tofr_b200::ParseError& e) {
+        set_err(err, errlen, std::to_string(e.line) + ":" + std::to_string(e.col) + ": " + e.what());
+        return TOFR_ERR_PARSE;
+    } catch (const ScopeError& e) {
+        set_err(err, errlen, e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return TOFR_ERR_SCENE;
+    }
+}

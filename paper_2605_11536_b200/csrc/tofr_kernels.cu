@@ -1,0 +1,748 @@
+// tofr_kernels.cu -- sm_100a kernels of the ToF ReSTIR frame pipeline.
+//
+//   k_gbuffer        primary hit per pixel (camera stage)
+//   k_init_gated     RIS over m_init path trees (+ shrink initializer)
+//   k_init_transient RIS into per-(pixel, bin) reservoirs
+//   k_temporal       reprojection + path-length shift + GRIS merge
+//   k_spatial        golden-angle neighbours, shift fwd/inv + GRIS merge
+//   k_binreuse       +-1 bin merge with the bin pitch as shift delta
+//   k_shade_gated    f * W * gate -> image (+ running frame sum)
+//   k_shade_transient per-bin final shading accumulated into the histogram
+//   k_hist_plain     trace-only transient deposits (Jarabo-style baseline)
+//   k_reference      brute-force gated estimator (mean and standard error)
+//
+// One thread owns one pixel (or pixel-bin) for the whole stage, which keeps
+// the reference's per-pixel sequential RNG semantics (the WRS pick stream is
+// consumed in candidate emission order, spatial neighbours merge in order).
+// Scenes are tiny, so each CTA stages the BVH nodes and triangle
+// intersection records of the frames it touches in shared memory.
+#include <cuda_runtime.h>
+
+#include "tofr_ellipsoid.cuh"
+#include "tofr_kernels.h"
+#include "tofr_store.cuh"
+
+namespace tofr_b200 {
+
+// ---------------------------------------------------------------------------
+// shared-memory staging of the traversal arrays
+
+__device__ __forceinline__ void stage_frame(FrameView& F, unsigned char* smem, size_t& off) {
+    if (size_t(F.n_nodes) * sizeof(GNode) + size_t(F.n_tris) * sizeof(GTriIsect) > kSmemStageLimit)
+        return;  // large mesh: traverse from global memory (L1/L2 cached)
+    size_t nb = size_t(F.n_nodes) * sizeof(GNode);
+    size_t tb = size_t(F.n_tris) * sizeof(GTriIsect);
+    GNode* sn = reinterpret_cast<GNode*>(smem + off);
+    off += (nb + 15) & ~size_t(15);
+    GTriIsect* st = reinterpret_cast<GTriIsect*>(smem + off);
+    off += (tb + 15) & ~size_t(15);
+    const double* gn = reinterpret_cast<const double*>(F.nodes);
+    double* dn = reinterpret_cast<double*>(sn);
+    for (size_t i = threadIdx.x; i < nb / 8; i += blockDim.x) dn[i] = gn[i];
+    const double* gt = reinterpret_cast<const double*>(F.tri_isect);
+    double* dt = reinterpret_cast<double*>(st);
+    for (size_t i = threadIdx.x; i < tb / 8; i += blockDim.x) dt[i] = gt[i];
+    F.nodes = sn;
+    F.tri_isect = st;
+}
+
+size_t frame_smem_bytes(const FrameView& F) {
+    size_t nb = size_t(F.n_nodes) * sizeof(GNode);
+    size_t tb = size_t(F.n_tris) * sizeof(GTriIsect);
+    if (nb + tb > kSmemStageLimit) return 0;
+    return ((nb + 15) & ~size_t(15)) + ((tb + 15) & ~size_t(15));
+}
+
+// ---------------------------------------------------------------------------
+// shift counters: per-thread u32, warp-reduced, one u64 atomic per warp
+
+__device__ __forceinline__ void flush_ctr(const uint32_t* c, unsigned long long* out) {
+    if (!out) return;
+#pragma unroll
+    for (int k = 0; k < SC_COUNT; ++k) {
+        unsigned long long v = c[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[k], v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// camera stage
+
+__global__ void __launch_bounds__(256) k_gbuffer(FrameView F, GHit* g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = p / W;
+        V3 d = primary_dir(F.cam, px, py);
+        Hit h;
+        GHit o;
+        o.pad = 0;
+        if (intersect(F, F.cam.pos, d, h)) {
+            o.t = h.t;
+            o.tri = h.tri;
+        } else {
+            o.t = kInf;
+            o.tri = -1;
+        }
+        g[p] = o;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// initial candidates
+
+// RIS into one in-register reservoir (stage::initial_sampling run_ris,
+// pipeline.hpp:114-128); winner record built when it wins.
+struct RisSink {
+    const FrameView* F;
+    double center, width, inv;
+    Rng* pick;
+    double w_sum;
+    int has;
+    double phat;
+    Sample* win;
+    __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ void emit(const Cand& c, double mis, const RecSrc& rs) {
+        double p = luminance(c.f) * gate_w(center, width, c.len);
+        if (p <= 0 || !(c.pdf > 0)) return;
+        double w = mis * inv * p / c.pdf;
+        if (!isfinite(w) || w < 0) return;
+        if (w <= 0) return;
+        w_sum += w;
+        if (rng_next(*pick) * w_sum < w) {
+            win->f = c.f;
+            win->len = c.len;
+            win->depth = c.depth;
+            build_record(*F, rs, win->rec);
+            has = 1;
+            phat = p;
+        }
+    }
+};
+
+template <class Ell>
+__device__ void run_ris(const FrameView& F, const PathCfg& cfg, const GHit& g, int px, int py,
+                        uint64_t pix, int frame_idx, int trees, double center, double width,
+                        Rng& pick, Sample& win, Res& out, WalkV* v, Ell& ell) {
+    out.has = 0;
+    out.W = 0;
+    out.phat = 0;
+    out.M = 0;
+    if (trees <= 0) return;
+    RisSink sink{&F, center, width, 1.0 / trees, &pick, 0.0, 0, 0.0, &win};
+    for (int s = 0; s < trees; ++s) {
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
+        Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
+        trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+    }
+    out.has = sink.has;
+    out.phat = sink.phat;
+    out.W = (sink.has && sink.phat > 0) ? sink.w_sum / sink.phat : 0;
+    out.M = 1;
+}
+
+template <class Ell>
+__device__ void init_pixel(const FrameView& F, const PathCfg& cfg, const InitParams& ip, const GHit& g,
+                           int px, int py, int frame_idx, Res& out, WalkV* v, Ell& ell) {
+    uint64_t pix = uint64_t(py) * F.cam.w + px;
+    Rng pick = rng_make(cfg.seed, uint64_t(frame_idx), pix, 0, 9);
+    if (ip.mode != INIT_SHRINK) {
+        run_ris(F, cfg, g, px, py, pix, frame_idx, ip.m_init, ip.center, ip.width, pick, out.y, out, v, ell);
+        out.M = 1;
+        return;
+    }
+    // shrink initializer (pipeline.hpp:137-183)
+    int m_rough = int(llround(ip.shrink_r * ip.m_init));
+    m_rough = m_rough < 0 ? 0 : (m_rough > ip.m_init ? ip.m_init : m_rough);
+    int m_fine = ip.m_init - m_rough;
+    Res rough;
+    run_ris(F, cfg, g, px, py, pix, frame_idx, m_rough, ip.center, ip.width * ip.shrink_k, pick, rough.y,
+            rough, v, ell);
+    run_ris(F, cfg, g, px, py, pix, frame_idx, m_fine, ip.center, ip.width, pick, out.y, out, v, ell);
+    out.M = 1;
+    if (res_empty(rough)) return;
+    Dom dom{px, py, ip.center, ip.width, &F, nullptr};
+    Sample fwd;
+    double fjac = 0;
+    bool fok = shrink_map(rough.y, dom, ip.shrink_k, true, cfg, fwd, fjac);
+    if (m_fine == 0) {
+        double w_sum = 0;
+        int has = 0;
+        double ph = 0;
+        if (fok) {
+            double pyv = luminance(fwd.f) * gate_w(ip.center, ip.width, fwd.len);
+            double w = pyv * rough.W * fjac;
+            if (isfinite(w) && w > 0) {
+                w_sum += w;
+                if (rng_next(pick) * w_sum < w) {
+                    has = 1;
+                    ph = pyv;
+                    out.y = fwd;
+                }
+            }
+        }
+        out.has = has;
+        out.phat = ph;
+        out.W = (has && ph > 0) ? w_sum / ph : 0;
+        out.M = 1;
+        return;
+    }
+    MergeShift ms{0, 1.0, 0.0};
+    if (fok) {
+        ms.valid = 1;
+        ms.jac = fjac;
+    }
+    if (!res_empty(out)) {
+        Sample inv;
+        double ijac = 0;
+        if (shrink_map(out.y, dom, ip.shrink_k, false, cfg, inv, ijac))
+            ms.phat_src_of_dst =
+                luminance(inv.f) * gate_w(ip.center, ip.width * ip.shrink_k, inv.len) * ijac;
+    }
+    gris_merge(out, rough, ms, fwd, ip.center, ip.width, cfg.m_cap, pick);
+}
+
+__global__ void __launch_bounds__(128) k_init_gated(FrameView F, const GHit* gbuf, PathCfg cfg,
+                                                    InitParams ip, int frame_idx, ResStore cur) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h;
+    WalkV v[kMaxVerts];
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = p / W;
+        Res r;
+        GHit g = gbuf[p];
+        if (cfg.ellipsoidal) {
+            EllStep ell;
+            init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
+        } else {
+            NoEll ell;
+            init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
+        }
+        res_store(cur, size_t(p), r);
+    }
+}
+
+// Transient RIS: candidates land in the reservoir of bin_of(len); p-hat is
+// evaluated against that bin's (inclusive) gate (pipeline.hpp:421-445).
+struct BinSink {
+    const FrameView* F;
+    HistSpec h;
+    double inv;
+    Rng* pick;
+    ResStore st;
+    size_t base;
+    __device__ bool wants(double len) const {
+        int b = bin_of(h, len);
+        return b >= 0 && gate_w(bin_center(h, b), h.bw, len) > 0;
+    }
+    __device__ void emit(const Cand& c, double mis, const RecSrc& rs) {
+        int b = bin_of(h, c.len);
+        if (b < 0 || !(c.pdf > 0)) return;
+        double p = luminance(c.f) * gate_w(bin_center(h, b), h.bw, c.len);
+        if (p <= 0) return;
+        double w = mis * inv * p / c.pdf;
+        if (!isfinite(w) || w < 0) return;
+        if (w <= 0) return;
+        size_t i = base + b;
+        double2 c0 = ld2(st, 0, i);  // (w_sum during init, M)
+        double w_sum = c0.x + w;
+        st2(st, 0, i, w_sum, c0.y);
+        if (rng_next(*pick) * w_sum < w) {
+            Res r;
+            r.W = w_sum;
+            r.M = c0.y;
+            r.has = 1;
+            r.phat = p;
+            r.y.f = c.f;
+            r.y.len = c.len;
+            r.y.depth = c.depth;
+            build_record(*F, rs, r.y.rec);
+            res_store(st, i, r);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(128) k_init_transient(FrameView F, const GHit* gbuf, PathCfg cfg,
+                                                        InitParams ip, HistSpec h, int frame_idx,
+                                                        ResStore cur) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h, B = h.bins;
+    WalkV v[kMaxVerts];
+    NoEll ell;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        size_t base = size_t(p) * B;
+        for (int b = 0; b < B; ++b) res_store_empty(cur, base + b, 0.0);
+        Rng pick = rng_make(cfg.seed, uint64_t(frame_idx), pix, 0, 9);
+        BinSink sink{&F, h, 1.0 / ip.m_init, &pick, cur, base};
+        GHit g = gbuf[p];
+        for (int s = 0; s < ip.m_init; ++s) {
+            Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
+            Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
+            trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+        }
+        for (int b = 0; b < B; ++b) {  // ris_finalize + M = 1
+            size_t i = base + b;
+            double2 c0 = ld2(cur, 0, i);
+            Meta m = ld_meta(cur, i);
+            double phat = m.has ? ld2(cur, 1, i).x : 0.0;
+            double Wv = (m.has && phat > 0) ? c0.x / phat : 0;
+            st2(cur, 0, i, Wv, 1.0);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// temporal reuse (stage::temporal_reuse, pipeline.hpp:209-229)
+
+__device__ __forceinline__ void gate_of(const GateGrid& gg, int b, double& c, double& w) {
+    if (gg.transient) {
+        c = bin_center(gg.h, b);
+        w = gg.h.bw;
+    } else {
+        c = gg.center;
+        w = gg.width;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_temporal(FrameView Fc, const GHit* gc, FrameView Fp,
+                                                  const GHit* gp, PathCfg cfg, GateGrid cur_gate,
+                                                  GateGrid prev_gate, int frame_idx, ResStore cur,
+                                                  ResStore prev, unsigned long long* ctr_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(Fc, smem, off);
+    stage_frame(Fp, smem, off);
+    __syncthreads();
+    int W = Fc.cam.w, H = Fc.cam.h, B = cur_gate.transient ? cur_gate.h.bins : 1;
+    uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    size_t n_items = size_t(W) * H * B;
+    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+         it += size_t(gridDim.x) * blockDim.x) {
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        GHit g = gc[p];
+        if (g.tri < 0) continue;
+        V3 d0 = primary_dir(Fc.cam, px, py);
+        V3 hp = Fc.cam.pos + d0 * g.t;
+        int qx, qy;
+        if (!project(Fp.cam, hp, qx, qy)) continue;
+        size_t src_i = (size_t(qy) * W + qx) * B + b;
+        double sW, sM;
+        int shas;
+        res_load_hdr(prev, src_i, sW, sM, shas);
+        if (sM <= 0) continue;
+        double dc, dw, sc, sw;
+        gate_of(cur_gate, b, dc, dw);
+        gate_of(prev_gate, b, sc, sw);
+        Res dst, src;
+        res_load(cur, it, dst);
+        res_load(prev, src_i, src);
+        Dom dd{px, py, dc, dw, &Fc, gc};
+        Dom sd{qx, qy, sc, sw, &Fp, gp};
+        MergeShift ms{0, 1.0, 0.0};
+        Sample mapped;
+        if (!res_empty(src)) {
+            double jac;
+            if (shift_sample(src.y, sd, dd, cfg, ctr, mapped, jac)) {
+                ms.valid = 1;
+                ms.jac = jac;
+            }
+        }
+        if (!res_empty(dst)) {
+            Sample inv;
+            double jac;
+            if (shift_sample(dst.y, dd, sd, cfg, nullptr, inv, jac))
+                ms.phat_src_of_dst = luminance(inv.f) * gate_w(sc, sw, inv.len) * jac;
+        }
+        uint64_t pix = uint64_t(py) * W + px;
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
+        gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        res_store(cur, it, dst);
+    }
+    flush_ctr(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// spatial reuse (stage::spatial_reuse + neighbor_offset, pipeline.hpp:232-269)
+
+__device__ __forceinline__ void neighbor_offset(int j, int count, double radius, uint64_t rot_key,
+                                                int& dx, int& dy) {
+    double rot = double(mix64(rot_key) >> 11) * 0x1.0p-53 * 2.0 * kPi;
+    double rr = radius * sqrt((j + 0.5) / count);
+    double th = j * 2.39996322972865332 + rot;
+    dx = int(llround(rr * cos(th)));
+    dy = int(llround(rr * sin(th)));
+}
+
+__global__ void __launch_bounds__(128) k_spatial(FrameView F, const GHit* gbuf, PathCfg cfg,
+                                                 GateGrid gate, SpatialParams sp, int pass,
+                                                 int frame_idx, ResStore src_grid, ResStore dst_grid,
+                                                 unsigned long long* ctr_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    size_t n_items = size_t(W) * H * B;
+    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+         it += size_t(gridDim.x) * blockDim.x) {
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        Res out;
+        res_load(src_grid, it, out);
+        if (sp.neighbors > 0 && sp.radius > 0) {
+            double dc, dw;
+            gate_of(gate, b, dc, dw);
+            uint64_t pix = uint64_t(py) * W + px;
+            Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(pass * 131 + b), 10);
+            Dom dd{px, py, dc, dw, &F, gbuf};
+            uint64_t rk = mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + uint64_t(cfg.seed) +
+                                uint64_t(frame_idx) * 97);
+            for (int j = 0; j < sp.neighbors; ++j) {
+                int dx, dy;
+                neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+                int nx = px + dx, ny = py + dy;
+                if (nx == px && ny == py) continue;
+                if (nx < 0 || nx >= W || ny < 0 || ny >= H) continue;
+                size_t si = (size_t(ny) * W + nx) * B + b;
+                double sW, sM;
+                int shas;
+                res_load_hdr(src_grid, si, sW, sM, shas);
+                if (sM <= 0) continue;
+                Res src;
+                res_load(src_grid, si, src);
+                Dom sd{nx, ny, dc, dw, &F, gbuf};
+                MergeShift ms{0, 1.0, 0.0};
+                Sample mapped;
+                if (!res_empty(src)) {
+                    double jac;
+                    if (shift_sample(src.y, sd, dd, cfg, ctr, mapped, jac)) {
+                        ms.valid = 1;
+                        ms.jac = jac;
+                    }
+                }
+                if (!res_empty(out)) {
+                    Sample inv;
+                    double jac;
+                    if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
+                        ms.phat_src_of_dst = luminance(inv.f) * gate_w(dc, dw, inv.len) * jac;
+                }
+                gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+            }
+        }
+        res_store(dst_grid, it, out);
+    }
+    flush_ctr(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// bin reuse (stage::bin_reuse, pipeline.hpp:273-299)
+
+__global__ void __launch_bounds__(128) k_binreuse(FrameView F, const GHit* gbuf, PathCfg cfg, HistSpec h,
+                                                  int frame_idx, ResStore src_grid, ResStore dst_grid,
+                                                  unsigned long long* ctr_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h, B = h.bins;
+    uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    size_t n_items = size_t(W) * H * B;
+    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+         it += size_t(gridDim.x) * blockDim.x) {
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        Res out;
+        res_load(src_grid, it, out);
+        double dc = bin_center(h, b), dw = h.bw;
+        Dom dd{px, py, dc, dw, &F, gbuf};
+        uint64_t pix = uint64_t(py) * W + px;
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 12);
+        for (int k = 0; k < 2; ++k) {
+            int nb = k == 0 ? b - 1 : b + 1;
+            if (nb < 0 || nb >= B) continue;
+            size_t si = size_t(p) * B + nb;
+            double sW, sM;
+            int shas;
+            res_load_hdr(src_grid, si, sW, sM, shas);
+            if (sM <= 0) continue;
+            Res src;
+            res_load(src_grid, si, src);
+            double sc = bin_center(h, nb);
+            Dom sd{px, py, sc, dw, &F, gbuf};
+            MergeShift ms{0, 1.0, 0.0};
+            Sample mapped;
+            if (!res_empty(src)) {
+                double jac;
+                if (shift_sample(src.y, sd, dd, cfg, ctr, mapped, jac)) {
+                    ms.valid = 1;
+                    ms.jac = jac;
+                }
+            }
+            if (!res_empty(out)) {
+                Sample inv;
+                double jac;
+                if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
+                    ms.phat_src_of_dst = luminance(inv.f) * gate_w(sc, dw, inv.len) * jac;
+            }
+            gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        }
+        res_store(dst_grid, it, out);
+    }
+    flush_ctr(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// final shading (ris.hpp:108-111)
+
+__device__ __forceinline__ V3 shade_item(const ResStore& s, size_t i, double c, double w) {
+    double W, M;
+    int has;
+    res_load_hdr(s, i, W, M, has);
+    if (!has || W <= 0) return splat(0);
+    double2 c1 = ld2(s, 1, i), c2 = ld2(s, 2, i), c3 = ld2(s, 3, i);
+    V3 f{c2.x, c2.y, c3.x};
+    return f * (W * gate_w(c, w, c1.y));
+}
+
+__global__ void k_shade_gated(ResStore cur, int n_pix, double center, double width, double* image,
+                              double* accum) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_pix; p += gridDim.x * blockDim.x) {
+        V3 v = shade_item(cur, size_t(p), center, width);
+        image[3 * size_t(p) + 0] = v.x;
+        image[3 * size_t(p) + 1] = v.y;
+        image[3 * size_t(p) + 2] = v.z;
+        accum[3 * size_t(p) + 0] += v.x;
+        accum[3 * size_t(p) + 1] += v.y;
+        accum[3 * size_t(p) + 2] += v.z;
+    }
+}
+
+__global__ void k_shade_transient(ResStore cur, size_t n_items, HistSpec h, double* hist) {
+    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+         it += size_t(gridDim.x) * blockDim.x) {
+        int b = int(it % h.bins);
+        V3 v = shade_item(cur, it, bin_center(h, b), h.bw);
+        if (v.x != 0 || v.y != 0 || v.z != 0) {
+            hist[3 * it + 0] += v.x;
+            hist[3 * it + 1] += v.y;
+            hist[3 * it + 2] += v.z;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// trace-only transient deposits (render_transient_plain, pipeline.hpp:531-571;
+// TransientHistogram::deposit, transport.hpp:121-126).  Each thread owns its
+// pixel's B bins, so deposits are plain read-modify-writes in emission order.
+
+struct PlainSink {
+    HistSpec h;
+    int m_init;
+    double* rgb;
+    uint32_t* count;
+    size_t base;
+    __device__ bool wants(double len) const { return bin_of(h, len) >= 0; }
+    __device__ void emit(const Cand& c, double mis, const RecSrc&) {
+        if (!(c.pdf > 0)) return;
+        V3 val = c.f * (mis / c.pdf / m_init);
+        int b = bin_of(h, c.len);
+        if (b < 0) return;
+        size_t i = base + b;
+        rgb[3 * i + 0] += val.x;
+        rgb[3 * i + 1] += val.y;
+        rgb[3 * i + 2] += val.z;
+        count[i] += 1;
+    }
+};
+
+__global__ void __launch_bounds__(128) k_hist_plain(FrameView F, const GHit* gbuf, PathCfg cfg, HistSpec h,
+                                                    int m_init, int frame_idx, double* rgb,
+                                                    uint32_t* count) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h;
+    WalkV v[kMaxVerts];
+    NoEll ell;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins};
+        GHit g = gbuf[p];
+        for (int s = 0; s < m_init; ++s) {
+            Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
+            Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
+            trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// brute-force gated reference (reference_gated_pixel, transport.hpp:591-617)
+
+struct RefSink {
+    double center, width;
+    V3 est;
+    __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ void emit(const Cand& c, double mis, const RecSrc&) {
+        double w = gate_w(center, width, c.len);
+        if (w > 0 && c.pdf > 0) est = est + c.f * (mis * w / c.pdf);
+    }
+};
+
+__global__ void __launch_bounds__(128) k_reference(FrameView F, const GHit* gbuf, PathCfg cfg, double center,
+                                                   double width, int spp, uint64_t frame_key, double* mean,
+                                                   double* se) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h;
+    WalkV v[kMaxVerts];
+    NoEll ell;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        GHit g = gbuf[p];
+        V3 sum = splat(0), sum2 = splat(0);
+        for (int s = 0; s < spp; ++s) {
+            RefSink sink{center, width, splat(0)};
+            Rng rng = rng_make(cfg.seed, frame_key, pix, uint64_t(s), 0);
+            Rng erng = rng_make(cfg.seed, frame_key, pix, uint64_t(s), 2);
+            trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+            sum = sum + sink.est;
+            sum2 = sum2 + sink.est * sink.est;
+        }
+        V3 m = sum / double(spp);
+        V3 var = sum2 / double(spp) - m * m;
+        var = V3{dmax(0.0, var.x), dmax(0.0, var.y), dmax(0.0, var.z)};
+        mean[3 * size_t(p) + 0] = m.x;
+        mean[3 * size_t(p) + 1] = m.y;
+        mean[3 * size_t(p) + 2] = m.z;
+        se[3 * size_t(p) + 0] = sqrt(var.x / spp);
+        se[3 * size_t(p) + 1] = sqrt(var.y / spp);
+        se[3 * size_t(p) + 2] = sqrt(var.z / spp);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// debug / parity probes
+
+__global__ void k_probe_rays(FrameView F, const double* rays, int n, int mode, double* out_t, int* out_tri) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = rays + 8 * size_t(i);  // o.xyz, d.xyz, tmin, tmax
+    V3 o{r[0], r[1], r[2]}, d{r[3], r[4], r[5]};
+    if (mode == 0) {
+        Hit h;
+        if (trace_closest(F, o, d, r[6], r[7], h)) {
+            out_t[i] = h.t;
+            out_tri[i] = h.tri;
+        } else {
+            out_t[i] = kInf;
+            out_tri[i] = -1;
+        }
+    } else {
+        // occluded(a = o, b = d)
+        out_tri[i] = occluded(F, o, d) ? 1 : 0;
+        out_t[i] = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+static int grid_for(size_t n, int block) {
+    size_t g = (n + block - 1) / block;
+    if (g > 148 * 64) g = 148 * 64;
+    if (g < 1) g = 1;
+    return int(g);
+}
+
+void set_gauss_rule(const double* x, const double* w, cudaStream_t s) {
+    cudaMemcpyToSymbolAsync(c_gl_x, x, 32 * sizeof(double), 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_gl_w, w, 32 * sizeof(double), 0, cudaMemcpyHostToDevice, s);
+}
+
+void launch_gbuffer(const FrameView& F, GHit* g, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h;
+    k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, g);
+}
+
+void launch_init_gated(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
+                       int frame_idx, ResStore cur, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h;
+    k_init_gated<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, ip, frame_idx, cur);
+}
+
+void launch_init_transient(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
+                           const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h;
+    k_init_transient<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, ip, h, frame_idx, cur);
+}
+
+void launch_temporal(const FrameView& Fc, const GHit* gc, const FrameView& Fp, const GHit* gp,
+                     const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
+                     ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s) {
+    size_t n = size_t(Fc.cam.w) * Fc.cam.h * (cg.transient ? cg.h.bins : 1);
+    size_t sm = frame_smem_bytes(Fc) + frame_smem_bytes(Fp);
+    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, ctr);
+}
+
+void launch_spatial(const FrameView& F, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                    const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
+                    unsigned long long* ctr, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h * (gg.transient ? gg.h.bins : 1);
+    k_spatial<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, gg, sp, pass, frame_idx, src,
+                                                                 dst, ctr);
+}
+
+void launch_binreuse(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int frame_idx,
+                     ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h * h.bins;
+    k_binreuse<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, h, frame_idx, src, dst, ctr);
+}
+
+void launch_shade_gated(ResStore cur, int n_pix, double center, double width, double* image, double* accum,
+                        cudaStream_t s) {
+    k_shade_gated<<<grid_for(n_pix, 256), 256, 0, s>>>(cur, n_pix, center, width, image, accum);
+}
+
+void launch_shade_transient(ResStore cur, size_t n_items, const HistSpec& h, double* hist, cudaStream_t s) {
+    k_shade_transient<<<grid_for(n_items, 256), 256, 0, s>>>(cur, n_items, h, hist);
+}
+
+void launch_hist_plain(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int m_init,
+                       int frame_idx, double* rgb, uint32_t* count, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h;
+    k_hist_plain<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, h, m_init, frame_idx, rgb, count);
+}
+
+void launch_reference(const FrameView& F, const GHit* g, const PathCfg& cfg, double center, double width,
+                      int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s) {
+    size_t n = size_t(F.cam.w) * F.cam.h;
+    k_reference<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, center, width, spp, frame_key,
+                                                                  mean, se);
+}
+
+void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
+                       cudaStream_t s) {
+    k_probe_rays<<<(n + 127) / 128, 128, 0, s>>>(F, rays, n, mode, out_t, out_tri);
+}
+
+}  // namespace tofr_b200

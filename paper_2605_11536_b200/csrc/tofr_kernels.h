@@ -1,0 +1,61 @@
+// tofr_kernels.h -- host-visible launch interface of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "tofr_path.cuh"
+#include "tofr_store.cuh"
+
+namespace tofr_b200 {
+
+// Per-frame traversal arrays above this size stay in global memory.
+constexpr size_t kSmemStageLimit = 20 * 1024;
+
+enum : int { INIT_DIRECT = 0, INIT_ELLIPSOIDAL = 1, INIT_SHRINK = 2 };
+
+struct InitParams {
+    int mode;
+    int m_init;
+    double center, width;  // gate of this frame
+    double shrink_k, shrink_r;
+};
+
+// Gate per reservoir item: one gate (gated) or the bin gates (transient).
+struct GateGrid {
+    int transient;
+    double center, width;
+    HistSpec h;
+};
+
+struct SpatialParams {
+    int neighbors;
+    double radius;
+};
+
+size_t frame_smem_bytes(const FrameView& F);
+void set_gauss_rule(const double* x, const double* w, cudaStream_t s);
+void launch_gbuffer(const FrameView& F, GHit* g, cudaStream_t s);
+void launch_init_gated(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
+                       int frame_idx, ResStore cur, cudaStream_t s);
+void launch_init_transient(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
+                           const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s);
+void launch_temporal(const FrameView& Fc, const GHit* gc, const FrameView& Fp, const GHit* gp,
+                     const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
+                     ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s);
+void launch_spatial(const FrameView& F, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                    const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
+                    unsigned long long* ctr, cudaStream_t s);
+void launch_binreuse(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int frame_idx,
+                     ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s);
+void launch_shade_gated(ResStore cur, int n_pix, double center, double width, double* image, double* accum,
+                        cudaStream_t s);
+void launch_shade_transient(ResStore cur, size_t n_items, const HistSpec& h, double* hist, cudaStream_t s);
+void launch_hist_plain(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int m_init,
+                       int frame_idx, double* rgb, uint32_t* count, cudaStream_t s);
+void launch_reference(const FrameView& F, const GHit* g, const PathCfg& cfg, double center, double width,
+                      int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s);
+void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
+                       cudaStream_t s);
+
+}  // namespace tofr_b200

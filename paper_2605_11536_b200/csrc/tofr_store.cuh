@@ -1,0 +1,214 @@
+// tofr_store.cuh -- reservoir grids in HBM.
+//
+// A reservoir is 22 x 16 B chunks (352 B).  Grids are chunk-major: chunk c of
+// item i lives at base[c * stride + i], so when a warp touches 32 consecutive
+// items every 128-bit load/store instruction moves 512 contiguous bytes
+// (fully coalesced).  Readers that only need the header (confidence M,
+// emptiness) touch chunks 0 and 4 only; the replay lanes (chunks 20-21) are
+// read only when a record has k > 2.
+//
+//   0: W, M                     8: p1.y, p1.z         16: n2.z, wo2.x
+//   1: phat, len                9: wi1.x, wi1.y       17: wo2.y, wo2.z
+//   2: f.x, f.y                10: wi1.z, p.x         18: suffix_f.x, .y
+//   3: f.z, suffix_len         11: p.y, p.z           19: suffix_f.z, {m2, -}
+//   4: {has,valid,k,nl,skind,depth,-,-}, tri1, ptri
+//   5: prefix_pdf, prefix_len  12: pn.x, pn.y         20: lane_key, ctr[0..3]
+//   6: prefix_fw.x, .y         13: pn.z, p2.x         21: ctr[4..9], -
+//   7: prefix_fw.z, p1.x       14: p2.y, p2.z
+//                              15: n2.x, n2.y
+#pragma once
+
+#include "tofr_path.cuh"
+
+namespace tofr_b200 {
+
+constexpr int kResChunks = 22;
+
+struct ResStore {
+    double2* base;
+    size_t stride;  // items per chunk plane
+};
+
+#if defined(__CUDACC__)
+
+__device__ __forceinline__ double2 ld2(const ResStore& s, int c, size_t i) {
+    return __ldcg(&s.base[size_t(c) * s.stride + i]);
+}
+__device__ __forceinline__ void st2(const ResStore& s, int c, size_t i, double a, double b) {
+    __stcg(&s.base[size_t(c) * s.stride + i], make_double2(a, b));
+}
+
+struct Meta {
+    unsigned char has, valid, k, nl, skind, depth, pad0, pad1;
+    int tri1, ptri;
+};
+
+__device__ __forceinline__ Meta ld_meta(const ResStore& s, size_t i) {
+    double2 v = ld2(s, 4, i);
+    Meta m;
+    static_assert(sizeof(Meta) == 16, "meta chunk");
+    memcpy(&m, &v, 16);
+    return m;
+}
+
+// Header: W, M, has (enough for empty() and the src.M <= 0 tests)
+__device__ __forceinline__ void res_load_hdr(const ResStore& s, size_t i, double& W, double& M, int& has) {
+    double2 c0 = ld2(s, 0, i);
+    W = c0.x;
+    M = c0.y;
+    has = ld_meta(s, i).has;
+}
+
+__device__ void res_load(const ResStore& s, size_t i, Res& r) {
+    double2 c;
+    c = ld2(s, 0, i);
+    r.W = c.x;
+    r.M = c.y;
+    c = ld2(s, 1, i);
+    r.phat = c.x;
+    r.y.len = c.y;
+    c = ld2(s, 2, i);
+    r.y.f.x = c.x;
+    r.y.f.y = c.y;
+    c = ld2(s, 3, i);
+    r.y.f.z = c.x;
+    Rec& q = r.y.rec;
+    q.suffix_len = c.y;
+    Meta m = ld_meta(s, i);
+    r.has = m.has;
+    q.valid = m.valid;
+    q.k = m.k == 255 ? -1 : int(m.k);
+    q.n_lanes = m.nl;
+    q.skind = m.skind;
+    r.y.depth = m.depth;
+    q.tri1 = m.tri1;
+    q.ptri = m.ptri;
+    c = ld2(s, 5, i);
+    q.prefix_pdf = c.x;
+    q.prefix_len = c.y;
+    c = ld2(s, 6, i);
+    q.prefix_fw.x = c.x;
+    q.prefix_fw.y = c.y;
+    c = ld2(s, 7, i);
+    q.prefix_fw.z = c.x;
+    q.p1.x = c.y;
+    c = ld2(s, 8, i);
+    q.p1.y = c.x;
+    q.p1.z = c.y;
+    c = ld2(s, 9, i);
+    q.wi1.x = c.x;
+    q.wi1.y = c.y;
+    c = ld2(s, 10, i);
+    q.wi1.z = c.x;
+    q.p.x = c.y;
+    c = ld2(s, 11, i);
+    q.p.y = c.x;
+    q.p.z = c.y;
+    c = ld2(s, 12, i);
+    q.pn.x = c.x;
+    q.pn.y = c.y;
+    c = ld2(s, 13, i);
+    q.pn.z = c.x;
+    q.p2.x = c.y;
+    c = ld2(s, 14, i);
+    q.p2.y = c.x;
+    q.p2.z = c.y;
+    c = ld2(s, 15, i);
+    q.n2.x = c.x;
+    q.n2.y = c.y;
+    c = ld2(s, 16, i);
+    q.n2.z = c.x;
+    q.wo2.x = c.y;
+    c = ld2(s, 17, i);
+    q.wo2.y = c.x;
+    q.wo2.z = c.y;
+    c = ld2(s, 18, i);
+    q.suffix_f.x = c.x;
+    q.suffix_f.y = c.y;
+    c = ld2(s, 19, i);
+    q.suffix_f.z = c.x;
+    {
+        int2 mi;
+        memcpy(&mi, &c.y, 8);
+        q.m2 = mi.x;
+    }
+    if (q.n_lanes > 0) {
+        c = ld2(s, 20, i);
+        memcpy(&q.lane_key, &c.x, 8);
+        memcpy(&q.lane_ctr[0], &c.y, 8);
+        c = ld2(s, 21, i);
+        memcpy(&q.lane_ctr[4], &c, 12);
+    } else {
+        q.lane_key = 0;
+        for (int j = 0; j < kMaxLanes; ++j) q.lane_ctr[j] = 0;
+    }
+}
+
+__device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& r) {
+    Meta m;
+    const Rec& q = r.y.rec;
+    m.has = (unsigned char)(r.has ? 1 : 0);
+    m.valid = (unsigned char)q.valid;
+    m.k = q.k < 0 ? 255 : (unsigned char)q.k;
+    m.nl = (unsigned char)q.n_lanes;
+    m.skind = (unsigned char)q.skind;
+    m.depth = (unsigned char)r.y.depth;
+    m.pad0 = m.pad1 = 0;
+    m.tri1 = q.tri1;
+    m.ptri = q.ptri;
+    double2 v;
+    memcpy(&v, &m, 16);
+    st2(s, 4, i, v.x, v.y);
+}
+
+__device__ void res_store(const ResStore& s, size_t i, const Res& r) {
+    const Rec& q = r.y.rec;
+    st2(s, 0, i, r.W, r.M);
+    st2(s, 1, i, r.phat, r.y.len);
+    st2(s, 2, i, r.y.f.x, r.y.f.y);
+    st2(s, 3, i, r.y.f.z, q.suffix_len);
+    st_meta(s, i, r);
+    st2(s, 5, i, q.prefix_pdf, q.prefix_len);
+    st2(s, 6, i, q.prefix_fw.x, q.prefix_fw.y);
+    st2(s, 7, i, q.prefix_fw.z, q.p1.x);
+    st2(s, 8, i, q.p1.y, q.p1.z);
+    st2(s, 9, i, q.wi1.x, q.wi1.y);
+    st2(s, 10, i, q.wi1.z, q.p.x);
+    st2(s, 11, i, q.p.y, q.p.z);
+    st2(s, 12, i, q.pn.x, q.pn.y);
+    st2(s, 13, i, q.pn.z, q.p2.x);
+    st2(s, 14, i, q.p2.y, q.p2.z);
+    st2(s, 15, i, q.n2.x, q.n2.y);
+    st2(s, 16, i, q.n2.z, q.wo2.x);
+    st2(s, 17, i, q.wo2.y, q.wo2.z);
+    st2(s, 18, i, q.suffix_f.x, q.suffix_f.y);
+    double m2d;
+    int2 mi = make_int2(q.m2, 0);
+    memcpy(&m2d, &mi, 8);
+    st2(s, 19, i, q.suffix_f.z, m2d);
+    if (q.n_lanes > 0) {
+        double a, b;
+        memcpy(&a, &q.lane_key, 8);
+        memcpy(&b, &q.lane_ctr[0], 8);
+        st2(s, 20, i, a, b);
+        double2 t = make_double2(0, 0);
+        memcpy(&t, &q.lane_ctr[4], 12);
+        st2(s, 21, i, t.x, t.y);
+    }
+}
+
+// Header-only write for an empty reservoir: W, M and the has/meta chunk.
+__device__ __forceinline__ void res_store_empty(const ResStore& s, size_t i, double M) {
+    st2(s, 0, i, 0.0, M);
+    Meta m;
+    memset(&m, 0, sizeof(m));
+    m.k = 255;
+    m.tri1 = m.ptri = -1;
+    double2 v;
+    memcpy(&v, &m, 16);
+    st2(s, 4, i, v.x, v.y);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace tofr_b200
