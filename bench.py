@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- frames/s and Mpaths/s of the B200 ToF ReSTIR frame pipeline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3]
+
+A step is one frame of the interactive pipeline (render_gated's frame loop,
+pipeline.hpp:323-392): host build_frame + snapshot upload, G-buffer, initial
+RIS, temporal reuse, spatial reuse, final shading.  The default workload is
+BASELINE.json configs[2] ("C3"): the largest bundled scene (boxes_doppler,
+24 triangles, animated -> BVH rebuilt every frame) at 1920x1080, time-gated
+with a narrow gate (tau 12.0, dtau 0.041 = 0.5% of the scene diagonal),
+m_init 1, temporal + 1x3 spatial reuse of radius 10.
+
+Our arm prints one JSON line with the device-timed `value` (CUDA events on
+the library stream, max over ranks), `e2e` (the same frames through the
+public Session API, each step also reading the image back to pinned host
+memory), the `roofline` of the dominant kernel, `cpu_baseline` (the reference
+CPU renderer, oracle/_ref, timed on this host) and the clocks seen.
+`--impl reference` times the unmodified reference CPU renderer (oracle/_ref,
+built from /root/reference/proj/include) on the same workload.
+
+Multi-GPU (torchrun): the frame is split into row bands, one per rank, and
+the spatial-reuse halo rows are exchanged with NCCL (parallel.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+from paper_2605_11536_b200 import _ffi as F  # noqa: E402
+from paper_2605_11536_b200 import scenes  # noqa: E402
+from paper_2605_11536_b200.api import GateSpec, RenderConfig  # noqa: E402
+
+METRIC = "frames/sec and Mpaths/s at 1080p (time-gated & transient), 1/2/4/8 B200"
+
+
+def _gate(c, w):
+    return GateSpec(F.GATE_LENGTH, c, w, 1.0)
+
+
+# name -> (scene, width, height, RenderConfig(frames ignored), description)
+WORKLOADS = {
+    "c3": ("boxes_doppler", 1920, 1080,
+           RenderConfig(gate=_gate(12.0, 0.041), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
+                        spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+           "C3: boxes_doppler 1920x1080 gated tau=12.0 dtau=0.041, m_init 1, temporal + 1x3 spatial r10"),
+    "c3w": ("cornell_wide", 1920, 1080,
+            RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
+                         spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+            "C3': cornell_wide 1920x1080 gated tau=6.0 dtau=0.0173, m_init 1, temporal + 1x3 spatial r10"),
+    "c5": ("cornell_wide", 1920, 1080,
+           RenderConfig(gate=_gate(6.0, 0.0173), gate_step=0.01, m_init=1, temporal=True, spatial_passes=1,
+                        spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+           "C5: cornell_wide 1920x1080 gate sweep 0.01/frame, temporal + 1x3 spatial r10"),
+    "c1": ("cornell", 256, 256,
+           RenderConfig(gate=_gate(10.0, 0.0866), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
+                        spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+           "C1: cornell 256x256 gated tau=10.0 dtau=0.0866, m_init 1, temporal + 1x3 spatial r10"),
+}
+
+# launches of our kernels per frame: gbuffer, init, temporal, spatial x P, shade
+def launches_per_frame(cfg: RenderConfig, first: bool) -> int:
+    return 2 + (0 if first or not cfg.temporal else 1) + cfg.spatial_passes + 1
+
+
+# algorithmic bytes per pixel (compact reservoir R = 224 B)
+R_BYTES = 224
+GHIT_BYTES = 16
+
+
+def stage_bytes_per_pixel(cfg: RenderConfig) -> dict:
+    n = cfg.spatial_neighbors
+    return {
+        "init": GHIT_BYTES + R_BYTES,  # G-buffer read + reservoir write
+        "temporal": 3 * R_BYTES,  # prev read, cur read, cur write
+        "spatial": (1 + n) * R_BYTES + R_BYTES,  # per pass: (1+N) reads + 1 write
+        "shade": 24 + 12,
+    }
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the unmodified reference CPU renderer
+
+
+def cpu_reference_sample(wl: str, frames: int = 2) -> dict:
+    """render_gated of the reference (oracle/_ref) with all host threads on the
+    full workload, `frames` frames (frame 0 init + spatial, frame 1 adds the
+    temporal stage).  Returns seconds and the thread count."""
+    from oracle import ref as R
+    scene_name, w, h, cfg, _ = WORKLOADS[wl]
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    sd = scenes.bundled(scene_name, w, h)
+    rs = R.RefScene(sd)
+    c = RenderConfig(**{**cfg.__dict__})
+    c.frames = frames
+    t0 = time.perf_counter()
+    R.render_gated(rs, c)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "frames": frames, "cores": R.threads(), "pixels": w * h}
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    scene_name, w, h, cfg, desc = WORKLOADS[args.workload]
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.workload, 1)
+    secs, frames, cores = 0.0, 0, 1
+    for _ in range(args.steps):
+        r = cpu_reference_sample(args.workload, 2)
+        secs += r["seconds"]
+        frames += r["frames"]
+        cores = r["cores"]
+    fps = frames / secs
+    sample = (f"{args.steps} x render_gated(frames=2) of the full {w}x{h} workload "
+              f"(frame 0: init+spatial, frame 1: init+temporal+spatial)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / frames,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "resolution": f"{w}x{h}", "scene": scene_name},
+        "mpaths_per_s": w * h * cfg.m_init * fps / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args) -> None:
+    import torch
+    ws, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    from paper_2605_11536_b200 import parallel
+    from paper_2605_11536_b200.api import Renderer
+
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    scene_name, w, h, cfg, desc = WORKLOADS[args.workload]
+    sd = scenes.bundled(scene_name, w, h)
+    r = Renderer(local)
+    sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group)
+    for _ in range(args.warmup):
+        sess.step()
+    sess.sync()
+    parallel.barrier(group)
+
+    clk = ClockSampler(local) if rank == 0 else None
+    stage_tot = [0.0] * 6
+    t_ms = sess.timed_steps(args.steps, stage_tot)
+    clocks = clk.stop() if clk else None
+    t_max = parallel.max_over_ranks(t_ms, group)
+    frames = args.steps
+    fps = frames / (t_max * 1e-3)
+
+    # e2e through the public API: step + image read-back to pinned host memory
+    parallel.barrier(group)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sess.step()
+        sess.read_image_host()
+    e2e_s = time.perf_counter() - t0
+    e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
+    h2d, d2h = sess.io_bytes()
+
+    # roofline of the dominant kernel (average launch duration from CUDA events)
+    avg = [x / args.steps for x in stage_tot]
+    names = ["init", "temporal", "bin", "spatial", "shade"]
+    per_px = stage_bytes_per_pixel(cfg)
+    dom = max(range(5), key=lambda i: avg[i])
+    dom_name = names[dom]
+    launches = max(1, cfg.spatial_passes) if dom_name == "spatial" else 1
+    band_px = sess.owned_pixels()
+    algo = per_px.get(dom_name, 0) * band_px
+    dur_s = avg[dom] / launches * 1e-3
+    pk = peaks()
+    achieved = algo / dur_s / 1e9 if dur_s > 0 else 0.0
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{args.workload}:{dom_name}")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            c = cpu_reference_sample(args.workload, 2)
+            cpu = {"value": c["frames"] / c["seconds"], "unit": "frames/s", "cores": c["cores"],
+                   "kind": "reference",
+                   "sample": f"one render_gated(frames=2) of the full {w}x{h} workload ({c['seconds']:.1f} s)"}
+        except Exception as e:  # the oracle is a reported baseline only
+            cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / frames, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "scene": scene_name, "resolution": f"{w}x{h}",
+                       "parallelism": f"rowband{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
+            "mpaths_per_s": w * h * cfg.m_init * fps / 1e6,
+            "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},
+            "e2e": {"value": frames / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": f"k_{dom_name}", "achieved": achieved, "peak": pk["hbm_gbs"],
+                         "peak_src": pk["src"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                         "traffic": traffic, "algo_bytes_per_launch": algo, "avg_launch_ms": dur_s * 1e3},
+            "cpu_baseline": cpu,
+            "gpu_launches": sum(launches_per_frame(cfg, False) for _ in range(args.steps)) + sess.halo_launches(
+                args.steps),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

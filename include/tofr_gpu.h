@@ -186,15 +186,44 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* s, double frame, double 
                        int32_t spp, uint64_t seed, int32_t max_depth, double* mean, double* se);
 
 /* interactive sessions: the frame loop of render_gated / render_transient
- * one frame per call, reservoirs kept on the device between calls */
+ * one frame per call, reservoirs kept on the device between calls.  Steps are
+ * asynchronous (two frames in flight) unless `stats` is non-NULL. */
 int tofr_gpu_session_create(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
                             tofr_session** out);
+/* Row-band session (multi-GPU sharding, parallel.hpp:17-36 generalised to
+ * processes): computes image rows [y0, y1) and keeps `halo` rows on each side
+ * for spatial reuse (pass halo >= ceil(spatial_radius)).  y1 = -1 means H.
+ * RNG keys use global pixel indices, so a band is bit-identical to the same
+ * rows of a full-frame session. */
+int tofr_gpu_session_create_band(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, int32_t y0,
+                                 int32_t y1, int32_t halo, tofr_session** out);
+int tofr_gpu_session_band(tofr_session* ss, int32_t* y0, int32_t* y1, int32_t* r0, int32_t* r1);
+/* Halo exchange: before every spatial pass (pass >= 0) and, for moving
+ * cameras, after the final grid of a frame (pass = -1) the library packs the
+ * band's first rows into send_lo and last rows into send_hi (device buffers,
+ * chunk-major), calls fn(user, pass), then unpacks recv_lo into the rows above
+ * the band and recv_hi into the rows below.  fn must enqueue the transfer
+ * (e.g. NCCL send/recv with the upper / lower neighbour rank) on the session
+ * stream and return 0; a non-zero return aborts the step. */
+typedef int (*tofr_halo_exchange_fn)(void* user, int32_t pass);
+int tofr_gpu_session_set_halo_exchange(tofr_session* ss, tofr_halo_exchange_fn fn, void* user);
+int tofr_gpu_session_halo_buffers(tofr_session* ss, void** send_lo, void** recv_lo, uint64_t* bytes_lo,
+                                  void** send_hi, void** recv_hi, uint64_t* bytes_hi);
 int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats);
-/* last frame's image (gated) or bin-summed frame estimate (transient) */
+/* last frame's image of the band's rows (gated; (y1 - y0) * W * 3 doubles) */
 int tofr_gpu_session_read_image(tofr_session* ss, double* image);
 int tofr_gpu_session_sync(tofr_session* ss);
-/* device timing of the last step's kernels (ms) and the stage split */
+/* device timing of the last finished frame's kernels (ms) and the stage split
+ * {init (incl. camera), temporal, bin reuse, spatial (incl. halo), shade, total} */
 int tofr_gpu_session_last_ms(tofr_session* ss, double* total_ms, double* stage_ms /* [6] */);
+/* running sums of the stage split over all finished frames (+ halo exchanges) */
+int tofr_gpu_session_stage_totals(tofr_session* ss, double* stage_ms /* [6] */, int64_t* frames,
+                                  uint64_t* halo_exchanges, int32_t reset);
+/* the cudaStream_t all of the session's work is ordered on */
+int tofr_gpu_session_stream(tofr_session* ss, void** stream);
+/* bytes the last step uploaded (frame snapshot: BVH, triangles, camera, beam)
+ * and the size of one image read-back */
+int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t* d2h_image);
 void tofr_gpu_session_destroy(tofr_session* ss);
 
 /* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit

@@ -92,6 +92,9 @@ class Output(C.Structure):
                 ("stats_capacity", C.c_int32)]
 
 
+# int (*tofr_halo_exchange_fn)(void* user, int32_t pass)
+HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32)
+
 PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "_native" / "libtofr_b200.so"
 
@@ -127,6 +130,13 @@ def _declare(lib) -> None:
     lib.tofr_gpu_session_read_image.argtypes = [vp, P(C.c_double)]
     lib.tofr_gpu_session_sync.argtypes = [vp]
     lib.tofr_gpu_session_last_ms.argtypes = [vp, P(C.c_double), P(C.c_double)]
+    lib.tofr_gpu_session_stream.argtypes = [vp, P(vp)]
+    lib.tofr_gpu_session_create_band.argtypes = [vp, vp, P(RenderConfigC), C.c_int32, C.c_int32, C.c_int32, P(vp)]
+    lib.tofr_gpu_session_band.argtypes = [vp] + [P(C.c_int32)] * 4
+    lib.tofr_gpu_session_set_halo_exchange.argtypes = [vp, HALO_FN, vp]
+    lib.tofr_gpu_session_halo_buffers.argtypes = [vp, P(vp), P(vp), P(C.c_uint64), P(vp), P(vp), P(C.c_uint64)]
+    lib.tofr_gpu_session_stage_totals.argtypes = [vp, P(C.c_double), P(C.c_int64), P(C.c_uint64), C.c_int32]
+    lib.tofr_gpu_session_io_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     lib.tofr_gpu_session_destroy.argtypes = [vp]
     lib.tofr_gpu_session_destroy.restype = None
     lib.tofr_gpu_probe_rays.argtypes = [vp, vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
@@ -144,7 +154,9 @@ EXPORTED_SYMBOLS = (
     "tofr_scene_set_resolution", "tofr_scene_info", "tofr_gpu_render_gated", "tofr_gpu_render_doppler",
     "tofr_gpu_render_transient", "tofr_gpu_render_transient_plain", "tofr_gpu_reference",
     "tofr_gpu_session_create", "tofr_gpu_session_step", "tofr_gpu_session_read_image", "tofr_gpu_session_sync",
-    "tofr_gpu_session_last_ms", "tofr_gpu_session_destroy", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
+    "tofr_gpu_session_last_ms", "tofr_gpu_session_io_bytes", "tofr_gpu_session_stream",
+    "tofr_gpu_session_create_band", "tofr_gpu_session_band", "tofr_gpu_session_set_halo_exchange",
+    "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_destroy", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )
 
 
@@ -154,7 +166,8 @@ def load_library(path: Path | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+    p = Path(path) if path else Path(os.environ.get("TOFR_B200_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(f"native library {p} is missing; run __graft_entry__.build() "
                            "(the GPU path has no fallback)")

@@ -338,6 +338,19 @@ class Session:
         self._r._lib.tofr_gpu_session_last_ms(self.handle, C.byref(tot), st)
         return tot.value, list(st)
 
+    def io_bytes(self):
+        h2d, d2h = C.c_uint64(), C.c_uint64()
+        self._r._check(self._r._lib.tofr_gpu_session_io_bytes(self.handle, C.byref(h2d), C.byref(d2h)))
+        return int(h2d.value), int(d2h.value)
+
+    def stream_ptr(self) -> int:
+        p = C.c_void_p()
+        self._r._check(self._r._lib.tofr_gpu_session_stream(self.handle, C.byref(p)))
+        return int(p.value or 0)
+
+    def sync(self) -> None:
+        self._r._check(self._r._lib.tofr_gpu_session_sync(self.handle))
+
     def __del__(self):
         try:
             if self.handle:

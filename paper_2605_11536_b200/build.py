@@ -101,6 +101,33 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variants(variants: dict, verbose: bool = False) -> dict:
+    """Tuning builds: {tag: [-D...]} -> _native/variants/libtofr_b200_<tag>.so
+    (same host objects as the main library; only the device code differs).
+    Select one at run time with TOFR_B200_LIB=<path>."""
+    build(verbose=verbose)
+    vdir = OUT_DIR / "variants"
+    vdir.mkdir(parents=True, exist_ok=True)
+    host_objs = [BUILD_DIR / (src + ".o") for src in HOST_SOURCES]
+    procs, outs = [], {}
+    for tag, defs in variants.items():
+        obj = BUILD_DIR / f"tofr_kernels_{tag}.o"
+        cmd = [NVCC, "-std=c++17", GENCODE, "-O3", "-lineinfo", "--fmad=false", *defs,
+               "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", str(CSRC), "-I", str(INCLUDE),
+               "-c", str(CSRC / "tofr_kernels.cu"), "-o", str(obj)]
+        procs.append((tag, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for tag, obj, p in procs:
+        out, err = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"variant {tag} failed")
+        lib = vdir / f"libtofr_b200_{tag}.so"
+        _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(lib), str(obj)] + [str(o) for o in host_objs]
+             + ["-Xlinker", "-rpath,$ORIGIN"], verbose)
+        outs[tag] = lib
+    return outs
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

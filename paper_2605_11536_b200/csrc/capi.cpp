@@ -123,12 +123,33 @@ struct tofr_scene {
     HScene s;
 };
 
+// pinned host staging buffer (frame snapshot uploads)
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t bytes) {
+        if (bytes <= n) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        ck(cudaMallocHost(&p, bytes), "cudaMallocHost");
+        n = bytes;
+    }
+};
+
 // one uploaded frame snapshot
 struct FrameSlot {
     DevBuf blob;
+    PinnedBuf staging;
     PackedFrame pk;
     FrameView view;
-    DevBuf gbuf;
+    DevBuf gbuf;  // rows [r0, r1)
 };
 
 struct tofr_session {
@@ -137,26 +158,65 @@ struct tofr_session {
     tofr_render_config cfg;
     int W = 0, H = 0, B = 1;
     bool transient = false, plain = false;
+    // row band: compute rows [y0, y1), store rows [r0, r1)
+    int y0 = 0, y1 = 0, r0 = 0, r1 = 0;
+    bool cam_moves = false;
     FrameSlot slot[2];
     DevBuf res[3];
     int cur = 0, prev = 1, spare = 2;
-    DevBuf image, accum, hist, hist_count;
-    DevBuf ctr;  // [3 stages][SC_COUNT] u64
-    cudaEvent_t ev[7] = {};
+    DevBuf image, accum, hist, hist_count;  // owned rows only
+    DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag
+    DevBuf send_lo, send_hi, recv_lo, recv_hi;
+    tofr_halo_exchange_fn xfn = nullptr;
+    void* xuser = nullptr;
+    uint64_t halo_exchanges = 0;
+    // per-frame stage events, two frames in flight
+    cudaEvent_t ev[2][7] = {};
+    bool pending[2] = {false, false};
+    unsigned long long* err_host = nullptr;  // pinned [2]
     int f = 0;
     double prev_center = 0, prev_width = 0;
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+    double stage_tot[6] = {0, 0, 0, 0, 0, 0};
+    int64_t tot_frames = 0;
+    size_t last_h2d = 0;  // bytes uploaded by the last step (frame snapshot)
     int has_temporal = 0, has_bin = 0, has_spatial = 0;
 
+    size_t items_stored() const { return size_t(r1 - r0) * W * B; }
+    size_t owned_pixels() const { return size_t(y1 - y0) * W; }
+
     ~tofr_session() {
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
+        if (ctx && ctx->stream) cudaStreamSynchronize(ctx->stream);
+        for (auto& set : ev)
+            for (auto& e : set)
+                if (e) cudaEventDestroy(e);
+        if (err_host) cudaFreeHost(err_host);
     }
 };
 
 namespace {
 
-ResStore store_of(const DevBuf& b, size_t items) { return ResStore{b.as<double2>(), items}; }
+// Global-indexed views of band-local buffers (see Band in tofr_kernels.h).
+ResStore store_of(const tofr_session* s, const DevBuf& b) {
+    size_t items = s->items_stored();
+    return ResStore{b.as<double2>() - ptrdiff_t(size_t(s->r0) * s->W * s->B), items};
+}
+template <class T>
+T* rows_base(const DevBuf& b, int row0, size_t per_row) {
+    return b.as<T>() - ptrdiff_t(size_t(row0) * per_row);
+}
+
+Band band_of(tofr_session* s, bool prev_halo_valid) {
+    Band bd;
+    bd.y0 = s->y0;
+    bd.y1 = s->y1;
+    bd.r0 = s->r0;
+    bd.r1 = s->r1;
+    bd.t0 = prev_halo_valid ? s->r0 : s->y0;
+    bd.t1 = prev_halo_valid ? s->r1 : s->y1;
+    bd.err = s->ctr.as<unsigned long long>() + 3 * SC_COUNT;
+    return bd;
+}
 
 PathCfg path_cfg(const tofr_render_config& c, double center, double width) {
     PathCfg p;
@@ -180,12 +240,16 @@ void upload_frame(tofr_session* s, int which, double frame, int frame_id) {
     HFrame hf = build_frame(s->scene, frame);
     if (hf.max_depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
     sl.pk = pack_frame(s->scene, hf, frame_id);
-    sl.blob.ensure(sl.pk.blob.size());
-    ck(cudaMemcpyAsync(sl.blob.p, sl.pk.blob.data(), sl.pk.blob.size(), cudaMemcpyHostToDevice,
-                       s->ctx->stream),
-       "frame upload");
+    size_t nb = sl.pk.blob.size();
+    // the staging buffer of this slot was last copied two frames ago; that
+    // frame's events were synchronised before this call (flush_set)
+    sl.staging.ensure(nb);
+    std::memcpy(sl.staging.p, sl.pk.blob.data(), nb);
+    sl.blob.ensure(nb);
+    ck(cudaMemcpyAsync(sl.blob.p, sl.staging.p, nb, cudaMemcpyHostToDevice, s->ctx->stream), "frame upload");
     sl.view = rebase_view(sl.pk, static_cast<const unsigned char*>(sl.blob.p));
-    sl.gbuf.ensure(size_t(s->W) * s->H * sizeof(GHit));
+    sl.gbuf.ensure(size_t(s->r1 - s->r0) * s->W * sizeof(GHit));
+    s->last_h2d = nb;
 }
 
 void check_config(const tofr_render_config* c) {
@@ -198,7 +262,8 @@ void check_config(const tofr_render_config* c) {
 
 enum SessionKind { KIND_RESTIR = 0, KIND_PLAIN = 1, KIND_BARE = 2 };
 
-tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, int kind) {
+tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, int kind,
+                           int y0 = 0, int y1 = -1, int halo = 0) {
     check_config(cfg);
     auto s = std::make_unique<tofr_session>();
     s->ctx = ctx;
@@ -207,6 +272,21 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     s->W = sc->s.camera.width;
     s->H = sc->s.camera.height;
     if (s->W <= 0 || s->H <= 0) throw ScopeError(TOFR_ERR_INVALID, "empty image");
+    if (y1 < 0) y1 = s->H;
+    if (y0 < 0 || y1 > s->H || y0 >= y1 || halo < 0) throw ScopeError(TOFR_ERR_INVALID, "bad row band");
+    s->y0 = y0;
+    s->y1 = y1;
+    s->r0 = std::max(0, y0 - halo);
+    s->r1 = std::min(s->H, y1 + halo);
+    if ((y0 - s->r0) > (y1 - y0) || (s->r1 - y1) > (y1 - y0))
+        throw ScopeError(TOFR_ERR_INVALID, "row band thinner than its halo (use fewer ranks)");
+    s->cam_moves = !sc->s.camera.track.empty();
+    for (auto& set : s->ev)
+        for (auto& e : set) ck(cudaEventCreate(&e), "event");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&s->err_host), 2 * sizeof(unsigned long long)), "pinned");
+    s->err_host[0] = s->err_host[1] = 0;
+    s->ctr.ensure((3 * SC_COUNT + 1) * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), ctx->stream), "memset");
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
     s->plain = plain;
@@ -215,36 +295,45 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if (s->transient && (cfg->bins < 1 || !(cfg->hist_bin_width > 0)))
         throw ScopeError(TOFR_ERR_INVALID, "transient needs bins >= 1 and hist_bin_width > 0");
     if (!s->transient && cfg->m_init < 0) throw ScopeError(TOFR_ERR_INVALID, "m_init < 0");
-    size_t npix = size_t(s->W) * s->H;
-    size_t items = npix * s->B;
+    size_t own = s->owned_pixels() * s->B;
     if (plain) {
-        s->hist.ensure(items * 3 * sizeof(double));
-        s->hist_count.ensure(items * sizeof(uint32_t));
-        ck(cudaMemsetAsync(s->hist.p, 0, items * 3 * sizeof(double), ctx->stream), "memset");
-        ck(cudaMemsetAsync(s->hist_count.p, 0, items * sizeof(uint32_t), ctx->stream), "memset");
+        s->hist.ensure(own * 3 * sizeof(double));
+        s->hist_count.ensure(own * sizeof(uint32_t));
+        ck(cudaMemsetAsync(s->hist.p, 0, own * 3 * sizeof(double), ctx->stream), "memset");
+        ck(cudaMemsetAsync(s->hist_count.p, 0, own * sizeof(uint32_t), ctx->stream), "memset");
     } else {
         s->has_temporal = cfg->temporal ? 1 : 0;
         s->has_bin = (s->transient && cfg->bin_reuse) ? 1 : 0;
         s->has_spatial = cfg->spatial_passes > 0 ? 1 : 0;
-        size_t rb = items * kResChunks * 16;
+        size_t rb = s->items_stored() * kResChunks * 16;
         s->res[0].ensure(rb);
         s->res[1].ensure(rb);
         if (s->has_bin || s->has_spatial) s->res[2].ensure(rb);
         // a never-written grid must read as empty (M = 0) for temporal reuse
         ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
         ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
+        if (s->res[2].p) ck(cudaMemsetAsync(s->res[2].p, 0, rb, ctx->stream), "memset");
         if (s->transient) {
-            s->hist.ensure(items * 3 * sizeof(double));
-            ck(cudaMemsetAsync(s->hist.p, 0, items * 3 * sizeof(double), ctx->stream), "memset");
+            s->hist.ensure(own * 3 * sizeof(double));
+            ck(cudaMemsetAsync(s->hist.p, 0, own * 3 * sizeof(double), ctx->stream), "memset");
         } else {
+            size_t npix = s->owned_pixels();
             s->image.ensure(npix * 3 * sizeof(double));
             s->accum.ensure(npix * 3 * sizeof(double));
             ck(cudaMemsetAsync(s->accum.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
             ck(cudaMemsetAsync(s->image.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
         }
+        size_t per_row = size_t(s->W) * s->B * kResChunks * 16;
+        size_t lo = size_t(s->y0 - s->r0) * per_row, hi = size_t(s->r1 - s->y1) * per_row;
+        if (lo) {
+            s->send_lo.ensure(lo);
+            s->recv_lo.ensure(lo);
+        }
+        if (hi) {
+            s->send_hi.ensure(hi);
+            s->recv_hi.ensure(hi);
+        }
     }
-    s->ctr.ensure(3 * SC_COUNT * sizeof(unsigned long long));
-    for (auto& e : s->ev) ck(cudaEventCreate(&e), "event");
     return s.release();
 }
 
@@ -260,83 +349,142 @@ void fill_counts(tofr_shift_counts& o, const unsigned long long* c) {
     o.success = c[SC_SUCCESS];
 }
 
-// One frame of the pipeline (body of the frame loops).
+// Waits for the frame recorded in event set `set`, folds its stage times into
+// the running totals and checks the band error flag it copied out.
+void flush_set(tofr_session* s, int set) {
+    if (!s->pending[set]) return;
+    ck(cudaEventSynchronize(s->ev[set][6]), "frame");
+    s->pending[set] = false;
+    float ms[6];
+    for (int i = 0; i < 5; ++i) {
+        ms[i] = 0;
+        cudaEventElapsedTime(&ms[i], s->ev[set][i], s->ev[set][i + 1]);
+    }
+    ms[5] = 0;
+    cudaEventElapsedTime(&ms[5], s->ev[set][0], s->ev[set][6]);
+    // stage split: init (incl. camera), temporal, bin, spatial (incl. halo), shade, total
+    for (int i = 0; i < 6; ++i) {
+        s->stage_ms[i] = ms[i];
+        s->stage_tot[i] += ms[i];
+    }
+    s->tot_frames++;
+    if (s->err_host[set])
+        throw ScopeError(TOFR_ERR_UNSUPPORTED,
+                         "row band read outside its rows (camera motion larger than the halo, or a spatial "
+                         "radius larger than the halo)");
+}
+
+void flush_all(tofr_session* s) {
+    int a = s->f & 1;  // oldest pending first
+    flush_set(s, a);
+    flush_set(s, a ^ 1);
+}
+
+// Halo exchange of a global-indexed grid around the band: pack the edge rows
+// the neighbours need, let the caller move them (NCCL / P2P, ordered on the
+// session stream), unpack what arrived into the halo rows.
+void exchange_halo(tofr_session* s, ResStore g, int pass) {
+    if (s->r0 == s->y0 && s->r1 == s->y1) return;
+    if (!s->xfn) throw ScopeError(TOFR_ERR_INVALID, "band session with a halo needs a halo exchange callback");
+    cudaStream_t st = s->ctx->stream;
+    size_t per_row = size_t(s->W) * s->B;
+    size_t lo = size_t(s->y0 - s->r0) * per_row, hi = size_t(s->r1 - s->y1) * per_row;
+    launch_halo_pack(g, size_t(s->y0) * per_row, lo, s->send_lo.as<double2>(), st);
+    launch_halo_pack(g, size_t(s->y1) * per_row - hi, hi, s->send_hi.as<double2>(), st);
+    ck(cudaGetLastError(), "halo pack");
+    int rc = s->xfn(s->xuser, pass);
+    if (rc != 0) throw ScopeError(TOFR_ERR_CUDA, "halo exchange callback failed");
+    launch_halo_unpack(g, size_t(s->r0) * per_row, lo, s->recv_lo.as<double2>(), st);
+    launch_halo_unpack(g, size_t(s->y1) * per_row, hi, s->recv_hi.as<double2>(), st);
+    ck(cudaGetLastError(), "halo unpack");
+    s->halo_exchanges++;
+}
+
+// One frame of the pipeline (body of the frame loops).  Asynchronous unless
+// `st` is requested (then it waits for the frame and reads its counters).
 void session_step(tofr_session* s, tofr_frame_stats* st) {
     cudaStream_t stream = s->ctx->stream;
     const tofr_render_config& c = s->cfg;
     int f = s->f;
+    int set = f & 1;
+    flush_set(s, set);  // frame f-2: frees its event set and its staging buffer
     int sl = f & 1, psl = sl ^ 1;
     upload_frame(s, sl, c.frame0 + f, f);
     const FrameView& F = s->slot[sl].view;
-    GHit* g = s->slot[sl].gbuf.as<GHit>();
+    GHit* g_local = s->slot[sl].gbuf.as<GHit>();
+    const GHit* g = rows_base<GHit>(s->slot[sl].gbuf, s->r0, s->W);
     double center = c.gate_center + c.gate_step * f;
     double width = c.gate_width;
     PathCfg pc = path_cfg(c, center, width);
-    size_t npix = size_t(s->W) * s->H;
-    size_t items = npix * s->B;
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
-    ck(cudaMemsetAsync(ctr, 0, 3 * SC_COUNT * sizeof(unsigned long long), stream), "memset");
+    bool halo = !(s->r0 == s->y0 && s->r1 == s->y1);
+    bool prev_halo = halo && s->cam_moves;
+    Band bd = band_of(s, prev_halo);
+    cudaEvent_t* ev = s->ev[set];
+    ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
 
-    cudaEventRecord(s->ev[0], stream);
-    launch_gbuffer(F, g, stream);
+    cudaEventRecord(ev[0], stream);
+    launch_gbuffer(F, bd, g_local, stream);
     if (s->plain) {
-        launch_hist_plain(F, g, pc, h, c.m_init, f, s->hist.as<double>(), s->hist_count.as<uint32_t>(), stream);
-        for (int i = 1; i < 7; ++i) cudaEventRecord(s->ev[i], stream);
+        size_t pr = size_t(s->W) * s->B;
+        launch_hist_plain(F, bd, g, pc, h, c.m_init, f, rows_base<double>(s->hist, s->y0, pr * 3),
+                          rows_base<uint32_t>(s->hist_count, s->y0, pr), stream);
+        for (int i = 1; i < 6; ++i) cudaEventRecord(ev[i], stream);
     } else {
         InitParams ip{c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
-        ResStore cur = store_of(s->res[s->cur], items);
+        ResStore cur = store_of(s, s->res[s->cur]);
         if (s->transient)
-            launch_init_transient(F, g, pc, ip, h, f, cur, stream);
+            launch_init_transient(F, bd, g, pc, ip, h, f, cur, stream);
         else
-            launch_init_gated(F, g, pc, ip, f, cur, stream);
-        cudaEventRecord(s->ev[1], stream);
+            launch_init_gated(F, bd, g, pc, ip, f, cur, stream);
+        cudaEventRecord(ev[1], stream);
         GateGrid cg{s->transient ? 1 : 0, center, width, h};
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
-            launch_temporal(F, g, s->slot[psl].view, s->slot[psl].gbuf.as<GHit>(), pc, cg, pg, f, cur,
-                            store_of(s->res[s->prev], items), ctr + 0 * SC_COUNT, stream);
+            const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
+            launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
+                            ctr + 0 * SC_COUNT, stream);
         }
-        cudaEventRecord(s->ev[2], stream);
+        cudaEventRecord(ev[2], stream);
         if (s->transient && c.bin_reuse) {
-            launch_binreuse(F, g, pc, h, f, cur, store_of(s->res[s->spare], items), ctr + 2 * SC_COUNT, stream);
+            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, stream);
             std::swap(s->cur, s->spare);
-            cur = store_of(s->res[s->cur], items);
+            cur = store_of(s, s->res[s->cur]);
         }
-        cudaEventRecord(s->ev[3], stream);
+        cudaEventRecord(ev[3], stream);
         SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
         for (int pass = 0; pass < c.spatial_passes; ++pass) {
-            launch_spatial(F, g, pc, cg, sp, pass, f, cur, store_of(s->res[s->spare], items), ctr + 1 * SC_COUNT,
+            if (halo) exchange_halo(s, cur, pass);
+            launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), ctr + 1 * SC_COUNT,
                            stream);
             std::swap(s->cur, s->spare);
-            cur = store_of(s->res[s->cur], items);
+            cur = store_of(s, s->res[s->cur]);
         }
-        cudaEventRecord(s->ev[4], stream);
+        cudaEventRecord(ev[4], stream);
         if (s->transient)
-            launch_shade_transient(cur, items, h, s->hist.as<double>(), stream);
+            launch_shade_transient(cur, bd, s->W, h, rows_base<double>(s->hist, s->y0, size_t(s->W) * s->B * 3),
+                                   stream);
         else
-            launch_shade_gated(cur, int(npix), center, width, s->image.as<double>(), s->accum.as<double>(), stream);
-        cudaEventRecord(s->ev[5], stream);
-        cudaEventRecord(s->ev[6], stream);
+            launch_shade_gated(cur, bd, s->W, center, width, rows_base<double>(s->image, s->y0, size_t(s->W) * 3),
+                               rows_base<double>(s->accum, s->y0, size_t(s->W) * 3), stream);
+        // a moving camera reprojects across band edges: give the next
+        // frame's temporal stage the neighbours' final reservoirs too
+        if (prev_halo && c.temporal) exchange_halo(s, cur, -1);
+        cudaEventRecord(ev[5], stream);
         std::swap(s->cur, s->prev);  // bufs.flip()
     }
+    ck(cudaMemcpyAsync(&s->err_host[set], ctr + 3 * SC_COUNT, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       stream),
+       "flag");
+    cudaEventRecord(ev[6], stream);
     ck(cudaGetLastError(), "kernel launch");
-    ck(cudaEventSynchronize(s->ev[6]), "frame");
-    float ms[6];
-    for (int i = 0; i < 6; ++i) {
-        ms[i] = 0;
-        cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]);
-    }
-    float tot = 0;
-    cudaEventElapsedTime(&tot, s->ev[0], s->ev[6]);
-    // stage split: init(incl. camera), temporal, bin, spatial, shade, total
-    s->stage_ms[0] = ms[0];
-    s->stage_ms[1] = ms[1];
-    s->stage_ms[2] = ms[2];
-    s->stage_ms[3] = ms[3];
-    s->stage_ms[4] = ms[4];
-    s->stage_ms[5] = tot;
+    s->pending[set] = true;
+    s->prev_center = center;
+    s->prev_width = width;
+    s->f++;
     if (st) {
+        flush_all(s);
         std::memset(st, 0, sizeof(*st));
         st->frame = f;
         unsigned long long hc[3 * SC_COUNT];
@@ -344,15 +492,13 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         fill_counts(st->temporal.shift, hc + 0 * SC_COUNT);
         fill_counts(st->spatial.shift, hc + 1 * SC_COUNT);
         fill_counts(st->binwise.shift, hc + 2 * SC_COUNT);
+        const double* ms = s->stage_ms;
         st->t_init = ms[0] * 1e-3;
         st->temporal.seconds = (c.temporal && f > 0) ? ms[1] * 1e-3 : 0;
         st->binwise.seconds = (s->transient && c.bin_reuse) ? ms[2] * 1e-3 : 0;
         st->spatial.seconds = ms[3] * 1e-3;
         st->t_shade = ms[4] * 1e-3;
     }
-    s->prev_center = center;
-    s->prev_width = width;
-    s->f++;
 }
 
 template <class F>
@@ -376,18 +522,12 @@ int guard(tofr_gpu* ctx, F&& fn) {
     }
 }
 
-void render_loop(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, tofr_output* out,
-                 bool plain) {
-    if (!ctx || !sc) throw ScopeError(TOFR_ERR_INVALID, "null handle");
-    std::unique_ptr<tofr_session> s(make_session(ctx, sc, cfg, plain ? KIND_PLAIN : KIND_RESTIR));
+// Output of a (full-frame) session in RenderOutput form (pipeline.hpp:384-391,
+// :516-527, :563-570).
+void read_outputs(tofr_session* s, const tofr_render_config* cfg, tofr_output* out, bool plain) {
+    flush_all(s);
     int frames = cfg->frames;
-    for (int f = 0; f < frames; ++f) {
-        tofr_frame_stats st;
-        session_step(s.get(), &st);
-        if (out && out->stats && f < out->stats_capacity) out->stats[f] = st;
-    }
-    if (!out) return;
-    size_t npix = size_t(s->W) * s->H;
+    size_t npix = s->owned_pixels();
     if (!s->transient) {
         std::vector<double> img(npix * 3);
         if (cfg->accumulate && frames > 0) {
@@ -434,6 +574,24 @@ void render_loop(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* 
             out->image[3 * p + 2] = sz;
         }
     }
+}
+
+void render_loop(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, tofr_output* out,
+                 bool plain) {
+    if (!ctx || !sc) throw ScopeError(TOFR_ERR_INVALID, "null handle");
+    std::unique_ptr<tofr_session> s(make_session(ctx, sc, cfg, plain ? KIND_PLAIN : KIND_RESTIR));
+    int frames = cfg->frames;
+    for (int f = 0; f < frames; ++f) {
+        tofr_frame_stats st;
+        bool want = out && out->stats && f < out->stats_capacity;
+        session_step(s.get(), want ? &st : nullptr);
+        if (want) out->stats[f] = st;
+    }
+    if (!out) {
+        flush_all(s.get());
+        return;
+    }
+    read_outputs(s.get(), cfg, out, plain);
 }
 
 HScene scene_from_desc(const tofr_scene_desc* d) {
@@ -718,10 +876,11 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double
         ds.ensure(npix * 3 * 8);
         const FrameView& F = s->slot[0].view;
         GHit* g = s->slot[0].gbuf.as<GHit>();
-        launch_gbuffer(F, g, ctx->stream);
+        Band bd = band_of(s.get(), false);
+        launch_gbuffer(F, bd, g, ctx->stream);
         PathCfg pc = path_cfg(c, gate_center, gate_width);
         pc.ellipsoidal = 0;
-        launch_reference(F, g, pc, gate_center, gate_width, spp, uint64_t(frame), dm.as<double>(), ds.as<double>(),
+        launch_reference(F, bd, g, pc, gate_center, gate_width, spp, uint64_t(frame), dm.as<double>(), ds.as<double>(),
                          ctx->stream);
         ck(cudaGetLastError(), "reference launch");
         if (mean) ck(cudaMemcpyAsync(mean, dm.p, npix * 24, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
@@ -732,12 +891,47 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double
 
 int tofr_gpu_session_create(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg,
                             tofr_session** out) {
+    return tofr_gpu_session_create_band(ctx, s, cfg, 0, -1, 0, out);
+}
+
+int tofr_gpu_session_create_band(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, int32_t y0,
+                                 int32_t y1, int32_t halo, tofr_session** out) {
     if (!out) return TOFR_ERR_INVALID;
     *out = nullptr;
     return guard(ctx, [&] {
         if (!ctx || !s) throw ScopeError(TOFR_ERR_INVALID, "null handle");
-        *out = make_session(ctx, s, cfg, KIND_RESTIR);
+        if (cfg && cfg->mode == TOFR_MODE_TRANSIENT && cfg->bins < 1)
+            throw ScopeError(TOFR_ERR_INVALID, "transient needs bins >= 1");
+        *out = make_session(ctx, s, cfg, KIND_RESTIR, y0, y1, halo);
     });
+}
+
+int tofr_gpu_session_band(tofr_session* ss, int32_t* y0, int32_t* y1, int32_t* r0, int32_t* r1) {
+    if (!ss) return TOFR_ERR_INVALID;
+    if (y0) *y0 = ss->y0;
+    if (y1) *y1 = ss->y1;
+    if (r0) *r0 = ss->r0;
+    if (r1) *r1 = ss->r1;
+    return TOFR_OK;
+}
+
+int tofr_gpu_session_set_halo_exchange(tofr_session* ss, tofr_halo_exchange_fn fn, void* user) {
+    if (!ss) return TOFR_ERR_INVALID;
+    ss->xfn = fn;
+    ss->xuser = user;
+    return TOFR_OK;
+}
+
+int tofr_gpu_session_halo_buffers(tofr_session* ss, void** send_lo, void** recv_lo, uint64_t* bytes_lo,
+                                  void** send_hi, void** recv_hi, uint64_t* bytes_hi) {
+    if (!ss) return TOFR_ERR_INVALID;
+    if (send_lo) *send_lo = ss->send_lo.p;
+    if (recv_lo) *recv_lo = ss->recv_lo.p;
+    if (bytes_lo) *bytes_lo = ss->send_lo.n;
+    if (send_hi) *send_hi = ss->send_hi.p;
+    if (recv_hi) *recv_hi = ss->recv_hi.p;
+    if (bytes_hi) *bytes_hi = ss->send_hi.n;
+    return TOFR_OK;
 }
 
 int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats) {
@@ -748,26 +942,58 @@ int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats) {
 int tofr_gpu_session_read_image(tofr_session* ss, double* image) {
     if (!ss || !image) return TOFR_ERR_INVALID;
     return guard(ss->ctx, [&] {
-        size_t npix = size_t(ss->W) * ss->H;
-        if (!ss->transient) {
-            ck(cudaMemcpyAsync(image, ss->image.p, npix * 24, cudaMemcpyDeviceToHost, ss->ctx->stream), "d2h");
-            ck(cudaStreamSynchronize(ss->ctx->stream), "d2h");
-        } else {
-            throw ScopeError(TOFR_ERR_UNSUPPORTED, "read_image on a transient session");
-        }
+        if (ss->transient) throw ScopeError(TOFR_ERR_UNSUPPORTED, "read_image on a transient session");
+        ck(cudaMemcpyAsync(image, ss->image.p, ss->owned_pixels() * 24, cudaMemcpyDeviceToHost, ss->ctx->stream),
+           "d2h");
+        flush_all(ss);
     });
 }
 
 int tofr_gpu_session_sync(tofr_session* ss) {
     if (!ss) return TOFR_ERR_INVALID;
-    return guard(ss->ctx, [&] { ck(cudaStreamSynchronize(ss->ctx->stream), "sync"); });
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        ck(cudaStreamSynchronize(ss->ctx->stream), "sync");
+    });
 }
 
 int tofr_gpu_session_last_ms(tofr_session* ss, double* total_ms, double* stage_ms) {
     if (!ss) return TOFR_ERR_INVALID;
-    if (total_ms) *total_ms = ss->stage_ms[5];
-    if (stage_ms)
-        for (int i = 0; i < 6; ++i) stage_ms[i] = ss->stage_ms[i];
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        if (total_ms) *total_ms = ss->stage_ms[5];
+        if (stage_ms)
+            for (int i = 0; i < 6; ++i) stage_ms[i] = ss->stage_ms[i];
+    });
+}
+
+int tofr_gpu_session_stage_totals(tofr_session* ss, double* stage_ms, int64_t* frames, uint64_t* halo_exchanges,
+                                  int32_t reset) {
+    if (!ss) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        if (stage_ms)
+            for (int i = 0; i < 6; ++i) stage_ms[i] = ss->stage_tot[i];
+        if (frames) *frames = ss->tot_frames;
+        if (halo_exchanges) *halo_exchanges = ss->halo_exchanges;
+        if (reset) {
+            for (double& v : ss->stage_tot) v = 0;
+            ss->tot_frames = 0;
+            ss->halo_exchanges = 0;
+        }
+    });
+}
+
+int tofr_gpu_session_stream(tofr_session* ss, void** stream) {
+    if (!ss || !stream) return TOFR_ERR_INVALID;
+    *stream = static_cast<void*>(ss->ctx->stream);
+    return TOFR_OK;
+}
+
+int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t* d2h_image) {
+    if (!ss) return TOFR_ERR_INVALID;
+    if (h2d_per_step) *h2d_per_step = ss->last_h2d;
+    if (d2h_image) *d2h_image = uint64_t(ss->owned_pixels()) * 3 * sizeof(double);
     return TOFR_OK;
 }
 
@@ -781,7 +1007,10 @@ int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const
         tofr_render_config_default(&c);
         std::unique_ptr<tofr_session> s(make_session(ctx, sc, &c, KIND_BARE));
         upload_frame(s.get(), 0, frame, 0);
-        if (n == 0) return;
+        if (n == 0) {
+            ck(cudaStreamSynchronize(ctx->stream), "probe");
+            return;
+        }
         DevBuf dr, dt, di;
         dr.ensure(size_t(n) * 64);
         dt.ensure(size_t(n) * 8);

@@ -146,14 +146,22 @@ TOFR_HD bool ray_tri(const V3& o, const V3& d, const GTriIsect& tr, double tmin,
 }
 
 // Closest hit on (tmin, tmax); Bvh::intersect_min (geometry.hpp:168-201).
-TOFR_HD bool trace_closest(const FrameView& f, const V3& o, const V3& d, double tmin, double tmax,
-                           Hit& hit) {
+// The traversal bodies are out-of-line on the device (one copy per kernel,
+// arguments in registers) so that the many call sites of the reuse kernels
+// do not blow up the instruction footprint.
+struct TraceHit {
+    double t;
+    int slot;
+};
+
+TOFR_HD TraceHit trace_closest_impl(const GNode* nodes, const GTriIsect* tris, const V3& o, const V3& d,
+                                    double tmin, double tmax) {
     V3 inv = V3{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
     double best = tmax;
     int best_slot = -1;
     int ni = 0;
     while (ni >= 0) {
-        const GNode& n = f.nodes[ni];
+        const GNode& n = nodes[ni];
         if (!ray_box(o, inv, n, tmin, best)) {
             ni = n.miss_next;
             continue;
@@ -161,7 +169,7 @@ TOFR_HD bool trace_closest(const FrameView& f, const V3& o, const V3& d, double 
         if (n.count > 0) {
             for (int i = 0; i < n.count; ++i) {
                 double t;
-                if (ray_tri(o, d, f.tri_isect[n.first + i], tmin, best, t)) {
+                if (ray_tri(o, d, tris[n.first + i], tmin, best, t)) {
                     best = t;
                     best_slot = n.first + i;
                 }
@@ -169,29 +177,59 @@ TOFR_HD bool trace_closest(const FrameView& f, const V3& o, const V3& d, double 
         }
         ni = n.hit_next;
     }
-    if (best_slot < 0) return false;
-    hit.t = best;
-    hit.tri = f.tri_id[best_slot];
-    hit.pos = o + d * best;
-    return true;
+    return TraceHit{best, best_slot};
 }
 
-TOFR_HD bool trace_any(const FrameView& f, const V3& o, const V3& d, double tmin, double tmax) {
+TOFR_HD bool trace_any_impl(const GNode* nodes, const GTriIsect* tris, const V3& o, const V3& d, double tmin,
+                            double tmax) {
     V3 inv = V3{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
     int ni = 0;
     while (ni >= 0) {
-        const GNode& n = f.nodes[ni];
+        const GNode& n = nodes[ni];
         if (!ray_box(o, inv, n, tmin, tmax)) {
             ni = n.miss_next;
             continue;
         }
         for (int i = 0; i < n.count; ++i) {
             double t;
-            if (ray_tri(o, d, f.tri_isect[n.first + i], tmin, tmax, t)) return true;
+            if (ray_tri(o, d, tris[n.first + i], tmin, tmax, t)) return true;
         }
         ni = n.hit_next;
     }
     return false;
+}
+
+#if defined(__CUDACC__)
+static __device__ __noinline__ TraceHit trace_closest_dev(const GNode* nodes, const GTriIsect* tris, V3 o, V3 d,
+                                                   double tmin, double tmax) {
+    return trace_closest_impl(nodes, tris, o, d, tmin, tmax);
+}
+static __device__ __noinline__ bool trace_any_dev(const GNode* nodes, const GTriIsect* tris, V3 o, V3 d, double tmin,
+                                           double tmax) {
+    return trace_any_impl(nodes, tris, o, d, tmin, tmax);
+}
+#endif
+
+TOFR_HD bool trace_closest(const FrameView& f, const V3& o, const V3& d, double tmin, double tmax,
+                           Hit& hit) {
+#if defined(__CUDA_ARCH__)
+    TraceHit r = trace_closest_dev(f.nodes, f.tri_isect, o, d, tmin, tmax);
+#else
+    TraceHit r = trace_closest_impl(f.nodes, f.tri_isect, o, d, tmin, tmax);
+#endif
+    if (r.slot < 0) return false;
+    hit.t = r.t;
+    hit.tri = f.tri_id[r.slot];
+    hit.pos = o + d * r.t;
+    return true;
+}
+
+TOFR_HD bool trace_any(const FrameView& f, const V3& o, const V3& d, double tmin, double tmax) {
+#if defined(__CUDA_ARCH__)
+    return trace_any_dev(f.nodes, f.tri_isect, o, d, tmin, tmax);
+#else
+    return trace_any_impl(f.nodes, f.tri_isect, o, d, tmin, tmax);
+#endif
 }
 
 // Bvh::intersect: t_min = eps_ray, t_max = inf (geometry.hpp:164-166)

@@ -22,6 +22,12 @@
 #include "tofr_kernels.h"
 #include "tofr_store.cuh"
 
+// Minimum resident CTAs per SM requested for the reuse/initial kernels
+// (register cap 65536 / (128 * MINB)); tuned with ncu, overridable at build time.
+#ifndef TOFR_REUSE_MINB
+#define TOFR_REUSE_MINB 1
+#endif
+
 namespace tofr_b200 {
 
 // ---------------------------------------------------------------------------
@@ -69,14 +75,15 @@ __device__ __forceinline__ void flush_ctr(const uint32_t* c, unsigned long long*
 // ---------------------------------------------------------------------------
 // camera stage
 
-__global__ void __launch_bounds__(256) k_gbuffer(FrameView F, GHit* g) {
+__global__ void __launch_bounds__(256) k_gbuffer(FrameView F, Band bd, GHit* g) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
-        int px = p % W, py = p / W;
+    int W = F.cam.w;
+    int n = (bd.r1 - bd.r0) * W;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        int px = p % W, py = bd.r0 + p / W;
         V3 d = primary_dir(F.cam, px, py);
         Hit h;
         GHit o;
@@ -206,15 +213,15 @@ __device__ void init_pixel(const FrameView& F, const PathCfg& cfg, const InitPar
     gris_merge(out, rough, ms, fwd, ip.center, ip.width, cfg.m_cap, pick);
 }
 
-__global__ void __launch_bounds__(128) k_init_gated(FrameView F, const GHit* gbuf, PathCfg cfg,
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     InitParams ip, int frame_idx, ResStore cur) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h;
+    int W = F.cam.w;
     WalkV v[kMaxVerts];
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
         int px = p % W, py = p / W;
         Res r;
         GHit g = gbuf[p];
@@ -269,17 +276,17 @@ struct BinSink {
     }
 };
 
-__global__ void __launch_bounds__(128) k_init_transient(FrameView F, const GHit* gbuf, PathCfg cfg,
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                         InitParams ip, HistSpec h, int frame_idx,
                                                         ResStore cur) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h, B = h.bins;
+    int W = F.cam.w, B = h.bins;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         size_t base = size_t(p) * B;
@@ -316,7 +323,7 @@ __device__ __forceinline__ void gate_of(const GateGrid& gg, int b, double& c, do
     }
 }
 
-__global__ void __launch_bounds__(128) k_temporal(FrameView Fc, const GHit* gc, FrameView Fp,
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc, Band bd, const GHit* gc, FrameView Fp,
                                                   const GHit* gp, PathCfg cfg, GateGrid cur_gate,
                                                   GateGrid prev_gate, int frame_idx, ResStore cur,
                                                   ResStore prev, unsigned long long* ctr_out) {
@@ -325,10 +332,10 @@ __global__ void __launch_bounds__(128) k_temporal(FrameView Fc, const GHit* gc, 
     stage_frame(Fc, smem, off);
     stage_frame(Fp, smem, off);
     __syncthreads();
-    int W = Fc.cam.w, H = Fc.cam.h, B = cur_gate.transient ? cur_gate.h.bins : 1;
+    int W = Fc.cam.w, B = cur_gate.transient ? cur_gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t n_items = size_t(W) * H * B;
-    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+    size_t end = size_t(bd.y1) * W * B;
+    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
          it += size_t(gridDim.x) * blockDim.x) {
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -338,6 +345,10 @@ __global__ void __launch_bounds__(128) k_temporal(FrameView Fc, const GHit* gc, 
         V3 hp = Fc.cam.pos + d0 * g.t;
         int qx, qy;
         if (!project(Fp.cam, hp, qx, qy)) continue;
+        if (qy < bd.t0 || qy >= bd.t1) {  // reprojection left the rows this band holds
+            atomicAdd(bd.err, 1ull);
+            continue;
+        }
         size_t src_i = (size_t(qy) * W + qx) * B + b;
         double sW, sM;
         int shas;
@@ -386,7 +397,7 @@ __device__ __forceinline__ void neighbor_offset(int j, int count, double radius,
     dy = int(llround(rr * sin(th)));
 }
 
-__global__ void __launch_bounds__(128) k_spatial(FrameView F, const GHit* gbuf, PathCfg cfg,
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                  GateGrid gate, SpatialParams sp, int pass,
                                                  int frame_idx, ResStore src_grid, ResStore dst_grid,
                                                  unsigned long long* ctr_out) {
@@ -396,8 +407,8 @@ __global__ void __launch_bounds__(128) k_spatial(FrameView F, const GHit* gbuf, 
     __syncthreads();
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t n_items = size_t(W) * H * B;
-    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+    size_t end = size_t(bd.y1) * W * B;
+    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
          it += size_t(gridDim.x) * blockDim.x) {
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -417,6 +428,10 @@ __global__ void __launch_bounds__(128) k_spatial(FrameView F, const GHit* gbuf, 
                 int nx = px + dx, ny = py + dy;
                 if (nx == px && ny == py) continue;
                 if (nx < 0 || nx >= W || ny < 0 || ny >= H) continue;
+                if (ny < bd.r0 || ny >= bd.r1) {  // beyond the exchanged halo
+                    atomicAdd(bd.err, 1ull);
+                    continue;
+                }
                 size_t si = (size_t(ny) * W + nx) * B + b;
                 double sW, sM;
                 int shas;
@@ -451,17 +466,17 @@ __global__ void __launch_bounds__(128) k_spatial(FrameView F, const GHit* gbuf, 
 // ---------------------------------------------------------------------------
 // bin reuse (stage::bin_reuse, pipeline.hpp:273-299)
 
-__global__ void __launch_bounds__(128) k_binreuse(FrameView F, const GHit* gbuf, PathCfg cfg, HistSpec h,
-                                                  int frame_idx, ResStore src_grid, ResStore dst_grid,
-                                                  unsigned long long* ctr_out) {
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
+                                                  HistSpec h, int frame_idx, ResStore src_grid,
+                                                  ResStore dst_grid, unsigned long long* ctr_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h, B = h.bins;
+    int W = F.cam.w, B = h.bins;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t n_items = size_t(W) * H * B;
-    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+    size_t end = size_t(bd.y1) * W * B;
+    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
          it += size_t(gridDim.x) * blockDim.x) {
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -518,9 +533,9 @@ __device__ __forceinline__ V3 shade_item(const ResStore& s, size_t i, double c, 
     return f * (W * gate_w(c, w, c1.y));
 }
 
-__global__ void k_shade_gated(ResStore cur, int n_pix, double center, double width, double* image,
+__global__ void k_shade_gated(ResStore cur, int p0, int p1, double center, double width, double* image,
                               double* accum) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_pix; p += gridDim.x * blockDim.x) {
+    for (int p = p0 + blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += gridDim.x * blockDim.x) {
         V3 v = shade_item(cur, size_t(p), center, width);
         image[3 * size_t(p) + 0] = v.x;
         image[3 * size_t(p) + 1] = v.y;
@@ -531,8 +546,8 @@ __global__ void k_shade_gated(ResStore cur, int n_pix, double center, double wid
     }
 }
 
-__global__ void k_shade_transient(ResStore cur, size_t n_items, HistSpec h, double* hist) {
-    for (size_t it = blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < n_items;
+__global__ void k_shade_transient(ResStore cur, size_t i0, size_t i1, HistSpec h, double* hist) {
+    for (size_t it = i0 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < i1;
          it += size_t(gridDim.x) * blockDim.x) {
         int b = int(it % h.bins);
         V3 v = shade_item(cur, it, bin_center(h, b), h.bw);
@@ -569,17 +584,17 @@ struct PlainSink {
     }
 };
 
-__global__ void __launch_bounds__(128) k_hist_plain(FrameView F, const GHit* gbuf, PathCfg cfg, HistSpec h,
-                                                    int m_init, int frame_idx, double* rgb,
+__global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
+                                                    HistSpec h, int m_init, int frame_idx, double* rgb,
                                                     uint32_t* count) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h;
+    int W = F.cam.w;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins};
@@ -605,17 +620,17 @@ struct RefSink {
     }
 };
 
-__global__ void __launch_bounds__(128) k_reference(FrameView F, const GHit* gbuf, PathCfg cfg, double center,
-                                                   double width, int spp, uint64_t frame_key, double* mean,
-                                                   double* se) {
+__global__ void __launch_bounds__(128) k_reference(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
+                                                   double center, double width, int spp, uint64_t frame_key,
+                                                   double* mean, double* se) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
-    int W = F.cam.w, H = F.cam.h;
+    int W = F.cam.w;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < W * H; p += gridDim.x * blockDim.x) {
+    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         GHit g = gbuf[p];
@@ -665,6 +680,26 @@ __global__ void k_probe_rays(FrameView F, const double* rays, int n, int mode, d
 }
 
 // ---------------------------------------------------------------------------
+// halo staging (row-band sharding): one 16 B chunk per thread, coalesced on
+// both sides
+
+__global__ void k_halo_pack(ResStore grid, size_t item0, size_t n, double2* buf) {
+    size_t total = n * kResChunks;
+    for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
+        size_t c = j / n, i = j % n;
+        buf[j] = __ldcg(&grid.base[c * grid.stride + item0 + i]);
+    }
+}
+
+__global__ void k_halo_unpack(ResStore grid, size_t item0, size_t n, const double2* buf) {
+    size_t total = n * kResChunks;
+    for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
+        size_t c = j / n, i = j % n;
+        __stcg(&grid.base[c * grid.stride + item0 + i], __ldcg(&buf[j]));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 
 static int grid_for(size_t n, int block) {
@@ -679,65 +714,92 @@ void set_gauss_rule(const double* x, const double* w, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(c_gl_w, w, 32 * sizeof(double), 0, cudaMemcpyHostToDevice, s);
 }
 
-void launch_gbuffer(const FrameView& F, GHit* g, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h;
-    k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, g);
+static size_t band_pixels(const Band& bd, int W) { return size_t(bd.y1 - bd.y0) * W; }
+
+void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s) {
+    size_t n = size_t(bd.r1 - bd.r0) * F.cam.w;
+    if (!n) return;
+    k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, bd, g);
 }
 
-void launch_init_gated(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
-                       int frame_idx, ResStore cur, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h;
-    k_init_gated<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, ip, frame_idx, cur);
+void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
+                       const InitParams& ip, int frame_idx, ResStore cur, cudaStream_t s) {
+    size_t n = band_pixels(bd, F.cam.w);
+    if (!n) return;
+    k_init_gated<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, ip, frame_idx, cur);
 }
 
-void launch_init_transient(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
-                           const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h;
-    k_init_transient<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, ip, h, frame_idx, cur);
+void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
+                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s) {
+    size_t n = band_pixels(bd, F.cam.w);
+    if (!n) return;
+    k_init_transient<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, ip, h, frame_idx, cur);
 }
 
-void launch_temporal(const FrameView& Fc, const GHit* gc, const FrameView& Fp, const GHit* gp,
+void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
                      ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s) {
-    size_t n = size_t(Fc.cam.w) * Fc.cam.h * (cg.transient ? cg.h.bins : 1);
+    size_t n = band_pixels(bd, Fc.cam.w) * (cg.transient ? cg.h.bins : 1);
+    if (!n) return;
     size_t sm = frame_smem_bytes(Fc) + frame_smem_bytes(Fp);
-    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, ctr);
+    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, ctr);
 }
 
-void launch_spatial(const FrameView& F, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
                     unsigned long long* ctr, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h * (gg.transient ? gg.h.bins : 1);
-    k_spatial<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, gg, sp, pass, frame_idx, src,
+    size_t n = band_pixels(bd, F.cam.w) * (gg.transient ? gg.h.bins : 1);
+    if (!n) return;
+    k_spatial<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, gg, sp, pass, frame_idx, src,
                                                                  dst, ctr);
 }
 
-void launch_binreuse(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int frame_idx,
-                     ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h * h.bins;
-    k_binreuse<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, h, frame_idx, src, dst, ctr);
+void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
+                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s) {
+    size_t n = band_pixels(bd, F.cam.w) * h.bins;
+    if (!n) return;
+    k_binreuse<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, h, frame_idx, src, dst, ctr);
 }
 
-void launch_shade_gated(ResStore cur, int n_pix, double center, double width, double* image, double* accum,
-                        cudaStream_t s) {
-    k_shade_gated<<<grid_for(n_pix, 256), 256, 0, s>>>(cur, n_pix, center, width, image, accum);
+void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
+                        double* accum, cudaStream_t s) {
+    size_t n = band_pixels(bd, W);
+    if (!n) return;
+    k_shade_gated<<<grid_for(n, 256), 256, 0, s>>>(cur, bd.y0 * W, bd.y1 * W, center, width, image, accum);
 }
 
-void launch_shade_transient(ResStore cur, size_t n_items, const HistSpec& h, double* hist, cudaStream_t s) {
-    k_shade_transient<<<grid_for(n_items, 256), 256, 0, s>>>(cur, n_items, h, hist);
+void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
+                            cudaStream_t s) {
+    size_t n = band_pixels(bd, W) * h.bins;
+    if (!n) return;
+    size_t i0 = size_t(bd.y0) * W * h.bins;
+    k_shade_transient<<<grid_for(n, 256), 256, 0, s>>>(cur, i0, i0 + n, h, hist);
 }
 
-void launch_hist_plain(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int m_init,
-                       int frame_idx, double* rgb, uint32_t* count, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h;
-    k_hist_plain<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, h, m_init, frame_idx, rgb, count);
+void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
+                       int m_init, int frame_idx, double* rgb, uint32_t* count, cudaStream_t s) {
+    size_t n = band_pixels(bd, F.cam.w);
+    if (!n) return;
+    k_hist_plain<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, h, m_init, frame_idx, rgb,
+                                                                   count);
 }
 
-void launch_reference(const FrameView& F, const GHit* g, const PathCfg& cfg, double center, double width,
-                      int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s) {
-    size_t n = size_t(F.cam.w) * F.cam.h;
-    k_reference<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, g, cfg, center, width, spp, frame_key,
+void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
+                      double width, int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s) {
+    size_t n = band_pixels(bd, F.cam.w);
+    if (!n) return;
+    k_reference<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, center, width, spp, frame_key,
                                                                   mean, se);
+}
+
+void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s) {
+    if (!n_items) return;
+    k_halo_pack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+}
+
+void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s) {
+    if (!n_items) return;
+    k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
 }
 
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,

@@ -28,6 +28,18 @@ struct GateGrid {
     HistSpec h;
 };
 
+// Row band of a session (parallel.py): the kernels compute rows [y0, y1) of
+// the image; reservoir grids and G-buffers store rows [r0, r1) (the band plus
+// the spatial halo).  Device pointers handed to the kernels are rebased so
+// that they are indexed by GLOBAL pixel / item numbers (RNG keys and
+// neighbour arithmetic stay those of the full frame, pipeline.hpp:102).
+// Temporal reuse may read the previous grid on rows [t0, t1).  A read outside
+// the stored rows raises *err (the host turns it into an error).
+struct Band {
+    int y0, y1, r0, r1, t0, t1;
+    unsigned long long* err;
+};
+
 struct SpatialParams {
     int neighbors;
     double radius;
@@ -35,26 +47,33 @@ struct SpatialParams {
 
 size_t frame_smem_bytes(const FrameView& F);
 void set_gauss_rule(const double* x, const double* w, cudaStream_t s);
-void launch_gbuffer(const FrameView& F, GHit* g, cudaStream_t s);
-void launch_init_gated(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
-                       int frame_idx, ResStore cur, cudaStream_t s);
-void launch_init_transient(const FrameView& F, const GHit* g, const PathCfg& cfg, const InitParams& ip,
-                           const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s);
-void launch_temporal(const FrameView& Fc, const GHit* gc, const FrameView& Fp, const GHit* gp,
+// g (launch_gbuffer) is the band's local G-buffer (row r0 first); every other
+// G-buffer / grid / image pointer is global-indexed (see Band).
+void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s);
+void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
+                       const InitParams& ip, int frame_idx, ResStore cur, cudaStream_t s);
+void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
+                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s);
+void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
                      ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s);
-void launch_spatial(const FrameView& F, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
                     unsigned long long* ctr, cudaStream_t s);
-void launch_binreuse(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int frame_idx,
-                     ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s);
-void launch_shade_gated(ResStore cur, int n_pix, double center, double width, double* image, double* accum,
-                        cudaStream_t s);
-void launch_shade_transient(ResStore cur, size_t n_items, const HistSpec& h, double* hist, cudaStream_t s);
-void launch_hist_plain(const FrameView& F, const GHit* g, const PathCfg& cfg, const HistSpec& h, int m_init,
-                       int frame_idx, double* rgb, uint32_t* count, cudaStream_t s);
-void launch_reference(const FrameView& F, const GHit* g, const PathCfg& cfg, double center, double width,
-                      int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s);
+void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
+                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s);
+void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
+                        double* accum, cudaStream_t s);
+void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
+                            cudaStream_t s);
+void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
+                       int m_init, int frame_idx, double* rgb, uint32_t* count, cudaStream_t s);
+void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
+                      double width, int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s);
+// halo staging: rows [a, b) of a global-indexed grid <-> a contiguous buffer
+// laid out chunk-major ([kResChunks][(b - a) * W * B] x 16 B)
+void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s);
+void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s);
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
                        cudaStream_t s);
 

@@ -163,7 +163,7 @@ __device__ inline const WalkV& rs_vert(const RecSrc& s, int i) {
 }
 
 // build_record (transport.hpp:448-582), Length subset
-__device__ void build_record(const FrameView& F, const RecSrc& s, Rec& r) {
+__device__ __noinline__ void build_record(const FrameView& F, const RecSrc& s, Rec& r) {
     rec_clear(r);
     int last = s.q ? s.d + 1 : s.d;
     int k = -1;
@@ -456,7 +456,7 @@ __device__ inline SurfPt surf_from_hit(const FrameView& F, const Hit& h) {
 }
 
 // reproject_to_mesh (shiftmap.hpp:275-307)
-__device__ bool reproject(const FrameView& F, const SurfPt& cur, const V3& plane_pt, const V3& p1,
+__device__ __noinline__ bool reproject(const FrameView& F, const SurfPt& cur, const V3& plane_pt, const V3& p1,
                           SurfPt& out) {
     const GTriIsect& g = tri_geo(F, cur.tri);
     V3 tn = F.tri[cur.tri].n;
@@ -508,7 +508,7 @@ struct NewtonOut {
 };
 
 // newton_solve (shiftmap.hpp:314-378); max 5 iterations, 8 halvings
-__device__ NewtonOut newton_solve(const FrameView& F, const V3& p1, const V3& p2, const SurfPt& start,
+__device__ __noinline__ NewtonOut newton_solve(const FrameView& F, const V3& p1, const V3& p2, const SurfPt& start,
                                   double delta, int gauge, double tol, double eps_grad) {
     NewtonOut res;
     res.converged = 0;
@@ -568,7 +568,7 @@ struct Dom {
 
 // hybrid_base_shift (shiftmap.hpp:459-528): random replay of the prefix from
 // the destination pixel with the stored lanes.
-__device__ Prefix base_shift(const Dom& dom, const Rec& rec, const PathCfg& cfg) {
+__device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec, const PathCfg& cfg) {
     Prefix out;
     out.ok = 0;
     const FrameView& F = *dom.F;
@@ -656,7 +656,7 @@ __device__ inline Suffix suffix_geometry(const FrameView& F, const Rec& rec) {
 }
 
 // rebuild_sample (shiftmap.hpp:579-654)
-__device__ bool rebuild_sample(const FrameView& F, const Rec& rec, const Prefix& pre, const SurfPt& p,
+__device__ __noinline__ bool rebuild_sample(const FrameView& F, const Rec& rec, const Prefix& pre, const SurfPt& p,
                                const Suffix& suf, Sample& out) {
     V3 d1 = p.pos - pre.p1;
     double l1 = norm(d1);
@@ -729,7 +729,7 @@ __device__ inline Prefix stored_prefix(const FrameView& F, const Rec& rec) {
 }
 
 // shift_sample (shiftmap.hpp:662-783).  Returns true on a usable mapping.
-__device__ bool shift_sample(const Sample& src, const Dom& sd, const Dom& dd, const PathCfg& cfg,
+__device__ __noinline__ bool shift_sample(const Sample& src, const Dom& sd, const Dom& dd, const PathCfg& cfg,
                              uint32_t* ctr, Sample& mapped, double& jac_out) {
     ctr_add(ctr, SC_ATTEMPTS);
     const Rec& rec = src.rec;
@@ -803,7 +803,7 @@ __device__ bool shift_sample(const Sample& src, const Dom& sd, const Dom& dd, co
 
 // shrink_map (shiftmap.hpp:789-876): contract a wide-gate sample onto the fine
 // gate (forward) or expand (inverse); identity prefix, no replay.
-__device__ bool shrink_map(const Sample& src, const Dom& dom, double K, bool forward,
+__device__ __noinline__ bool shrink_map(const Sample& src, const Dom& dom, double K, bool forward,
                            const PathCfg& cfg, Sample& mapped, double& jac_out) {
     const Rec& rec = src.rec;
     const FrameView& F = *dom.F;
