@@ -227,6 +227,11 @@ def run_ours(args) -> None:
     frames = args.steps
     fps = frames / (t_max * 1e-3)
 
+    # shift counters of one more (synchronous) frame: the work behind the time
+    st = sess.step(stats=True)
+    shift_stats = {k: {n: st[k][n] for n in ("attempts", "solves", "iterations", "newton_ok", "occluded",
+                                              "success")} for k in ("temporal", "spatial")}
+
     # e2e through the public API: step + image read-back to pinned host memory
     parallel.barrier(group)
     t0 = time.perf_counter()
@@ -278,6 +283,7 @@ def run_ours(args) -> None:
                        "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
             "mpaths_per_s": w * h * cfg.m_init * fps / 1e6,
             "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},
+            "shift_stats_one_frame": shift_stats,
             "e2e": {"value": frames / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "kernel": f"k_{dom_name}", "achieved": achieved, "peak": pk["hbm_gbs"],

@@ -33,7 +33,7 @@ def build_if_possible() -> bool:
     container); the GPU box only uses the prebuilt library."""
     import subprocess
     if REF_INCLUDE.exists():
-        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+        subprocess.run(["make", "-s", "-C", str(HERE), "all", "shim"], check=True)
     return LIB.exists()
 
 

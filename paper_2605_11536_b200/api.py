@@ -296,8 +296,8 @@ class Renderer:
                                                   tri.ctypes.data_as(C.POINTER(C.c_int32))))
         return t, tri
 
-    def session(self, scene, cfg: RenderConfig) -> "Session":
-        return Session(self, self._scene(scene), cfg)
+    def session(self, scene, cfg: RenderConfig, band: tuple | None = None) -> "Session":
+        return Session(self, self._scene(scene), cfg, band)
 
     def __del__(self):
         try:
@@ -309,33 +309,81 @@ class Renderer:
 
 
 class Session:
-    """Interactive frame stepping (the body of the render_gated frame loop)."""
+    """Interactive frame stepping (the body of the render_gated frame loop).
 
-    def __init__(self, r: Renderer, scene: Scene, cfg: RenderConfig):
+    With `band=(y0, y1, halo)` the session renders image rows [y0, y1) only
+    and keeps `halo` rows on each side for spatial reuse (row-band sharding,
+    see parallel.py); the default is the whole frame."""
+
+    def __init__(self, r: Renderer, scene: Scene, cfg: RenderConfig, band: tuple | None = None):
         self._r = r
         self._scene = scene
         self.cfg = cfg
         self.handle = C.c_void_p()
         c = cfg.to_c()
-        r._check(r._lib.tofr_gpu_session_create(r.handle, scene.handle, C.byref(c), C.byref(self.handle)))
+        y0, y1, halo = band if band is not None else (0, -1, 0)
+        r._check(r._lib.tofr_gpu_session_create_band(r.handle, scene.handle, C.byref(c), y0, y1, halo,
+                                                     C.byref(self.handle)))
         info = scene.info()
         self.width, self.height = info["width"], info["height"]
+        a, b, c0, c1 = (C.c_int32() for _ in range(4))
+        r._check(r._lib.tofr_gpu_session_band(self.handle, C.byref(a), C.byref(b), C.byref(c0), C.byref(c1)))
+        self.y0, self.y1, self.r0, self.r1 = a.value, b.value, c0.value, c1.value
+        self._xfn = None
 
-    def step(self) -> dict:
+    def step(self, stats: bool = True) -> dict | None:
+        """One frame.  stats=False leaves the frame in flight (asynchronous)."""
+        if not stats:
+            self._r._check(self._r._lib.tofr_gpu_session_step(self.handle, None))
+            return None
         st = F.FrameStats()
         self._r._check(self._r._lib.tofr_gpu_session_step(self.handle, C.byref(st)))
         return stats_to_dicts([st], 1)[0]
 
     def read_image(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Last frame's image of this session's rows, [y1 - y0, W, 3]."""
         if out is None:
-            out = np.zeros((self.height, self.width, 3))
+            out = np.zeros((self.y1 - self.y0, self.width, 3))
         self._r._check(self._r._lib.tofr_gpu_session_read_image(self.handle, _dptr(out)))
         return out
+
+    def halo_buffers(self) -> dict:
+        p = [C.c_void_p() for _ in range(4)]
+        n = [C.c_uint64() for _ in range(2)]
+        self._r._check(self._r._lib.tofr_gpu_session_halo_buffers(
+            self.handle, C.byref(p[0]), C.byref(p[1]), C.byref(n[0]), C.byref(p[2]), C.byref(p[3]),
+            C.byref(n[1])))
+        return {"send_lo": int(p[0].value or 0), "recv_lo": int(p[1].value or 0), "bytes_lo": int(n[0].value),
+                "send_hi": int(p[2].value or 0), "recv_hi": int(p[3].value or 0), "bytes_hi": int(n[1].value)}
+
+    def set_halo_exchange(self, fn) -> None:
+        """fn(pass) -> None: move the packed halo rows (see tofr_gpu.h)."""
+        errors = self.halo_errors = []  # no reference back to self (no GC cycle)
+
+        def _cb(user, pass_):
+            try:
+                fn(int(pass_))
+                return 0
+            except Exception as e:  # never unwind through the C ABI
+                import traceback
+                traceback.print_exc()
+                errors.append(e)
+                return 1
+        self._xfn = F.HALO_FN(_cb)
+        self._r._check(self._r._lib.tofr_gpu_session_set_halo_exchange(self.handle, self._xfn, None))
+
+    def stage_totals(self, reset: bool = False):
+        ms = (C.c_double * 6)()
+        fr = C.c_int64()
+        hx = C.c_uint64()
+        self._r._check(self._r._lib.tofr_gpu_session_stage_totals(self.handle, ms, C.byref(fr), C.byref(hx),
+                                                                  int(reset)))
+        return list(ms), int(fr.value), int(hx.value)
 
     def last_ms(self):
         tot = C.c_double()
         st = (C.c_double * 6)()
-        self._r._lib.tofr_gpu_session_last_ms(self.handle, C.byref(tot), st)
+        self._r._check(self._r._lib.tofr_gpu_session_last_ms(self.handle, C.byref(tot), st))
         return tot.value, list(st)
 
     def io_bytes(self):
@@ -350,6 +398,11 @@ class Session:
 
     def sync(self) -> None:
         self._r._check(self._r._lib.tofr_gpu_session_sync(self.handle))
+
+    def sync_stream(self) -> None:
+        """Wait for the work enqueued so far (usable inside a halo callback)."""
+        import torch
+        torch.cuda.ExternalStream(self.stream_ptr()).synchronize()
 
     def __del__(self):
         try:

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -117,7 +118,20 @@ struct tofr_gpu {
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string err;
+    // sessions keep their context alive: tofr_gpu_destroy with live sessions
+    // only marks it, the last session destructor releases it (garbage
+    // collectors finalise handles in arbitrary order)
+    int live_sessions = 0;
+    bool closing = false;
 };
+
+namespace {
+void release_ctx(tofr_gpu* ctx) {
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+}  // namespace
 
 struct tofr_scene {
     HScene s;
@@ -167,6 +181,10 @@ struct tofr_session {
     DevBuf image, accum, hist, hist_count;  // owned rows only
     DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag
     DevBuf send_lo, send_hi, recv_lo, recv_hi;
+    DevBuf wo_cls, wo_counts, wo_perm;  // cost-ordered reuse (TOFR_ORDER=0 disables)
+    DevBuf sp_mapped, sp_ok, sp_rng, sp_list, sp_count;  // phased spatial pass (TOFR_SPATIAL=mono disables)
+    bool phased = false;
+    bool order = true;
     tofr_halo_exchange_fn xfn = nullptr;
     void* xuser = nullptr;
     uint64_t halo_exchanges = 0;
@@ -186,11 +204,26 @@ struct tofr_session {
     size_t owned_pixels() const { return size_t(y1 - y0) * W; }
 
     ~tofr_session() {
-        if (ctx && ctx->stream) cudaStreamSynchronize(ctx->stream);
+        if (ctx) {
+            cudaSetDevice(ctx->device);
+            if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        }
         for (auto& set : ev)
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
         if (err_host) cudaFreeHost(err_host);
+        release_buffers();
+        if (ctx && --ctx->live_sessions == 0 && ctx->closing) release_ctx(ctx);
+    }
+    void release_buffers() {
+        for (auto& sl : slot) {
+            sl.blob.release();
+            sl.gbuf.release();
+        }
+        for (auto& r : res) r.release();
+        for (DevBuf* b : {&image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+                          &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count})
+            b->release();
     }
 };
 
@@ -267,6 +300,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     check_config(cfg);
     auto s = std::make_unique<tofr_session>();
     s->ctx = ctx;
+    ctx->live_sessions++;
     s->scene = sc->s;
     s->cfg = *cfg;
     s->W = sc->s.camera.width;
@@ -313,6 +347,31 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
         ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
         if (s->res[2].p) ck(cudaMemsetAsync(s->res[2].p, 0, rb, ctx->stream), "memset");
+        const char* ord = std::getenv("TOFR_ORDER");
+        s->order = !(ord && ord[0] == '0');
+        {
+            // phased spatial pass: N planes of forward-shifted samples; only when
+            // they fit comfortably (gated frames; transient grids use k_spatial)
+            const char* sm = std::getenv("TOFR_SPATIAL");
+            size_t own_items = s->owned_pixels() * s->B;
+            size_t nj = size_t(std::max(0, cfg->spatial_neighbors));
+            size_t need = nj * own_items * kResChunks * 16;
+            s->phased = s->has_spatial && nj > 0 && cfg->spatial_radius > 0 && !(sm && std::strcmp(sm, "mono") == 0) &&
+                        need <= (size_t(16) << 30);
+            if (s->phased) {
+                s->sp_mapped.ensure(need);
+                s->sp_ok.ensure(nj * own_items);
+                s->sp_rng.ensure(own_items * sizeof(uint64_t));
+                s->sp_list.ensure(nj * own_items * sizeof(uint32_t));
+                s->sp_count.ensure(16);
+            }
+        }
+        if (s->order) {
+            size_t own_items = s->owned_pixels() * s->B;
+            s->wo_cls.ensure(own_items);
+            s->wo_perm.ensure(own_items * sizeof(uint32_t));
+            s->wo_counts.ensure(64 * sizeof(uint32_t));
+        }
         if (s->transient) {
             s->hist.ensure(own * 3 * sizeof(double));
             ck(cudaMemsetAsync(s->hist.p, 0, own * 3 * sizeof(double), ctx->stream), "memset");
@@ -422,6 +481,9 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     bool prev_halo = halo && s->cam_moves;
     Band bd = band_of(s, prev_halo);
     cudaEvent_t* ev = s->ev[set];
+    WorkOrder wo{nullptr, nullptr, nullptr};
+    if (s->order && s->wo_perm.p)
+        wo = WorkOrder{s->wo_cls.as<uint8_t>(), s->wo_counts.as<uint32_t>(), s->wo_perm.as<uint32_t>()};
     ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
 
     cudaEventRecord(ev[0], stream);
@@ -443,7 +505,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
-            launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
+            launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]), wo,
                             ctr + 0 * SC_COUNT, stream);
         }
         cudaEventRecord(ev[2], stream);
@@ -456,8 +518,19 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
         for (int pass = 0; pass < c.spatial_passes; ++pass) {
             if (halo) exchange_halo(s, cur, pass);
-            launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), ctr + 1 * SC_COUNT,
-                           stream);
+            SpatialScratch scr;
+            const SpatialScratch* scp = nullptr;
+            if (s->phased) {
+                size_t own_items = s->owned_pixels() * s->B;
+                scr.mapped = ResStore{s->sp_mapped.as<double2>(), own_items * size_t(c.spatial_neighbors)};
+                scr.ok = s->sp_ok.as<uint8_t>();
+                scr.rng_ctr = s->sp_rng.as<uint64_t>();
+                scr.list = s->sp_list.as<uint32_t>();
+                scr.count = s->sp_count.as<uint32_t>();
+                scp = &scr;
+            }
+            launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
+                           ctr + 1 * SC_COUNT, stream);
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur]);
         }
@@ -504,6 +577,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
 template <class F>
 int guard(tofr_gpu* ctx, F&& fn) {
     try {
+        if (ctx) ck(cudaSetDevice(ctx->device), "cudaSetDevice");
         fn();
         if (ctx) ctx->err.clear();
         return TOFR_OK;
@@ -712,8 +786,11 @@ int tofr_gpu_create(const int* devices, int n_devices, tofr_gpu** out) {
 
 void tofr_gpu_destroy(tofr_gpu* ctx) {
     if (!ctx) return;
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    if (ctx->live_sessions > 0) {
+        ctx->closing = true;
+        return;
+    }
+    release_ctx(ctx);
 }
 
 const char* tofr_gpu_last_error(const tofr_gpu* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

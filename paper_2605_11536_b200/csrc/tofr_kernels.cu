@@ -25,7 +25,7 @@
 // Minimum resident CTAs per SM requested for the reuse/initial kernels
 // (register cap 65536 / (128 * MINB)); tuned with ncu, overridable at build time.
 #ifndef TOFR_REUSE_MINB
-#define TOFR_REUSE_MINB 1
+#define TOFR_REUSE_MINB 4
 #endif
 
 namespace tofr_b200 {
@@ -70,6 +70,24 @@ __device__ __forceinline__ void flush_ctr(const uint32_t* c, unsigned long long*
         for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[k], v);
     }
+}
+
+// ---------------------------------------------------------------------------
+// work-ordering helpers (see k_cost_*)
+
+constexpr int kCostBuckets = 8;
+
+__device__ __forceinline__ bool shiftable(const ResStore& s, size_t i) {
+    double2 c0 = ld2(s, 0, i);
+    Meta m = ld_meta(s, i);
+    return m.has && c0.x > 0 && m.valid;
+}
+
+// Warp-aggregated append of item `loc` into bucket c.
+__device__ __forceinline__ void bucket_count(int c, uint32_t* counts) {
+    unsigned peers = __match_any_sync(__activemask(), c);
+    int leader = __ffs(peers) - 1;
+    if ((threadIdx.x & 31) == leader) atomicAdd(&counts[c], uint32_t(__popc(peers)));
 }
 
 // ---------------------------------------------------------------------------
@@ -326,7 +344,8 @@ __device__ __forceinline__ void gate_of(const GateGrid& gg, int b, double& c, do
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc, Band bd, const GHit* gc, FrameView Fp,
                                                   const GHit* gp, PathCfg cfg, GateGrid cur_gate,
                                                   GateGrid prev_gate, int frame_idx, ResStore cur,
-                                                  ResStore prev, unsigned long long* ctr_out) {
+                                                  ResStore prev, const uint32_t* perm,
+                                                  unsigned long long* ctr_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(Fc, smem, off);
@@ -334,9 +353,9 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
     __syncthreads();
     int W = Fc.cam.w, B = cur_gate.transient ? cur_gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t end = size_t(bd.y1) * W * B;
-    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
-         it += size_t(gridDim.x) * blockDim.x) {
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        size_t it = base + (perm ? size_t(perm[i]) : i);
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
         GHit g = gc[p];
@@ -400,16 +419,16 @@ __device__ __forceinline__ void neighbor_offset(int j, int count, double radius,
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                  GateGrid gate, SpatialParams sp, int pass,
                                                  int frame_idx, ResStore src_grid, ResStore dst_grid,
-                                                 unsigned long long* ctr_out) {
+                                                 const uint32_t* perm, unsigned long long* ctr_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t end = size_t(bd.y1) * W * B;
-    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
-         it += size_t(gridDim.x) * blockDim.x) {
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        size_t it = base + (perm ? size_t(perm[i]) : i);
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
         Res out;
@@ -461,6 +480,176 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
         res_store(dst_grid, it, out);
     }
     flush_ctr(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// Spatial reuse split into phases.  k_spatial runs a pixel's whole merge chain
+// in one thread: per neighbour j a forward shift (neighbour sample -> pixel),
+// an inverse shift (running output -> neighbour) and a GRIS merge.  On B200
+// that chain diverges badly (lanes of one warp sit in different shifts and
+// Newton iterations).  The forward shifts do not depend on the merge order,
+// so they run first as one flat, compacted list of (neighbour, pixel) jobs;
+// the inverse shift + merge of neighbour j then runs as one kernel per j with
+// the running output and the lane-10 RNG counter carried in HBM.  Same
+// arithmetic, same RNG draws in the same order, same counters.
+
+
+// Neighbour j of item `it`, with the k_spatial skip rules.  Returns false when
+// the reference skips it (self, outside the image, never-written M <= 0).
+__device__ __forceinline__ bool spatial_neighbor(const Band& bd, int W, int H, int B, int px, int py, int b,
+                                                 const SpatialParams& sp, uint64_t rk, int j,
+                                                 const ResStore& src_grid, int& nx, int& ny, size_t& si) {
+    int dx, dy;
+    neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+    nx = px + dx;
+    ny = py + dy;
+    if (nx == px && ny == py) return false;
+    if (nx < 0 || nx >= W || ny < 0 || ny >= H) return false;
+    if (ny < bd.r0 || ny >= bd.r1) {  // beyond the exchanged halo
+        atomicAdd(bd.err, 1ull);
+        return false;
+    }
+    si = (size_t(ny) * W + nx) * B + b;
+    double2 c0 = ld2(src_grid, 0, si);
+    return c0.y > 0;
+}
+
+__device__ __forceinline__ uint64_t spatial_rot_key(uint64_t pix, int pass, uint64_t seed, int frame_idx) {
+    return mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + seed + uint64_t(frame_idx) * 97);
+}
+
+__global__ void k_spatial_fwd_list(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                                   int frame_idx, ResStore src_grid, SpatialScratch sc) {
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    int lane = threadIdx.x & 31;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
+        for (int j = 0; j < sp.neighbors; ++j) {
+            int nx, ny;
+            size_t si = 0;
+            bool want = live && spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
+                        shiftable(src_grid, si);
+            unsigned m = __ballot_sync(0xffffffffu, want);
+            if (!m) continue;
+            uint32_t start = 0;
+            if (lane == __ffs(m) - 1) start = atomicAdd(sc.count, uint32_t(__popc(m)));
+            start = __shfl_sync(0xffffffffu, start, __ffs(m) - 1);
+            if (want) sc.list[start + __popc(m & ((1u << lane) - 1))] = uint32_t(size_t(j) * n + i);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
+    k_spatial_fwd(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                  int frame_idx, ResStore src_grid, SpatialScratch sc, unsigned long long* ctr_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t jobs = *sc.count;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < jobs; q += gridDim.x * blockDim.x) {
+        uint32_t e = sc.list[q];
+        int j = int(e / n);
+        size_t i = e % n, it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
+        int nx, ny, dx, dy;
+        neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+        nx = px + dx;
+        ny = py + dy;
+        size_t si = (size_t(ny) * W + nx) * B + b;
+        Res src;
+        res_load(src_grid, si, src);
+        Dom dd{px, py, dc, dw, &F, gbuf};
+        Dom sd{nx, ny, dc, dw, &F, gbuf};
+        Res m;
+        double jac;
+        if (shift_sample(src.y, sd, dd, cfg, ctr, m.y, jac)) {
+            m.has = 1;
+            m.W = jac;
+            m.M = 0;
+            m.phat = 0;
+            res_store(sc.mapped, e, m);
+            sc.ok[e] = 1;
+        }
+    }
+    flush_ctr(ctr, ctr_out);
+}
+
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
+    k_spatial_merge(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                    int j, int frame_idx, ResStore src_grid, ResStore dst_grid, SpatialScratch sc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        size_t it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        uint64_t rk = spatial_rot_key(pix, pass, cfg.seed, frame_idx);
+        int nx, ny;
+        size_t si = 0;
+        bool use = spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si);
+        if (!use) {
+            if (j == 0) {  // the output starts as the pass input
+                Res out;
+                res_load(src_grid, it, out);
+                res_store(dst_grid, it, out);
+            }
+            if (j + 1 < sp.neighbors && j == 0) sc.rng_ctr[i] = 0;
+            continue;
+        }
+        Res out;
+        res_load(j == 0 ? src_grid : dst_grid, it, out);
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(pass * 131 + b), 10);
+        if (j > 0) rng.ctr = sc.rng_ctr[i];
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        Res src;  // header only: gris_merge reads W, M, phat, has
+        {
+            double2 c0 = ld2(src_grid, 0, si), c1 = ld2(src_grid, 1, si);
+            src.W = c0.x;
+            src.M = c0.y;
+            src.phat = c1.x;
+            src.has = ld_meta(src_grid, si).has;
+        }
+        size_t e = size_t(j) * n + i;
+        MergeShift ms{0, 1.0, 0.0};
+        Res mapped;
+        if (!res_empty(src) && sc.ok[e]) {
+            res_load(sc.mapped, e, mapped);
+            ms.valid = 1;
+            ms.jac = mapped.W;
+        }
+        if (!res_empty(out)) {
+            Dom dd{px, py, dc, dw, &F, gbuf};
+            Dom sd{nx, ny, dc, dw, &F, gbuf};
+            Sample inv;
+            double jac;
+            if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
+                ms.phat_src_of_dst = luminance(inv.f) * gate_w(dc, dw, inv.len) * jac;
+        }
+        gris_merge(out, src, ms, mapped.y, dc, dw, cfg.m_cap, rng);
+        res_store(dst_grid, it, out);
+        if (j + 1 < sp.neighbors) sc.rng_ctr[i] = rng.ctr;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -518,6 +707,106 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, 
         res_store(dst_grid, it, out);
     }
     flush_ctr(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// Work ordering for the reuse kernels.  One thread owns one reservoir item for
+// the whole merge chain (the reference's per-pixel sequential semantics), and
+// the cost of an item is dominated by the shifts it attempts (replay, Newton,
+// re-projection and occlusion rays).  A cheap pre-pass estimates that count
+// from the reservoir headers, and the items are then processed heaviest first
+// in cost buckets, so that a warp's lanes carry similar shift loads instead of
+// mixing 6-shift pixels with empty ones.  Results do not depend on the order:
+// items are independent given the pass-input grid, counters are sums.
+
+__global__ void k_cost_temporal(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cur_gate,
+                                ResStore cur, ResStore prev, uint8_t* cls, uint32_t* counts) {
+    int W = Fc.cam.w, B = cur_gate.transient ? cur_gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        if (i >= n) continue;
+        size_t it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        int c = 0;
+        GHit g = gc[p];
+        if (g.tri >= 0) {
+            V3 d0 = primary_dir(Fc.cam, px, py);
+            V3 hp = Fc.cam.pos + d0 * g.t;
+            int qx, qy;
+            if (project(Fp.cam, hp, qx, qy) && qy >= bd.t0 && qy < bd.t1) {
+                size_t si = (size_t(qy) * W + qx) * B + b;
+                c = 1 + int(shiftable(prev, si)) * 3 + int(shiftable(cur, it)) * 3;
+            }
+        }
+        c = c > kCostBuckets - 1 ? kCostBuckets - 1 : c;
+        cls[i] = uint8_t(c);
+        bucket_count(c, counts);
+    }
+}
+
+__global__ void k_cost_spatial(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                               int frame_idx, ResStore src_grid, uint8_t* cls, uint32_t* counts) {
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        if (i >= n) continue;
+        size_t it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        int c = 0;
+        if (sp.neighbors > 0 && sp.radius > 0) {
+            bool self = shiftable(src_grid, it);
+            uint64_t pix = uint64_t(py) * W + px;
+            uint64_t rk = mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + uint64_t(cfg.seed) +
+                                uint64_t(frame_idx) * 97);
+            for (int j = 0; j < sp.neighbors; ++j) {
+                int dx, dy;
+                neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+                int nx = px + dx, ny = py + dy;
+                if (nx == px && ny == py) continue;
+                if (nx < 0 || nx >= W || ny < 0 || ny >= H || ny < bd.r0 || ny >= bd.r1) continue;
+                size_t si = (size_t(ny) * W + nx) * B + b;
+                bool nb = shiftable(src_grid, si);
+                c += int(nb) + int(self || nb);  // fwd shift; inverse once the output is non-empty
+            }
+        }
+        c = c > kCostBuckets - 1 ? kCostBuckets - 1 : c;
+        cls[i] = uint8_t(c);
+        bucket_count(c, counts);
+    }
+}
+
+// Heaviest bucket first: offsets from the counts, positions by warp-aggregated
+// cursors (counts[kCostBuckets + c]).
+__global__ void k_cost_scatter(const uint8_t* cls, size_t n, uint32_t* counts, uint32_t* perm) {
+    __shared__ uint32_t off[kCostBuckets];
+    if (threadIdx.x == 0) {
+        uint32_t o = 0;
+        for (int c = kCostBuckets - 1; c >= 0; --c) {
+            off[c] = o;
+            o += counts[c];
+        }
+    }
+    __syncthreads();
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        if (i >= n) continue;
+        int c = cls[i];
+        unsigned peers = __match_any_sync(__activemask(), c);
+        int leader = __ffs(peers) - 1;
+        int lane = threadIdx.x & 31;
+        uint32_t start = 0;
+        if (lane == leader) start = atomicAdd(&counts[kCostBuckets + c], uint32_t(__popc(peers)));
+        start = __shfl_sync(peers, start, leader);
+        uint32_t rank = __popc(peers & ((1u << lane) - 1));
+        perm[off[c] + start + rank] = uint32_t(i);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -736,22 +1025,53 @@ void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, co
     k_init_transient<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, ip, h, frame_idx, cur);
 }
 
+static void order_items(const uint8_t* cls, size_t n, const WorkOrder& wo, cudaStream_t s) {
+    k_cost_scatter<<<grid_for(n, 256), 256, 0, s>>>(cls, n, wo.counts, wo.perm);
+}
+
 void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
-                     ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s) {
+                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr, cudaStream_t s) {
     size_t n = band_pixels(bd, Fc.cam.w) * (cg.transient ? cg.h.bins : 1);
     if (!n) return;
+    const uint32_t* perm = nullptr;
+    if (wo.perm) {
+        cudaMemsetAsync(wo.counts, 0, 2 * kCostBuckets * sizeof(uint32_t), s);
+        k_cost_temporal<<<grid_for(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, cur, prev, wo.cls, wo.counts);
+        order_items(wo.cls, n, wo, s);
+        perm = wo.perm;
+    }
     size_t sm = frame_smem_bytes(Fc) + frame_smem_bytes(Fp);
-    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, ctr);
+    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, perm,
+                                                  ctr);
 }
 
 void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
-                    unsigned long long* ctr, cudaStream_t s) {
+                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w) * (gg.transient ? gg.h.bins : 1);
     if (!n) return;
-    k_spatial<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, gg, sp, pass, frame_idx, src,
-                                                                 dst, ctr);
+    size_t sm = frame_smem_bytes(F);
+    if (sc && sp.neighbors > 0 && sp.radius > 0) {
+        cudaMemsetAsync(sc->count, 0, sizeof(uint32_t), s);
+        cudaMemsetAsync(sc->ok, 0, n * size_t(sp.neighbors), s);
+        k_spatial_fwd_list<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, *sc);
+        k_spatial_fwd<<<grid_for(n * size_t(sp.neighbors), 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass,
+                                                                                frame_idx, src, *sc, ctr);
+        for (int j = 0; j < sp.neighbors; ++j)
+            k_spatial_merge<<<grid_for(n, 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass, j, frame_idx, src, dst,
+                                                              *sc);
+        return;
+    }
+    const uint32_t* perm = nullptr;
+    if (wo.perm) {
+        cudaMemsetAsync(wo.counts, 0, 2 * kCostBuckets * sizeof(uint32_t), s);
+        k_cost_spatial<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, wo.cls,
+                                                         wo.counts);
+        order_items(wo.cls, n, wo, s);
+        perm = wo.perm;
+    }
+    k_spatial<<<grid_for(n, 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass, frame_idx, src, dst, perm, ctr);
 }
 
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,

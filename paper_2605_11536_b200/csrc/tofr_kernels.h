@@ -40,6 +40,26 @@ struct Band {
     unsigned long long* err;
 };
 
+// Cost-ordered processing of the reuse kernels (see k_cost_* in the .cu):
+// per-item cost class, bucket counters/cursors [16], the permutation.
+// perm == nullptr processes items in storage order.
+struct WorkOrder {
+    uint8_t* cls;
+    uint32_t* counts;
+    uint32_t* perm;
+};
+
+// Scratch of the phased spatial pass (k_spatial_fwd_list / k_spatial_fwd /
+// k_spatial_merge): forward-shifted samples of every (neighbour j, item i)
+// job, their usable flags, the running lane-10 RNG position, the job list.
+struct SpatialScratch {
+    ResStore mapped;    // item j * n + i (jac in the W slot), stride N * n
+    uint8_t* ok;        // [N * n]
+    uint64_t* rng_ctr;  // [n]
+    uint32_t* list;     // [N * n]
+    uint32_t* count;    // [1]
+};
+
 struct SpatialParams {
     int neighbors;
     double radius;
@@ -56,10 +76,10 @@ void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, co
                            const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s);
 void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
-                     ResStore cur, ResStore prev, unsigned long long* ctr, cudaStream_t s);
+                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr, cudaStream_t s);
 void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
-                    unsigned long long* ctr, cudaStream_t s);
+                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, cudaStream_t s);
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
                      int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s);
 void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,

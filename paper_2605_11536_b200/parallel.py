@@ -8,7 +8,15 @@ a band renders exactly what the full frame renders for those rows.  The only
 exchange is the spatial-reuse halo: before every spatial pass each rank sends
 its `halo` edge rows of the pass-input reservoir grid to its neighbours and
 receives theirs (pipeline.hpp:232-269 reads neighbours within
-|dy| <= lround(radius) of a snapshot grid).
+|dy| <= lround(radius) of a snapshot grid).  The library packs/unpacks the
+rows on its stream (tofr_gpu_session_halo_buffers); the transfer itself is a
+torch.distributed batch of isend/irecv (NCCL over NVLink on B200, gloo on
+CPU for the tests) enqueued on that same stream.
+
+Temporal reuse reads the previous frame at the reprojected pixel; for a static
+camera (every bundled scene) that is the pixel itself, so it stays inside the
+band.  For a moving camera the library also exchanges the final grid's halo
+(pass -1) and flags any reprojection beyond it as an error.
 """
 from __future__ import annotations
 
@@ -24,9 +32,12 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
     return y0, y0 + base + (1 if rank < rem else 0)
 
 
-def halo_rows(radius: float) -> int:
+def halo_rows(radius: float, passes: int = 1) -> int:
     """Rows a spatial pass may read beyond a band: neighbor_offset rounds
-    rr*sin(th) with rr < radius (pipeline.hpp:232-239), so |dy| <= ceil(radius)."""
+    rr*sin(th) with rr < radius (pipeline.hpp:232-239), so |dy| <= ceil(radius).
+    No spatial passes -> no halo."""
+    if passes <= 0:
+        return 0
     return int(math.ceil(max(0.0, radius)))
 
 
@@ -36,15 +47,78 @@ def barrier(group) -> None:
         dist.barrier(group=group)
 
 
+def _dev(group):
+    import torch
+    import torch.distributed as dist
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+
+
 def max_over_ranks(x: float, group) -> float:
     if group is None:
         return float(x)
     import torch
     import torch.distributed as dist
-    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_dev(group))
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+class HaloExchanger:
+    """Swaps halo rows with the upper (rank-1) and lower (rank+1) neighbour.
+
+    send_lo / recv_lo: this band's first rows / the rows above it (neighbour
+    rank-1); send_hi / recv_hi: the band's last rows / the rows below it
+    (rank+1).  Tensors are flat byte buffers (device memory owned by the
+    library on GPU, plain CPU tensors in the gloo tests)."""
+
+    def __init__(self, rank: int, world: int, group, send_lo, recv_lo, send_hi, recv_hi, stream=None):
+        self.rank, self.world, self.group = rank, world, group
+        self.send_lo, self.recv_lo, self.send_hi, self.recv_hi = send_lo, recv_lo, send_hi, recv_hi
+        self.stream = stream
+        self.calls = 0
+
+    def _ops(self):
+        import torch.distributed as dist
+        ops = []
+        if self.rank > 0 and self.send_lo is not None and self.send_lo.numel():
+            ops.append(dist.P2POp(dist.isend, self.send_lo, self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.recv_lo, self.rank - 1, self.group))
+        if self.rank < self.world - 1 and self.send_hi is not None and self.send_hi.numel():
+            ops.append(dist.P2POp(dist.isend, self.send_hi, self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.recv_hi, self.rank + 1, self.group))
+        return ops
+
+    def __call__(self, pass_: int = 0) -> None:
+        import torch
+        import torch.distributed as dist
+        ops = self._ops()
+        self.calls += 1
+        if not ops:
+            return
+        if self.stream is not None:
+            # NCCL waits on the session stream (the pack kernels) and the
+            # session stream waits on NCCL (the unpack kernels follow)
+            with torch.cuda.stream(self.stream):
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+        else:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+
+class _DevBytes:
+    """__cuda_array_interface__ view of a device allocation owned by the library."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap(ptr: int, nbytes: int, device):
+    import torch
+    if not ptr or not nbytes:
+        return None
+    return torch.as_tensor(_DevBytes(ptr, nbytes), device=device)
 
 
 class BandSession:
@@ -52,50 +126,90 @@ class BandSession:
 
     def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None):
         import torch
-        if world != 1:
-            raise NotImplementedError("row-band sessions for world > 1 are not built yet")
         self.r = renderer
         self.cfg = cfg
         self.rank, self.world, self.group = rank, world, group
-        self.sess = renderer.session(scene_def, cfg)
+        H = scene_def.camera.height
+        self.y0, self.y1 = band_rows(H, world, rank)
+        halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if world > 1 else 0
+        if world > 1 and min(band_rows(H, world, g)[1] - band_rows(H, world, g)[0] for g in range(world)) < halo:
+            raise ValueError(f"{world} bands of a {H}-row image are thinner than the {halo}-row halo")
+        self.sess = renderer.session(scene_def, cfg, band=(self.y0, self.y1, halo))
         self.W, self.H = self.sess.width, self.sess.height
-        self.y0, self.y1 = band_rows(self.H, world, rank)
         self.stream = torch.cuda.ExternalStream(self.sess.stream_ptr())
+        self.exchanger = None
+        if world > 1:
+            hb = self.sess.halo_buffers()
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self.exchanger = HaloExchanger(rank, world, group, _wrap(hb["send_lo"], hb["bytes_lo"], dev),
+                                           _wrap(hb["recv_lo"], hb["bytes_lo"], dev),
+                                           _wrap(hb["send_hi"], hb["bytes_hi"], dev),
+                                           _wrap(hb["recv_hi"], hb["bytes_hi"], dev), stream=self.stream)
+            self.sess.set_halo_exchange(self.exchanger)
         self._pinned = None
 
     def owned_pixels(self) -> int:
         return (self.y1 - self.y0) * self.W
 
-    def step(self) -> dict:
-        return self.sess.step()
+    def step(self, stats: bool = False):
+        return self.sess.step(stats=stats)
 
     def sync(self) -> None:
         self.sess.sync()
 
     def timed_steps(self, k: int, stage_tot: list) -> float:
-        """Device time (ms) of k frames: CUDA events on the session stream."""
+        """Device time (ms) of k frames: CUDA events on the session stream
+        around k asynchronous steps; adds the per-stage event sums to stage_tot."""
         import torch
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         self.sync()
+        self.sess.stage_totals(reset=True)
         start.record(self.stream)
         for _ in range(k):
-            self.sess.step()
-            _, st = self.sess.last_ms()
-            for i in range(6):
-                stage_tot[i] += st[i]
+            self.sess.step(stats=False)
         end.record(self.stream)
         end.synchronize()
+        ms, _, _ = self.sess.stage_totals(reset=True)
+        for i in range(6):
+            stage_tot[i] += ms[i]
         return start.elapsed_time(end)
 
     def read_image_host(self) -> np.ndarray:
+        """This band's image into pinned host memory (waits for the frame)."""
         import torch
         if self._pinned is None:
-            self._pinned = torch.empty((self.H, self.W, 3), dtype=torch.float64, pin_memory=True).numpy()
+            self._pinned = torch.empty((self.y1 - self.y0, self.W, 3), dtype=torch.float64,
+                                       pin_memory=True).numpy()
         return self.sess.read_image(self._pinned)
+
+    def gather_image(self) -> np.ndarray | None:
+        """Full image on rank 0 (None elsewhere): all_gather of the bands."""
+        import torch
+        import torch.distributed as dist
+        band = torch.from_numpy(self.sess.read_image().copy())
+        if self.world == 1:
+            return band.numpy()
+        dev = _dev(self.group)
+        hmax = max(band_rows(self.H, self.world, g)[1] - band_rows(self.H, self.world, g)[0]
+                   for g in range(self.world))
+        pad = torch.zeros((hmax, self.W, 3), dtype=torch.float64, device=dev)
+        pad[: band.shape[0]] = band.to(dev)
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(parts, pad, group=self.group)
+        if self.rank != 0:
+            return None
+        rows = [parts[g][: band_rows(self.H, self.world, g)[1] - band_rows(self.H, self.world, g)[0]]
+                for g in range(self.world)]
+        return torch.cat(rows).cpu().numpy()
 
     def io_bytes(self):
         return self.sess.io_bytes()
 
     def halo_launches(self, steps: int) -> int:
-        return 0
+        """pack + unpack launches per exchange (one per non-empty side)."""
+        if self.exchanger is None:
+            return 0
+        sides = int(self.rank > 0) + int(self.rank < self.world - 1)
+        per_frame = self.cfg.spatial_passes
+        return steps * per_frame * 2 * sides

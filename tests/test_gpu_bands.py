@@ -1,0 +1,103 @@
+"""Row-band sessions on one GPU: n band sessions (one context / stream each,
+driven from n threads, halo rows moved by device copies inside the library's
+exchange callback) must reproduce the full-frame session bit for bit -- the
+device analogue of the reference's worker-count determinism test
+(test_pipeline.cpp:80-106).  The multi-process NCCL transport is the same
+callback with isend/irecv (parallel.HaloExchanger, covered with gloo in
+test_multirank.py)."""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2605_11536_b200 import _ffi as F
+from paper_2605_11536_b200 import scenes
+from paper_2605_11536_b200.api import GateSpec, RenderConfig, Renderer
+from paper_2605_11536_b200.parallel import _wrap, band_rows, halo_rows
+
+pytestmark = pytest.mark.gpu
+
+
+def _moving_camera(res):
+    sd = scenes.bundled("cornell_wide", res)
+    base = sd.camera.base
+    sd.camera.track = [(0.0, scenes.CameraPose((0.0, 0.0, 3.0), base.forward, base.up)),
+                       (10.0, scenes.CameraPose((0.0, 0.02, 3.0), base.forward, base.up))]
+    return sd
+
+
+CASES = {
+    "cornell_c1": (lambda: scenes.bundled("cornell", 48),
+                   RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=2, temporal=True,
+                                spatial_passes=2, spatial_neighbors=3, spatial_radius=5, frames=3)),
+    "doppler_animated": (lambda: scenes.bundled("boxes_doppler", 40),
+                         RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True,
+                                      spatial_passes=1, spatial_neighbors=4, spatial_radius=6, frames=3)),
+    "moving_camera": (lambda: _moving_camera(40),
+                      RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1, temporal=True,
+                                   spatial_passes=1, spatial_neighbors=3, spatial_radius=4, frames=3)),
+}
+
+
+def _render_bands(sd, cfg, world):
+    import torch
+    H = sd.camera.height
+    halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes)
+    rs = [Renderer(0) for _ in range(world)]
+    ss = [rs[g].session(sd, cfg, band=(*band_rows(H, world, g), halo)) for g in range(world)]
+    dev = torch.device("cuda", 0)
+    bufs = []
+    for s in ss:
+        hb = s.halo_buffers()
+        bufs.append({k: _wrap(hb[k], hb["bytes_lo" if k.endswith("lo") else "bytes_hi"], dev)
+                     for k in ("send_lo", "recv_lo", "send_hi", "recv_hi")})
+    bar = threading.Barrier(world)
+
+    def make_cb(g):
+        def cb(pass_):
+            ss[g].sync_stream()
+            bar.wait()  # every band has packed its edge rows
+            if g > 0 and bufs[g]["recv_lo"] is not None:
+                bufs[g]["recv_lo"].copy_(bufs[g - 1]["send_hi"])
+            if g < world - 1 and bufs[g]["recv_hi"] is not None:
+                bufs[g]["recv_hi"].copy_(bufs[g + 1]["send_lo"])
+            torch.cuda.synchronize()
+            bar.wait()  # nobody repacks before every copy landed
+        return cb
+
+    for g, s in enumerate(ss):
+        s.set_halo_exchange(make_cb(g))
+    errs = []
+
+    def run(g):
+        try:
+            for _ in range(cfg.frames):
+                ss[g].step(stats=False)
+            ss[g].sync()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+            bar.abort()
+
+    ts = [threading.Thread(target=run, args=(g,)) for g in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    return np.concatenate([s.read_image() for s in ss])
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("world", [2, 3])
+def test_bands_equal_full_frame(name, world):
+    build, cfg = CASES[name]
+    sd = build()
+    full = Renderer(0).session(sd, cfg)
+    for _ in range(cfg.frames):
+        full.step(stats=False)
+    ref = full.read_image()
+    got = _render_bands(sd, cfg, world)
+    assert ref.max() > 0
+    assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"

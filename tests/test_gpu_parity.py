@@ -118,3 +118,20 @@ def test_traversal_bitexact(renderer, ref, scene_name, frame):
     _, occ = renderer.probe_rays(sd, frame, seg, 1)
     _, rocc = ref.probe_rays(ref.RefScene(sd), frame, seg, 1)
     assert np.array_equal(occ, rocc)
+
+
+def test_cpp_shim_drop_in():
+    """include/tofr_gpu.hpp: a C++ program using the reference's own SceneDef /
+    RenderConfig / RenderOutput renders through the GPU and through the
+    reference CPU renderer in one process and compares (tools/shim_check.cpp)."""
+    import json
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "shim_check"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/shim_check not built (needs /root/reference at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.returncode == 0, res
+    assert res["gated_within"] >= 0.999 and res["plain_count_diff"] == 0
