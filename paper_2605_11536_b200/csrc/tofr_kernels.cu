@@ -60,22 +60,29 @@ size_t frame_smem_bytes(const FrameView& F) {
 }
 
 // ---------------------------------------------------------------------------
-// shift counters: per-thread u32, warp-reduced, one u64 atomic per warp
+// shift counters: per-thread u32, summed in shared memory, one u64 atomic per
+// counter and CTA (every thread of the CTA must reach the call)
 
-__device__ __forceinline__ void flush_ctr(const uint32_t* c, unsigned long long* out) {
-    if (!out) return;
-#pragma unroll
-    for (int k = 0; k < SC_COUNT; ++k) {
-        unsigned long long v = c[k];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[k], v);
-    }
+__device__ __noinline__ void flush_ctr(const uint32_t* c, unsigned long long* out) {
+    __shared__ unsigned int sc[SC_COUNT];
+    if (threadIdx.x < SC_COUNT) sc[threadIdx.x] = 0;
+    __syncthreads();
+    if (out)
+        for (int k = 0; k < SC_COUNT; ++k)
+            if (c[k]) atomicAdd(&sc[k], c[k]);
+    __syncthreads();
+    if (out && threadIdx.x < SC_COUNT && sc[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
 // work-ordering helpers (see k_cost_*)
 
 constexpr int kCostBuckets = 8;
+
+__device__ __forceinline__ bool nonempty(const ResStore& s, size_t i) {
+    double2 c0 = ld2(s, 0, i);
+    return ld_meta(s, i).has && c0.x > 0;
+}
 
 __device__ __forceinline__ bool shiftable(const ResStore& s, size_t i) {
     double2 c0 = ld2(s, 0, i);
@@ -534,8 +541,10 @@ __global__ void k_spatial_fwd_list(FrameView F, Band bd, PathCfg cfg, GateGrid g
         for (int j = 0; j < sp.neighbors; ++j) {
             int nx, ny;
             size_t si = 0;
+            // every non-empty neighbour is a forward shift attempt (counted even
+            // when its record has no reconnection vertex, as the reference does)
             bool want = live && spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
-                        shiftable(src_grid, si);
+                        nonempty(src_grid, si);
             unsigned m = __ballot_sync(0xffffffffu, want);
             if (!m) continue;
             uint32_t start = 0;
