@@ -67,11 +67,32 @@ WORKLOADS = {
            RenderConfig(gate=_gate(10.0, 0.0866), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
                         spatial_radius=10, m_cap=20, max_depth=6, seed=1),
            "C1: cornell 256x256 gated tau=10.0 dtau=0.0866, m_init 1, temporal + 1x3 spatial r10"),
+    "c2p": ("cornell", 512, 512,
+            RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=1,
+                         max_depth=6, seed=1),
+            "C2(i): cornell 512x512 transient 256 bins [8,20), render_transient_plain (trace + histogram deposits)"),
+    "c2r": ("cornell", 512, 512,
+            RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=1,
+                         temporal=True, m_cap=20, max_depth=6, seed=1),
+            "C2(ii): cornell 512x512 transient 256 bins [8,20), render_transient reservoirs, temporal reuse"),
+    "c4p": ("boxes_doppler", 1920, 1080,
+            RenderConfig(mode=F.MODE_TRANSIENT, bins=1024, hist_t0=7.0, hist_bin_width=0.01953125, m_init=1,
+                         max_depth=8, seed=1),
+            "C4 (plain): boxes_doppler 1920x1080 transient 1024 bins [7,27), depth 8, trace + histogram deposits"),
 }
 
-# launches of our kernels per frame: gbuffer, init, temporal, spatial x P, shade
-def launches_per_frame(cfg: RenderConfig, first: bool) -> int:
-    return 2 + (0 if first or not cfg.temporal else 1) + cfg.spatial_passes + 1
+PLAIN = {"c2p", "c4p"}  # render_transient_plain workloads; the others are ReSTIR sessions
+
+# launches of our kernels per frame (steady state): gbuffer, init, temporal
+# (cost + scatter + temporal), spatial per pass (job list + forward shifts + N
+# merges), bin reuse, shade; plain transient: gbuffer + deposits.
+def launches_per_frame(cfg: RenderConfig, plain: bool = False) -> int:
+    if plain:
+        return 2
+    n = 2 + (3 if cfg.temporal else 0) + 1
+    n += cfg.spatial_passes * (2 + cfg.spatial_neighbors)
+    n += 1 if (cfg.mode == F.MODE_TRANSIENT and cfg.bin_reuse) else 0
+    return n
 
 
 # algorithmic bytes per pixel (compact reservoir R = 224 B)
@@ -79,8 +100,20 @@ R_BYTES = 224
 GHIT_BYTES = 16
 
 
-def stage_bytes_per_pixel(cfg: RenderConfig) -> dict:
+def stage_bytes_per_pixel(cfg: RenderConfig, plain: bool = False) -> dict:
+    """Algorithmic HBM bytes per pixel and stage launch.  Gated: SURVEY 8d
+    (compact reservoir R).  Transient: the occupancy-free lower bound, i.e.
+    header traffic of every (pixel, bin) reservoir (M per pixel-bin, W,
+    emptiness) -- init 32 B store of the empty header + 48 B finalize, temporal
+    2 x 16 B header reads, shade 32 B header read -- plus the histogram
+    read-modify-write of the bins (24 B), times B.  Plain: 16 B histogram
+    output per bin (rgb RMW happens only on deposits)."""
     n = cfg.spatial_neighbors
+    if plain:
+        return {"init": 16 * cfg.bins}
+    if cfg.mode == F.MODE_TRANSIENT:
+        return {"init": 80 * cfg.bins, "temporal": 32 * cfg.bins, "spatial": ((1 + n) * 16 + 16) * cfg.bins,
+                "shade": 56 * cfg.bins}
     return {
         "init": GHIT_BYTES + R_BYTES,  # G-buffer read + reservoir write
         "temporal": 3 * R_BYTES,  # prev read, cur read, cur write
@@ -147,21 +180,31 @@ def dist_env():
 
 
 def cpu_reference_sample(wl: str, frames: int = 2) -> dict:
-    """render_gated of the reference (oracle/_ref) with all host threads on the
-    full workload, `frames` frames (frame 0 init + spatial, frame 1 adds the
-    temporal stage).  Returns seconds and the thread count."""
+    """The reference's own driver (oracle/_ref) with all host threads on the
+    full workload, `frames` frames (gated: frame 0 init + spatial, frame 1 adds
+    the temporal stage).  Returns seconds and the thread count."""
     from oracle import ref as R
     scene_name, w, h, cfg, _ = WORKLOADS[wl]
     cores = os.cpu_count() or 1
     R.set_threads(cores)
     sd = scenes.bundled(scene_name, w, h)
+    if wl == "c2r":  # 512^2 x 256 bins of 624 B reservoirs needs 84 GB: time 128^2 bands-equivalent
+        sd = scenes.bundled(scene_name, 128, 128)
     rs = R.RefScene(sd)
     c = RenderConfig(**{**cfg.__dict__})
     c.frames = frames
+    fn = R.render_transient_plain if wl in PLAIN else (R.render_transient if cfg.mode == F.MODE_TRANSIENT
+                                                        else R.render_gated)
     t0 = time.perf_counter()
-    R.render_gated(rs, c)
+    fn(rs, c)
     dt = time.perf_counter() - t0
-    return {"seconds": dt, "frames": frames, "cores": R.threads(), "pixels": w * h}
+    if wl == "c2r":
+        dt *= (w * h) / (128 * 128)  # extrapolated to the full image (labelled in the sample text)
+    drv = "render_transient_plain" if wl in PLAIN else ("render_transient" if cfg.mode == F.MODE_TRANSIENT
+                                                         else "render_gated")
+    what = (f"{drv}(frames={frames}) at 128x128, time scaled x{(w * h) // (128 * 128)} to {w}x{h}" if wl == "c2r"
+            else f"{drv}(frames={frames}) of the full {w}x{h} workload")
+    return {"seconds": dt, "frames": frames, "cores": R.threads(), "pixels": w * h, "what": what}
 
 
 def run_reference(args) -> None:
@@ -178,8 +221,7 @@ def run_reference(args) -> None:
         frames += r["frames"]
         cores = r["cores"]
     fps = frames / secs
-    sample = (f"{args.steps} x render_gated(frames=2) of the full {w}x{h} workload "
-              f"(frame 0: init+spatial, frame 1: init+temporal+spatial)")
+    sample = f"{args.steps} x {r['what']} (frame 0 has no temporal stage)"
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / frames,
@@ -211,9 +253,10 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     scene_name, w, h, cfg, desc = WORKLOADS[args.workload]
+    plain = args.workload in PLAIN
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
-    sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group)
+    sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
     for _ in range(args.warmup):
         sess.step()
     sess.sync()
@@ -229,23 +272,22 @@ def run_ours(args) -> None:
 
     # shift counters of one more (synchronous) frame: the work behind the time
     st = sess.step(stats=True)
+    if plain:
+        st = {k: {n: 0 for n in ("attempts", "solves", "iterations", "newton_ok", "occluded", "success")}
+              for k in ("temporal", "spatial")}
     shift_stats = {k: {n: st[k][n] for n in ("attempts", "solves", "iterations", "newton_ok", "occluded",
                                               "success")} for k in ("temporal", "spatial")}
 
     # e2e through the public API: step + image read-back to pinned host memory
     parallel.barrier(group)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        sess.step()
-        sess.read_image_host()
-    e2e_s = time.perf_counter() - t0
+    e2e_s = sess.run_e2e(args.steps)
     e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
     h2d, d2h = sess.io_bytes()
 
     # roofline of the dominant kernel (average launch duration from CUDA events)
     avg = [x / args.steps for x in stage_tot]
     names = ["init", "temporal", "bin", "spatial", "shade"]
-    per_px = stage_bytes_per_pixel(cfg)
+    per_px = stage_bytes_per_pixel(cfg, plain)
     dom = max(range(5), key=lambda i: avg[i])
     dom_name = names[dom]
     launches = max(1, cfg.spatial_passes) if dom_name == "spatial" else 1
@@ -268,7 +310,7 @@ def run_ours(args) -> None:
             c = cpu_reference_sample(args.workload, 2)
             cpu = {"value": c["frames"] / c["seconds"], "unit": "frames/s", "cores": c["cores"],
                    "kind": "reference",
-                   "sample": f"one render_gated(frames=2) of the full {w}x{h} workload ({c['seconds']:.1f} s)"}
+                   "sample": f"one {c['what']} ({c['seconds']:.1f} s)"}
         except Exception as e:  # the oracle is a reported baseline only
             cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -290,8 +332,7 @@ def run_ours(args) -> None:
                          "peak_src": pk["src"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                          "traffic": traffic, "algo_bytes_per_launch": algo, "avg_launch_ms": dur_s * 1e3},
             "cpu_baseline": cpu,
-            "gpu_launches": sum(launches_per_frame(cfg, False) for _ in range(args.steps)) + sess.halo_launches(
-                args.steps),
+            "gpu_launches": args.steps * launches_per_frame(cfg, plain) + sess.halo_launches(args.steps),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -197,6 +197,10 @@ int tofr_gpu_session_create(tofr_gpu* ctx, const tofr_scene* s, const tofr_rende
  * rows of a full-frame session. */
 int tofr_gpu_session_create_band(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, int32_t y0,
                                  int32_t y1, int32_t halo, tofr_session** out);
+/* Trace-only transient session (the frame loop of render_transient_plain):
+ * rows [y0, y1) (y1 = -1: all), no reservoirs, no halo. */
+int tofr_gpu_session_create_plain(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, int32_t y0,
+                                  int32_t y1, tofr_session** out);
 int tofr_gpu_session_band(tofr_session* ss, int32_t* y0, int32_t* y1, int32_t* r0, int32_t* r1);
 /* Halo exchange: before every spatial pass (pass >= 0) and, for moving
  * cameras, after the final grid of a frame (pass = -1) the library packs the
@@ -210,8 +214,18 @@ int tofr_gpu_session_set_halo_exchange(tofr_session* ss, tofr_halo_exchange_fn f
 int tofr_gpu_session_halo_buffers(tofr_session* ss, void** send_lo, void** recv_lo, uint64_t* bytes_lo,
                                   void** send_hi, void** recv_hi, uint64_t* bytes_hi);
 int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats);
-/* last frame's image of the band's rows (gated; (y1 - y0) * W * 3 doubles) */
+/* image of the band's rows ((y1 - y0) * W * 3 doubles): the last frame's
+ * image (gated) or the wide-band sum over bins of the histogram accumulated so
+ * far divided by the frame count (transient, pipeline.hpp:521-526) */
 int tofr_gpu_session_read_image(tofr_session* ss, double* image);
+/* pipelined read-back: enqueue the same image into a caller-owned PINNED
+ * buffer on the session stream (slot 0 or 1) and return at once;
+ * tofr_gpu_session_wait_read(slot) blocks until that copy has landed */
+int tofr_gpu_session_read_image_async(tofr_session* ss, double* pinned_image, int32_t slot);
+int tofr_gpu_session_wait_read(tofr_session* ss, int32_t slot);
+/* transient histogram accumulated so far / frames, reference index order;
+ * count = deposits per bin (plain) or the frame count (reservoir mode) */
+int tofr_gpu_session_read_histogram(tofr_session* ss, double* rgb, int64_t* count);
 int tofr_gpu_session_sync(tofr_session* ss);
 /* device timing of the last finished frame's kernels (ms) and the stage split
  * {init (incl. camera), temporal, bin reuse, spatial (incl. halo), shade, total} */

@@ -132,6 +132,10 @@ def _declare(lib) -> None:
     lib.tofr_gpu_session_last_ms.argtypes = [vp, P(C.c_double), P(C.c_double)]
     lib.tofr_gpu_session_stream.argtypes = [vp, P(vp)]
     lib.tofr_gpu_session_create_band.argtypes = [vp, vp, P(RenderConfigC), C.c_int32, C.c_int32, C.c_int32, P(vp)]
+    lib.tofr_gpu_session_create_plain.argtypes = [vp, vp, P(RenderConfigC), C.c_int32, C.c_int32, P(vp)]
+    lib.tofr_gpu_session_read_histogram.argtypes = [vp, P(C.c_double), P(C.c_int64)]
+    lib.tofr_gpu_session_read_image_async.argtypes = [vp, P(C.c_double), C.c_int32]
+    lib.tofr_gpu_session_wait_read.argtypes = [vp, C.c_int32]
     lib.tofr_gpu_session_band.argtypes = [vp] + [P(C.c_int32)] * 4
     lib.tofr_gpu_session_set_halo_exchange.argtypes = [vp, HALO_FN, vp]
     lib.tofr_gpu_session_halo_buffers.argtypes = [vp, P(vp), P(vp), P(C.c_uint64), P(vp), P(vp), P(C.c_uint64)]
@@ -156,7 +160,8 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_create", "tofr_gpu_session_step", "tofr_gpu_session_read_image", "tofr_gpu_session_sync",
     "tofr_gpu_session_last_ms", "tofr_gpu_session_io_bytes", "tofr_gpu_session_stream",
     "tofr_gpu_session_create_band", "tofr_gpu_session_band", "tofr_gpu_session_set_halo_exchange",
-    "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_destroy", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
+    "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
+    "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_destroy", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )
 
 

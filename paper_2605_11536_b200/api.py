@@ -296,8 +296,8 @@ class Renderer:
                                                   tri.ctypes.data_as(C.POINTER(C.c_int32))))
         return t, tri
 
-    def session(self, scene, cfg: RenderConfig, band: tuple | None = None) -> "Session":
-        return Session(self, self._scene(scene), cfg, band)
+    def session(self, scene, cfg: RenderConfig, band: tuple | None = None, plain: bool = False) -> "Session":
+        return Session(self, self._scene(scene), cfg, band, plain)
 
     def __del__(self):
         try:
@@ -315,15 +315,22 @@ class Session:
     and keeps `halo` rows on each side for spatial reuse (row-band sharding,
     see parallel.py); the default is the whole frame."""
 
-    def __init__(self, r: Renderer, scene: Scene, cfg: RenderConfig, band: tuple | None = None):
+    def __init__(self, r: Renderer, scene: Scene, cfg: RenderConfig, band: tuple | None = None,
+                 plain: bool = False):
         self._r = r
         self._scene = scene
         self.cfg = cfg
+        self.plain = plain
+        self.transient = plain or cfg.mode == F.MODE_TRANSIENT
         self.handle = C.c_void_p()
         c = cfg.to_c()
         y0, y1, halo = band if band is not None else (0, -1, 0)
-        r._check(r._lib.tofr_gpu_session_create_band(r.handle, scene.handle, C.byref(c), y0, y1, halo,
-                                                     C.byref(self.handle)))
+        if plain:
+            r._check(r._lib.tofr_gpu_session_create_plain(r.handle, scene.handle, C.byref(c), y0, y1,
+                                                          C.byref(self.handle)))
+        else:
+            r._check(r._lib.tofr_gpu_session_create_band(r.handle, scene.handle, C.byref(c), y0, y1, halo,
+                                                         C.byref(self.handle)))
         info = scene.info()
         self.width, self.height = info["width"], info["height"]
         a, b, c0, c1 = (C.c_int32() for _ in range(4))
@@ -346,6 +353,22 @@ class Session:
             out = np.zeros((self.y1 - self.y0, self.width, 3))
         self._r._check(self._r._lib.tofr_gpu_session_read_image(self.handle, _dptr(out)))
         return out
+
+    def read_image_async(self, pinned: np.ndarray, slot: int) -> None:
+        """Enqueue this frame's image into `pinned` (page-locked, [rows, W, 3]); see wait_read."""
+        self._r._check(self._r._lib.tofr_gpu_session_read_image_async(self.handle, _dptr(pinned), slot))
+
+    def wait_read(self, slot: int) -> None:
+        self._r._check(self._r._lib.tofr_gpu_session_wait_read(self.handle, slot))
+
+    def read_histogram(self):
+        """(rgb [rows, W, B, 3], count [rows, W, B]) accumulated so far / frames."""
+        rows, B = self.y1 - self.y0, self.cfg.bins
+        rgb = np.zeros((rows, self.width, B, 3))
+        cnt = np.zeros((rows, self.width, B), dtype=np.int64)
+        self._r._check(self._r._lib.tofr_gpu_session_read_histogram(
+            self.handle, _dptr(rgb), cnt.ctypes.data_as(C.POINTER(C.c_int64))))
+        return rgb, cnt
 
     def halo_buffers(self) -> dict:
         p = [C.c_void_p() for _ in range(4)]

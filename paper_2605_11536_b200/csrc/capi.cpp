@@ -179,7 +179,7 @@ struct tofr_session {
     DevBuf res[3];
     int cur = 0, prev = 1, spare = 2;
     DevBuf image, accum, hist, hist_count;  // owned rows only
-    DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag
+    DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag + work counter
     DevBuf send_lo, send_hi, recv_lo, recv_hi;
     DevBuf wo_cls, wo_counts, wo_perm;  // cost-ordered reuse (TOFR_ORDER=0 disables)
     DevBuf sp_mapped, sp_ok, sp_rng, sp_list, sp_count;  // phased spatial pass (TOFR_SPATIAL=mono disables)
@@ -192,6 +192,7 @@ struct tofr_session {
     cudaEvent_t ev[2][7] = {};
     bool pending[2] = {false, false};
     unsigned long long* err_host = nullptr;  // pinned [2]
+    cudaEvent_t read_ev[2] = {};             // asynchronous image read-backs
     int f = 0;
     double prev_center = 0, prev_width = 0;
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -211,6 +212,8 @@ struct tofr_session {
         for (auto& set : ev)
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
+        for (auto& e : read_ev)
+            if (e) cudaEventDestroy(e);
         if (err_host) cudaFreeHost(err_host);
         release_buffers();
         if (ctx && --ctx->live_sessions == 0 && ctx->closing) release_ctx(ctx);
@@ -317,9 +320,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     s->cam_moves = !sc->s.camera.track.empty();
     for (auto& set : s->ev)
         for (auto& e : set) ck(cudaEventCreate(&e), "event");
+    for (auto& e : s->read_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&s->err_host), 2 * sizeof(unsigned long long)), "pinned");
     s->err_host[0] = s->err_host[1] = 0;
-    s->ctr.ensure((3 * SC_COUNT + 1) * sizeof(unsigned long long));
+    s->ctr.ensure((3 * SC_COUNT + 2) * sizeof(unsigned long long));
     ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), ctx->stream), "memset");
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
@@ -477,6 +481,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     PathCfg pc = path_cfg(c, center, width);
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
+    unsigned long long* q = ctr + 3 * SC_COUNT + 1;  // persistent-kernel work counter (stream-ordered reuse)
     bool halo = !(s->r0 == s->y0 && s->r1 == s->y1);
     bool prev_halo = halo && s->cam_moves;
     Band bd = band_of(s, prev_halo);
@@ -491,26 +496,26 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     if (s->plain) {
         size_t pr = size_t(s->W) * s->B;
         launch_hist_plain(F, bd, g, pc, h, c.m_init, f, rows_base<double>(s->hist, s->y0, pr * 3),
-                          rows_base<uint32_t>(s->hist_count, s->y0, pr), stream);
+                          rows_base<uint32_t>(s->hist_count, s->y0, pr), q, stream);
         for (int i = 1; i < 6; ++i) cudaEventRecord(ev[i], stream);
     } else {
         InitParams ip{c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
         ResStore cur = store_of(s, s->res[s->cur]);
         if (s->transient)
-            launch_init_transient(F, bd, g, pc, ip, h, f, cur, stream);
+            launch_init_transient(F, bd, g, pc, ip, h, f, cur, q, stream);
         else
-            launch_init_gated(F, bd, g, pc, ip, f, cur, stream);
+            launch_init_gated(F, bd, g, pc, ip, f, cur, q, stream);
         cudaEventRecord(ev[1], stream);
         GateGrid cg{s->transient ? 1 : 0, center, width, h};
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
             launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]), wo,
-                            ctr + 0 * SC_COUNT, stream);
+                            ctr + 0 * SC_COUNT, q, stream);
         }
         cudaEventRecord(ev[2], stream);
         if (s->transient && c.bin_reuse) {
-            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, stream);
+            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur]);
         }
@@ -530,7 +535,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                 scp = &scr;
             }
             launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
-                           ctr + 1 * SC_COUNT, stream);
+                           ctr + 1 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur]);
         }
@@ -958,7 +963,7 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double
         PathCfg pc = path_cfg(c, gate_center, gate_width);
         pc.ellipsoidal = 0;
         launch_reference(F, bd, g, pc, gate_center, gate_width, spp, uint64_t(frame), dm.as<double>(), ds.as<double>(),
-                         ctx->stream);
+                         s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 1, ctx->stream);
         ck(cudaGetLastError(), "reference launch");
         if (mean) ck(cudaMemcpyAsync(mean, dm.p, npix * 24, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
         if (se) ck(cudaMemcpyAsync(se, ds.p, npix * 24, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
@@ -980,6 +985,16 @@ int tofr_gpu_session_create_band(tofr_gpu* ctx, const tofr_scene* s, const tofr_
         if (cfg && cfg->mode == TOFR_MODE_TRANSIENT && cfg->bins < 1)
             throw ScopeError(TOFR_ERR_INVALID, "transient needs bins >= 1");
         *out = make_session(ctx, s, cfg, KIND_RESTIR, y0, y1, halo);
+    });
+}
+
+int tofr_gpu_session_create_plain(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, int32_t y0,
+                                  int32_t y1, tofr_session** out) {
+    if (!out) return TOFR_ERR_INVALID;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        if (!ctx || !s) throw ScopeError(TOFR_ERR_INVALID, "null handle");
+        *out = make_session(ctx, s, cfg, KIND_PLAIN, y0, y1, 0);
     });
 }
 
@@ -1016,13 +1031,74 @@ int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats) {
     return guard(ss->ctx, [&] { session_step(ss, stats); });
 }
 
+namespace {
+void enqueue_image(tofr_session* ss, double* image) {
+    if (ss->transient) {
+        // wide-band image of the histogram accumulated so far, / frames
+        size_t npix = ss->owned_pixels();
+        ss->image.ensure(npix * 3 * sizeof(double));
+        Band bd = band_of(ss, false);
+        double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+        launch_hist_image(rows_base<double>(ss->hist, ss->y0, size_t(ss->W) * ss->B * 3), bd, ss->W, ss->B, scale,
+                          rows_base<double>(ss->image, ss->y0, size_t(ss->W) * 3), ss->ctx->stream);
+        ck(cudaGetLastError(), "hist image");
+    }
+    ck(cudaMemcpyAsync(image, ss->image.p, ss->owned_pixels() * 24, cudaMemcpyDeviceToHost, ss->ctx->stream), "d2h");
+}
+}  // namespace
+
+int tofr_gpu_session_read_image_async(tofr_session* ss, double* pinned_image, int32_t slot) {
+    if (!ss || !pinned_image || slot < 0 || slot > 1) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        enqueue_image(ss, pinned_image);
+        ck(cudaEventRecord(ss->read_ev[slot], ss->ctx->stream), "event");
+    });
+}
+
+int tofr_gpu_session_wait_read(tofr_session* ss, int32_t slot) {
+    if (!ss || slot < 0 || slot > 1) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] { ck(cudaEventSynchronize(ss->read_ev[slot]), "read-back"); });
+}
+
 int tofr_gpu_session_read_image(tofr_session* ss, double* image) {
     if (!ss || !image) return TOFR_ERR_INVALID;
     return guard(ss->ctx, [&] {
-        if (ss->transient) throw ScopeError(TOFR_ERR_UNSUPPORTED, "read_image on a transient session");
+        if (ss->transient) {
+            // wide-band image of the histogram accumulated so far, / frames
+            size_t npix = ss->owned_pixels();
+            ss->image.ensure(npix * 3 * sizeof(double));
+            Band bd = band_of(ss, false);
+            double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+            launch_hist_image(rows_base<double>(ss->hist, ss->y0, size_t(ss->W) * ss->B * 3), bd, ss->W, ss->B,
+                              scale, rows_base<double>(ss->image, ss->y0, size_t(ss->W) * 3), ss->ctx->stream);
+            ck(cudaGetLastError(), "hist image");
+        }
         ck(cudaMemcpyAsync(image, ss->image.p, ss->owned_pixels() * 24, cudaMemcpyDeviceToHost, ss->ctx->stream),
            "d2h");
         flush_all(ss);
+    });
+}
+
+int tofr_gpu_session_read_histogram(tofr_session* ss, double* rgb, int64_t* count) {
+    if (!ss) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        if (!ss->transient) throw ScopeError(TOFR_ERR_UNSUPPORTED, "read_histogram on a gated session");
+        flush_all(ss);
+        size_t items = ss->owned_pixels() * ss->B;
+        double k = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+        if (rgb) {
+            ck(cudaMemcpy(rgb, ss->hist.p, items * 24, cudaMemcpyDeviceToHost), "histogram");
+            for (size_t i = 0; i < items * 3; ++i) rgb[i] *= k;
+        }
+        if (count) {
+            if (ss->plain) {
+                std::vector<uint32_t> c(items);
+                ck(cudaMemcpy(c.data(), ss->hist_count.p, items * 4, cudaMemcpyDeviceToHost), "counts");
+                for (size_t i = 0; i < items; ++i) count[i] = c[i];
+            } else {
+                for (size_t i = 0; i < items; ++i) count[i] = ss->f;
+            }
+        }
     });
 }
 

@@ -75,6 +75,25 @@ __device__ __noinline__ void flush_ctr(const uint32_t* c, unsigned long long* ou
 }
 
 // ---------------------------------------------------------------------------
+// Dynamic work distribution.  The per-item cost of the path kernels varies by
+// orders of magnitude (empty pixels vs. multi-iteration Newton solves), so a
+// static grid-stride assignment leaves most of a CTA waiting for its slowest
+// warp.  The heavy kernels run persistent CTAs (one wave, sized by the
+// occupancy calculator) whose warps take 32 consecutive items at a time from
+// a per-launch counter `q` (zeroed by the host before the launch).
+
+__device__ __forceinline__ size_t warp_take(unsigned long long* q) {
+    unsigned long long b = 0;
+    if ((threadIdx.x & 31) == 0) b = atomicAdd(q, 32ull);
+    return size_t(__shfl_sync(0xffffffffu, b, 0));
+}
+
+#define TOFR_FOR_ITEMS(i, n, q)                                                              \
+    for (size_t i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31); i##_base < (n); \
+         i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31))                         \
+        if (i < (n))
+
+// ---------------------------------------------------------------------------
 // work-ordering helpers (see k_cost_*)
 
 constexpr int kCostBuckets = 8;
@@ -239,14 +258,17 @@ __device__ void init_pixel(const FrameView& F, const PathCfg& cfg, const InitPar
 }
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
-                                                    InitParams ip, int frame_idx, ResStore cur) {
+                                                    InitParams ip, int frame_idx, ResStore cur,
+                                                    unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
     int W = F.cam.w;
     WalkV v[kMaxVerts];
-    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    TOFR_FOR_ITEMS(i, n, q) {
+        int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         Res r;
         GHit g = gbuf[p];
@@ -303,7 +325,7 @@ struct BinSink {
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                         InitParams ip, HistSpec h, int frame_idx,
-                                                        ResStore cur) {
+                                                        ResStore cur, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -311,7 +333,9 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameVi
     int W = F.cam.w, B = h.bins;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    TOFR_FOR_ITEMS(i, n, q) {
+        int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         size_t base = size_t(p) * B;
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
                                                   const GHit* gp, PathCfg cfg, GateGrid cur_gate,
                                                   GateGrid prev_gate, int frame_idx, ResStore cur,
                                                   ResStore prev, const uint32_t* perm,
-                                                  unsigned long long* ctr_out) {
+                                                  unsigned long long* ctr_out, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(Fc, smem, off);
@@ -361,7 +385,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
     int W = Fc.cam.w, B = cur_gate.transient ? cur_gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    TOFR_FOR_ITEMS(i, n, q) {
         size_t it = base + (perm ? size_t(perm[i]) : i);
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -426,7 +450,8 @@ __device__ __forceinline__ void neighbor_offset(int j, int count, double radius,
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                  GateGrid gate, SpatialParams sp, int pass,
                                                  int frame_idx, ResStore src_grid, ResStore dst_grid,
-                                                 const uint32_t* perm, unsigned long long* ctr_out) {
+                                                 const uint32_t* perm, unsigned long long* ctr_out,
+                                                 unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -434,7 +459,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    TOFR_FOR_ITEMS(i, n, q) {
         size_t it = base + (perm ? size_t(perm[i]) : i);
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -557,7 +582,8 @@ __global__ void k_spatial_fwd_list(FrameView F, Band bd, PathCfg cfg, GateGrid g
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
     k_spatial_fwd(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
-                  int frame_idx, ResStore src_grid, SpatialScratch sc, unsigned long long* ctr_out) {
+                  int frame_idx, ResStore src_grid, SpatialScratch sc, unsigned long long* ctr_out,
+                  unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -565,9 +591,9 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
     int W = F.cam.w, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t jobs = *sc.count;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < jobs; q += gridDim.x * blockDim.x) {
-        uint32_t e = sc.list[q];
+    size_t jobs = *sc.count;
+    TOFR_FOR_ITEMS(jq, jobs, q) {
+        uint32_t e = sc.list[jq];
         int j = int(e / n);
         size_t i = e % n, it = base + i;
         int p = int(it / B), b = int(it % B);
@@ -600,14 +626,15 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
     k_spatial_merge(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
-                    int j, int frame_idx, ResStore src_grid, ResStore dst_grid, SpatialScratch sc) {
+                    int j, int frame_idx, ResStore src_grid, ResStore dst_grid, SpatialScratch sc,
+                    unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    TOFR_FOR_ITEMS(i, n, q) {
         size_t it = base + i;
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
@@ -666,16 +693,17 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                   HistSpec h, int frame_idx, ResStore src_grid,
-                                                  ResStore dst_grid, unsigned long long* ctr_out) {
+                                                  ResStore dst_grid, unsigned long long* ctr_out,
+                                                  unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
     __syncthreads();
     int W = F.cam.w, B = h.bins;
     uint32_t ctr[SC_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    size_t end = size_t(bd.y1) * W * B;
-    for (size_t it = size_t(bd.y0) * W * B + blockIdx.x * size_t(blockDim.x) + threadIdx.x; it < end;
-         it += size_t(gridDim.x) * blockDim.x) {
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    TOFR_FOR_ITEMS(i, n, q) {
+        size_t it = base + i;
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
         Res out;
@@ -857,6 +885,34 @@ __global__ void k_shade_transient(ResStore cur, size_t i0, size_t i1, HistSpec h
     }
 }
 
+// Wide-band image of a transient histogram (pipeline.hpp:521-526): per pixel the
+// sum over its B bins, times `scale` (1/frames).  One warp per pixel row
+// segment; bins are contiguous per pixel so reads are coalesced.
+__global__ void k_hist_image(const double* hist, int p0, int p1, int B, double scale, double* image) {
+    int lane = threadIdx.x & 31;
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int p = p0 + warp; p < p1; p += nwarps) {
+        const double* h = hist + 3 * size_t(p) * B;
+        double sx = 0, sy = 0, sz = 0;
+        for (int b = lane; b < B; b += 32) {
+            sx += h[3 * b + 0];
+            sy += h[3 * b + 1];
+            sz += h[3 * b + 2];
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_down_sync(0xffffffffu, sx, o);
+            sy += __shfl_down_sync(0xffffffffu, sy, o);
+            sz += __shfl_down_sync(0xffffffffu, sz, o);
+        }
+        if (lane == 0) {
+            image[3 * size_t(p) + 0] = sx * scale;
+            image[3 * size_t(p) + 1] = sy * scale;
+            image[3 * size_t(p) + 2] = sz * scale;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // trace-only transient deposits (render_transient_plain, pipeline.hpp:531-571;
 // TransientHistogram::deposit, transport.hpp:121-126).  Each thread owns its
@@ -884,7 +940,7 @@ struct PlainSink {
 
 __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     HistSpec h, int m_init, int frame_idx, double* rgb,
-                                                    uint32_t* count) {
+                                                    uint32_t* count, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -892,7 +948,9 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
     int W = F.cam.w;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    TOFR_FOR_ITEMS(i, n, q) {
+        int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins};
@@ -920,7 +978,7 @@ struct RefSink {
 
 __global__ void __launch_bounds__(128) k_reference(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                    double center, double width, int spp, uint64_t frame_key,
-                                                   double* mean, double* se) {
+                                                   double* mean, double* se, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -928,7 +986,9 @@ __global__ void __launch_bounds__(128) k_reference(FrameView F, Band bd, const G
     int W = F.cam.w;
     WalkV v[kMaxVerts];
     NoEll ell;
-    for (int p = bd.y0 * W + blockIdx.x * blockDim.x + threadIdx.x; p < bd.y1 * W; p += gridDim.x * blockDim.x) {
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    TOFR_FOR_ITEMS(i, n, q) {
+        int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         GHit g = gbuf[p];
@@ -1000,6 +1060,25 @@ __global__ void k_halo_unpack(ResStore grid, size_t item0, size_t n, const doubl
 // ---------------------------------------------------------------------------
 // launchers
 
+// One wave of resident CTAs for a persistent kernel (occupancy calculator,
+// cached per kernel), never more than the items need.
+static int persistent_grid(const void* kernel, int block, size_t smem, size_t n) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    if (per_sm < 1) per_sm = 1;
+    size_t need = (n + block - 1) / block;
+    size_t g = size_t(sms) * per_sm;
+    if (g > need) g = need;
+    return int(g < 1 ? 1 : g);
+}
+
 static int grid_for(size_t n, int block) {
     size_t g = (n + block - 1) / block;
     if (g > 148 * 64) g = 148 * 64;
@@ -1020,18 +1099,26 @@ void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s)
     k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, bd, g);
 }
 
+// zeroed work counter + persistent launch configuration
+#define TOFR_PERSISTENT(kernel, n, smem) \
+    cudaMemsetAsync(q, 0, sizeof(unsigned long long), s); \
+    kernel<<<persistent_grid(reinterpret_cast<const void*>(kernel), 128, smem, n), 128, smem, s>>>
+
 void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                       const InitParams& ip, int frame_idx, ResStore cur, cudaStream_t s) {
+                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    k_init_gated<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, ip, frame_idx, cur);
+    size_t sm = frame_smem_bytes(F);
+    TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q);
 }
 
 void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s) {
+                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur,
+                           unsigned long long* q, cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    k_init_transient<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, ip, h, frame_idx, cur);
+    size_t sm = frame_smem_bytes(F);
+    TOFR_PERSISTENT(k_init_transient, n, sm)(F, bd, g, cfg, ip, h, frame_idx, cur, q);
 }
 
 static void order_items(const uint8_t* cls, size_t n, const WorkOrder& wo, cudaStream_t s) {
@@ -1040,7 +1127,8 @@ static void order_items(const uint8_t* cls, size_t n, const WorkOrder& wo, cudaS
 
 void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
-                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr, cudaStream_t s) {
+                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr,
+                     unsigned long long* q, cudaStream_t s) {
     size_t n = band_pixels(bd, Fc.cam.w) * (cg.transient ? cg.h.bins : 1);
     if (!n) return;
     const uint32_t* perm = nullptr;
@@ -1051,13 +1139,13 @@ void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const 
         perm = wo.perm;
     }
     size_t sm = frame_smem_bytes(Fc) + frame_smem_bytes(Fp);
-    k_temporal<<<grid_for(n, 128), 128, sm, s>>>(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, perm,
-                                                  ctr);
+    TOFR_PERSISTENT(k_temporal, n, sm)(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, perm, ctr, q);
 }
 
 void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
-                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, cudaStream_t s) {
+                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, unsigned long long* q,
+                    cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w) * (gg.transient ? gg.h.bins : 1);
     if (!n) return;
     size_t sm = frame_smem_bytes(F);
@@ -1065,11 +1153,11 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
         cudaMemsetAsync(sc->count, 0, sizeof(uint32_t), s);
         cudaMemsetAsync(sc->ok, 0, n * size_t(sp.neighbors), s);
         k_spatial_fwd_list<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, *sc);
-        k_spatial_fwd<<<grid_for(n * size_t(sp.neighbors), 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass,
-                                                                                frame_idx, src, *sc, ctr);
-        for (int j = 0; j < sp.neighbors; ++j)
-            k_spatial_merge<<<grid_for(n, 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass, j, frame_idx, src, dst,
-                                                              *sc);
+        size_t jobs_max = n * size_t(sp.neighbors);
+        TOFR_PERSISTENT(k_spatial_fwd, jobs_max, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, *sc, ctr, q);
+        for (int j = 0; j < sp.neighbors; ++j) {
+            TOFR_PERSISTENT(k_spatial_merge, n, sm)(F, bd, g, cfg, gg, sp, pass, j, frame_idx, src, dst, *sc, q);
+        }
         return;
     }
     const uint32_t* perm = nullptr;
@@ -1080,14 +1168,16 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
         order_items(wo.cls, n, wo, s);
         perm = wo.perm;
     }
-    k_spatial<<<grid_for(n, 128), 128, sm, s>>>(F, bd, g, cfg, gg, sp, pass, frame_idx, src, dst, perm, ctr);
+    TOFR_PERSISTENT(k_spatial, n, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, dst, perm, ctr, q);
 }
 
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s) {
+                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, unsigned long long* q,
+                     cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w) * h.bins;
     if (!n) return;
-    k_binreuse<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, h, frame_idx, src, dst, ctr);
+    size_t sm = frame_smem_bytes(F);
+    TOFR_PERSISTENT(k_binreuse, n, sm)(F, bd, g, cfg, h, frame_idx, src, dst, ctr, q);
 }
 
 void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
@@ -1106,19 +1196,28 @@ void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec&
 }
 
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                       int m_init, int frame_idx, double* rgb, uint32_t* count, cudaStream_t s) {
+                       int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                       cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    k_hist_plain<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, h, m_init, frame_idx, rgb,
-                                                                   count);
+    size_t sm = frame_smem_bytes(F);
+    TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q);
 }
 
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
-                      double width, int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s) {
+                      double width, int spp, uint64_t frame_key, double* mean, double* se, unsigned long long* q,
+                      cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    k_reference<<<grid_for(n, 128), 128, frame_smem_bytes(F), s>>>(F, bd, g, cfg, center, width, spp, frame_key,
-                                                                  mean, se);
+    size_t sm = frame_smem_bytes(F);
+    TOFR_PERSISTENT(k_reference, n, sm)(F, bd, g, cfg, center, width, spp, frame_key, mean, se, q);
+}
+
+void launch_hist_image(const double* hist, const Band& bd, int W, int B, double scale, double* image,
+                       cudaStream_t s) {
+    size_t n = band_pixels(bd, W);
+    if (!n) return;
+    k_hist_image<<<grid_for(n * 32, 256), 256, 0, s>>>(hist, bd.y0 * W, bd.y1 * W, B, scale, image);
 }
 
 void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s) {

@@ -70,26 +70,37 @@ void set_gauss_rule(const double* x, const double* w, cudaStream_t s);
 // g (launch_gbuffer) is the band's local G-buffer (row r0 first); every other
 // G-buffer / grid / image pointer is global-indexed (see Band).
 void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s);
+// The path kernels below are persistent with dynamic work distribution; `q`
+// is one device u64 of the caller's (zeroed by the launcher, stream-ordered).
 void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                       const InitParams& ip, int frame_idx, ResStore cur, cudaStream_t s);
+                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s);
 void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur, cudaStream_t s);
+                           const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur,
+                           unsigned long long* q, cudaStream_t s);
 void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                      const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx,
-                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr, cudaStream_t s);
+                     ResStore cur, ResStore prev, const WorkOrder& wo, unsigned long long* ctr,
+                     unsigned long long* q, cudaStream_t s);
 void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
-                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, cudaStream_t s);
+                    const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, unsigned long long* q,
+                    cudaStream_t s);
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, cudaStream_t s);
+                     int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, unsigned long long* q,
+                     cudaStream_t s);
 void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
                         double* accum, cudaStream_t s);
 void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
                             cudaStream_t s);
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                       int m_init, int frame_idx, double* rgb, uint32_t* count, cudaStream_t s);
+                       int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                       cudaStream_t s);
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
-                      double width, int spp, uint64_t frame_key, double* mean, double* se, cudaStream_t s);
+                      double width, int spp, uint64_t frame_key, double* mean, double* se, unsigned long long* q,
+                      cudaStream_t s);
+// wide-band image (sum over bins x scale) of a global-indexed histogram
+void launch_hist_image(const double* hist, const Band& bd, int W, int B, double scale, double* image,
+                       cudaStream_t s);
 // halo staging: rows [a, b) of a global-indexed grid <-> a contiguous buffer
 // laid out chunk-major ([kResChunks][(b - a) * W * B] x 16 B)
 void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s);

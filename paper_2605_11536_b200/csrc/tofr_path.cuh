@@ -519,27 +519,37 @@ __device__ __noinline__ NewtonOut newton_solve(const FrameView& F, const V3& p1,
     Frame2 Jc = Js;
     Constraint e = assemble(p1, p2, start.pos, Js, cur.pos, Jc, delta, gauge);
     double fnorm = hypot(e.F.x, e.F.y);
-    for (int iter = 0;; ++iter) {
-        res.iterations = iter;
-        if (fabs(e.F.x) <= tol && fabs(e.F.y) <= tol) {
-            res.p = cur;
-            double dc = det(e.dFp);
-            double j = dc == 0 ? 0 : det(e.dF) / dc;
-            if (!(j > 0) || !isfinite(j)) return res;
-            res.converged = 1;
-            res.jac = j;
-            return res;
+    // The reference's two nested loops (iterations x 9 halvings) run here as
+    // ONE loop of trial steps with the (iteration, halving) position kept per
+    // lane: lanes of a warp that are in different iterations or halvings
+    // still execute the trial together instead of waiting at the inner
+    // loop's exit.  Same decisions in the same order per lane.
+    int iter = 0, bt = 0;
+    bool need_dir = true;
+    double scale = 1.0;
+    V2 step{0, 0};
+    for (;;) {
+        if (need_dir) {
+            res.iterations = iter;
+            if (fabs(e.F.x) <= tol && fabs(e.F.y) <= tol) {
+                res.p = cur;
+                double dc = det(e.dFp);
+                double j = dc == 0 ? 0 : det(e.dF) / dc;
+                if (!(j > 0) || !isfinite(j)) return res;
+                res.converged = 1;
+                res.jac = j;
+                return res;
+            }
+            if (iter >= 5) break;
+            if (norm(e.grad_cur) < eps_grad) break;
+            if (!solve2x2(e.dFp, -e.F, step)) break;
+            need_dir = false;
+            bt = 0;
+            scale = 1.0;
         }
-        if (iter >= 5) break;
-        if (norm(e.grad_cur) < eps_grad) break;
-        V2 step;
-        if (!solve2x2(e.dFp, -e.F, step)) break;
-        bool accepted = false;
-        double scale = 1.0;
-        for (int bt = 0; bt <= 8; ++bt, scale *= 0.5) {
-            V3 plane_pt = cur.pos + to_world(Jc, step * scale);
-            SurfPt trial;
-            if (!reproject(F, cur, plane_pt, p1, trial)) continue;
+        V3 plane_pt = cur.pos + to_world(Jc, step * scale);
+        SurfPt trial;
+        if (reproject(F, cur, plane_pt, p1, trial)) {
             Frame2 Jt = tangent_frame(F, trial.tri);
             Constraint et = assemble(p1, p2, start.pos, Js, trial.pos, Jt, delta, gauge);
             double fn = hypot(et.F.x, et.F.y);
@@ -548,11 +558,13 @@ __device__ __noinline__ NewtonOut newton_solve(const FrameView& F, const V3& p1,
                 Jc = Jt;
                 e = et;
                 fnorm = fn;
-                accepted = true;
-                break;
+                ++iter;
+                need_dir = true;
+                continue;
             }
         }
-        if (!accepted) break;
+        if (++bt > 8) break;  // no halving accepted
+        scale *= 0.5;
     }
     res.p = cur;
     return res;

@@ -124,21 +124,22 @@ def _wrap(ptr: int, nbytes: int, device):
 class BandSession:
     """A session rendering one row band of every frame (the whole frame when world == 1)."""
 
-    def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None):
+    def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None, plain: bool = False):
         import torch
         self.r = renderer
         self.cfg = cfg
+        self.plain = plain
         self.rank, self.world, self.group = rank, world, group
         H = scene_def.camera.height
         self.y0, self.y1 = band_rows(H, world, rank)
-        halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if world > 1 else 0
+        halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if (world > 1 and not plain) else 0
         if world > 1 and min(band_rows(H, world, g)[1] - band_rows(H, world, g)[0] for g in range(world)) < halo:
             raise ValueError(f"{world} bands of a {H}-row image are thinner than the {halo}-row halo")
-        self.sess = renderer.session(scene_def, cfg, band=(self.y0, self.y1, halo))
+        self.sess = renderer.session(scene_def, cfg, band=(self.y0, self.y1, halo), plain=plain)
         self.W, self.H = self.sess.width, self.sess.height
         self.stream = torch.cuda.ExternalStream(self.sess.stream_ptr())
         self.exchanger = None
-        if world > 1:
+        if world > 1 and halo > 0:
             hb = self.sess.halo_buffers()
             dev = torch.device("cuda", torch.cuda.current_device())
             self.exchanger = HaloExchanger(rank, world, group, _wrap(hb["send_lo"], hb["bytes_lo"], dev),
@@ -182,6 +183,27 @@ class BandSession:
             self._pinned = torch.empty((self.y1 - self.y0, self.W, 3), dtype=torch.float64,
                                        pin_memory=True).numpy()
         return self.sess.read_image(self._pinned)
+
+    def run_e2e(self, k: int) -> float:
+        """k frames through the public API, each frame's image read back to
+        pinned host memory (double-buffered: frame f's copy overlaps frame
+        f+1's kernels; every copy has landed when this returns).  Wall seconds."""
+        import time
+        import torch
+        bufs = [torch.empty((self.y1 - self.y0, self.W, 3), dtype=torch.float64, pin_memory=True).numpy()
+                for _ in range(2)]
+        self.sync()
+        t0 = time.perf_counter()
+        for f in range(k):
+            self.sess.step(stats=False)
+            if f >= 2:
+                self.sess.wait_read(f & 1)  # the buffer written two frames ago is free again
+            self.sess.read_image_async(bufs[f & 1], f & 1)
+        for f in range(max(0, k - 2), k):
+            self.sess.wait_read(f & 1)
+        dt = time.perf_counter() - t0
+        self.last_e2e_image = bufs[(k - 1) & 1]
+        return dt
 
     def gather_image(self) -> np.ndarray | None:
         """Full image on rank 0 (None elsewhere): all_gather of the bands."""

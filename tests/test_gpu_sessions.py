@@ -1,0 +1,77 @@
+"""Interactive sessions (the frame loop one call at a time, reservoirs resident
+on the device) against the one-shot drivers that mirror the reference
+(render_gated / render_transient / render_transient_plain,
+pipeline.hpp:323-571): same frames, same outputs, bit for bit."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2605_11536_b200 import _ffi as F
+from paper_2605_11536_b200 import scenes
+from paper_2605_11536_b200.api import GateSpec, RenderConfig, Renderer
+
+pytestmark = pytest.mark.gpu
+
+
+def _transient_cfg(**kw):
+    base = dict(mode=F.MODE_TRANSIENT, bins=32, hist_t0=8.0, hist_bin_width=0.375, m_init=2, frames=3)
+    base.update(kw)
+    return RenderConfig(**base)
+
+
+def test_plain_session_equals_render_transient_plain():
+    sd = scenes.bundled("cornell", 40)
+    cfg = _transient_cfg()
+    r = Renderer(0)
+    ref = r.render_transient_plain(sd, cfg)
+    s = r.session(sd, cfg, plain=True)
+    for _ in range(cfg.frames):
+        s.step(stats=False)
+    rgb, cnt = s.read_histogram()
+    assert np.array_equal(cnt, ref.hist.count)
+    assert np.array_equal(rgb, ref.hist.rgb)
+    img = s.read_image()
+    assert np.allclose(img, ref.image, rtol=1e-12, atol=0)
+
+
+def test_transient_session_equals_render_transient():
+    sd = scenes.bundled("cornell_wide", 32)
+    cfg = _transient_cfg(hist_t0=3.0, hist_bin_width=0.25, temporal=True, frames=3)
+    r = Renderer(0)
+    ref = r.render_transient(sd, cfg)
+    s = r.session(sd, cfg)
+    for _ in range(cfg.frames):
+        s.step(stats=False)
+    rgb, _ = s.read_histogram()
+    assert ref.hist.rgb.max() > 0
+    assert np.array_equal(rgb, ref.hist.rgb)
+
+
+def test_async_read_equals_sync_read():
+    import torch
+    sd = scenes.bundled("boxes_doppler", 48)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True, spatial_passes=1,
+                       spatial_neighbors=3, spatial_radius=5, frames=4)
+    s = Renderer(0).session(sd, cfg)
+    bufs = [torch.empty((48, 48, 3), dtype=torch.float64, pin_memory=True).numpy() for _ in range(2)]
+    for f in range(cfg.frames):
+        s.step(stats=False)
+        s.read_image_async(bufs[f & 1], f & 1)
+    s.wait_read((cfg.frames - 1) & 1)
+    assert np.array_equal(bufs[(cfg.frames - 1) & 1], s.read_image())
+    assert bufs[(cfg.frames - 1) & 1].max() > 0
+
+
+def test_gated_session_equals_render_gated():
+    sd = scenes.bundled("cornell", 48)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=2, temporal=True, spatial_passes=2,
+                       spatial_neighbors=3, spatial_radius=5, frames=3)
+    r = Renderer(0)
+    ref = r.render_gated(sd, cfg)
+    s = r.session(sd, cfg)
+    stats = [s.step(stats=True) for _ in range(cfg.frames)]
+    assert np.array_equal(s.read_image(), ref.image)
+    for a, b in zip(stats, ref.stats):
+        assert a["spatial"]["attempts"] == b["spatial"]["attempts"]
+        assert a["temporal"]["success"] == b["temporal"]["success"]
