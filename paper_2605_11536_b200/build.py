@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-DEVICE_SOURCES = ["tofr_kernels.cu"]
+DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu"]
 HOST_SOURCES = ["host_scene.cpp", "capi.cpp"]
 HEADERS = [
     "tofr_core.h",
@@ -34,6 +34,7 @@ HEADERS = [
     "tofr_path.cuh",
     "tofr_ellipsoid.cuh",
     "tofr_store.cuh",
+    "tofr_kcommon.cuh",
     "tofr_kernels.h",
     "host_scene.h",
 ]
@@ -111,21 +112,27 @@ def build_variants(variants: dict, verbose: bool = False) -> dict:
     host_objs = [BUILD_DIR / (src + ".o") for src in HOST_SOURCES]
     procs, outs = [], {}
     for tag, defs in variants.items():
-        obj = BUILD_DIR / f"tofr_kernels_{tag}.o"
-        cmd = [NVCC, "-std=c++17", GENCODE, "-O3", "-lineinfo", "--fmad=false", *defs,
-               "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", str(CSRC), "-I", str(INCLUDE),
-               "-c", str(CSRC / "tofr_kernels.cu"), "-o", str(obj)]
-        procs.append((tag, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
-    for tag, obj, p in procs:
+        objs = []
+        for src in DEVICE_SOURCES:
+            obj = BUILD_DIR / f"{Path(src).stem}_{tag}.o"
+            cmd = [NVCC, "-std=c++17", GENCODE, "-O3", "-lineinfo", "--fmad=false", *defs,
+                   "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", str(CSRC), "-I", str(INCLUDE),
+                   "-c", str(CSRC / src), "-o", str(obj)]
+            procs.append((tag, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+            objs.append(obj)
+        outs[tag] = objs
+    for tag, p in procs:
         out, err = p.communicate()
         if p.returncode != 0:
             sys.stderr.write(out + err)
             raise RuntimeError(f"variant {tag} failed")
+    libs = {}
+    for tag, objs in outs.items():
         lib = vdir / f"libtofr_b200_{tag}.so"
-        _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(lib), str(obj)] + [str(o) for o in host_objs]
-             + ["-Xlinker", "-rpath,$ORIGIN"], verbose)
-        outs[tag] = lib
-    return outs
+        _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(lib)] + [str(o) for o in objs]
+             + [str(o) for o in host_objs] + ["-Xlinker", "-rpath,$ORIGIN"], verbose)
+        libs[tag] = lib
+    return libs
 
 
 if __name__ == "__main__":

@@ -185,6 +185,10 @@ struct tofr_session {
     DevBuf sp_mapped, sp_ok, sp_rng, sp_list, sp_count;  // phased spatial pass (TOFR_SPATIAL=mono disables)
     bool phased = false;
     bool order = true;
+    // wavefront reuse (tofr_wave.cu; TOFR_REUSE=legacy selects the per-item kernels)
+    bool wave = false;
+    DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng;
+    size_t wv_cap = 0;
     tofr_halo_exchange_fn xfn = nullptr;
     void* xuser = nullptr;
     uint64_t halo_exchanges = 0;
@@ -225,7 +229,8 @@ struct tofr_session {
         }
         for (auto& r : res) r.release();
         for (DevBuf* b : {&image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
-                          &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count})
+                          &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
+                          &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng})
             b->release();
     }
 };
@@ -351,6 +356,31 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
         ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
         if (s->res[2].p) ck(cudaMemsetAsync(s->res[2].p, 0, rb, ctx->stream), "memset");
+        {
+            // wavefront reuse: job queue of (N + 1) jobs per item for the spatial
+            // pass (2 for temporal), bounded for the transient grids, whose
+            // non-empty reservoirs are a small fraction of W x H x B
+            const char* rv = std::getenv("TOFR_REUSE");
+            size_t own_items = s->owned_pixels() * s->B;
+            size_t nj = size_t(std::max(0, cfg->spatial_neighbors));
+            s->wave = (s->has_temporal || s->has_spatial) && !(rv && std::strcmp(rv, "legacy") == 0);
+            if (s->wave) {
+                size_t per = wave_jobs_per_item(s->has_spatial ? cfg->spatial_neighbors : 0);
+                size_t cap = per * own_items;
+                size_t limit = size_t(32) << 20;
+                if (const char* cl = std::getenv("TOFR_WAVE_CAP")) limit = size_t(std::strtoull(cl, nullptr, 10));
+                if (cap > limit) cap = limit;
+                if (cap > 0xfffffff0ull) cap = 0xfffffff0ull;
+                s->wv_cap = cap;
+                s->wv_jobs.ensure(cap * kJobChunks * 16);
+                s->wv_out.ensure(cap * kResChunks * 16);
+                s->wv_ctl.ensure(16);
+                s->wv_map_a.ensure(std::max<size_t>(1, nj) * own_items * sizeof(uint32_t));
+                s->wv_map_b.ensure(own_items * sizeof(uint32_t));
+                s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
+                s->wv_rng.ensure(own_items * sizeof(uint64_t));
+            }
+        }
         const char* ord = std::getenv("TOFR_ORDER");
         s->order = !(ord && ord[0] == '0');
         {
@@ -360,8 +390,8 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             size_t own_items = s->owned_pixels() * s->B;
             size_t nj = size_t(std::max(0, cfg->spatial_neighbors));
             size_t need = nj * own_items * kResChunks * 16;
-            s->phased = s->has_spatial && nj > 0 && cfg->spatial_radius > 0 && !(sm && std::strcmp(sm, "mono") == 0) &&
-                        need <= (size_t(16) << 30);
+            s->phased = !s->wave && s->has_spatial && nj > 0 && cfg->spatial_radius > 0 &&
+                        !(sm && std::strcmp(sm, "mono") == 0) && need <= (size_t(16) << 30);
             if (s->phased) {
                 s->sp_mapped.ensure(need);
                 s->sp_ok.ensure(nj * own_items);
@@ -370,7 +400,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->sp_count.ensure(16);
             }
         }
-        if (s->order) {
+        if (s->order && !s->wave) {
             size_t own_items = s->owned_pixels() * s->B;
             s->wo_cls.ensure(own_items);
             s->wo_perm.ensure(own_items * sizeof(uint32_t));
@@ -431,6 +461,10 @@ void flush_set(tofr_session* s, int set) {
         s->stage_tot[i] += ms[i];
     }
     s->tot_frames++;
+    if (s->err_host[set] >> 32)
+        throw ScopeError(TOFR_ERR_OOM,
+                         "reuse shift queue overflow: more shifts than TOFR_WAVE_CAP jobs in one stage (raise it, or "
+                         "TOFR_REUSE=legacy)");
     if (s->err_host[set])
         throw ScopeError(TOFR_ERR_UNSUPPORTED,
                          "row band read outside its rows (camera motion larger than the halo, or a spatial "
@@ -487,6 +521,19 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     Band bd = band_of(s, prev_halo);
     cudaEvent_t* ev = s->ev[set];
     WorkOrder wo{nullptr, nullptr, nullptr};
+    WaveScratch wv;
+    if (s->wave) {
+        size_t own_items = s->owned_pixels() * s->B;
+        (void)own_items;
+        wv.q.jobs = s->wv_jobs.as<double2>();
+        wv.q.cap = s->wv_cap;
+        wv.q.out = ResStore{s->wv_out.as<double2>(), s->wv_cap};
+        wv.q.ctl = s->wv_ctl.as<uint32_t>();
+        wv.map_a = s->wv_map_a.as<uint32_t>();
+        wv.map_b = s->wv_map_b.as<uint32_t>();
+        wv.tsrc = s->wv_tsrc.as<uint64_t>();
+        wv.rng_ctr = s->wv_rng.as<uint64_t>();
+    }
     if (s->order && s->wo_perm.p)
         wo = WorkOrder{s->wo_cls.as<uint8_t>(), s->wo_counts.as<uint32_t>(), s->wo_perm.as<uint32_t>()};
     ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
@@ -510,8 +557,12 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
-            launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]), wo,
-                            ctr + 0 * SC_COUNT, q, stream);
+            if (s->wave)
+                launch_temporal_wave(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur,
+                                     store_of(s, s->res[s->prev]), wv, ctr + 0 * SC_COUNT, q, stream);
+            else
+                launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
+                                wo, ctr + 0 * SC_COUNT, q, stream);
         }
         cudaEventRecord(ev[2], stream);
         if (s->transient && c.bin_reuse) {
@@ -534,8 +585,12 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                 scr.count = s->sp_count.as<uint32_t>();
                 scp = &scr;
             }
-            launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
-                           ctr + 1 * SC_COUNT, q, stream);
+            if (s->wave && sp.neighbors > 0 && sp.radius > 0)
+                launch_spatial_wave(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wv,
+                                    ctr + 1 * SC_COUNT, q, stream);
+            else
+                launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
+                               ctr + 1 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur]);
         }

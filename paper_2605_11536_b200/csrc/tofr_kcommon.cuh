@@ -1,0 +1,118 @@
+// tofr_kcommon.cuh -- device helpers shared by the kernel translation units
+// (tofr_kernels.cu: camera/initial/shading/legacy reuse kernels;
+//  tofr_wave.cu: the wavefront shift engine and the reuse stages built on it).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tofr_kernels.h"
+
+namespace tofr_b200 {
+
+// ---------------------------------------------------------------------------
+// shared-memory staging of the traversal arrays
+
+__device__ __forceinline__ void stage_frame(FrameView& F, unsigned char* smem, size_t& off) {
+    if (size_t(F.n_nodes) * sizeof(GNode) + size_t(F.n_tris) * sizeof(GTriIsect) > kSmemStageLimit)
+        return;  // large mesh: traverse from global memory (L1/L2 cached)
+    size_t nb = size_t(F.n_nodes) * sizeof(GNode);
+    size_t tb = size_t(F.n_tris) * sizeof(GTriIsect);
+    GNode* sn = reinterpret_cast<GNode*>(smem + off);
+    off += (nb + 15) & ~size_t(15);
+    GTriIsect* st = reinterpret_cast<GTriIsect*>(smem + off);
+    off += (tb + 15) & ~size_t(15);
+    const double* gn = reinterpret_cast<const double*>(F.nodes);
+    double* dn = reinterpret_cast<double*>(sn);
+    for (size_t i = threadIdx.x; i < nb / 8; i += blockDim.x) dn[i] = gn[i];
+    const double* gt = reinterpret_cast<const double*>(F.tri_isect);
+    double* dt = reinterpret_cast<double*>(st);
+    for (size_t i = threadIdx.x; i < tb / 8; i += blockDim.x) dt[i] = gt[i];
+    F.nodes = sn;
+    F.tri_isect = st;
+}
+
+// ---------------------------------------------------------------------------
+// shift counters: per-thread u32, summed in shared memory, one u64 atomic per
+// counter and CTA (every thread of the CTA must reach the call)
+
+static __device__ __noinline__ void flush_ctr(const uint32_t* c, unsigned long long* out) {
+    __shared__ unsigned int sc[SC_COUNT];
+    if (threadIdx.x < SC_COUNT) sc[threadIdx.x] = 0;
+    __syncthreads();
+    if (out)
+        for (int k = 0; k < SC_COUNT; ++k)
+            if (c[k]) atomicAdd(&sc[k], c[k]);
+    __syncthreads();
+    if (out && threadIdx.x < SC_COUNT && sc[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// Dynamic work distribution.  The per-item cost of the path kernels varies by
+// orders of magnitude (empty pixels vs. multi-iteration Newton solves), so a
+// static grid-stride assignment leaves most of a CTA waiting for its slowest
+// warp.  The heavy kernels run persistent CTAs (one wave, sized by the
+// occupancy calculator) whose warps take 32 consecutive items at a time from
+// a per-launch counter `q` (zeroed by the host before the launch).
+
+__device__ __forceinline__ size_t warp_take(unsigned long long* q) {
+    unsigned long long b = 0;
+    if ((threadIdx.x & 31) == 0) b = atomicAdd(q, 32ull);
+    return size_t(__shfl_sync(0xffffffffu, b, 0));
+}
+
+#define TOFR_FOR_ITEMS(i, n, q)                                                              \
+    for (size_t i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31); i##_base < (n); \
+         i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31))                         \
+        if (i < (n))
+
+// ---------------------------------------------------------------------------
+// gates and spatial neighbours
+
+__device__ __forceinline__ void gate_of(const GateGrid& gg, int b, double& c, double& w) {
+    if (gg.transient) {
+        c = bin_center(gg.h, b);
+        w = gg.h.bw;
+    } else {
+        c = gg.center;
+        w = gg.width;
+    }
+}
+
+__device__ __forceinline__ void neighbor_offset(int j, int count, double radius, uint64_t rot_key,
+                                                int& dx, int& dy) {
+    double rot = double(mix64(rot_key) >> 11) * 0x1.0p-53 * 2.0 * kPi;
+    double rr = radius * sqrt((j + 0.5) / count);
+    double th = j * 2.39996322972865332 + rot;
+    dx = int(llround(rr * cos(th)));
+    dy = int(llround(rr * sin(th)));
+}
+
+// Neighbour j of item `it`, with the k_spatial skip rules.  Returns false when
+// the reference skips it (self, outside the image, never-written M <= 0).
+__device__ __forceinline__ bool spatial_neighbor(const Band& bd, int W, int H, int B, int px, int py, int b,
+                                                 const SpatialParams& sp, uint64_t rk, int j,
+                                                 const ResStore& src_grid, int& nx, int& ny, size_t& si) {
+    int dx, dy;
+    neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+    nx = px + dx;
+    ny = py + dy;
+    if (nx == px && ny == py) return false;
+    if (nx < 0 || nx >= W || ny < 0 || ny >= H) return false;
+    if (ny < bd.r0 || ny >= bd.r1) {  // beyond the exchanged halo
+        atomicAdd(bd.err, 1ull);
+        return false;
+    }
+    si = (size_t(ny) * W + nx) * B + b;
+    double2 c0 = ld2(src_grid, 0, si);
+    return c0.y > 0;
+}
+
+__device__ __forceinline__ uint64_t spatial_rot_key(uint64_t pix, int pass, uint64_t seed, int frame_idx) {
+    return mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + seed + uint64_t(frame_idx) * 97);
+}
+
+// One wave of resident CTAs for a persistent kernel (occupancy calculator),
+// never more than the items need.
+int persistent_grid(const void* kernel, int block, size_t smem, size_t n);
+
+}  // namespace tofr_b200

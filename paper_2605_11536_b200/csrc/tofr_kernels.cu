@@ -19,7 +19,7 @@
 #include <cuda_runtime.h>
 
 #include "tofr_ellipsoid.cuh"
-#include "tofr_kernels.h"
+#include "tofr_kcommon.cuh"
 #include "tofr_store.cuh"
 
 // Minimum resident CTAs per SM requested for the reuse/initial kernels
@@ -30,28 +30,6 @@
 
 namespace tofr_b200 {
 
-// ---------------------------------------------------------------------------
-// shared-memory staging of the traversal arrays
-
-__device__ __forceinline__ void stage_frame(FrameView& F, unsigned char* smem, size_t& off) {
-    if (size_t(F.n_nodes) * sizeof(GNode) + size_t(F.n_tris) * sizeof(GTriIsect) > kSmemStageLimit)
-        return;  // large mesh: traverse from global memory (L1/L2 cached)
-    size_t nb = size_t(F.n_nodes) * sizeof(GNode);
-    size_t tb = size_t(F.n_tris) * sizeof(GTriIsect);
-    GNode* sn = reinterpret_cast<GNode*>(smem + off);
-    off += (nb + 15) & ~size_t(15);
-    GTriIsect* st = reinterpret_cast<GTriIsect*>(smem + off);
-    off += (tb + 15) & ~size_t(15);
-    const double* gn = reinterpret_cast<const double*>(F.nodes);
-    double* dn = reinterpret_cast<double*>(sn);
-    for (size_t i = threadIdx.x; i < nb / 8; i += blockDim.x) dn[i] = gn[i];
-    const double* gt = reinterpret_cast<const double*>(F.tri_isect);
-    double* dt = reinterpret_cast<double*>(st);
-    for (size_t i = threadIdx.x; i < tb / 8; i += blockDim.x) dt[i] = gt[i];
-    F.nodes = sn;
-    F.tri_isect = st;
-}
-
 size_t frame_smem_bytes(const FrameView& F) {
     size_t nb = size_t(F.n_nodes) * sizeof(GNode);
     size_t tb = size_t(F.n_tris) * sizeof(GTriIsect);
@@ -60,53 +38,14 @@ size_t frame_smem_bytes(const FrameView& F) {
 }
 
 // ---------------------------------------------------------------------------
-// shift counters: per-thread u32, summed in shared memory, one u64 atomic per
-// counter and CTA (every thread of the CTA must reach the call)
-
-__device__ __noinline__ void flush_ctr(const uint32_t* c, unsigned long long* out) {
-    __shared__ unsigned int sc[SC_COUNT];
-    if (threadIdx.x < SC_COUNT) sc[threadIdx.x] = 0;
-    __syncthreads();
-    if (out)
-        for (int k = 0; k < SC_COUNT; ++k)
-            if (c[k]) atomicAdd(&sc[k], c[k]);
-    __syncthreads();
-    if (out && threadIdx.x < SC_COUNT && sc[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
-}
-
-// ---------------------------------------------------------------------------
-// Dynamic work distribution.  The per-item cost of the path kernels varies by
-// orders of magnitude (empty pixels vs. multi-iteration Newton solves), so a
-// static grid-stride assignment leaves most of a CTA waiting for its slowest
-// warp.  The heavy kernels run persistent CTAs (one wave, sized by the
-// occupancy calculator) whose warps take 32 consecutive items at a time from
-// a per-launch counter `q` (zeroed by the host before the launch).
-
-__device__ __forceinline__ size_t warp_take(unsigned long long* q) {
-    unsigned long long b = 0;
-    if ((threadIdx.x & 31) == 0) b = atomicAdd(q, 32ull);
-    return size_t(__shfl_sync(0xffffffffu, b, 0));
-}
-
-#define TOFR_FOR_ITEMS(i, n, q)                                                              \
-    for (size_t i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31); i##_base < (n); \
-         i##_base = warp_take(q), i = i##_base + (threadIdx.x & 31))                         \
-        if (i < (n))
-
-// ---------------------------------------------------------------------------
 // work-ordering helpers (see k_cost_*)
 
 constexpr int kCostBuckets = 8;
 
-__device__ __forceinline__ bool nonempty(const ResStore& s, size_t i) {
-    double2 c0 = ld2(s, 0, i);
-    return ld_meta(s, i).has && c0.x > 0;
-}
+__device__ __forceinline__ bool nonempty(const ResStore& s, size_t i) { return ld2(s, 0, i).x > 0; }
 
 __device__ __forceinline__ bool shiftable(const ResStore& s, size_t i) {
-    double2 c0 = ld2(s, 0, i);
-    Meta m = ld_meta(s, i);
-    return m.has && c0.x > 0 && m.valid;
+    return ld2(s, 0, i).x > 0 && ld_meta(s, i).valid;
 }
 
 // Warp-aggregated append of item `loc` into bucket c.
@@ -279,7 +218,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F
             NoEll ell;
             init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
         }
-        res_store(cur, size_t(p), r);
+        res_store_result(cur, size_t(p), r);
     }
 }
 
@@ -339,7 +278,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameVi
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         size_t base = size_t(p) * B;
-        for (int b = 0; b < B; ++b) res_store_empty(cur, base + b, 0.0);
+        for (int b = 0; b < B; ++b) res_store_w(cur, base + b, 0.0, 0.0);
         Rng pick = rng_make(cfg.seed, uint64_t(frame_idx), pix, 0, 9);
         BinSink sink{&F, h, 1.0 / ip.m_init, &pick, cur, base};
         GHit g = gbuf[p];
@@ -350,10 +289,12 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameVi
         }
         for (int b = 0; b < B; ++b) {  // ris_finalize + M = 1
             size_t i = base + b;
-            double2 c0 = ld2(cur, 0, i);
-            Meta m = ld_meta(cur, i);
-            double phat = m.has ? ld2(cur, 1, i).x : 0.0;
-            double Wv = (m.has && phat > 0) ? c0.x / phat : 0;
+            double2 c0 = ld2(cur, 0, i);  // (w_sum, -): w_sum > 0 iff a candidate was picked
+            double Wv = 0;
+            if (c0.x > 0) {
+                double phat = ld2(cur, 1, i).x;
+                Wv = phat > 0 ? c0.x / phat : 0;
+            }
             st2(cur, 0, i, Wv, 1.0);
         }
     }
@@ -361,16 +302,6 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_transient(FrameVi
 
 // ---------------------------------------------------------------------------
 // temporal reuse (stage::temporal_reuse, pipeline.hpp:209-229)
-
-__device__ __forceinline__ void gate_of(const GateGrid& gg, int b, double& c, double& w) {
-    if (gg.transient) {
-        c = bin_center(gg.h, b);
-        w = gg.h.bw;
-    } else {
-        c = gg.center;
-        w = gg.width;
-    }
-}
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc, Band bd, const GHit* gc, FrameView Fp,
                                                   const GHit* gp, PathCfg cfg, GateGrid cur_gate,
@@ -400,16 +331,17 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
             continue;
         }
         size_t src_i = (size_t(qy) * W + qx) * B + b;
-        double sW, sM;
-        int shas;
-        res_load_hdr(prev, src_i, sW, sM, shas);
-        if (sM <= 0) continue;
+        Res dst, src;
+        res_load_head(prev, src_i, src);
+        if (src.M <= 0) continue;
         double dc, dw, sc, sw;
         gate_of(cur_gate, b, dc, dw);
         gate_of(prev_gate, b, sc, sw);
-        Res dst, src;
         res_load(cur, it, dst);
-        res_load(prev, src_i, src);
+        if (src.has) {
+            res_load_value(prev, src_i, src);
+            res_load_rec(prev, src_i, src.y);
+        }
         Dom dd{px, py, dc, dw, &Fc, gc};
         Dom sd{qx, qy, sc, sw, &Fp, gp};
         MergeShift ms{0, 1.0, 0.0};
@@ -429,23 +361,17 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
         }
         uint64_t pix = uint64_t(py) * W + px;
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
-        gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
-        res_store(cur, it, dst);
+        int which = gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        if (which == 2)
+            res_store(cur, it, dst);
+        else  // in place: the kept sample and its p-hat are already stored
+            res_store_w(cur, it, dst.W, dst.M);
     }
     flush_ctr(ctr, ctr_out);
 }
 
 // ---------------------------------------------------------------------------
 // spatial reuse (stage::spatial_reuse + neighbor_offset, pipeline.hpp:232-269)
-
-__device__ __forceinline__ void neighbor_offset(int j, int count, double radius, uint64_t rot_key,
-                                                int& dx, int& dy) {
-    double rot = double(mix64(rot_key) >> 11) * 0x1.0p-53 * 2.0 * kPi;
-    double rr = radius * sqrt((j + 0.5) / count);
-    double th = j * 2.39996322972865332 + rot;
-    dx = int(llround(rr * cos(th)));
-    dy = int(llround(rr * sin(th)));
-}
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                  GateGrid gate, SpatialParams sp, int pass,
@@ -484,12 +410,13 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
                     continue;
                 }
                 size_t si = (size_t(ny) * W + nx) * B + b;
-                double sW, sM;
-                int shas;
-                res_load_hdr(src_grid, si, sW, sM, shas);
-                if (sM <= 0) continue;
                 Res src;
-                res_load(src_grid, si, src);
+                res_load_head(src_grid, si, src);
+                if (src.M <= 0) continue;
+                if (src.has) {
+                    res_load_value(src_grid, si, src);
+                    res_load_rec(src_grid, si, src.y);
+                }
                 Dom sd{nx, ny, dc, dw, &F, gbuf};
                 MergeShift ms{0, 1.0, 0.0};
                 Sample mapped;
@@ -509,7 +436,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
                 gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
             }
         }
-        res_store(dst_grid, it, out);
+        res_store_result(dst_grid, it, out);
     }
     flush_ctr(ctr, ctr_out);
 }
@@ -525,30 +452,6 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
 // the running output and the lane-10 RNG counter carried in HBM.  Same
 // arithmetic, same RNG draws in the same order, same counters.
 
-
-// Neighbour j of item `it`, with the k_spatial skip rules.  Returns false when
-// the reference skips it (self, outside the image, never-written M <= 0).
-__device__ __forceinline__ bool spatial_neighbor(const Band& bd, int W, int H, int B, int px, int py, int b,
-                                                 const SpatialParams& sp, uint64_t rk, int j,
-                                                 const ResStore& src_grid, int& nx, int& ny, size_t& si) {
-    int dx, dy;
-    neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
-    nx = px + dx;
-    ny = py + dy;
-    if (nx == px && ny == py) return false;
-    if (nx < 0 || nx >= W || ny < 0 || ny >= H) return false;
-    if (ny < bd.r0 || ny >= bd.r1) {  // beyond the exchanged halo
-        atomicAdd(bd.err, 1ull);
-        return false;
-    }
-    si = (size_t(ny) * W + nx) * B + b;
-    double2 c0 = ld2(src_grid, 0, si);
-    return c0.y > 0;
-}
-
-__device__ __forceinline__ uint64_t spatial_rot_key(uint64_t pix, int pass, uint64_t seed, int frame_idx) {
-    return mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + seed + uint64_t(frame_idx) * 97);
-}
 
 __global__ void k_spatial_fwd_list(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
                                    int frame_idx, ResStore src_grid, SpatialScratch sc) {
@@ -647,7 +550,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
             if (j == 0) {  // the output starts as the pass input
                 Res out;
                 res_load(src_grid, it, out);
-                res_store(dst_grid, it, out);
+                res_store_result(dst_grid, it, out);
             }
             if (j + 1 < sp.neighbors && j == 0) sc.rng_ctr[i] = 0;
             continue;
@@ -659,18 +562,14 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
         double dc, dw;
         gate_of(gate, b, dc, dw);
         Res src;  // header only: gris_merge reads W, M, phat, has
-        {
-            double2 c0 = ld2(src_grid, 0, si), c1 = ld2(src_grid, 1, si);
-            src.W = c0.x;
-            src.M = c0.y;
-            src.phat = c1.x;
-            src.has = ld_meta(src_grid, si).has;
-        }
+        res_load_head(src_grid, si, src);
+        if (src.has) src.phat = ld2(src_grid, 1, si).x;
         size_t e = size_t(j) * n + i;
         MergeShift ms{0, 1.0, 0.0};
-        Res mapped;
+        Res mapped;  // f, len, jac now; the record only if it is selected
         if (!res_empty(src) && sc.ok[e]) {
-            res_load(sc.mapped, e, mapped);
+            res_load_head(sc.mapped, e, mapped);
+            res_load_value(sc.mapped, e, mapped);
             ms.valid = 1;
             ms.jac = mapped.W;
         }
@@ -682,8 +581,15 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
             if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
                 ms.phat_src_of_dst = luminance(inv.f) * gate_w(dc, dw, inv.len) * jac;
         }
-        gris_merge(out, src, ms, mapped.y, dc, dw, cfg.m_cap, rng);
-        res_store(dst_grid, it, out);
+        int which = gris_merge(out, src, ms, mapped.y, dc, dw, cfg.m_cap, rng);
+        if (which == 2) {
+            res_load_rec(sc.mapped, e, out.y);
+            res_store(dst_grid, it, out);
+        } else if (which == 1 && j > 0) {  // in place: sample and p-hat already stored
+            res_store_w(dst_grid, it, out.W, out.M);
+        } else {
+            res_store_result(dst_grid, it, out);
+        }
         if (j + 1 < sp.neighbors) sc.rng_ctr[i] = rng.ctr;
     }
 }
@@ -716,12 +622,13 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, 
             int nb = k == 0 ? b - 1 : b + 1;
             if (nb < 0 || nb >= B) continue;
             size_t si = size_t(p) * B + nb;
-            double sW, sM;
-            int shas;
-            res_load_hdr(src_grid, si, sW, sM, shas);
-            if (sM <= 0) continue;
             Res src;
-            res_load(src_grid, si, src);
+            res_load_head(src_grid, si, src);
+            if (src.M <= 0) continue;
+            if (src.has) {
+                res_load_value(src_grid, si, src);
+                res_load_rec(src_grid, si, src.y);
+            }
             double sc = bin_center(h, nb);
             Dom sd{px, py, sc, dw, &F, gbuf};
             MergeShift ms{0, 1.0, 0.0};
@@ -741,7 +648,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, 
             }
             gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
         }
-        res_store(dst_grid, it, out);
+        res_store_result(dst_grid, it, out);
     }
     flush_ctr(ctr, ctr_out);
 }
@@ -1062,7 +969,7 @@ __global__ void k_halo_unpack(ResStore grid, size_t item0, size_t n, const doubl
 
 // One wave of resident CTAs for a persistent kernel (occupancy calculator,
 // cached per kernel), never more than the items need.
-static int persistent_grid(const void* kernel, int block, size_t smem, size_t n) {
+int persistent_grid(const void* kernel, int block, size_t smem, size_t n) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;

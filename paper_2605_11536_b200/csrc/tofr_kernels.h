@@ -65,6 +65,53 @@ struct SpatialParams {
     double radius;
 };
 
+// ---------------------------------------------------------------------------
+// Wavefront shift engine (tofr_wave.cu).  A shift job maps the sample stored
+// at (store, item) from a source domain (frame, pixel, gate centre) into a
+// destination domain (frame, pixel, gate centre and width) -- shift_sample,
+// shiftmap.hpp:662-783.  Stages append jobs to a compacted queue; two kernels
+// run the shifts (k_shift_solve: record, prefix, suffix and the Newton solve;
+// k_shift_finish: occlusion, Jacobian, rebuild); the stage's merge kernel then
+// reads the per-job outputs.
+constexpr int kJobChunks = 7;
+enum : uint32_t {
+    JOB_REC1 = 1u,    // source record lives in store 1 (else store 0)
+    JOB_SRC1 = 2u,    // source domain is frame 1 (else frame 0)
+    JOB_DST1 = 4u,    // destination domain is frame 1
+    JOB_FULL = 8u,    // output the mapped record (else only p-hat of the source gate)
+    JOB_COUNT = 16u,  // accumulate the shift counters (forward shifts)
+};
+constexpr uint32_t kNoJob = 0xffffffffu;
+
+struct ShiftQueue {
+    double2* jobs;  // chunk-major job records: chunk c of job k at jobs[c * cap + k]
+    size_t cap;
+    // Per-job output, indexed by job id.  Chunk 0 = (value, ok): value is the
+    // Jacobian (JOB_FULL) or p-hat_src(S^-1 y) * |J| (otherwise), ok = 1 when the
+    // shift succeeded.  JOB_FULL jobs also get the mapped record in chunks 1-21.
+    ResStore out;
+    uint32_t* ctl;  // [0] first job of the current batch, [1] end, [2] mark
+};
+
+struct WaveScratch {
+    ShiftQueue q;
+    uint32_t* map_a;    // spatial: forward job of (j, i) [N * n]; temporal: forward job of i [n]
+    uint32_t* map_b;    // spatial: inverse job of i [n]; temporal: inverse job of i [n]
+    uint64_t* tsrc;     // temporal: reprojected source item of i, or ~0
+    uint64_t* rng_ctr;  // spatial: lane-10 RNG position per item
+};
+
+// jobs per item a stage can enqueue (capacity planning)
+inline size_t wave_jobs_per_item(int neighbors) { return size_t(neighbors > 1 ? neighbors + 1 : 2); }
+
+void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
+                          const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx, ResStore cur,
+                          ResStore prev, const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q,
+                          cudaStream_t s);
+void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                         const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
+                         const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q, cudaStream_t s);
+
 size_t frame_smem_bytes(const FrameView& F);
 void set_gauss_rule(const double* x, const double* w, cudaStream_t s);
 // g (launch_gbuffer) is the band's local G-buffer (row r0 first); every other

@@ -163,7 +163,7 @@ __device__ inline const WalkV& rs_vert(const RecSrc& s, int i) {
 }
 
 // build_record (transport.hpp:448-582), Length subset
-__device__ __noinline__ void build_record(const FrameView& F, const RecSrc& s, Rec& r) {
+static __device__ __noinline__ void build_record(const FrameView& F, const RecSrc& s, Rec& r) {
     rec_clear(r);
     int last = s.q ? s.d + 1 : s.d;
     int k = -1;
@@ -405,7 +405,7 @@ __device__ inline M3 lc_hess(const V3& p1, const V3& p2, const V3& p) {
 }
 
 // assemble_constraint (shiftmap.hpp:155-217)
-__device__ Constraint assemble(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
+__device__ inline Constraint assemble(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
                                const V3& pc, const Frame2& Jc, double delta, int gauge) {
     Constraint e;
     V3 g3s = lc_grad(p1, p2, ps);
@@ -456,7 +456,7 @@ __device__ inline SurfPt surf_from_hit(const FrameView& F, const Hit& h) {
 }
 
 // reproject_to_mesh (shiftmap.hpp:275-307)
-__device__ __noinline__ bool reproject(const FrameView& F, const SurfPt& cur, const V3& plane_pt, const V3& p1,
+static __device__ __noinline__ bool reproject(const FrameView& F, const SurfPt& cur, const V3& plane_pt, const V3& p1,
                           SurfPt& out) {
     const GTriIsect& g = tri_geo(F, cur.tri);
     V3 tn = F.tri[cur.tri].n;
@@ -508,7 +508,7 @@ struct NewtonOut {
 };
 
 // newton_solve (shiftmap.hpp:314-378); max 5 iterations, 8 halvings
-__device__ __noinline__ NewtonOut newton_solve(const FrameView& F, const V3& p1, const V3& p2, const SurfPt& start,
+static __device__ __noinline__ NewtonOut newton_solve(const FrameView& F, const V3& p1, const V3& p2, const SurfPt& start,
                                   double delta, int gauge, double tol, double eps_grad) {
     NewtonOut res;
     res.converged = 0;
@@ -580,7 +580,7 @@ struct Dom {
 
 // hybrid_base_shift (shiftmap.hpp:459-528): random replay of the prefix from
 // the destination pixel with the stored lanes.
-__device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec, const PathCfg& cfg) {
+static __device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec, const PathCfg& cfg) {
     Prefix out;
     out.ok = 0;
     const FrameView& F = *dom.F;
@@ -668,7 +668,7 @@ __device__ inline Suffix suffix_geometry(const FrameView& F, const Rec& rec) {
 }
 
 // rebuild_sample (shiftmap.hpp:579-654)
-__device__ __noinline__ bool rebuild_sample(const FrameView& F, const Rec& rec, const Prefix& pre, const SurfPt& p,
+static __device__ __noinline__ bool rebuild_sample(const FrameView& F, const Rec& rec, const Prefix& pre, const SurfPt& p,
                                const Suffix& suf, Sample& out) {
     V3 d1 = p.pos - pre.p1;
     double l1 = norm(d1);
@@ -741,7 +741,7 @@ __device__ inline Prefix stored_prefix(const FrameView& F, const Rec& rec) {
 }
 
 // shift_sample (shiftmap.hpp:662-783).  Returns true on a usable mapping.
-__device__ __noinline__ bool shift_sample(const Sample& src, const Dom& sd, const Dom& dd, const PathCfg& cfg,
+static __device__ __noinline__ bool shift_sample(const Sample& src, const Dom& sd, const Dom& dd, const PathCfg& cfg,
                              uint32_t* ctr, Sample& mapped, double& jac_out) {
     ctr_add(ctr, SC_ATTEMPTS);
     const Rec& rec = src.rec;
@@ -815,7 +815,7 @@ __device__ __noinline__ bool shift_sample(const Sample& src, const Dom& sd, cons
 
 // shrink_map (shiftmap.hpp:789-876): contract a wide-gate sample onto the fine
 // gate (forward) or expand (inverse); identity prefix, no replay.
-__device__ __noinline__ bool shrink_map(const Sample& src, const Dom& dom, double K, bool forward,
+static __device__ __noinline__ bool shrink_map(const Sample& src, const Dom& dom, double K, bool forward,
                            const PathCfg& cfg, Sample& mapped, double& jac_out) {
     const Rec& rec = src.rec;
     const FrameView& F = *dom.F;
@@ -868,8 +868,10 @@ struct MergeShift {
     double phat_src_of_dst;
 };
 
-// Merges `src` (mapped into dst's domain as `mapped`) into dst.
-__device__ void gris_merge(Res& dst, const Res& src, const MergeShift& ms, const Sample& mapped,
+// Merges `src` (mapped into dst's domain as `mapped`) into dst.  Returns the
+// selected input: 0 none (dst is now empty), 1 dst's own sample (kept, only W
+// and M change), 2 the mapped source sample.
+__device__ __forceinline__ int gris_merge(Res& dst, const Res& src, const MergeShift& ms, const Sample& mapped,
                            double dst_center, double dst_width, double m_cap, Rng& rng) {
     double Mc = dst.M, Ms = src.M;
     double w_sum = 0;
@@ -903,6 +905,7 @@ __device__ void gris_merge(Res& dst, const Res& src, const MergeShift& ms, const
     dst.phat = phat_out;
     dst.W = (dst.has && phat_out > 0) ? w_sum / phat_out : 0;
     dst.M = M;
+    return dst.W > 0 ? which : 0;
 }
 
 #endif  // __CUDACC__

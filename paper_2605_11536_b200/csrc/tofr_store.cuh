@@ -51,19 +51,31 @@ __device__ __forceinline__ Meta ld_meta(const ResStore& s, size_t i) {
     return m;
 }
 
-// Header: W, M, has (enough for empty() and the src.M <= 0 tests)
+// Emptiness lives in chunk 0 alone: a reservoir holds a sample iff W > 0.
+// (has <=> W > 0: ris_finalize and gris_merge set W = w_sum / phat > 0 exactly
+// when a candidate was selected, and W = 0 otherwise, ris.hpp:52-56, :101-103.)
+// Readers therefore touch chunk 0 first and the sample chunks only for
+// non-empty reservoirs, and writers of an empty result store chunk 0 only --
+// the sample chunks of an empty reservoir are never read.
 __device__ __forceinline__ void res_load_hdr(const ResStore& s, size_t i, double& W, double& M, int& has) {
     double2 c0 = ld2(s, 0, i);
     W = c0.x;
     M = c0.y;
-    has = ld_meta(s, i).has;
+    has = W > 0;
 }
 
-__device__ void res_load(const ResStore& s, size_t i, Res& r) {
+// chunk 0 only (W, M, has); the sample is not loaded
+__device__ __forceinline__ void res_load_head(const ResStore& s, size_t i, Res& r) {
+    double2 c0 = ld2(s, 0, i);
+    r.W = c0.x;
+    r.M = c0.y;
+    r.has = r.W > 0;
+    r.phat = 0;
+}
+
+// chunks 1-3: phat, len, f, suffix_len (what a merge reads of a candidate)
+__device__ __forceinline__ void res_load_value(const ResStore& s, size_t i, Res& r) {
     double2 c;
-    c = ld2(s, 0, i);
-    r.W = c.x;
-    r.M = c.y;
     c = ld2(s, 1, i);
     r.phat = c.x;
     r.y.len = c.y;
@@ -72,15 +84,19 @@ __device__ void res_load(const ResStore& s, size_t i, Res& r) {
     r.y.f.y = c.y;
     c = ld2(s, 3, i);
     r.y.f.z = c.x;
-    Rec& q = r.y.rec;
-    q.suffix_len = c.y;
+    r.y.rec.suffix_len = c.y;
+}
+
+// chunks 4-21: the reconnection record (+ depth)
+__device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y) {
+    double2 c;
+    Rec& q = y.rec;
     Meta m = ld_meta(s, i);
-    r.has = m.has;
     q.valid = m.valid;
     q.k = m.k == 255 ? -1 : int(m.k);
     q.n_lanes = m.nl;
     q.skind = m.skind;
-    r.y.depth = m.depth;
+    y.depth = m.depth;
     q.tri1 = m.tri1;
     q.ptri = m.ptri;
     c = ld2(s, 5, i);
@@ -144,6 +160,22 @@ __device__ void res_load(const ResStore& s, size_t i, Res& r) {
     }
 }
 
+// Header first; the sample only when the reservoir is non-empty.
+__device__ __forceinline__ void res_load(const ResStore& s, size_t i, Res& r) {
+    res_load_head(s, i, r);
+    if (r.has) {
+        res_load_value(s, i, r);
+        res_load_rec(s, i, r.y);
+    }
+}
+
+// Every chunk, whatever the header says (scratch planes).
+__device__ __forceinline__ void res_load_all(const ResStore& s, size_t i, Res& r) {
+    res_load_head(s, i, r);
+    res_load_value(s, i, r);
+    res_load_rec(s, i, r.y);
+}
+
 __device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& r) {
     Meta m;
     const Rec& q = r.y.rec;
@@ -161,7 +193,7 @@ __device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& 
     st2(s, 4, i, v.x, v.y);
 }
 
-__device__ void res_store(const ResStore& s, size_t i, const Res& r) {
+__device__ inline void res_store(const ResStore& s, size_t i, const Res& r) {
     const Rec& q = r.y.rec;
     st2(s, 0, i, r.W, r.M);
     st2(s, 1, i, r.phat, r.y.len);
@@ -197,16 +229,17 @@ __device__ void res_store(const ResStore& s, size_t i, const Res& r) {
     }
 }
 
-// Header-only write for an empty reservoir: W, M and the has/meta chunk.
-__device__ __forceinline__ void res_store_empty(const ResStore& s, size_t i, double M) {
-    st2(s, 0, i, 0.0, M);
-    Meta m;
-    memset(&m, 0, sizeof(m));
-    m.k = 255;
-    m.tri1 = m.ptri = -1;
-    double2 v;
-    memcpy(&v, &m, 16);
-    st2(s, 4, i, v.x, v.y);
+// Chunk-0 write: an empty reservoir (W = 0), or a reservoir whose sample and
+// p-hat are already in place and only W and M changed.
+__device__ __forceinline__ void res_store_w(const ResStore& s, size_t i, double W, double M) { st2(s, 0, i, W, M); }
+
+// Store of a merge/RIS result: the full record when it is non-empty, else the
+// header.
+__device__ __forceinline__ void res_store_result(const ResStore& s, size_t i, const Res& r) {
+    if (r.W > 0)
+        res_store(s, i, r);
+    else
+        res_store_w(s, i, 0.0, r.M);
 }
 
 #endif  // __CUDACC__

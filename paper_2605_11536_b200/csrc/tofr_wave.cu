@@ -1,0 +1,956 @@
+// tofr_wave.cu -- wavefront shift engine and the reuse stages built on it.
+//
+// The path-length-preserving shift (shift_sample, shiftmap.hpp:662-783) is the
+// hot operation of temporal and spatial reuse.  Run as one monolithic device
+// function per reservoir it keeps whole samples in local memory and serialises
+// very different phases (prefix replay, Newton, occlusion, rebuild) inside a
+// warp.  Here a reuse stage is a short pipeline over compacted job queues:
+//
+//   prep     one thread per reservoir item decides which shifts the merge
+//            needs (forward: neighbour sample -> pixel; inverse: the pixel's
+//            sample -> neighbour) and appends them to the queue with warp
+//            ballots + one atomic per warp;
+//   solve    k_shift_solve: record checks, prefix (stored / G-buffer / lane
+//            replay), suffix and the Newton solve.  Lanes refill from the
+//            queue as soon as their job finishes, so a warp always runs 32
+//            Newton trials together (persistent threads, per-lane refill);
+//   finish   k_shift_finish: the two occlusion rays, Jacobian clamp, rebuild
+//            of the shifted sample, output (the mapped record for forward
+//            shifts, p-hat of the source gate for inverse shifts);
+//   apply    one thread per item runs the GRIS merge with the reference's RNG
+//            stream and writes the reservoir (chunk 0 only when the kept sample
+//            is already in place).
+//
+// Same IEEE operations in the same order as the per-reservoir code, same RNG
+// draws, same integer counters: results are bit-identical to it.
+#include <cuda_runtime.h>
+
+// The shift kernels are small enough to take FP64 division and square root
+// inline: out-of-line math (tofr_core.h) would force the Newton state across
+// call boundaries (caller-saved registers -> local memory).
+#define TOFR_OUTLINE_MATH 0
+
+#include "tofr_kcommon.cuh"
+#include "tofr_store.cuh"
+
+#ifndef TOFR_WAVE_MINB
+#define TOFR_WAVE_MINB 4
+#endif
+
+namespace tofr_b200 {
+
+// ---------------------------------------------------------------------------
+// job records (chunk-major, kJobChunks x 16 B)
+//   0: item (u64), meta (u32), -      2: s_center, d_center     4-6: solve -> finish
+//   1: spx, spy, dpx, dpy (i32)       3: d_width, -                  (see sol_*)
+
+struct Job {
+    size_t item;
+    uint32_t meta;
+    int spx, spy, dpx, dpy;
+    double sc, dc, dw;
+};
+
+__device__ __forceinline__ double2 jld(const ShiftQueue& q, int c, uint32_t k) {
+    return __ldcg(&q.jobs[size_t(c) * q.cap + k]);
+}
+__device__ __forceinline__ void jst(const ShiftQueue& q, int c, uint32_t k, double2 v) {
+    __stcg(&q.jobs[size_t(c) * q.cap + k], v);
+}
+
+__device__ __forceinline__ void job_put(const ShiftQueue& q, uint32_t k, size_t item, uint32_t meta, int spx, int spy,
+                                        int dpx, int dpy, double sc, double dc, double dw) {
+    double2 c0;
+    uint64_t it = item;
+    uint2 mm = make_uint2(meta, 0);
+    memcpy(&c0.x, &it, 8);
+    memcpy(&c0.y, &mm, 8);
+    jst(q, 0, k, c0);
+    int4 px = make_int4(spx, spy, dpx, dpy);
+    double2 c1;
+    memcpy(&c1, &px, 16);
+    jst(q, 1, k, c1);
+    jst(q, 2, k, make_double2(sc, dc));
+    jst(q, 3, k, make_double2(dw, 0.0));
+}
+
+__device__ __forceinline__ Job job_get(const ShiftQueue& q, uint32_t k) {
+    Job j;
+    double2 c0 = jld(q, 0, k), c1 = jld(q, 1, k), c2 = jld(q, 2, k), c3 = jld(q, 3, k);
+    uint64_t it;
+    uint2 mm;
+    memcpy(&it, &c0.x, 8);
+    memcpy(&mm, &c0.y, 8);
+    int4 px;
+    memcpy(&px, &c1, 16);
+    j.item = size_t(it);
+    j.meta = mm.x;
+    j.spx = px.x;
+    j.spy = px.y;
+    j.dpx = px.z;
+    j.dpy = px.w;
+    j.sc = c2.x;
+    j.dc = c2.y;
+    j.dw = c3.x;
+    return j;
+}
+
+// solve -> finish hand-off: solved point and triangle, J_newton, status
+// (bit 0: proceed to occlusion; bit 1: the point's normal is still the
+// record's pn -- it never left the start triangle -- else it is the normal of
+// the triangle a re-projection ray hit, reproject_to_mesh)
+__device__ __forceinline__ void sol_put(const ShiftQueue& q, uint32_t k, const V3& pos, int tri, double jn,
+                                        int status) {
+    jst(q, 4, k, make_double2(pos.x, pos.y));
+    jst(q, 5, k, make_double2(pos.z, jn));
+    double2 c6;
+    c6.x = 0;
+    int2 ts = make_int2(tri, status);
+    memcpy(&c6.y, &ts, 8);
+    jst(q, 6, k, c6);
+}
+__device__ __forceinline__ void sol_fail(const ShiftQueue& q, uint32_t k) { sol_put(q, k, splat(0), -1, 0.0, 0); }
+
+// Warp-aggregated append: every lane of the warp must call it (converged).
+// Returns the job slot for lanes with `want`, kNoJob otherwise; a full queue
+// raises the overflow bit of the band error flag.
+__device__ __forceinline__ uint32_t queue_append(const ShiftQueue& q, bool want, unsigned long long* err) {
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return kNoJob;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&q.ctl[1], uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    uint32_t k = base + __popc(m & ((1u << lane) - 1));
+    if (!want) return kNoJob;
+    if (k >= q.cap) {
+        atomicAdd(err, 1ull << 32);
+        return kNoJob;
+    }
+    return k;
+}
+
+// ---------------------------------------------------------------------------
+// record fields straight from the reservoir store (tofr_store.cuh layout)
+
+__device__ __forceinline__ V3 rec_p(const ResStore& s, size_t i) {
+    double2 a = ld2(s, 10, i), b = ld2(s, 11, i);
+    return V3{a.y, b.x, b.y};
+}
+__device__ __forceinline__ V3 rec_pn(const ResStore& s, size_t i) {
+    double2 a = ld2(s, 12, i), b = ld2(s, 13, i);
+    return V3{a.x, a.y, b.x};
+}
+__device__ __forceinline__ V3 rec_p2(const ResStore& s, size_t i) {
+    double2 a = ld2(s, 13, i), b = ld2(s, 14, i);
+    return V3{a.y, b.x, b.y};
+}
+__device__ __forceinline__ V3 rec_n2(const ResStore& s, size_t i) {
+    double2 a = ld2(s, 15, i), b = ld2(s, 16, i);
+    return V3{a.x, a.y, b.x};
+}
+__device__ __forceinline__ V3 rec_wo2(const ResStore& s, size_t i) {
+    double2 a = ld2(s, 16, i), b = ld2(s, 17, i);
+    return V3{a.y, b.x, b.y};
+}
+__device__ __forceinline__ V3 rec_suffix_f(const ResStore& s, size_t i, int& m2) {
+    double2 a = ld2(s, 18, i), b = ld2(s, 19, i);
+    int2 mi;
+    memcpy(&mi, &b.y, 8);
+    m2 = mi.x;
+    return V3{a.x, a.y, b.x};
+}
+
+// stored_prefix (identity shift: same pixel and frame), from the store
+__device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const ResStore& s, size_t i, int tri1) {
+    Prefix pre;
+    double2 c5 = ld2(s, 5, i), c6 = ld2(s, 6, i), c7 = ld2(s, 7, i), c8 = ld2(s, 8, i), c9 = ld2(s, 9, i),
+            c10 = ld2(s, 10, i);
+    pre.ok = 1;
+    pre.pdf = c5.x;
+    pre.len = c5.y;
+    pre.fw = V3{c6.x, c6.y, c7.x};
+    pre.p1 = V3{c7.y, c8.x, c8.y};
+    pre.n1 = F.tri[tri1].n;
+    pre.wi1 = V3{c9.x, c9.y, c10.x};
+    pre.tri1 = tri1;
+    pre.m1 = F.tri[tri1].mat;
+    return pre;
+}
+
+// hybrid_base_shift for k = 2 (shiftmap.hpp:459-528 with no replayed bounce):
+// the prefix is the destination pixel's primary hit.
+__device__ __forceinline__ Prefix gbuffer_prefix(const FrameView& F, const GHit* gbuf, int px, int py) {
+    Prefix out;
+    out.ok = 0;
+    GHit g = gbuf[size_t(py) * F.cam.w + px];
+    if (g.tri < 0) return out;
+    V3 d0 = primary_dir(F.cam, px, py);
+    int mat = F.tri[g.tri].mat;
+    if (!F.mats[mat].reconnectable) return out;
+    out.ok = 1;
+    out.pdf = 1;
+    out.len = g.t;
+    out.fw = splat(1);
+    out.p1 = F.cam.pos + d0 * g.t;
+    out.n1 = F.tri[g.tri].n;
+    out.wi1 = -d0;
+    out.tri1 = g.tri;
+    out.m1 = mat;
+    return out;
+}
+
+// hybrid_base_shift with k - 2 replayed bounces (mirror / low-roughness
+// scenes): lanes read from the store.  Out of line: rare and ray-heavy.
+static __device__ __noinline__ Prefix replay_prefix(const FrameView* Fp, const GHit* gbuf, int px, int py,
+                                                    ResStore s, size_t item, int k, int use_rr) {
+    Rec rec;
+    rec.k = k;
+    double2 c20 = ld2(s, 20, item), c21 = ld2(s, 21, item);
+    memcpy(&rec.lane_key, &c20.x, 8);
+    memcpy(&rec.lane_ctr[0], &c20.y, 8);
+    memcpy(&rec.lane_ctr[4], &c21, 12);
+    Dom dom{px, py, 0.0, 0.0, Fp, gbuf};
+    PathCfg cfg;
+    cfg.use_rr = use_rr;
+    return base_shift(dom, rec, cfg);
+}
+
+__device__ __forceinline__ Prefix job_prefix(const FrameView& F, const GHit* gbuf, const Job& jb, bool identity,
+                                             const ResStore& st, const Meta& mt, int use_rr) {
+    if (identity) return stored_prefix_at(F, st, jb.item, mt.tri1);
+    if (mt.k == 2) return gbuffer_prefix(F, gbuf, jb.dpx, jb.dpy);
+    return replay_prefix(&F, gbuf, jb.dpx, jb.dpy, st, jb.item, mt.k, use_rr);
+}
+
+// suffix_geometry (shiftmap.hpp:546-575)
+__device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore& st, size_t item, int skind) {
+    Suffix s;
+    s.ok = 0;
+    s.n2 = splat(0);
+    if (skind == SK_SURFACE) {
+        s.p2 = rec_p2(st, item);
+        s.n2 = rec_n2(st, item);
+        s.len = ld2(st, 3, item).y;
+        s.ok = 1;
+    } else if (skind == SK_LIGHT) {
+        s.p2 = F.light.pos;
+        s.len = 0;
+        s.ok = 1;
+    } else {
+        if (!F.lsub.valid) return s;
+        s.p2 = F.lsub.pos;
+        s.n2 = F.lsub.n;
+        s.len = F.lsub.chain_len;
+        s.ok = 1;
+    }
+    return s;
+}
+
+// reproject_to_mesh (shiftmap.hpp:275-307), ray fallbacks: the plane point left
+// the current triangle.  Out of line, arguments by value.
+struct SurfR {
+    V3 pos, n;
+    int tri, ok;
+};
+static __device__ __noinline__ SurfR reproject_rays(const FrameView* Fp, int cur_tri, V3 plane_pt, V3 p1) {
+    const FrameView& F = *Fp;
+    SurfR out;
+    out.ok = 0;
+    V3 tn = F.tri[cur_tri].n;
+    V3 dir = plane_pt - p1;
+    double dl = norm(dir);
+    Hit h;
+    if (dl > 0) {
+        dir = dir / dl;
+        if (fabs(dot(dir, tn)) > 1e-4) {
+            if (intersect(F, p1, dir, h)) {
+                out.pos = h.pos;
+                out.n = F.tri[h.tri].n;
+                out.tri = h.tri;
+                out.ok = 1;
+                return out;
+            }
+        }
+    }
+    double off = 1e-3 * F.diag;
+    if (trace_closest(F, plane_pt + tn * off, -tn, 0, 2 * off, h) ||
+        trace_closest(F, plane_pt - tn * off, tn, 0, 2 * off, h)) {
+        out.pos = h.pos;
+        out.n = F.tri[h.tri].n;
+        out.tri = h.tri;
+        out.ok = 1;
+    }
+    return out;
+}
+
+// in-triangle test of reproject_to_mesh
+__device__ __forceinline__ bool in_triangle(const FrameView& F, int tri, const V3& plane_pt) {
+    const GTriIsect& g = tri_geo(F, tri);
+    V3 e1 = g.e1, e2 = g.e2, d = plane_pt - g.v0;
+    double d11 = dot(e1, e1), d12 = dot(e1, e2), d22 = dot(e2, e2);
+    double dv1 = dot(d, e1), dv2 = dot(d, e2);
+    double dt = d11 * d22 - d12 * d12;
+    if (!(dt > 0)) return false;
+    double u = (d22 * dv1 - d12 * dv2) / dt;
+    double v = (d11 * dv2 - d12 * dv1) / dt;
+    return u >= 0 && v >= 0 && u + v <= 1;
+}
+
+// per-thread shift counters in registers (constant indices only)
+struct Ctr {
+    uint32_t v[SC_COUNT];
+};
+__device__ __forceinline__ void ctr_flush(const Ctr& c, unsigned long long* out) {
+    uint32_t t[SC_COUNT];
+#pragma unroll
+    for (int k = 0; k < SC_COUNT; ++k) t[k] = c.v[k];
+    flush_ctr(t, out);
+}
+
+// stage the two frames of a reuse stage in shared memory (once when equal)
+__device__ __forceinline__ void stage_two(FrameView& F0, FrameView& F1, FrameView* sF, unsigned char* smem) {
+    size_t off = 0;
+    bool same = F1.nodes == F0.nodes && F1.tri_isect == F0.tri_isect;
+    stage_frame(F0, smem, off);
+    if (same) {
+        F1.nodes = F0.nodes;
+        F1.tri_isect = F0.tri_isect;
+    } else {
+        stage_frame(F1, smem, off);
+    }
+    if (threadIdx.x == 0) {
+        sF[0] = F0;
+        sF[1] = F1;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// solve: checks, prefix, suffix, Newton (newton_solve, shiftmap.hpp:314-378)
+
+__global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
+    k_shift_solve(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
+                  ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ FrameView sF[2];
+    stage_two(F0, F1, sF, smem);
+    const uint32_t j0 = q.ctl[0];
+    uint32_t j1 = q.ctl[1];
+    if (j1 > q.cap) j1 = uint32_t(q.cap);
+    const int lane = threadIdx.x & 31;
+    Ctr ctr;
+#pragma unroll
+    for (int k = 0; k < SC_COUNT; ++k) ctr.v[k] = 0;
+
+    bool active = false, exhausted = false, init = false, count = false;
+    uint32_t job = 0;
+    int dsel = 0;
+    V3 p1, p2, spos, cpos;
+    int stri = -1, ctri = -1;
+    bool cn_rec = true;  // current point's normal = the record's pn
+    Frame2 Js, Jc;
+    double delta = 0, tol = 0, fnorm = 0, scale = 1, edet = 0, engrad = 0;
+    V2 eF{0, 0}, step{0, 0};
+    M2 edFp{0, 0, 0, 0};
+    int iter = 0, bt = 0;
+
+    for (;;) {
+        // ---- refill: lanes without a job take the next ones (one atomic per warp)
+        bool need = !active && !exhausted;
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(wq, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (need) {
+                unsigned long long kk = j0 + base + __popc(m & ((1u << lane) - 1));
+                if (kk >= j1) {
+                    exhausted = true;
+                } else {
+                    job = uint32_t(kk);
+                    Job jb = job_get(q, job);
+                    dsel = (jb.meta & JOB_DST1) ? 1 : 0;
+                    const FrameView& F = sF[dsel];
+                    const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+                    count = (jb.meta & JOB_COUNT) != 0;
+                    if (count) ctr.v[SC_ATTEMPTS]++;
+                    Meta mt = ld_meta(st, jb.item);
+                    bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
+                    bool ok = mt.valid && !(!same_frame && mt.skind == SK_SURFACE && F.geo_motion);
+                    Prefix pre;
+                    Suffix suf;
+                    if (ok) {
+                        bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
+                        pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, cfg.use_rr);
+                        ok = pre.ok;
+                    }
+                    if (ok) {
+                        suf = job_suffix(F, st, jb.item, mt.skind);
+                        ok = suf.ok;
+                    }
+                    if (!ok) {
+                        if (count) ctr.v[SC_REPLAY_FAILED]++;
+                        sol_fail(q, job);
+                    } else {
+                        spos = rec_p(st, jb.item);
+                        stri = mt.ptri;
+                        if (!cfg.newton) {
+                            sol_put(q, job, spos, stri, 1.0, 3);
+                        } else {
+                            p1 = pre.p1;
+                            p2 = suf.p2;
+                            double src_len = ld2(st, 1, jb.item).y;
+                            double gate_delta = jb.dc - jb.sc;
+                            double target_local = src_len + gate_delta - pre.len - suf.len;
+                            delta = target_local - lc_value(p1, p2, spos);
+                            tol = 0.01 * jb.dw;
+                            if (count) ctr.v[SC_SOLVES]++;
+                            Js = tangent_frame(F, stri);
+                            init = true;
+                            active = true;
+                        }
+                    }
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, exhausted)) break;
+        if (!active) continue;
+
+        // ---- one Newton trial (the initial evaluation at the start point is trial 0)
+        const FrameView& F = sF[dsel];
+        V3 tpos;
+        int ttri;
+        bool have, tn_rec;
+        if (init) {
+            tpos = spos;
+            tn_rec = true;
+            ttri = stri;
+            have = true;
+        } else {
+            V3 plane_pt = cpos + to_world(Jc, step * scale);
+            if (in_triangle(F, ctri, plane_pt)) {
+                tpos = plane_pt;
+                tn_rec = cn_rec;
+                ttri = ctri;
+                have = true;
+            } else {
+                SurfR r = reproject_rays(&F, ctri, plane_pt, p1);
+                tpos = r.pos;
+                tn_rec = false;
+                ttri = r.tri;
+                have = r.ok;
+            }
+        }
+        bool accept = false, fin = false, conv = false;
+        double jac = 0;
+        if (have) {
+            Frame2 Jt = init ? Js : tangent_frame(F, ttri);
+            Constraint et = assemble(p1, p2, spos, Js, tpos, Jt, delta, cfg.gauge);
+            double fn = hypot(et.F.x, et.F.y);
+            if (init || fn < fnorm) {
+                accept = true;
+                cpos = tpos;
+                cn_rec = tn_rec;
+                ctri = ttri;
+                Jc = Jt;
+                eF = et.F;
+                edFp = et.dFp;
+                edet = det(et.dF);
+                engrad = norm(et.grad_cur);
+                fnorm = fn;
+                if (!init) ++iter;
+            }
+        }
+        if (accept) {
+            init = false;
+            if (fabs(eF.x) <= tol && fabs(eF.y) <= tol) {
+                double dc = det(edFp);
+                double j = dc == 0 ? 0 : edet / dc;
+                fin = true;
+                conv = (j > 0) && isfinite(j);
+                jac = j;
+            } else if (iter >= 5 || engrad < 1e-8 * F.diag || !solve2x2(edFp, -eF, step)) {
+                fin = true;
+            } else {
+                bt = 0;
+                scale = 1.0;
+            }
+        } else if (++bt > 8) {
+            fin = true;  // no halving accepted
+        } else {
+            scale *= 0.5;
+        }
+        if (fin) {
+            if (count) ctr.v[SC_ITERATIONS] += uint32_t(iter);
+            if (conv && !F.mats[F.tri[ctri].mat].reconnectable) {
+                if (count) {
+                    ctr.v[SC_NEWTON_OK]++;
+                    ctr.v[SC_NEWTON_FAILED]++;
+                }
+                sol_fail(q, job);
+            } else if (conv) {
+                if (count) ctr.v[SC_NEWTON_OK]++;
+                sol_put(q, job, cpos, ctri, jac, cn_rec ? 3 : 1);
+            } else {
+                if (count) ctr.v[SC_NEWTON_FAILED]++;
+                sol_fail(q, job);
+            }
+            active = false;
+            iter = 0;
+        }
+    }
+    ctr_flush(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// finish: occlusion, Jacobian, rebuild (shift_sample tail + rebuild_sample,
+// shiftmap.hpp:579-654, :740-783), output
+
+__device__ __forceinline__ void out_fail(const ShiftQueue& q, uint32_t k) { st2(q.out, 0, k, 0.0, 0.0); }
+
+__global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
+    k_shift_finish(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
+                   ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ FrameView sF[2];
+    stage_two(F0, F1, sF, smem);
+    const uint32_t j0 = q.ctl[0];
+    uint32_t j1 = q.ctl[1];
+    if (j1 > q.cap) j1 = uint32_t(q.cap);
+    size_t njobs = j1 > j0 ? j1 - j0 : 0;
+    Ctr ctr;
+#pragma unroll
+    for (int k = 0; k < SC_COUNT; ++k) ctr.v[k] = 0;
+    TOFR_FOR_ITEMS(i, njobs, wq) {
+        uint32_t k = j0 + uint32_t(i);
+        double2 c6 = jld(q, 6, k);
+        int2 ts;
+        memcpy(&ts, &c6.y, 8);
+        if (!(ts.y & 1)) {
+            out_fail(q, k);
+            continue;
+        }
+        Job jb = job_get(q, k);
+        int dsel = (jb.meta & JOB_DST1) ? 1 : 0;
+        const FrameView& F = sF[dsel];
+        const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+        bool count = (jb.meta & JOB_COUNT) != 0;
+        Meta mt = ld_meta(st, jb.item);
+        bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
+        bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
+        Prefix pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, cfg.use_rr);
+        Suffix suf = job_suffix(F, st, jb.item, mt.skind);
+        double2 c4 = jld(q, 4, k), c5 = jld(q, 5, k);
+        V3 ppos{c4.x, c4.y, c5.x};
+        int ptri = ts.x;
+        V3 pnrm = (ts.y & 2) ? rec_pn(st, jb.item) : F.tri[ptri].n;
+        double j_newton = c5.y;
+        if (occluded(F, pre.p1, ppos) || occluded(F, ppos, suf.p2)) {
+            if (count) ctr.v[SC_OCCLUDED]++;
+            out_fail(q, k);
+            continue;
+        }
+        double rec_prefix_pdf = ld2(st, 5, jb.item).x;
+        double jac = (rec_prefix_pdf / pre.pdf) * j_newton;
+        if (!isfinite(jac) || jac < cfg.jac_min || jac > cfg.jac_max) {
+            if (count) ctr.v[SC_JAC_CLAMPED]++;
+            out_fail(q, k);
+            continue;
+        }
+        // rebuild_sample
+        V3 d1 = ppos - pre.p1;
+        double l1 = norm(d1);
+        V3 d2 = suf.p2 - ppos;
+        double l2 = norm(d2);
+        bool ok = !(l1 <= 2 * F.eps_ray) && !(l2 <= 2 * F.eps_ray);
+        V3 f = splat(0);
+        int m2 = -1;
+        if (ok) {
+            V3 u1 = d1 / l1;
+            V3 u2 = d2 / l2;
+            const GMat& m1 = F.mats[pre.m1];
+            f = pre.fw * eval_bsdf(m1, pre.n1, pre.wi1, u1) * geom_term(pre.p1, pre.n1, ppos, pnrm);
+            const GMat& mp = F.mats[F.tri[ptri].mat];
+            f = f * eval_bsdf(mp, pnrm, -u1, u2);
+            if (mt.skind == SK_SURFACE) {
+                V3 sf = rec_suffix_f(st, jb.item, m2);
+                V3 n2 = suf.n2, p2 = suf.p2;
+                const GMat& mm2 = F.mats[m2];
+                V3 f2 = mm2.kind == MAT_MIRROR ? splat(0) : eval_bsdf(mm2, n2, -u2, rec_wo2(st, jb.item));
+                f = f * (geom_term(ppos, pnrm, p2, n2) * f2 * sf);
+            } else if (mt.skind == SK_LIGHT) {
+                LightSample ls;
+                if (!light_sample(F.light, ppos, ls)) {
+                    f = splat(0);
+                } else {
+                    f = f * (fabs(dot(pnrm, u2)) * ls.value);
+                }
+            } else {
+                V3 fs = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -u2, F.lsub.wo_light);
+                f = f * (geom_term(ppos, pnrm, F.lsub.pos, F.lsub.n) * fs * F.lsub.power);
+            }
+            ok = finite3(f);
+        }
+        if (!ok) {
+            if (count) ctr.v[SC_REPLAY_FAILED]++;
+            out_fail(q, k);
+            continue;
+        }
+        double len = pre.len + l1 + l2 + suf.len;
+        if (count && gate_w(jb.dc, jb.dw, len) > 0 && luminance(f) > 0) ctr.v[SC_SUCCESS]++;
+        if (!(jb.meta & JOB_FULL)) {  // inverse shift: p-hat of the source gate times |J|
+            st2(q.out, 0, k, luminance(f) * gate_w(jb.dc, jb.dw, len) * jac, 1.0);
+            continue;
+        }
+        // mapped record (rebuild_sample's record update, stored as res_store would)
+        const ResStore& o = q.out;
+        st2(o, 0, k, jac, 1.0);
+        st2(o, 1, k, 0.0, len);
+        st2(o, 2, k, f.x, f.y);
+        double suffix_len = mt.skind == SK_LIGHTSUB ? F.lsub.chain_len : ld2(st, 3, jb.item).y;
+        st2(o, 3, k, f.z, suffix_len);
+        {
+            Meta om = mt;
+            om.has = 1;
+            om.pad0 = om.pad1 = 0;
+            om.tri1 = pre.tri1;
+            om.ptri = ptri;
+            double2 v;
+            memcpy(&v, &om, 16);
+            st2(o, 4, k, v.x, v.y);
+        }
+        st2(o, 5, k, pre.pdf, pre.len);
+        st2(o, 6, k, pre.fw.x, pre.fw.y);
+        st2(o, 7, k, pre.fw.z, pre.p1.x);
+        st2(o, 8, k, pre.p1.y, pre.p1.z);
+        st2(o, 9, k, pre.wi1.x, pre.wi1.y);
+        st2(o, 10, k, pre.wi1.z, ppos.x);
+        st2(o, 11, k, ppos.y, ppos.z);
+        st2(o, 12, k, pnrm.x, pnrm.y);
+        V3 p2o = mt.skind == SK_LIGHTSUB ? F.lsub.pos : (mt.skind == SK_LIGHT ? F.light.pos : suf.p2);
+        st2(o, 13, k, pnrm.z, p2o.x);
+        st2(o, 14, k, p2o.y, p2o.z);
+        double2 c15 = ld2(st, 15, jb.item), c16 = ld2(st, 16, jb.item);
+        if (mt.skind == SK_LIGHTSUB) {
+            c15 = make_double2(F.lsub.n.x, F.lsub.n.y);
+            c16.x = F.lsub.n.z;
+        }
+        __stcg(&o.base[15 * o.stride + k], c15);
+        __stcg(&o.base[16 * o.stride + k], c16);
+        for (int c = 17; c < (mt.nl > 0 ? kResChunks : 20); ++c)
+            __stcg(&o.base[size_t(c) * o.stride + k], ld2(st, c, jb.item));
+    }
+    ctr_flush(ctr, ctr_out);
+}
+
+// ---------------------------------------------------------------------------
+// merge-side helpers
+
+// Selected mapped record (job k) -> reservoir `it` with the merge's W, M, p-hat.
+__device__ __forceinline__ void put_mapped(const ResStore& o, uint32_t k, const ResStore& dst, size_t it, double W,
+                                           double M, double phat) {
+    st2(dst, 0, it, W, M);
+    st2(dst, 1, it, phat, ld2(o, 1, k).y);
+    double2 c4 = ld2(o, 4, k);
+    Meta mt;
+    memcpy(&mt, &c4, 16);
+    int nc = mt.nl > 0 ? kResChunks : 20;
+    for (int c = 2; c < nc; ++c) __stcg(&dst.base[size_t(c) * dst.stride + it], ld2(o, c, k));
+}
+
+// Reservoir copy src[it] -> dst[it] with a new W, M (sample and p-hat kept).
+__device__ __forceinline__ void copy_res(const ResStore& src, const ResStore& dst, size_t it, double W, double M) {
+    st2(dst, 0, it, W, M);
+    double2 c4 = ld2(src, 4, it);
+    Meta mt;
+    memcpy(&mt, &c4, 16);
+    int nc = mt.nl > 0 ? kResChunks : 20;
+    for (int c = 1; c < nc; ++c) __stcg(&dst.base[size_t(c) * dst.stride + it], ld2(src, c, it));
+}
+
+// header (W, M, has, p-hat) of a reservoir
+__device__ __forceinline__ void res_head_phat(const ResStore& s, size_t i, Res& r) {
+    res_load_head(s, i, r);
+    if (r.has) r.phat = ld2(s, 1, i).x;
+}
+
+// forward-shift output of job k: ok, Jacobian, mapped f and length
+__device__ __forceinline__ void fwd_output(const ShiftQueue& q, uint32_t k, MergeShift& ms, Sample& mapped) {
+    if (k == kNoJob) return;
+    double2 o0 = ld2(q.out, 0, k);
+    if (!(o0.y > 0)) return;
+    ms.valid = 1;
+    ms.jac = o0.x;
+    double2 o1 = ld2(q.out, 1, k), o2 = ld2(q.out, 2, k), o3 = ld2(q.out, 3, k);
+    mapped.len = o1.y;
+    mapped.f = V3{o2.x, o2.y, o3.x};
+}
+
+__device__ __forceinline__ double inv_output(const ShiftQueue& q, uint32_t k) {
+    if (k == kNoJob) return 0.0;
+    double2 o0 = ld2(q.out, 0, k);
+    return o0.y > 0 ? o0.x : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// temporal reuse (stage::temporal_reuse, pipeline.hpp:209-229)
+
+__global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg,
+                                ResStore cur, ResStore prev, WaveScratch ws) {
+    int W = Fc.cam.w, B = cg.transient ? cg.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        bool merge = false, fwd = false, inv = false;
+        size_t src_i = 0;
+        int qx = 0, qy = 0;
+        if (live) {
+            GHit g = gc[p];
+            if (g.tri >= 0) {
+                V3 d0 = primary_dir(Fc.cam, px, py);
+                V3 hp = Fc.cam.pos + d0 * g.t;
+                if (project(Fp.cam, hp, qx, qy)) {
+                    if (qy < bd.t0 || qy >= bd.t1) {  // reprojection left the rows this band holds
+                        atomicAdd(bd.err, 1ull);
+                    } else {
+                        src_i = (size_t(qy) * W + qx) * B + b;
+                        double2 s0 = ld2(prev, 0, src_i);
+                        if (s0.y > 0) {
+                            merge = true;
+                            fwd = s0.x > 0;
+                            inv = ld2(cur, 0, it).x > 0;
+                        }
+                    }
+                }
+            }
+        }
+        double dc, dw, sc, sw;
+        gate_of(cg, b, dc, dw);
+        gate_of(pg, b, sc, sw);
+        uint32_t kf = queue_append(ws.q, fwd, bd.err);
+        uint32_t ki = queue_append(ws.q, inv, bd.err);
+        if (kf != kNoJob) job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
+        if (ki != kNoJob) job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
+        if (live) {
+            ws.tsrc[i] = merge ? uint64_t(src_i) : ~uint64_t(0);
+            ws.map_a[i] = kf;
+            ws.map_b[i] = ki;
+        }
+    }
+}
+
+__global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int frame_idx, ResStore cur,
+                                 ResStore prev, WaveScratch ws) {
+    int B = cg.transient ? cg.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        uint64_t s = ws.tsrc[i];
+        if (s == ~uint64_t(0)) continue;
+        size_t src_i = size_t(s), it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        double dc, dw;
+        gate_of(cg, b, dc, dw);
+        Res dst, src;
+        res_head_phat(cur, it, dst);
+        res_head_phat(prev, src_i, src);
+        MergeShift ms{0, 1.0, 0.0};
+        Sample mapped;
+        uint32_t kf = ws.map_a[i];
+        fwd_output(ws.q, kf, ms, mapped);
+        ms.phat_src_of_dst = inv_output(ws.q, ws.map_b[i]);
+        uint64_t pix = uint64_t(py) * W + px;
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
+        int which = gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        if (which == 2)
+            put_mapped(ws.q.out, kf, cur, it, dst.W, dst.M, dst.phat);
+        else  // in place: the kept sample and its p-hat are already stored
+            res_store_w(cur, it, dst.W, dst.M);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// spatial reuse (stage::spatial_reuse, pipeline.hpp:232-269): forward shifts of
+// every (neighbour j, item) pair first, then per neighbour the inverse shifts
+// of the running output and the merge (the running output and the lane-10 RNG
+// position stay in HBM between neighbours; same draws in the same order).
+
+__global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                                   int frame_idx, ResStore src_grid, WaveScratch ws) {
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
+        for (int j = 0; j < sp.neighbors; ++j) {
+            int nx = 0, ny = 0;
+            size_t si = 0;
+            // every non-empty neighbour is a forward shift attempt (counted even
+            // when its record has no reconnection vertex, as the reference does)
+            bool want = live && spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
+                        ld2(src_grid, 0, si).x > 0;
+            uint32_t k = queue_append(ws.q, want, bd.err);
+            if (k != kNoJob) job_put(ws.q, k, si, JOB_FULL | JOB_COUNT, nx, ny, px, py, dc, dc, dw);
+            if (live) ws.map_a[size_t(j) * n + i] = k;
+        }
+    }
+}
+
+__global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
+                                   int j, int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + 31) & ~size_t(31);
+    const ResStore& out_grid = j == 0 ? src_grid : dst_grid;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        int nx = 0, ny = 0;
+        size_t si = 0;
+        bool want = false;
+        if (live) {
+            uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
+            want = spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
+                   ld2(out_grid, 0, it).x > 0;
+        }
+        uint32_t k = queue_append(ws.q, want, bd.err);
+        if (k != kNoJob) job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
+        if (live) ws.map_b[i] = k;
+    }
+}
+
+__global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass, int j,
+                                int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
+    int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        size_t it = base + i;
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        uint64_t rk = spatial_rot_key(pix, pass, cfg.seed, frame_idx);
+        int nx, ny;
+        size_t si = 0;
+        bool use = spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si);
+        if (!use) {
+            if (j == 0) {  // the output starts as the pass input
+                double2 c0 = ld2(src_grid, 0, it);
+                if (c0.x > 0)
+                    copy_res(src_grid, dst_grid, it, c0.x, c0.y);
+                else
+                    res_store_w(dst_grid, it, 0.0, c0.y);
+                if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
+            }
+            continue;
+        }
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        Res out, src;
+        res_head_phat(j == 0 ? src_grid : dst_grid, it, out);
+        res_head_phat(src_grid, si, src);
+        MergeShift ms{0, 1.0, 0.0};
+        Sample mapped;
+        uint32_t kf = ws.map_a[size_t(j) * n + i];
+        if (!res_empty(src)) fwd_output(ws.q, kf, ms, mapped);
+        ms.phat_src_of_dst = inv_output(ws.q, ws.map_b[i]);
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(pass * 131 + b), 10);
+        if (j > 0) rng.ctr = ws.rng_ctr[i];
+        int which = gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        if (which == 2)
+            put_mapped(ws.q.out, kf, dst_grid, it, out.W, out.M, out.phat);
+        else if (which == 1 && j == 0)
+            copy_res(src_grid, dst_grid, it, out.W, out.M);
+        else  // kept in place (j > 0) or empty
+            res_store_w(dst_grid, it, out.W, out.M);
+        if (j + 1 < sp.neighbors) ws.rng_ctr[i] = rng.ctr;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// queue control and launchers
+
+// op 0: empty queue; op 1: mark the end (the next batch starts after it);
+// op 2: rewind to the mark.
+__global__ void k_queue_ctl(uint32_t* ctl, int op) {
+    if (op == 0) {
+        ctl[0] = ctl[1] = ctl[2] = 0;
+    } else if (op == 1) {
+        ctl[2] = ctl[1];
+        ctl[0] = ctl[1];
+    } else {
+        ctl[0] = ctl[2];
+        ctl[1] = ctl[2];
+    }
+}
+
+static int grid_n(size_t n, int block) {
+    size_t g = (n + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return int(g);
+}
+
+static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0, const GHit* g1, ResStore st0,
+                       ResStore st1, const ShiftQueue& q, const PathCfg& cfg, unsigned long long* ctr,
+                       unsigned long long* wq, cudaStream_t s) {
+    bool same = F1.nodes == F0.nodes && F1.tri_isect == F0.tri_isect;
+    size_t sm = frame_smem_bytes(F0) + (same ? 0 : frame_smem_bytes(F1));
+    size_t cap_jobs = q.cap;
+    cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
+    k_shift_solve<<<persistent_grid(reinterpret_cast<const void*>(k_shift_solve), 128, sm, cap_jobs), 128, sm, s>>>(
+        F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+    cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
+    k_shift_finish<<<persistent_grid(reinterpret_cast<const void*>(k_shift_finish), 128, sm, cap_jobs), 128, sm, s>>>(
+        F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+}
+
+void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
+                          const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx, ResStore cur,
+                          ResStore prev, const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q,
+                          cudaStream_t s) {
+    size_t n = size_t(bd.y1 - bd.y0) * Fc.cam.w * (cg.transient ? cg.h.bins : 1);
+    if (!n) return;
+    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cur, prev, ws);
+    run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, cfg, ctr, q, s);
+    k_temporal_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cfg, frame_idx, cur, prev, ws);
+}
+
+void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                         const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
+                         const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q, cudaStream_t s) {
+    size_t n = size_t(bd.y1 - bd.y0) * F.cam.w * (gg.transient ? gg.h.bins : 1);
+    if (!n) return;
+    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
+    run_shifts(F, F, g, g, src, dst, ws.q, cfg, ctr, q, s);
+    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 1);
+    for (int j = 0; j < sp.neighbors; ++j) {
+        if (j > 0) k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 2);
+        k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        run_shifts(F, F, g, g, src, dst, ws.q, cfg, nullptr, q, s);
+        k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+    }
+}
+
+}  // namespace tofr_b200
