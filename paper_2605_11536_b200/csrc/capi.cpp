@@ -259,7 +259,7 @@ Band band_of(tofr_session* s, bool prev_halo_valid) {
     return bd;
 }
 
-PathCfg path_cfg(const tofr_render_config& c, double center, double width) {
+PathCfg path_cfg(const tofr_render_config& c, double center, double width, const HScene& sc) {
     PathCfg p;
     std::memset(&p, 0, sizeof(p));
     p.max_depth = c.max_depth;
@@ -273,6 +273,9 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width) {
     p.jac_max = 50.0;
     p.m_cap = c.m_cap;
     p.seed = c.seed;
+    p.replay = 0;
+    for (const HMaterial& m : sc.materials)
+        if (!m.reconnectable()) p.replay = 1;
     return p;
 }
 
@@ -512,7 +515,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     const GHit* g = rows_base<GHit>(s->slot[sl].gbuf, s->r0, s->W);
     double center = c.gate_center + c.gate_step * f;
     double width = c.gate_width;
-    PathCfg pc = path_cfg(c, center, width);
+    PathCfg pc = path_cfg(c, center, width, s->scene);
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
     unsigned long long* q = ctr + 3 * SC_COUNT + 1;  // persistent-kernel work counter (stream-ordered reuse)
@@ -1015,7 +1018,7 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double
         GHit* g = s->slot[0].gbuf.as<GHit>();
         Band bd = band_of(s.get(), false);
         launch_gbuffer(F, bd, g, ctx->stream);
-        PathCfg pc = path_cfg(c, gate_center, gate_width);
+        PathCfg pc = path_cfg(c, gate_center, gate_width, s->scene);
         pc.ellipsoidal = 0;
         launch_reference(F, bd, g, pc, gate_center, gate_width, spp, uint64_t(frame), dm.as<double>(), ds.as<double>(),
                          s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 1, ctx->stream);

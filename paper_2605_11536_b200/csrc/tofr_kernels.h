@@ -73,7 +73,7 @@ struct SpatialParams {
 // run the shifts (k_shift_solve: record, prefix, suffix and the Newton solve;
 // k_shift_finish: occlusion, Jacobian, rebuild); the stage's merge kernel then
 // reads the per-job outputs.
-constexpr int kJobChunks = 7;
+constexpr int kJobChunks = 13;
 enum : uint32_t {
     JOB_REC1 = 1u,    // source record lives in store 1 (else store 0)
     JOB_SRC1 = 2u,    // source domain is frame 1 (else frame 0)

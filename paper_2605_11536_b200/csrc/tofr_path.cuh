@@ -96,6 +96,7 @@ struct PathCfg {
     double jac_min, jac_max;
     double m_cap;
     uint64_t seed;
+    int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
 };
 
 // rr_survival (transport.hpp:193-196)

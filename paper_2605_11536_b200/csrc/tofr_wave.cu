@@ -217,11 +217,45 @@ static __device__ __noinline__ Prefix replay_prefix(const FrameView* Fp, const G
     return base_shift(dom, rec, cfg);
 }
 
+// replayed prefix of job k (k_shift_replay) in job chunks 7-12
+__device__ __forceinline__ void replay_put(const ShiftQueue& q, uint32_t k, const Prefix& p) {
+    jst(q, 7, k, make_double2(p.pdf, p.len));
+    jst(q, 8, k, make_double2(p.fw.x, p.fw.y));
+    jst(q, 9, k, make_double2(p.fw.z, p.p1.x));
+    jst(q, 10, k, make_double2(p.p1.y, p.p1.z));
+    jst(q, 11, k, make_double2(p.wi1.x, p.wi1.y));
+    double2 c12;
+    c12.x = p.wi1.z;
+    int2 to = make_int2(p.ok ? p.tri1 : -1, p.ok);
+    memcpy(&c12.y, &to, 8);
+    jst(q, 12, k, c12);
+}
+__device__ __forceinline__ Prefix replay_get(const FrameView& F, const ShiftQueue& q, uint32_t k) {
+    Prefix p;
+    double2 c7 = jld(q, 7, k), c8 = jld(q, 8, k), c9 = jld(q, 9, k), c10 = jld(q, 10, k), c11 = jld(q, 11, k),
+            c12 = jld(q, 12, k);
+    int2 to;
+    memcpy(&to, &c12.y, 8);
+    p.ok = to.y;
+    if (!p.ok) return p;
+    p.pdf = c7.x;
+    p.len = c7.y;
+    p.fw = V3{c8.x, c8.y, c9.x};
+    p.p1 = V3{c9.y, c10.x, c10.y};
+    p.wi1 = V3{c11.x, c11.y, c12.x};
+    p.tri1 = to.x;
+    p.n1 = F.tri[p.tri1].n;  // hybrid_base_shift: n = the hit triangle's normal
+    p.m1 = F.tri[p.tri1].mat;
+    return p;
+}
+
+// prefix of the destination path: stored (identity), the primary hit (k = 2)
+// or the replayed bounces computed by k_shift_replay (k > 2)
 __device__ __forceinline__ Prefix job_prefix(const FrameView& F, const GHit* gbuf, const Job& jb, bool identity,
-                                             const ResStore& st, const Meta& mt, int use_rr) {
+                                             const ResStore& st, const Meta& mt, const ShiftQueue& q, uint32_t k) {
     if (identity) return stored_prefix_at(F, st, jb.item, mt.tri1);
     if (mt.k == 2) return gbuffer_prefix(F, gbuf, jb.dpx, jb.dpy);
-    return replay_prefix(&F, gbuf, jb.dpx, jb.dpy, st, jb.item, mt.k, use_rr);
+    return replay_get(F, q, k);
 }
 
 // suffix_geometry (shiftmap.hpp:546-575)
@@ -328,6 +362,140 @@ __device__ __forceinline__ void stage_two(FrameView& F0, FrameView& F1, FrameVie
 }
 
 // ---------------------------------------------------------------------------
+// Newton constraint, split into its start-point half (constant per job) and
+// its trial-point half.  assemble_constraint (shiftmap.hpp:155-217) evaluates
+// both at every trial; the start-point terms (gradient, length, projected
+// Hessian at the start point) are computed once here with the same operations,
+// so every value is bit-identical to assemble().
+
+// lc_value / lc_grad / lc_hess at p, sharing the edge vectors
+struct LcEval {
+    double val;   // |p1 - p| + |p2 - p|
+    V3 grad;      // -(normalize(p1 - p) + normalize(p2 - p))
+    M2 hess;      // project_sym(J, lc_hess(p1, p2, p)), only when `with_hess`
+};
+__device__ __forceinline__ LcEval lc_eval(const V3& p1, const V3& p2, const V3& p, const Frame2& J, bool with_hess) {
+    LcEval r;
+    V3 e1 = p1 - p, e2 = p2 - p;
+    double l1 = norm(e1), l2 = norm(e2);
+    V3 d1 = e1 / l1, d2 = e2 / l2;
+    r.val = l1 + l2;
+    r.grad = -(d1 + d2);
+    r.hess = M2{0, 0, 0, 0};
+    if (with_hess) {
+        // A = (I - d1 d1^T) * (1/l1) + (I - d2 d2^T) * (1/l2), row by row
+        double s1 = 1.0 / l1, s2 = 1.0 / l2;
+        double At[3], Ab[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double di1 = comp(d1, i), di2 = comp(d2, i);
+            double a0 = ((i == 0 ? 1.0 : 0.0) - di1 * d1.x) * s1 + ((i == 0 ? 1.0 : 0.0) - di2 * d2.x) * s2;
+            double a1 = ((i == 1 ? 1.0 : 0.0) - di1 * d1.y) * s1 + ((i == 1 ? 1.0 : 0.0) - di2 * d2.y) * s2;
+            double a2 = ((i == 2 ? 1.0 : 0.0) - di1 * d1.z) * s1 + ((i == 2 ? 1.0 : 0.0) - di2 * d2.z) * s2;
+            At[i] = a0 * J.t.x + a1 * J.t.y + a2 * J.t.z;
+            Ab[i] = a0 * J.b.x + a1 * J.b.y + a2 * J.b.z;
+        }
+        V3 vt{At[0], At[1], At[2]}, vb{Ab[0], Ab[1], Ab[2]};
+        r.hess = M2{dot(J.t, vt), dot(J.t, vb), dot(J.b, vt), dot(J.b, vb)};
+    }
+    return r;
+}
+
+struct StartTerms {
+    V3 g3s;     // gradient at the start point
+    V2 gs;      // ... in the start frame
+    double lvs; // path length through the start point
+    M2 Hs;      // projected Hessian at the start point (gauge != FIXED)
+};
+
+__device__ __forceinline__ StartTerms start_terms(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
+                                                  int gauge) {
+    StartTerms t;
+    LcEval e = lc_eval(p1, p2, ps, Js, gauge != GAUGE_FIXED);
+    t.g3s = e.grad;
+    t.gs = to_local(Js, e.grad);
+    t.lvs = e.val;
+    t.Hs = e.hess;
+    return t;
+}
+
+struct TrialEval {
+    V2 F;
+    M2 dFp;
+    double det_dF;   // det(dF), dF = d F / d(start coordinates)
+    double ngrad;    // |grad_cur|
+};
+
+__device__ __forceinline__ TrialEval trial_eval(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
+                                                const StartTerms& st, const V3& pc, const Frame2& Jc, double delta,
+                                                int gauge) {
+    TrialEval r;
+    LcEval e = lc_eval(p1, p2, pc, Jc, gauge != GAUGE_FIXED);
+    V2 gc = to_local(Jc, e.grad);
+    r.ngrad = norm(gc);
+    V3 disp = pc - ps;
+    V2 us = to_local(Js, disp);
+    V2 uc = to_local(Jc, disp);
+    r.F.x = e.val - st.lvs - delta;
+    V2 row_c, row_s, m_c, m_s;
+    if (gauge == GAUGE_FIXED) {
+        m_c = to_local(Jc, to_world(Js, V2{1, 0}));
+        m_s = V2{1, 0};
+        r.F.y = dot(rot90(m_c), uc);
+        row_c = rot90(m_c);
+        row_s = rot90(m_s);
+    } else if (gauge == GAUGE_RAW) {
+        m_c = to_local(Jc, st.g3s);
+        m_s = st.gs;
+        r.F.y = dot(rot90(m_c), uc);
+        row_c = rot90(m_c);
+        row_s = rot90(m_s) + st.Hs * rot90(us);
+    } else {
+        V3 mw = (st.g3s + e.grad) * 0.5;
+        m_c = to_local(Jc, mw);
+        m_s = to_local(Js, mw);
+        r.F.y = dot(rot90(m_c), uc);
+        row_c = rot90(m_c) - (e.hess * rot90(uc)) * 0.5;
+        row_s = rot90(m_s) + (st.Hs * rot90(us)) * 0.5;
+    }
+    r.dFp = M2{gc.x, gc.y, row_c.x, row_c.y};
+    r.det_dF = det(M2{-st.gs.x, -st.gs.y, -row_s.x, -row_s.y});
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// replay: prefixes with k - 2 > 0 replayed bounces (hybrid_base_shift,
+// shiftmap.hpp:459-528).  Only scenes with a non-reconnectable material (mirror,
+// glossy roughness < 0.2) have records with k > 2; the host skips this stage
+// for the others.
+
+__global__ void __launch_bounds__(128)
+    k_shift_replay(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
+                   ShiftQueue q, PathCfg cfg, unsigned long long* wq) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ FrameView sF[2];
+    stage_two(F0, F1, sF, smem);
+    const uint32_t j0 = q.ctl[0];
+    uint32_t j1 = q.ctl[1];
+    if (j1 > q.cap) j1 = uint32_t(q.cap);
+    size_t njobs = j1 > j0 ? j1 - j0 : 0;
+    TOFR_FOR_ITEMS(i, njobs, wq) {
+        uint32_t k = j0 + uint32_t(i);
+        Job jb = job_get(q, k);
+        int dsel = (jb.meta & JOB_DST1) ? 1 : 0;
+        const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+        Meta mt = ld_meta(st, jb.item);
+        bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
+        bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
+        if (!mt.valid || identity || mt.k == 2) continue;
+        const FrameView& F = sF[dsel];
+        if (!same_frame && mt.skind == SK_SURFACE && F.geo_motion) continue;
+        Prefix p = replay_prefix(&F, dsel ? g1 : g0, jb.dpx, jb.dpy, st, jb.item, mt.k, cfg.use_rr);
+        replay_put(q, k, p);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // solve: checks, prefix, suffix, Newton (newton_solve, shiftmap.hpp:314-378)
 
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
@@ -340,20 +508,24 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     uint32_t j1 = q.ctl[1];
     if (j1 > q.cap) j1 = uint32_t(q.cap);
     const int lane = threadIdx.x & 31;
-    Ctr ctr;
-#pragma unroll
-    for (int k = 0; k < SC_COUNT; ++k) ctr.v[k] = 0;
+    // shift counters: CTA-wide in shared memory (keeps 9 registers free for the
+    // Newton state); one global atomic per counter and CTA at the end
+    __shared__ unsigned int sctr[SC_COUNT];
+    if (threadIdx.x < SC_COUNT) sctr[threadIdx.x] = 0;
+    __syncthreads();
+#define SCTR(k, v) atomicAdd_block(&sctr[k], (unsigned)(v))
 
+    // per-lane Newton state (one job at a time)
     bool active = false, exhausted = false, init = false, count = false;
     uint32_t job = 0;
     int dsel = 0;
-    V3 p1, p2, spos, cpos;
-    int stri = -1, ctri = -1;
+    V3 p1{0, 0, 0}, p2{0, 0, 0}, spos{0, 0, 0}, cpos{0, 0, 0};
+    int stri = 0, ctri = 0;
     bool cn_rec = true;  // current point's normal = the record's pn
-    Frame2 Js, Jc;
-    double delta = 0, tol = 0, fnorm = 0, scale = 1, edet = 0, engrad = 0;
-    V2 eF{0, 0}, step{0, 0};
-    M2 edFp{0, 0, 0, 0};
+    Frame2 Js{{1, 0, 0}, {0, 1, 0}}, Jc{{1, 0, 0}, {0, 1, 0}};
+    StartTerms stt;
+    double delta = 0, tol = 0, fnorm = 0, scale = 1;
+    V2 step{0, 0};
     int iter = 0, bt = 0;
 
     for (;;) {
@@ -376,7 +548,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     const FrameView& F = sF[dsel];
                     const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
                     count = (jb.meta & JOB_COUNT) != 0;
-                    if (count) ctr.v[SC_ATTEMPTS]++;
+                    if (count) SCTR(SC_ATTEMPTS, 1);
                     Meta mt = ld_meta(st, jb.item);
                     bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
                     bool ok = mt.valid && !(!same_frame && mt.skind == SK_SURFACE && F.geo_motion);
@@ -384,7 +556,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     Suffix suf;
                     if (ok) {
                         bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
-                        pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, cfg.use_rr);
+                        pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, job);
                         ok = pre.ok;
                     }
                     if (ok) {
@@ -392,7 +564,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                         ok = suf.ok;
                     }
                     if (!ok) {
-                        if (count) ctr.v[SC_REPLAY_FAILED]++;
+                        if (count) SCTR(SC_REPLAY_FAILED, 1);
                         sol_fail(q, job);
                     } else {
                         spos = rec_p(st, jb.item);
@@ -407,8 +579,18 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             double target_local = src_len + gate_delta - pre.len - suf.len;
                             delta = target_local - lc_value(p1, p2, spos);
                             tol = 0.01 * jb.dw;
-                            if (count) ctr.v[SC_SOLVES]++;
+                            if (count) SCTR(SC_SOLVES, 1);
                             Js = tangent_frame(F, stri);
+                            stt = start_terms(p1, p2, spos, Js, cfg.gauge);
+                            // trial 0 evaluates the start point itself
+                            cpos = spos;
+                            ctri = stri;
+                            cn_rec = true;
+                            Jc = Js;
+                            step = V2{0, 0};
+                            scale = 1.0;
+                            iter = 0;
+                            bt = 0;
                             init = true;
                             active = true;
                         }
@@ -417,62 +599,46 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             }
         }
         if (__all_sync(0xffffffffu, exhausted)) break;
+        unsigned am = __ballot_sync(0xffffffffu, active);
         if (!active) continue;
 
-        // ---- one Newton trial (the initial evaluation at the start point is trial 0)
+        // ---- one Newton trial (trial 0 = the initial evaluation at the start point)
         const FrameView& F = sF[dsel];
-        V3 tpos;
-        int ttri;
-        bool have, tn_rec;
-        if (init) {
-            tpos = spos;
-            tn_rec = true;
-            ttri = stri;
-            have = true;
-        } else {
-            V3 plane_pt = cpos + to_world(Jc, step * scale);
-            if (in_triangle(F, ctri, plane_pt)) {
-                tpos = plane_pt;
-                tn_rec = cn_rec;
-                ttri = ctri;
-                have = true;
-            } else {
-                SurfR r = reproject_rays(&F, ctri, plane_pt, p1);
+        V3 tpos = cpos + to_world(Jc, step * scale);  // plane point
+        int ttri = ctri;
+        bool tn_rec = cn_rec, have = true;
+        if (init) tpos = spos;
+        if (!init && !in_triangle(F, ctri, tpos)) {  // re-projection rays (reproject_to_mesh)
+            SurfR r = reproject_rays(&F, ctri, tpos, p1);
+            have = r.ok;
+            if (have) {
                 tpos = r.pos;
-                tn_rec = false;
                 ttri = r.tri;
-                have = r.ok;
+                tn_rec = false;
             }
         }
-        bool accept = false, fin = false, conv = false;
+        __syncwarp(am);
+        Frame2 Jt = tangent_frame(F, ttri);
+        TrialEval et = trial_eval(p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
+        double fn = hypot(et.F.x, et.F.y);
+        bool accept = have && (init || fn < fnorm);
+        bool fin = false, conv = false;
         double jac = 0;
-        if (have) {
-            Frame2 Jt = init ? Js : tangent_frame(F, ttri);
-            Constraint et = assemble(p1, p2, spos, Js, tpos, Jt, delta, cfg.gauge);
-            double fn = hypot(et.F.x, et.F.y);
-            if (init || fn < fnorm) {
-                accept = true;
-                cpos = tpos;
-                cn_rec = tn_rec;
-                ctri = ttri;
-                Jc = Jt;
-                eF = et.F;
-                edFp = et.dFp;
-                edet = det(et.dF);
-                engrad = norm(et.grad_cur);
-                fnorm = fn;
-                if (!init) ++iter;
-            }
-        }
         if (accept) {
+            if (!init) ++iter;
             init = false;
-            if (fabs(eF.x) <= tol && fabs(eF.y) <= tol) {
-                double dc = det(edFp);
-                double j = dc == 0 ? 0 : edet / dc;
+            cpos = tpos;
+            cn_rec = tn_rec;
+            ctri = ttri;
+            Jc = Jt;
+            fnorm = fn;
+            if (fabs(et.F.x) <= tol && fabs(et.F.y) <= tol) {
+                double dc = det(et.dFp);
+                double j = dc == 0 ? 0 : et.det_dF / dc;
                 fin = true;
                 conv = (j > 0) && isfinite(j);
                 jac = j;
-            } else if (iter >= 5 || engrad < 1e-8 * F.diag || !solve2x2(edFp, -eF, step)) {
+            } else if (iter >= 5 || et.ngrad < 1e-8 * F.diag || !solve2x2(et.dFp, -et.F, step)) {
                 fin = true;
             } else {
                 bt = 0;
@@ -484,25 +650,27 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             scale *= 0.5;
         }
         if (fin) {
-            if (count) ctr.v[SC_ITERATIONS] += uint32_t(iter);
+            if (count) SCTR(SC_ITERATIONS, iter);
             if (conv && !F.mats[F.tri[ctri].mat].reconnectable) {
                 if (count) {
-                    ctr.v[SC_NEWTON_OK]++;
-                    ctr.v[SC_NEWTON_FAILED]++;
+                    SCTR(SC_NEWTON_OK, 1);
+                    SCTR(SC_NEWTON_FAILED, 1);
                 }
                 sol_fail(q, job);
             } else if (conv) {
-                if (count) ctr.v[SC_NEWTON_OK]++;
+                if (count) SCTR(SC_NEWTON_OK, 1);
                 sol_put(q, job, cpos, ctri, jac, cn_rec ? 3 : 1);
             } else {
-                if (count) ctr.v[SC_NEWTON_FAILED]++;
+                if (count) SCTR(SC_NEWTON_FAILED, 1);
                 sol_fail(q, job);
             }
             active = false;
-            iter = 0;
         }
     }
-    ctr_flush(ctr, ctr_out);
+    __syncthreads();
+    if (ctr_out && threadIdx.x < SC_COUNT && sctr[threadIdx.x])
+        atomicAdd(&ctr_out[threadIdx.x], (unsigned long long)sctr[threadIdx.x]);
+#undef SCTR
 }
 
 // ---------------------------------------------------------------------------
@@ -541,7 +709,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         Meta mt = ld_meta(st, jb.item);
         bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
         bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
-        Prefix pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, cfg.use_rr);
+        Prefix pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, k);
         Suffix suf = job_suffix(F, st, jb.item, mt.skind);
         double2 c4 = jld(q, 4, k), c5 = jld(q, 5, k);
         V3 ppos{c4.x, c4.y, c5.x};
@@ -916,6 +1084,11 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
     bool same = F1.nodes == F0.nodes && F1.tri_isect == F0.tri_isect;
     size_t sm = frame_smem_bytes(F0) + (same ? 0 : frame_smem_bytes(F1));
     size_t cap_jobs = q.cap;
+    if (cfg.replay) {
+        cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
+        k_shift_replay<<<persistent_grid(reinterpret_cast<const void*>(k_shift_replay), 128, sm, cap_jobs), 128, sm,
+                         s>>>(F0, F1, g0, g1, st0, st1, q, cfg, wq);
+    }
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
     k_shift_solve<<<persistent_grid(reinterpret_cast<const void*>(k_shift_solve), 128, sm, cap_jobs), 128, sm, s>>>(
         F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
