@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu"]
+DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu", "tofr_trace.cu"]
 HOST_SOURCES = ["host_scene.cpp", "capi.cpp"]
 HEADERS = [
     "tofr_core.h",

@@ -199,6 +199,35 @@ TOFR_HD bool trace_any_impl(const GNode* nodes, const GTriIsect* tris, const V3&
     return false;
 }
 
+// One traversal for both ray kinds: closest hit (any = false) or the first hit
+// on the segment (any = true; Bvh::occluded keeps t_max fixed and returns at
+// the first hit, which is what the unshrunk `best` gives until that hit).
+// Lets a kernel trace shadow and extension rays of different lanes together.
+TOFR_HD TraceHit trace_ray_impl(const GNode* nodes, const GTriIsect* tris, const V3& o, const V3& d, double tmin,
+                                double tmax, bool any) {
+    V3 inv = V3{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+    double best = tmax;
+    int best_slot = -1;
+    int ni = 0;
+    while (ni >= 0) {
+        const GNode& n = nodes[ni];
+        if (!ray_box(o, inv, n, tmin, best)) {
+            ni = n.miss_next;
+            continue;
+        }
+        for (int i = 0; i < n.count; ++i) {
+            double t;
+            if (ray_tri(o, d, tris[n.first + i], tmin, best, t)) {
+                best = t;
+                best_slot = n.first + i;
+                if (any) return TraceHit{best, best_slot};
+            }
+        }
+        ni = n.hit_next;
+    }
+    return TraceHit{best, best_slot};
+}
+
 #if defined(__CUDACC__)
 static __device__ __noinline__ TraceHit trace_closest_dev(const GNode* nodes, const GTriIsect* tris, V3 o, V3 d,
                                                    double tmin, double tmax) {

@@ -18,6 +18,9 @@
 // intersection records of the frames it touches in shared memory.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "tofr_ellipsoid.cuh"
 #include "tofr_kcommon.cuh"
 #include "tofr_store.cuh"
@@ -1000,6 +1003,16 @@ void set_gauss_rule(const double* x, const double* w, cudaStream_t s) {
 
 static size_t band_pixels(const Band& bd, int W) { return size_t(bd.y1 - bd.y0) * W; }
 
+// TOFR_TRACE=legacy keeps the nested-loop trace kernels (A/B and debugging)
+static bool trace_wave() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TOFR_TRACE");
+        v = (e && std::strcmp(e, "legacy") == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s) {
     size_t n = size_t(bd.r1 - bd.r0) * F.cam.w;
     if (!n) return;
@@ -1015,6 +1028,10 @@ void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const 
                        const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
+    if (ip.mode == INIT_DIRECT && !cfg.ellipsoidal && trace_wave()) {
+        launch_trace_gated(F, bd, g, cfg, ip.m_init, ip.center, ip.width, frame_idx, cur, q, s);
+        return;
+    }
     size_t sm = frame_smem_bytes(F);
     TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q);
 }
@@ -1024,6 +1041,10 @@ void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, co
                            unsigned long long* q, cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
+    if (trace_wave()) {
+        launch_trace_transient(F, bd, g, cfg, ip.m_init, h, frame_idx, cur, q, s);
+        return;
+    }
     size_t sm = frame_smem_bytes(F);
     TOFR_PERSISTENT(k_init_transient, n, sm)(F, bd, g, cfg, ip, h, frame_idx, cur, q);
 }
@@ -1107,6 +1128,13 @@ void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const 
                        cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
+    // the nested-loop kernel measured faster for plain deposits (every candidate
+    // in the histogram range is traced, so its lanes stay in step); the state
+    // machine is selected with TOFR_TRACE=wave
+    if (std::getenv("TOFR_TRACE") && std::strcmp(std::getenv("TOFR_TRACE"), "wave") == 0) {
+        launch_trace_plain(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q, s);
+        return;
+    }
     size_t sm = frame_smem_bytes(F);
     TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q);
 }
@@ -1116,6 +1144,10 @@ void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const P
                       cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
+    if (trace_wave()) {
+        launch_trace_reference(F, bd, g, cfg, center, width, spp, frame_key, mean, se, q, s);
+        return;
+    }
     size_t sm = frame_smem_bytes(F);
     TOFR_PERSISTENT(k_reference, n, sm)(F, bd, g, cfg, center, width, spp, frame_key, mean, se, q);
 }

@@ -112,6 +112,22 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
                          const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
                          const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q, cudaStream_t s);
 
+// Path-tree tracing as a per-lane state machine (tofr_trace.cu): direct
+// initial sampling (gated / transient), plain transient deposits, the brute-
+// force reference.  The launchers below route to these unless the ellipsoidal
+// or shrink initialiser is selected (or TOFR_TRACE=legacy).
+void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
+                        double center, double width, int frame_idx, ResStore cur, unsigned long long* q,
+                        cudaStream_t s);
+void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
+                            const HistSpec& h, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s);
+void launch_trace_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
+                        int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                        cudaStream_t s);
+void launch_trace_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
+                            double width, int spp, uint64_t frame_key, double* mean, double* se,
+                            unsigned long long* q, cudaStream_t s);
+
 size_t frame_smem_bytes(const FrameView& F);
 void set_gauss_rule(const double* x, const double* w, cudaStream_t s);
 // g (launch_gbuffer) is the band's local G-buffer (row r0 first); every other
