@@ -187,7 +187,7 @@ struct tofr_session {
     bool order = true;
     // wavefront reuse (tofr_wave.cu; TOFR_REUSE=legacy selects the per-item kernels)
     bool wave = false;
-    DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng;
+    DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng, wv_mlist;
     size_t wv_cap = 0;
     tofr_halo_exchange_fn xfn = nullptr;
     void* xuser = nullptr;
@@ -230,7 +230,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (DevBuf* b : {&image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
-                          &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng})
+                          &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
     }
 };
@@ -382,6 +382,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_map_b.ensure(own_items * sizeof(uint32_t));
                 s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
+                s->wv_mlist.ensure(own_items * sizeof(uint32_t));
             }
         }
         const char* ord = std::getenv("TOFR_ORDER");
@@ -536,6 +537,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         wv.map_b = s->wv_map_b.as<uint32_t>();
         wv.tsrc = s->wv_tsrc.as<uint64_t>();
         wv.rng_ctr = s->wv_rng.as<uint64_t>();
+        wv.mlist = s->wv_mlist.as<uint32_t>();
     }
     if (s->order && s->wo_perm.p)
         wo = WorkOrder{s->wo_cls.as<uint8_t>(), s->wo_counts.as<uint32_t>(), s->wo_perm.as<uint32_t>()};

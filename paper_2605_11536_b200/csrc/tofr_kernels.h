@@ -90,15 +90,16 @@ struct ShiftQueue {
     // Jacobian (JOB_FULL) or p-hat_src(S^-1 y) * |J| (otherwise), ok = 1 when the
     // shift succeeded.  JOB_FULL jobs also get the mapped record in chunks 1-21.
     ResStore out;
-    uint32_t* ctl;  // [0] first job of the current batch, [1] end, [2] mark
+    uint32_t* ctl;  // [0] first job of the current batch, [1] end, [2] mark, [3] merge-list length
 };
 
 struct WaveScratch {
     ShiftQueue q;
     uint32_t* map_a;    // spatial: forward job of (j, i) [N * n]; temporal: forward job of i [n]
     uint32_t* map_b;    // spatial: inverse job of i [n]; temporal: inverse job of i [n]
-    uint64_t* tsrc;     // temporal: reprojected source item of i, or ~0
+    uint64_t* tsrc;     // temporal: reprojected source pixel of each band pixel, or ~0
     uint64_t* rng_ctr;  // spatial: lane-10 RNG position per item
+    uint32_t* mlist;    // items whose merge has a non-empty side (count in q.ctl[3])
 };
 
 // jobs per item a stage can enqueue (capacity planning)

@@ -36,6 +36,14 @@
 #ifndef TOFR_WAVE_MINB
 #define TOFR_WAVE_MINB 4
 #endif
+// idle lanes a warp of k_shift_solve collects before it refills them
+#ifndef TOFR_REFILL
+#define TOFR_REFILL 16
+#endif
+// lanes needing re-projection rays a warp collects before it traces them
+#ifndef TOFR_RAYBATCH
+#define TOFR_RAYBATCH 8
+#endif
 
 namespace tofr_b200 {
 
@@ -129,6 +137,19 @@ __device__ __forceinline__ uint32_t queue_append(const ShiftQueue& q, bool want,
         return kNoJob;
     }
     return k;
+}
+
+// Warp-aggregated append to the merge list (items whose merge needs a sample:
+// at least one side non-empty); count in q.ctl[3].  All lanes must call it.
+__device__ __forceinline__ void mlist_append(const WaveScratch& ws, bool want, uint32_t item) {
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&ws.q.ctl[3], uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (want) ws.mlist[base + __popc(m & ((1u << lane) - 1))] = item;
 }
 
 // ---------------------------------------------------------------------------
@@ -516,7 +537,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 #define SCTR(k, v) atomicAdd_block(&sctr[k], (unsigned)(v))
 
     // per-lane Newton state (one job at a time)
-    bool active = false, exhausted = false, init = false, count = false;
+    bool active = false, exhausted = false, init = false, count = false, parked = false;
     uint32_t job = 0;
     int dsel = 0;
     V3 p1{0, 0, 0}, p2{0, 0, 0}, spos{0, 0, 0}, cpos{0, 0, 0};
@@ -529,8 +550,13 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     int iter = 0, bt = 0;
 
     for (;;) {
-        // ---- refill: lanes without a job take the next ones (one atomic per warp)
-        bool need = !active && !exhausted;
+        // ---- refill: idle lanes take the next jobs (one atomic per warp), but only
+        // once at least TOFR_REFILL lanes are idle (or none is busy), so the
+        // divergent setup code runs for many lanes at a time
+        bool idle = !active && !exhausted;
+        unsigned im = __ballot_sync(0xffffffffu, idle);
+        unsigned bm = __ballot_sync(0xffffffffu, active);
+        bool need = idle && (__popc(im) >= TOFR_REFILL || bm == 0);
         unsigned m = __ballot_sync(0xffffffffu, need);
         if (m) {
             int leader = __ffs(m) - 1;
@@ -599,8 +625,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             }
         }
         if (__all_sync(0xffffffffu, exhausted)) break;
-        unsigned am = __ballot_sync(0xffffffffu, active);
-        if (!active) continue;
 
         // ---- one Newton trial (trial 0 = the initial evaluation at the start point)
         const FrameView& F = sF[dsel];
@@ -608,7 +632,13 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int ttri = ctri;
         bool tn_rec = cn_rec, have = true;
         if (init) tpos = spos;
-        if (!init && !in_triangle(F, ctri, tpos)) {  // re-projection rays (reproject_to_mesh)
+        // A plane point outside the current triangle needs re-projection rays
+        // (reproject_to_mesh).  Such lanes park until TOFR_RAYBATCH lanes of the
+        // warp need rays (or no other lane can proceed) and then trace together.
+        if (active && !parked && !init && !in_triangle(F, ctri, tpos)) parked = true;
+        unsigned pm = __ballot_sync(0xffffffffu, parked);
+        unsigned rm = __ballot_sync(0xffffffffu, active && !parked);
+        if (parked && (__popc(pm) >= TOFR_RAYBATCH || rm == 0)) {
             SurfR r = reproject_rays(&F, ctri, tpos, p1);
             have = r.ok;
             if (have) {
@@ -616,8 +646,11 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 ttri = r.tri;
                 tn_rec = false;
             }
+            parked = false;
         }
-        __syncwarp(am);
+        unsigned em = __ballot_sync(0xffffffffu, active && !parked);
+        if (!active || parked) continue;
+        __syncwarp(em);
         Frame2 Jt = tangent_frame(F, ttri);
         TrialEval et = trial_eval(p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
         double fn = hypot(et.F.x, et.F.y);
@@ -866,8 +899,12 @@ __device__ __forceinline__ double inv_output(const ShiftQueue& q, uint32_t k) {
 // ---------------------------------------------------------------------------
 // temporal reuse (stage::temporal_reuse, pipeline.hpp:209-229)
 
+// ws.tsrc holds, per pixel of the band, the reprojected source pixel qy * W + qx
+// (or ~0: no primary hit, off-screen, or outside the rows the band holds);
+// job maps are written only for items that have the job (the apply kernel
+// reads them under the same non-emptiness tests).
 __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg,
-                                ResStore cur, ResStore prev, WaveScratch ws) {
+                                PathCfg cfg, ResStore cur, ResStore prev, WaveScratch ws) {
     int W = Fc.cam.w, B = cg.transient ? cg.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     size_t stride = size_t(gridDim.x) * blockDim.x;
@@ -877,64 +914,74 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
         size_t it = base + (live ? i : 0);
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
-        bool merge = false, fwd = false, inv = false;
+        bool fwd = false, inv = false, merge = false;
         size_t src_i = 0;
         int qx = 0, qy = 0;
         if (live) {
             GHit g = gc[p];
+            uint64_t src_pix = ~uint64_t(0);
             if (g.tri >= 0) {
                 V3 d0 = primary_dir(Fc.cam, px, py);
                 V3 hp = Fc.cam.pos + d0 * g.t;
                 if (project(Fp.cam, hp, qx, qy)) {
                     if (qy < bd.t0 || qy >= bd.t1) {  // reprojection left the rows this band holds
-                        atomicAdd(bd.err, 1ull);
+                        if (b == 0) atomicAdd(bd.err, 1ull);
                     } else {
-                        src_i = (size_t(qy) * W + qx) * B + b;
+                        src_pix = uint64_t(qy) * W + qx;
+                        src_i = size_t(src_pix) * B + b;
                         double2 s0 = ld2(prev, 0, src_i);
                         if (s0.y > 0) {
-                            merge = true;
+                            double2 c0 = ld2(cur, 0, it);
                             fwd = s0.x > 0;
-                            inv = ld2(cur, 0, it).x > 0;
+                            inv = c0.x > 0;
+                            merge = fwd || inv;
+                            // both empty: the merge only adds the confidences (no RNG draw)
+                            if (!merge) res_store_w(cur, it, 0.0, dmin(c0.y + s0.y, cfg.m_cap));
                         }
                     }
                 }
             }
+            if (b == 0) ws.tsrc[size_t(p) - size_t(bd.y0) * W] = src_pix;
         }
         double dc, dw, sc, sw;
         gate_of(cg, b, dc, dw);
         gate_of(pg, b, sc, sw);
         uint32_t kf = queue_append(ws.q, fwd, bd.err);
         uint32_t ki = queue_append(ws.q, inv, bd.err);
-        if (kf != kNoJob) job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
-        if (ki != kNoJob) job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
-        if (live) {
-            ws.tsrc[i] = merge ? uint64_t(src_i) : ~uint64_t(0);
+        if (kf != kNoJob) {
+            job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
             ws.map_a[i] = kf;
+        }
+        if (ki != kNoJob) {
+            job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
             ws.map_b[i] = ki;
         }
+        mlist_append(ws, merge, uint32_t(i));
     }
 }
 
 __global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int frame_idx, ResStore cur,
                                  ResStore prev, WaveScratch ws) {
     int B = cg.transient ? cg.h.bins : 1;
-    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        uint64_t s = ws.tsrc[i];
-        if (s == ~uint64_t(0)) continue;
-        size_t src_i = size_t(s), it = base + i;
+    size_t base = size_t(bd.y0) * W * B;
+    uint32_t cnt = ws.q.ctl[3];
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < cnt; l += gridDim.x * blockDim.x) {
+        size_t i = ws.mlist[l], it = base + i;
         int p = int(it / B), b = int(it % B);
+        size_t src_i = size_t(ws.tsrc[size_t(p) - size_t(bd.y0) * W]) * B + b;
+        Res dst, src;
+        res_load_head(prev, src_i, src);
+        res_load_head(cur, it, dst);
+        if (dst.has) dst.phat = ld2(cur, 1, it).x;
+        if (src.has) src.phat = ld2(prev, 1, src_i).x;
         int px = p % W, py = p / W;
         double dc, dw;
         gate_of(cg, b, dc, dw);
-        Res dst, src;
-        res_head_phat(cur, it, dst);
-        res_head_phat(prev, src_i, src);
         MergeShift ms{0, 1.0, 0.0};
         Sample mapped;
-        uint32_t kf = ws.map_a[i];
+        uint32_t kf = src.has ? ws.map_a[i] : kNoJob;
         fwd_output(ws.q, kf, ms, mapped);
-        ms.phat_src_of_dst = inv_output(ws.q, ws.map_b[i]);
+        ms.phat_src_of_dst = inv_output(ws.q, dst.has ? ws.map_b[i] : kNoJob);
         uint64_t pix = uint64_t(py) * W + px;
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
         int which = gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
@@ -995,15 +1042,34 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
         gate_of(gate, b, dc, dw);
         int nx = 0, ny = 0;
         size_t si = 0;
-        bool want = false;
+        bool want = false, merge = false;
         if (live) {
             uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
-            want = spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
-                   ld2(out_grid, 0, it).x > 0;
+            if (!spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si)) {
+                if (j == 0) {  // the output starts as the pass input
+                    double2 c0 = ld2(src_grid, 0, it);
+                    if (c0.x > 0)
+                        copy_res(src_grid, dst_grid, it, c0.x, c0.y);
+                    else
+                        res_store_w(dst_grid, it, 0.0, c0.y);
+                    if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
+                }
+            } else {
+                double2 o0 = ld2(out_grid, 0, it), s0 = ld2(src_grid, 0, si);
+                want = o0.x > 0;
+                merge = want || s0.x > 0;
+                if (!merge) {  // both empty: the merge only adds the confidences (no RNG draw)
+                    res_store_w(dst_grid, it, 0.0, dmin(o0.y + s0.y, cfg.m_cap));
+                    if (j == 0 && j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
+                }
+            }
         }
         uint32_t k = queue_append(ws.q, want, bd.err);
-        if (k != kNoJob) job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
-        if (live) ws.map_b[i] = k;
+        if (k != kNoJob) {
+            job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
+            ws.map_b[i] = k;
+        }
+        mlist_append(ws, merge, uint32_t(i));
     }
 }
 
@@ -1011,36 +1077,28 @@ __global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate
                                 int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        size_t it = base + i;
+    uint32_t cnt = ws.q.ctl[3];
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < cnt; l += gridDim.x * blockDim.x) {
+        size_t i = ws.mlist[l], it = base + i;
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         uint64_t rk = spatial_rot_key(pix, pass, cfg.seed, frame_idx);
         int nx, ny;
         size_t si = 0;
-        bool use = spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si);
-        if (!use) {
-            if (j == 0) {  // the output starts as the pass input
-                double2 c0 = ld2(src_grid, 0, it);
-                if (c0.x > 0)
-                    copy_res(src_grid, dst_grid, it, c0.x, c0.y);
-                else
-                    res_store_w(dst_grid, it, 0.0, c0.y);
-                if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
-            }
-            continue;
-        }
+        spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si);
+        Res out, src;
+        res_load_head(j == 0 ? src_grid : dst_grid, it, out);
+        res_load_head(src_grid, si, src);
+        if (out.has) out.phat = ld2(j == 0 ? src_grid : dst_grid, 1, it).x;
+        if (src.has) src.phat = ld2(src_grid, 1, si).x;
         double dc, dw;
         gate_of(gate, b, dc, dw);
-        Res out, src;
-        res_head_phat(j == 0 ? src_grid : dst_grid, it, out);
-        res_head_phat(src_grid, si, src);
         MergeShift ms{0, 1.0, 0.0};
         Sample mapped;
-        uint32_t kf = ws.map_a[size_t(j) * n + i];
-        if (!res_empty(src)) fwd_output(ws.q, kf, ms, mapped);
-        ms.phat_src_of_dst = inv_output(ws.q, ws.map_b[i]);
+        uint32_t kf = src.has ? ws.map_a[size_t(j) * n + i] : kNoJob;
+        fwd_output(ws.q, kf, ms, mapped);
+        ms.phat_src_of_dst = inv_output(ws.q, out.has ? ws.map_b[i] : kNoJob);
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(pass * 131 + b), 10);
         if (j > 0) rng.ctr = ws.rng_ctr[i];
         int which = gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
@@ -1069,6 +1127,7 @@ __global__ void k_queue_ctl(uint32_t* ctl, int op) {
         ctl[0] = ctl[2];
         ctl[1] = ctl[2];
     }
+    ctl[3] = 0;  // merge list of the batch
 }
 
 static int grid_n(size_t n, int block) {
@@ -1104,7 +1163,7 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
     size_t n = size_t(bd.y1 - bd.y0) * Fc.cam.w * (cg.transient ? cg.h.bins : 1);
     if (!n) return;
     k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
-    k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cur, prev, ws);
+    k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
     run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, cfg, ctr, q, s);
     k_temporal_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cfg, frame_idx, cur, prev, ws);
 }
