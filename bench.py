@@ -34,6 +34,8 @@ import tempfile
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
@@ -83,43 +85,36 @@ WORKLOADS = {
 
 PLAIN = {"c2p", "c4p"}  # render_transient_plain workloads; the others are ReSTIR sessions
 
-# launches of our kernels per frame (steady state): gbuffer, init, temporal
-# (cost + scatter + temporal), spatial per pass (job list + forward shifts + N
-# merges), bin reuse, shade; plain transient: gbuffer + deposits.
-def launches_per_frame(cfg: RenderConfig, plain: bool = False) -> int:
-    if plain:
-        return 2
-    n = 2 + (3 if cfg.temporal else 0) + 1
-    n += cfg.spatial_passes * (2 + cfg.spatial_neighbors)
-    n += 1 if (cfg.mode == F.MODE_TRANSIENT and cfg.bin_reuse) else 0
-    return n
-
-
-# algorithmic bytes per pixel (compact reservoir R = 224 B)
+# Algorithmic HBM bytes per unit of work of each kernel (
+# R = 224 B compact reservoir).  Units are counted on the device
+# (shift jobs, pixels, reservoir items) or known from the launch (pixels).
 R_BYTES = 224
 GHIT_BYTES = 16
-
-
-def stage_bytes_per_pixel(cfg: RenderConfig, plain: bool = False) -> dict:
-    """Algorithmic HBM bytes per pixel and stage launch.  Gated: SURVEY 8d
-    (compact reservoir R).  Transient: the occupancy-free lower bound, i.e.
-    header traffic of every (pixel, bin) reservoir (M per pixel-bin, W,
-    emptiness) -- init 32 B store of the empty header + 48 B finalize, temporal
-    2 x 16 B header reads, shade 32 B header read -- plus the histogram
-    read-modify-write of the bins (24 B), times B.  Plain: 16 B histogram
-    output per bin (rgb RMW happens only on deposits)."""
-    n = cfg.spatial_neighbors
-    if plain:
-        return {"init": 16 * cfg.bins}
-    if cfg.mode == F.MODE_TRANSIENT:
-        return {"init": 80 * cfg.bins, "temporal": 32 * cfg.bins, "spatial": ((1 + n) * 16 + 16) * cfg.bins,
-                "shade": 56 * cfg.bins}
-    return {
-        "init": GHIT_BYTES + R_BYTES,  # G-buffer read + reservoir write
-        "temporal": 3 * R_BYTES,  # prev read, cur read, cur write
-        "spatial": (1 + n) * R_BYTES + R_BYTES,  # per pass: (1+N) reads + 1 write
-        "shade": 24 + 12,
-    }
+KERNEL_BYTES = {
+    # shift jobs: job record (64 B) + the source record's geometry (112 B) + hand-off (48 B)
+    "k_shift_solve": ("job", 64 + 112 + 48),
+    # job + hand-off (112 B) + source record R + mapped record R (forward shifts; inverse: 16 B)
+    "k_shift_finish": ("job", 112 + 2 * R_BYTES),
+    "k_shift_replay": ("job", 64 + 16),
+    # path trees: G-buffer read + reservoir write
+    "k_trace_gated": ("pixel", GHIT_BYTES + R_BYTES),
+    "k_init_gated": ("pixel", GHIT_BYTES + R_BYTES),
+    # transient RIS: G-buffer read + per-bin (w_sum, M) read-modify-write on deposits (counted as 1 bin/pixel)
+    "k_trace_bins": ("pixel", GHIT_BYTES + 32 + R_BYTES),
+    # plain deposits: 32 B rgb+count read-modify-write per deposit (deposits/pixel measured)
+    "k_hist_plain": ("deposit", 32),
+    "k_trace_plain": ("deposit", 32),
+    "k_ris_finalize": ("item", 32),
+    # merge stages: header reads of both sides + header write per item
+    "k_temporal_prep": ("item", 16 + 16 + 16),
+    "k_temporal_apply": ("item", 3 * R_BYTES),
+    "k_spatial_prep_fwd": ("item", 16),
+    "k_spatial_prep_inv": ("item", 16 + 16),
+    "k_spatial_apply": ("item", 3 * R_BYTES),
+    "k_shade_gated": ("pixel", 24 + 12 + 24),
+    "k_shade_transient": ("item", 16 + 24),
+    "k_gbuffer": ("pixel", GHIT_BYTES),
+}
 
 
 def peaks() -> dict:
@@ -262,9 +257,19 @@ def run_ours(args) -> None:
     sess.sync()
     parallel.barrier(group)
 
+    # timed region: per-kernel CUDA events (library launch accounting, on the
+    # session stream), exact launch count and device work counters around it
     clk = ClockSampler(local) if rank == 0 else None
     stage_tot = [0.0] * 6
+    F.kernel_times(reset=True)
+    F.kernel_timing(True)
+    work0 = sess.work()
+    l0 = F.kernel_launches()
     t_ms = sess.timed_steps(args.steps, stage_tot)
+    launches = F.kernel_launches() - l0
+    work1 = sess.work()
+    F.kernel_timing(False)
+    ktimes = F.kernel_times(reset=True)
     clocks = clk.stop() if clk else None
     t_max = parallel.max_over_ranks(t_ms, group)
     frames = args.steps
@@ -284,25 +289,37 @@ def run_ours(args) -> None:
     e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
     h2d, d2h = sess.io_bytes()
 
-    # roofline of the dominant kernel (average launch duration from CUDA events)
+    # roofline of the dominant kernel: algorithmic bytes per launch / average
+    # launch duration (CUDA events on the session stream, timed region above)
     avg = [x / args.steps for x in stage_tot]
     names = ["init", "temporal", "bin", "spatial", "shade"]
-    per_px = stage_bytes_per_pixel(cfg, plain)
-    dom = max(range(5), key=lambda i: avg[i])
-    dom_name = names[dom]
-    launches = max(1, cfg.spatial_passes) if dom_name == "spatial" else 1
     band_px = sess.owned_pixels()
-    algo = per_px.get(dom_name, 0) * band_px
-    dur_s = avg[dom] / launches * 1e-3
+    items = band_px * (cfg.bins if cfg.mode == F.MODE_TRANSIENT or plain else 1)
+    dom = max(ktimes, key=lambda k: ktimes[k][0]) if ktimes else None
+    work = {k: work1[k] - work0[k] for k in work1} if work1 else {}
+    units = {"pixel": band_px, "item": items}
+    if dom and KERNEL_BYTES.get(dom, ("", 0))[0] == "job":
+        per_launch_jobs = work.get("shift_jobs", 0) / max(1, sum(v[1] for k, v in ktimes.items()
+                                                                  if k == "k_shift_finish"))
+        units["job"] = per_launch_jobs
+    if plain:  # deposits per launch (one deposit launch per frame)
+        units["deposit"] = work.get("deposits", 0) / args.steps
+    unit, per_unit = KERNEL_BYTES.get(dom, ("pixel", 0))
+    dom_ms, dom_n = ktimes[dom] if dom else (0.0, 1)
+    dur_s = dom_ms / max(1, dom_n) * 1e-3
+    algo = per_unit * units.get(unit, 0)
     pk = peaks()
     achieved = algo / dur_s / 1e9 if dur_s > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{args.workload}:{dom_name}")
+            traffic = json.loads(tf.read_text()).get(f"{args.workload}:{dom}")
         except Exception:
             traffic = None
+    kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
+    rays = (work.get("rays_closest", 0) + work.get("rays_any", 0)) if work else 0
+    t_s = t_max * 1e-3
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -328,11 +345,18 @@ def run_ours(args) -> None:
             "shift_stats_one_frame": shift_stats,
             "e2e": {"value": frames / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "roofline": {"bound": "hbm", "kernel": f"k_{dom_name}", "achieved": achieved, "peak": pk["hbm_gbs"],
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "peak_src": pk["src"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                         "traffic": traffic, "algo_bytes_per_launch": algo, "avg_launch_ms": dur_s * 1e3},
+                         "traffic": traffic, "algo_bytes_per_launch": algo, "bytes_per_unit": per_unit,
+                         "unit_of_work": unit, "units_per_launch": units.get(unit, 0),
+                         "avg_launch_ms": dur_s * 1e3, "launches": dom_n,
+                         "note": "FP64 latency/divergence-bound shift and trace kernels: HBM fraction is small "
+                                 "by construction (SURVEY 8d); see rays_per_s and kernel_ms"},
+            "kernel_ms_per_step": kernel_ms,
+            "rays_per_s": rays / t_s if t_s > 0 else None,
+            "shift_jobs_per_s": work.get("shift_jobs", 0) / t_s if (t_s > 0 and work) else None,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * launches_per_frame(cfg, plain) + sess.halo_launches(args.steps),
+            "gpu_launches": launches,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

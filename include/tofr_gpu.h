@@ -238,7 +238,20 @@ int tofr_gpu_session_stream(tofr_session* ss, void** stream);
 /* bytes the last step uploaded (frame snapshot: BVH, triangles, camera, beam)
  * and the size of one image read-back */
 int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t* d2h_image);
+/* device work counted since the session was created: out[0] shift jobs,
+ * out[1] closest-hit rays (incl. camera rays), out[2] any-hit (shadow /
+ * occlusion) rays, out[3] transient histogram deposits */
+int tofr_gpu_session_work(tofr_session* ss, uint64_t* out /* [4] */);
 void tofr_gpu_session_destroy(tofr_session* ss);
+
+/* launch accounting of the library's kernels (process-wide): every launch is
+ * counted; with timing enabled each launch is bracketed by CUDA events on its
+ * stream and the per-kernel totals are read after the work finished */
+int tofr_gpu_kernel_timing(int32_t enable); /* returns the previous setting */
+uint64_t tofr_gpu_kernel_launches(void);
+/* names: cap x name_len chars; returns the number of kernels written */
+int tofr_gpu_kernel_times(char* names, int32_t name_len, double* total_ms, uint64_t* launches, int32_t cap);
+void tofr_gpu_kernel_times_reset(void);
 
 /* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit
  * (Bvh::intersect_min) -> t, tri; mode 1 = occluded(a = o, b = d) -> tri = 0/1 */

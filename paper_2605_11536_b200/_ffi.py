@@ -143,6 +143,13 @@ def _declare(lib) -> None:
     lib.tofr_gpu_session_io_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     lib.tofr_gpu_session_destroy.argtypes = [vp]
     lib.tofr_gpu_session_destroy.restype = None
+    lib.tofr_gpu_session_work.argtypes = [vp, P(C.c_uint64)]
+    lib.tofr_gpu_kernel_timing.argtypes = [C.c_int32]
+    lib.tofr_gpu_kernel_launches.argtypes = []
+    lib.tofr_gpu_kernel_launches.restype = C.c_uint64
+    lib.tofr_gpu_kernel_times.argtypes = [C.c_char_p, C.c_int32, P(C.c_double), P(C.c_uint64), C.c_int32]
+    lib.tofr_gpu_kernel_times_reset.argtypes = []
+    lib.tofr_gpu_kernel_times_reset.restype = None
     lib.tofr_gpu_probe_rays.argtypes = [vp, vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
                                         P(C.c_double), P(C.c_int32)]
     lib.tofr_scene_probe_rays_host.argtypes = [vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
@@ -161,7 +168,8 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_last_ms", "tofr_gpu_session_io_bytes", "tofr_gpu_session_stream",
     "tofr_gpu_session_create_band", "tofr_gpu_session_band", "tofr_gpu_session_set_halo_exchange",
     "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
-    "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_destroy", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
+    "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_destroy",
+    "tofr_gpu_kernel_timing", "tofr_gpu_kernel_launches", "tofr_gpu_kernel_times", "tofr_gpu_kernel_times_reset", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )
 
 
@@ -181,3 +189,32 @@ def load_library(path: Path | None = None):
     if path is None:
         _lib = lib
     return lib
+
+
+# ---------------------------------------------------------------------------
+# launch accounting (tofr_gpu_kernel_*)
+
+def kernel_timing(enable: bool) -> bool:
+    return bool(load_library().tofr_gpu_kernel_timing(1 if enable else 0))
+
+
+def kernel_launches() -> int:
+    return int(load_library().tofr_gpu_kernel_launches())
+
+
+def kernel_times(reset: bool = False) -> dict:
+    """{kernel name: (total ms, launches)} of the launches timed so far."""
+    lib = load_library()
+    cap, nl = 64, 48
+    names = C.create_string_buffer(cap * nl)
+    ms = (C.c_double * cap)()
+    n = (C.c_uint64 * cap)()
+    k = lib.tofr_gpu_kernel_times(names, nl, ms, n, cap)
+    out = {}
+    for i in range(k):
+        nm = names.raw[i * nl:(i + 1) * nl].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(n[i]))
+    if reset:
+        lib.tofr_gpu_kernel_times_reset()
+    return out
+

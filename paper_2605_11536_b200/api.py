@@ -409,6 +409,13 @@ class Session:
         self._r._check(self._r._lib.tofr_gpu_session_last_ms(self.handle, C.byref(tot), st))
         return tot.value, list(st)
 
+    def work(self) -> dict:
+        """Device work since the session was created (waits for pending frames)."""
+        w = (C.c_uint64 * 4)()
+        self._r._check(self._r._lib.tofr_gpu_session_work(self.handle, w))
+        return {"shift_jobs": int(w[0]), "rays_closest": int(w[1]), "rays_any": int(w[2]),
+                "deposits": int(w[3])}
+
     def io_bytes(self):
         h2d, d2h = C.c_uint64(), C.c_uint64()
         self._r._check(self._r._lib.tofr_gpu_session_io_bytes(self.handle, C.byref(h2d), C.byref(d2h)))

@@ -27,7 +27,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu", "tofr_trace.cu"]
-HOST_SOURCES = ["host_scene.cpp", "capi.cpp"]
+HOST_SOURCES = ["host_scene.cpp", "capi.cpp", "ktime.cpp"]
 HEADERS = [
     "tofr_core.h",
     "tofr_geom.h",
@@ -35,6 +35,7 @@ HEADERS = [
     "tofr_ellipsoid.cuh",
     "tofr_store.cuh",
     "tofr_kcommon.cuh",
+    "ktime.h",
     "tofr_kernels.h",
     "host_scene.h",
 ]

@@ -25,6 +25,7 @@
 
 #include "../../include/tofr_gpu.h"
 #include "host_scene.h"
+#include "ktime.h"
 #include "tofr_kernels.h"
 
 using namespace tofr_b200;
@@ -202,6 +203,7 @@ struct tofr_session {
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
     double stage_tot[6] = {0, 0, 0, 0, 0, 0};
     int64_t tot_frames = 0;
+    uint64_t camera_rays = 0;  // G-buffer rays (host count; the kernel has no counters)
     size_t last_h2d = 0;  // bytes uploaded by the last step (frame snapshot)
     int has_temporal = 0, has_bin = 0, has_spatial = 0;
 
@@ -274,6 +276,7 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width, const
     p.m_cap = c.m_cap;
     p.seed = c.seed;
     p.replay = 0;
+    p.work = nullptr;
     for (const HMaterial& m : sc.materials)
         if (!m.reconnectable()) p.replay = 1;
     return p;
@@ -331,8 +334,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     for (auto& e : s->read_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&s->err_host), 2 * sizeof(unsigned long long)), "pinned");
     s->err_host[0] = s->err_host[1] = 0;
-    s->ctr.ensure((3 * SC_COUNT + 2) * sizeof(unsigned long long));
-    ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), ctx->stream), "memset");
+    // [3 stages x SC_COUNT][band error][work counter q][WK_COUNT device work]
+    s->ctr.ensure((3 * SC_COUNT + 2 + WK_COUNT) * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 2 + WK_COUNT) * sizeof(unsigned long long), ctx->stream),
+       "memset");
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
     s->plain = plain;
@@ -452,6 +457,7 @@ void flush_set(tofr_session* s, int set) {
     if (!s->pending[set]) return;
     ck(cudaEventSynchronize(s->ev[set][6]), "frame");
     s->pending[set] = false;
+    if (kt_enabled()) kt_collect();
     float ms[6];
     for (int i = 0; i < 5; ++i) {
         ms[i] = 0;
@@ -517,6 +523,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     double center = c.gate_center + c.gate_step * f;
     double width = c.gate_width;
     PathCfg pc = path_cfg(c, center, width, s->scene);
+    pc.work = s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 2;
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
     unsigned long long* q = ctr + 3 * SC_COUNT + 1;  // persistent-kernel work counter (stream-ordered reuse)
@@ -545,6 +552,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
 
     cudaEventRecord(ev[0], stream);
     launch_gbuffer(F, bd, g_local, stream);
+    s->camera_rays += uint64_t(s->r1 - s->r0) * s->W;
     if (s->plain) {
         size_t pr = size_t(s->W) * s->B;
         launch_hist_plain(F, bd, g, pc, h, c.m_init, f, rows_base<double>(s->hist, s->y0, pr * 3),
@@ -1210,7 +1218,40 @@ int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t
     return TOFR_OK;
 }
 
+int tofr_gpu_session_work(tofr_session* ss, uint64_t* out) {
+    if (!ss || !out) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        unsigned long long w[WK_COUNT];
+        ck(cudaMemcpy(w, ss->ctr.as<unsigned long long>() + 3 * SC_COUNT + 2, sizeof(w), cudaMemcpyDeviceToHost),
+           "work");
+        out[0] = w[WK_JOBS];
+        out[1] = w[WK_CLOSEST] + ss->camera_rays;
+        out[2] = w[WK_ANY];
+        out[3] = w[WK_DEPOSITS];
+    });
+}
+
 void tofr_gpu_session_destroy(tofr_session* ss) { delete ss; }
+
+int tofr_gpu_kernel_timing(int32_t enable) {
+    bool prev = kt_enabled();
+    if (!enable) kt_collect();
+    kt_set_enabled(enable != 0);
+    return prev ? 1 : 0;
+}
+
+uint64_t tofr_gpu_kernel_launches(void) { return kt_launches(); }
+
+int tofr_gpu_kernel_times(char* names, int32_t name_len, double* total_ms, uint64_t* launches, int32_t cap) {
+    kt_collect();
+    return kt_read(names, name_len, total_ms, launches, cap);
+}
+
+void tofr_gpu_kernel_times_reset(void) {
+    kt_collect();
+    kt_reset();
+}
 
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const double* rays, int32_t n,
                         int32_t mode, double* out_t, int32_t* out_tri) {

@@ -22,6 +22,7 @@
 #include <cstring>
 
 #include "tofr_ellipsoid.cuh"
+#include "ktime.h"
 #include "tofr_kcommon.cuh"
 #include "tofr_store.cuh"
 
@@ -834,6 +835,7 @@ struct PlainSink {
     double* rgb;
     uint32_t* count;
     size_t base;
+    uint32_t* n_dep;
     __device__ bool wants(double len) const { return bin_of(h, len) >= 0; }
     __device__ void emit(const Cand& c, double mis, const RecSrc&) {
         if (!(c.pdf > 0)) return;
@@ -845,6 +847,7 @@ struct PlainSink {
         rgb[3 * i + 1] += val.y;
         rgb[3 * i + 2] += val.z;
         count[i] += 1;
+        ++*n_dep;
     }
 };
 
@@ -859,11 +862,12 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
     WalkV v[kMaxVerts];
     NoEll ell;
     size_t n = size_t(bd.y1 - bd.y0) * W;
+    uint32_t n_dep = 0;
     TOFR_FOR_ITEMS(i, n, q) {
         int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
-        PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins};
+        PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins, &n_dep};
         GHit g = gbuf[p];
         for (int s = 0; s < m_init; ++s) {
             Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
@@ -871,6 +875,7 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
             trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
         }
     }
+    work_add(cfg.work, WK_DEPOSITS, n_dep);
 }
 
 // ---------------------------------------------------------------------------
@@ -1016,7 +1021,10 @@ static bool trace_wave() {
 void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s) {
     size_t n = size_t(bd.r1 - bd.r0) * F.cam.w;
     if (!n) return;
-    k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, bd, g);
+    {
+        KScope ks("k_gbuffer", s);
+        k_gbuffer<<<grid_for(n, 256), 256, frame_smem_bytes(F), s>>>(F, bd, g);
+    }
 }
 
 // zeroed work counter + persistent launch configuration
@@ -1033,7 +1041,10 @@ void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const 
         return;
     }
     size_t sm = frame_smem_bytes(F);
-    TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q);
+    {
+        KScope ks("k_init_gated", s);
+        TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q);
+    }
 }
 
 void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
@@ -1046,11 +1057,17 @@ void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, co
         return;
     }
     size_t sm = frame_smem_bytes(F);
-    TOFR_PERSISTENT(k_init_transient, n, sm)(F, bd, g, cfg, ip, h, frame_idx, cur, q);
+    {
+        KScope ks("k_init_transient", s);
+        TOFR_PERSISTENT(k_init_transient, n, sm)(F, bd, g, cfg, ip, h, frame_idx, cur, q);
+    }
 }
 
 static void order_items(const uint8_t* cls, size_t n, const WorkOrder& wo, cudaStream_t s) {
-    k_cost_scatter<<<grid_for(n, 256), 256, 0, s>>>(cls, n, wo.counts, wo.perm);
+    {
+        KScope ks("k_cost_scatter", s);
+        k_cost_scatter<<<grid_for(n, 256), 256, 0, s>>>(cls, n, wo.counts, wo.perm);
+    }
 }
 
 void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
@@ -1062,12 +1079,18 @@ void launch_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const 
     const uint32_t* perm = nullptr;
     if (wo.perm) {
         cudaMemsetAsync(wo.counts, 0, 2 * kCostBuckets * sizeof(uint32_t), s);
-        k_cost_temporal<<<grid_for(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, cur, prev, wo.cls, wo.counts);
+        {
+            KScope ks("k_cost_temporal", s);
+            k_cost_temporal<<<grid_for(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, cur, prev, wo.cls, wo.counts);
+        }
         order_items(wo.cls, n, wo, s);
         perm = wo.perm;
     }
     size_t sm = frame_smem_bytes(Fc) + frame_smem_bytes(Fp);
-    TOFR_PERSISTENT(k_temporal, n, sm)(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, perm, ctr, q);
+    {
+        KScope ks("k_temporal", s);
+        TOFR_PERSISTENT(k_temporal, n, sm)(Fc, bd, gc, Fp, gp, cfg, cg, pg, frame_idx, cur, prev, perm, ctr, q);
+    }
 }
 
 void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
@@ -1080,23 +1103,38 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
     if (sc && sp.neighbors > 0 && sp.radius > 0) {
         cudaMemsetAsync(sc->count, 0, sizeof(uint32_t), s);
         cudaMemsetAsync(sc->ok, 0, n * size_t(sp.neighbors), s);
-        k_spatial_fwd_list<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, *sc);
+        {
+            KScope ks("k_spatial_fwd_list", s);
+            k_spatial_fwd_list<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, *sc);
+        }
         size_t jobs_max = n * size_t(sp.neighbors);
-        TOFR_PERSISTENT(k_spatial_fwd, jobs_max, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, *sc, ctr, q);
+        {
+            KScope ks("k_spatial_fwd", s);
+            TOFR_PERSISTENT(k_spatial_fwd, jobs_max, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, *sc, ctr, q);
+        }
         for (int j = 0; j < sp.neighbors; ++j) {
-            TOFR_PERSISTENT(k_spatial_merge, n, sm)(F, bd, g, cfg, gg, sp, pass, j, frame_idx, src, dst, *sc, q);
+            {
+                KScope ks("k_spatial_merge", s);
+                TOFR_PERSISTENT(k_spatial_merge, n, sm)(F, bd, g, cfg, gg, sp, pass, j, frame_idx, src, dst, *sc, q);
+            }
         }
         return;
     }
     const uint32_t* perm = nullptr;
     if (wo.perm) {
         cudaMemsetAsync(wo.counts, 0, 2 * kCostBuckets * sizeof(uint32_t), s);
-        k_cost_spatial<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, wo.cls,
-                                                         wo.counts);
+        {
+            KScope ks("k_cost_spatial", s);
+            k_cost_spatial<<<grid_for(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, wo.cls,
+                                                             wo.counts);
+        }
         order_items(wo.cls, n, wo, s);
         perm = wo.perm;
     }
-    TOFR_PERSISTENT(k_spatial, n, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, dst, perm, ctr, q);
+    {
+        KScope ks("k_spatial", s);
+        TOFR_PERSISTENT(k_spatial, n, sm)(F, bd, g, cfg, gg, sp, pass, frame_idx, src, dst, perm, ctr, q);
+    }
 }
 
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
@@ -1105,14 +1143,20 @@ void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const Pa
     size_t n = band_pixels(bd, F.cam.w) * h.bins;
     if (!n) return;
     size_t sm = frame_smem_bytes(F);
-    TOFR_PERSISTENT(k_binreuse, n, sm)(F, bd, g, cfg, h, frame_idx, src, dst, ctr, q);
+    {
+        KScope ks("k_binreuse", s);
+        TOFR_PERSISTENT(k_binreuse, n, sm)(F, bd, g, cfg, h, frame_idx, src, dst, ctr, q);
+    }
 }
 
 void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
                         double* accum, cudaStream_t s) {
     size_t n = band_pixels(bd, W);
     if (!n) return;
-    k_shade_gated<<<grid_for(n, 256), 256, 0, s>>>(cur, bd.y0 * W, bd.y1 * W, center, width, image, accum);
+    {
+        KScope ks("k_shade_gated", s);
+        k_shade_gated<<<grid_for(n, 256), 256, 0, s>>>(cur, bd.y0 * W, bd.y1 * W, center, width, image, accum);
+    }
 }
 
 void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
@@ -1120,7 +1164,10 @@ void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec&
     size_t n = band_pixels(bd, W) * h.bins;
     if (!n) return;
     size_t i0 = size_t(bd.y0) * W * h.bins;
-    k_shade_transient<<<grid_for(n, 256), 256, 0, s>>>(cur, i0, i0 + n, h, hist);
+    {
+        KScope ks("k_shade_transient", s);
+        k_shade_transient<<<grid_for(n, 256), 256, 0, s>>>(cur, i0, i0 + n, h, hist);
+    }
 }
 
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
@@ -1136,7 +1183,10 @@ void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const 
         return;
     }
     size_t sm = frame_smem_bytes(F);
-    TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q);
+    {
+        KScope ks("k_hist_plain", s);
+        TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q);
+    }
 }
 
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
@@ -1149,29 +1199,44 @@ void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const P
         return;
     }
     size_t sm = frame_smem_bytes(F);
-    TOFR_PERSISTENT(k_reference, n, sm)(F, bd, g, cfg, center, width, spp, frame_key, mean, se, q);
+    {
+        KScope ks("k_reference", s);
+        TOFR_PERSISTENT(k_reference, n, sm)(F, bd, g, cfg, center, width, spp, frame_key, mean, se, q);
+    }
 }
 
 void launch_hist_image(const double* hist, const Band& bd, int W, int B, double scale, double* image,
                        cudaStream_t s) {
     size_t n = band_pixels(bd, W);
     if (!n) return;
-    k_hist_image<<<grid_for(n * 32, 256), 256, 0, s>>>(hist, bd.y0 * W, bd.y1 * W, B, scale, image);
+    {
+        KScope ks("k_hist_image", s);
+        k_hist_image<<<grid_for(n * 32, 256), 256, 0, s>>>(hist, bd.y0 * W, bd.y1 * W, B, scale, image);
+    }
 }
 
 void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s) {
     if (!n_items) return;
-    k_halo_pack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+    {
+        KScope ks("k_halo_pack", s);
+        k_halo_pack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+    }
 }
 
 void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s) {
     if (!n_items) return;
-    k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+    {
+        KScope ks("k_halo_unpack", s);
+        k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+    }
 }
 
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
                        cudaStream_t s) {
-    k_probe_rays<<<(n + 127) / 128, 128, 0, s>>>(F, rays, n, mode, out_t, out_tri);
+    {
+        KScope ks("k_probe_rays", s);
+        k_probe_rays<<<(n + 127) / 128, 128, 0, s>>>(F, rays, n, mode, out_t, out_tri);
+    }
 }
 
 }  // namespace tofr_b200

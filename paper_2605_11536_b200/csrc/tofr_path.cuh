@@ -97,7 +97,20 @@ struct PathCfg {
     double m_cap;
     uint64_t seed;
     int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
+    unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
 };
+
+// device work counters (cumulative per session): shift jobs, closest-hit rays,
+// any-hit (shadow / occlusion) rays, transient histogram deposits
+enum : int { WK_JOBS = 0, WK_CLOSEST = 1, WK_ANY = 2, WK_DEPOSITS = 3, WK_COUNT = 4 };
+
+#if defined(__CUDACC__)
+// warp-aggregated add of a per-lane count (all lanes of the warp must call it)
+__device__ __forceinline__ void work_add(unsigned long long* work, int k, uint32_t v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (work && (threadIdx.x & 31) == 0 && v) atomicAdd(&work[k], (unsigned long long)v);
+}
+#endif
 
 // rr_survival (transport.hpp:193-196)
 TOFR_HD double rr_survival(int bounce, int use_rr) { return (!use_rr || bounce < 3) ? 1.0 : 0.7; }

@@ -27,6 +27,7 @@
 
 #define TOFR_OUTLINE_MATH 0
 
+#include "ktime.h"
 #include "tofr_kcommon.cuh"
 #include "tofr_store.cuh"
 
@@ -84,6 +85,7 @@ struct GatedSink {
         double W = (has && phat > 0) ? w_sum / phat : 0;
         res_store_w(cur, item, W, 1.0);
     }
+    __device__ void flush(unsigned long long*) {}
 };
 
 // RIS into per-(pixel, bin) reservoirs: chunk 0 holds (w_sum, -) during the
@@ -130,6 +132,7 @@ struct BinsSink {
         }
     }
     __device__ void end() {}
+    __device__ void flush(unsigned long long*) {}
 };
 
 // TransientHistogram::deposit of every candidate (f * mis / pdf / m_init)
@@ -139,6 +142,7 @@ struct PlainSink2 {
     double* rgb;
     uint32_t* count;
     size_t base;
+    uint32_t deposits;
     __device__ void begin(const PathCfg&, uint64_t, uint64_t, size_t p, int) { base = p * size_t(h.bins); }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
@@ -153,8 +157,10 @@ struct PlainSink2 {
         rgb[3 * i + 1] += val.y;
         rgb[3 * i + 2] += val.z;
         count[i] += 1;
+        ++deposits;
     }
     __device__ void end() {}
+    __device__ void flush(unsigned long long* work) { work_add(work, WK_DEPOSITS, deposits); }
 };
 
 // reference_gated_pixel: per-tree estimate, mean and standard error
@@ -192,6 +198,7 @@ struct RefSink2 {
         se[3 * item + 1] = sqrt(var.y / spp);
         se[3 * item + 2] = sqrt(var.z / spp);
     }
+    __device__ void flush(unsigned long long*) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -231,6 +238,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
     c.pdf = 0;
     V3 rd{0, 0, 1};
     double rtmax = 0, bs_pdf = 0, surv = 1;
+    uint32_t n_closest = 0, n_any = 0;
 
     for (;;) {
         // ---- refill: lanes without a pixel take the next ones
@@ -258,7 +266,12 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                 }
             }
         }
-        if (__all_sync(0xffffffffu, exhausted)) break;
+        if (__all_sync(0xffffffffu, exhausted)) {
+            work_add(cfg.work, WK_CLOSEST, n_closest);
+            work_add(cfg.work, WK_ANY, n_any);
+            sk.flush(cfg.work);
+            break;
+        }
 
         // ---- advance to the next ray (no ray needed for these steps)
         bool ray = false, any = false;
@@ -367,7 +380,13 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
 
         // ---- trace: one traversal for every lane with a ray
         TraceHit th{0, -1};
-        if (ray) th = trace_ray_impl(Fs.nodes, Fs.tri_isect, x.p, rd, eps, rtmax, any);
+        if (ray) {
+            th = trace_ray_impl(Fs.nodes, Fs.tri_isect, x.p, rd, eps, rtmax, any);
+            if (any)
+                ++n_any;
+            else
+                ++n_closest;
+        }
 
         // ---- consume
         if (state == ST_SHADOW) {
@@ -423,14 +442,17 @@ __global__ void k_ris_finalize(ResStore st, size_t i0, size_t i1) {
 // launchers
 
 template <class Sink>
-static void launch_trace(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int trees,
-                         uint64_t frame_key, const Sink& sk, unsigned long long* q, cudaStream_t s) {
+static void launch_trace(const char* kname, const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
+                         int trees, uint64_t frame_key, const Sink& sk, unsigned long long* q, cudaStream_t s) {
     size_t n = size_t(bd.y1 - bd.y0) * F.cam.w;
     if (!n) return;
     size_t sm = frame_smem_bytes(F);
     cudaMemsetAsync(q, 0, sizeof(unsigned long long), s);
     const void* kf = reinterpret_cast<const void*>(k_trace<Sink>);
-    k_trace<Sink><<<persistent_grid(kf, 128, sm, n), 128, sm, s>>>(F, bd, g, cfg, trees, frame_key, sk, q);
+    {
+        KScope ks(kname, s);
+        k_trace<Sink><<<persistent_grid(kf, 128, sm, n), 128, sm, s>>>(F, bd, g, cfg, trees, frame_key, sk, q);
+    }
 }
 
 void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
@@ -441,7 +463,7 @@ void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const
     sk.center = center;
     sk.width = width;
     sk.inv = 1.0 / m_init;
-    launch_trace(F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+    launch_trace("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
 }
 
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
@@ -454,10 +476,13 @@ void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, c
     sk.st = cur;
     sk.h = h;
     sk.inv = 1.0 / m_init;
-    launch_trace(F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+    launch_trace("k_trace_bins", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
     size_t blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
-    k_ris_finalize<<<int(blocks), 256, 0, s>>>(cur, i0, i0 + n);
+    {
+        KScope ks("k_ris_finalize", s);
+        k_ris_finalize<<<int(blocks), 256, 0, s>>>(cur, i0, i0 + n);
+    }
 }
 
 void launch_trace_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
@@ -468,7 +493,8 @@ void launch_trace_plain(const FrameView& F, const Band& bd, const GHit* g, const
     sk.m_init = m_init;
     sk.rgb = rgb;
     sk.count = count;
-    launch_trace(F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+    sk.deposits = 0;
+    launch_trace("k_trace_plain", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
 }
 
 void launch_trace_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
@@ -479,7 +505,7 @@ void launch_trace_reference(const FrameView& F, const Band& bd, const GHit* g, c
     sk.width = width;
     sk.mean = mean;
     sk.se = se;
-    launch_trace(F, bd, g, cfg, spp, frame_key, sk, q, s);
+    launch_trace("k_trace_reference", F, bd, g, cfg, spp, frame_key, sk, q, s);
 }
 
 }  // namespace tofr_b200

@@ -30,6 +30,7 @@
 // call boundaries (caller-saved registers -> local memory).
 #define TOFR_OUTLINE_MATH 0
 
+#include "ktime.h"
 #include "tofr_kcommon.cuh"
 #include "tofr_store.cuh"
 
@@ -308,11 +309,13 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
 struct SurfR {
     V3 pos, n;
     int tri, ok;
+    int rays;  // closest-hit rays traced
 };
 static __device__ __noinline__ SurfR reproject_rays(const FrameView* Fp, int cur_tri, V3 plane_pt, V3 p1) {
     const FrameView& F = *Fp;
     SurfR out;
     out.ok = 0;
+    out.rays = 0;
     V3 tn = F.tri[cur_tri].n;
     V3 dir = plane_pt - p1;
     double dl = norm(dir);
@@ -320,6 +323,7 @@ static __device__ __noinline__ SurfR reproject_rays(const FrameView* Fp, int cur
     if (dl > 0) {
         dir = dir / dl;
         if (fabs(dot(dir, tn)) > 1e-4) {
+            out.rays = 1;
             if (intersect(F, p1, dir, h)) {
                 out.pos = h.pos;
                 out.n = F.tri[h.tri].n;
@@ -330,8 +334,13 @@ static __device__ __noinline__ SurfR reproject_rays(const FrameView* Fp, int cur
         }
     }
     double off = 1e-3 * F.diag;
-    if (trace_closest(F, plane_pt + tn * off, -tn, 0, 2 * off, h) ||
-        trace_closest(F, plane_pt - tn * off, tn, 0, 2 * off, h)) {
+    out.rays += 1;
+    bool hit = trace_closest(F, plane_pt + tn * off, -tn, 0, 2 * off, h);
+    if (!hit) {
+        out.rays += 1;
+        hit = trace_closest(F, plane_pt - tn * off, tn, 0, 2 * off, h);
+    }
+    if (hit) {
         out.pos = h.pos;
         out.n = F.tri[h.tri].n;
         out.tri = h.tri;
@@ -538,6 +547,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 
     // per-lane Newton state (one job at a time)
     bool active = false, exhausted = false, init = false, count = false, parked = false;
+    uint32_t n_rays = 0;
     uint32_t job = 0;
     int dsel = 0;
     V3 p1{0, 0, 0}, p2{0, 0, 0}, spos{0, 0, 0}, cpos{0, 0, 0};
@@ -624,7 +634,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 }
             }
         }
-        if (__all_sync(0xffffffffu, exhausted)) break;
+        if (__all_sync(0xffffffffu, exhausted)) {
+            work_add(cfg.work, WK_CLOSEST, n_rays);
+            break;
+        }
 
         // ---- one Newton trial (trial 0 = the initial evaluation at the start point)
         const FrameView& F = sF[dsel];
@@ -640,6 +653,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned rm = __ballot_sync(0xffffffffu, active && !parked);
         if (parked && (__popc(pm) >= TOFR_RAYBATCH || rm == 0)) {
             SurfR r = reproject_rays(&F, ctri, tpos, p1);
+            n_rays += uint32_t(r.rays);
             have = r.ok;
             if (have) {
                 tpos = r.pos;
@@ -710,6 +724,16 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 // finish: occlusion, Jacobian, rebuild (shift_sample tail + rebuild_sample,
 // shiftmap.hpp:579-654, :740-783), output
 
+// Bvh::occluded, counting the rays it traces
+__device__ __forceinline__ bool occluded_n(const FrameView& F, const V3& a, const V3& b, uint32_t& nr) {
+    V3 dd = b - a;
+    double dist = norm(dd);
+    if (dist <= 2 * F.eps_ray) return false;
+    ++nr;
+    V3 d = dd / dist;
+    return trace_any(F, a, d, F.eps_ray, dist - F.eps_ray);
+}
+
 __device__ __forceinline__ void out_fail(const ShiftQueue& q, uint32_t k) { st2(q.out, 0, k, 0.0, 0.0); }
 
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
@@ -725,6 +749,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     Ctr ctr;
 #pragma unroll
     for (int k = 0; k < SC_COUNT; ++k) ctr.v[k] = 0;
+    uint32_t n_any = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cfg.work && njobs) atomicAdd(&cfg.work[WK_JOBS], (unsigned long long)njobs);
     TOFR_FOR_ITEMS(i, njobs, wq) {
         uint32_t k = j0 + uint32_t(i);
         double2 c6 = jld(q, 6, k);
@@ -749,7 +775,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int ptri = ts.x;
         V3 pnrm = (ts.y & 2) ? rec_pn(st, jb.item) : F.tri[ptri].n;
         double j_newton = c5.y;
-        if (occluded(F, pre.p1, ppos) || occluded(F, ppos, suf.p2)) {
+        if (occluded_n(F, pre.p1, ppos, n_any) || occluded_n(F, ppos, suf.p2, n_any)) {
             if (count) ctr.v[SC_OCCLUDED]++;
             out_fail(q, k);
             continue;
@@ -844,6 +870,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         for (int c = 17; c < (mt.nl > 0 ? kResChunks : 20); ++c)
             __stcg(&o.base[size_t(c) * o.stride + k], ld2(st, c, jb.item));
     }
+    work_add(cfg.work, WK_ANY, n_any);
     ctr_flush(ctr, ctr_out);
 }
 
@@ -1145,15 +1172,24 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
     size_t cap_jobs = q.cap;
     if (cfg.replay) {
         cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
-        k_shift_replay<<<persistent_grid(reinterpret_cast<const void*>(k_shift_replay), 128, sm, cap_jobs), 128, sm,
-                         s>>>(F0, F1, g0, g1, st0, st1, q, cfg, wq);
+        {
+            KScope ks("k_shift_replay", s);
+            k_shift_replay<<<persistent_grid(reinterpret_cast<const void*>(k_shift_replay), 128, sm, cap_jobs), 128, sm,
+                             s>>>(F0, F1, g0, g1, st0, st1, q, cfg, wq);
+        }
     }
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
-    k_shift_solve<<<persistent_grid(reinterpret_cast<const void*>(k_shift_solve), 128, sm, cap_jobs), 128, sm, s>>>(
-        F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+    {
+        KScope ks("k_shift_solve", s);
+        k_shift_solve<<<persistent_grid(reinterpret_cast<const void*>(k_shift_solve), 128, sm, cap_jobs), 128, sm, s>>>(
+            F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+    }
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
-    k_shift_finish<<<persistent_grid(reinterpret_cast<const void*>(k_shift_finish), 128, sm, cap_jobs), 128, sm, s>>>(
-        F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+    {
+        KScope ks("k_shift_finish", s);
+        k_shift_finish<<<persistent_grid(reinterpret_cast<const void*>(k_shift_finish), 128, sm, cap_jobs), 128, sm, s>>>(
+            F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+    }
 }
 
 void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
@@ -1162,10 +1198,19 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
                           cudaStream_t s) {
     size_t n = size_t(bd.y1 - bd.y0) * Fc.cam.w * (cg.transient ? cg.h.bins : 1);
     if (!n) return;
-    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
-    k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    }
+    {
+        KScope ks("k_temporal_prep", s);
+        k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
+    }
     run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, cfg, ctr, q, s);
-    k_temporal_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cfg, frame_idx, cur, prev, ws);
+    {
+        KScope ks("k_temporal_apply", s);
+        k_temporal_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cfg, frame_idx, cur, prev, ws);
+    }
 }
 
 void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
@@ -1173,15 +1218,33 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
                          const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q, cudaStream_t s) {
     size_t n = size_t(bd.y1 - bd.y0) * F.cam.w * (gg.transient ? gg.h.bins : 1);
     if (!n) return;
-    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
-    k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    }
+    {
+        KScope ks("k_spatial_prep_fwd", s);
+        k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
+    }
     run_shifts(F, F, g, g, src, dst, ws.q, cfg, ctr, q, s);
-    k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 1);
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 1);
+    }
     for (int j = 0; j < sp.neighbors; ++j) {
-        if (j > 0) k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 2);
-        k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        if (j > 0) {
+            KScope ks("k_queue_ctl", s);
+            k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 2);
+        }
+        {
+            KScope ks("k_spatial_prep_inv", s);
+            k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        }
         run_shifts(F, F, g, g, src, dst, ws.q, cfg, nullptr, q, s);
-        k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        {
+            KScope ks("k_spatial_apply", s);
+            k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        }
     }
 }
 

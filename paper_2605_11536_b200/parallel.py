@@ -228,6 +228,9 @@ class BandSession:
     def io_bytes(self):
         return self.sess.io_bytes()
 
+    def work(self) -> dict:
+        return self.sess.work()
+
     def halo_launches(self, steps: int) -> int:
         """pack + unpack launches per exchange (one per non-empty side)."""
         if self.exchanger is None:

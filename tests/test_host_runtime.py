@@ -29,7 +29,7 @@ REF_SCENES = Path("/root/reference/proj/scenes")
 def test_library_exports_every_declared_symbol():
     lib = F.load_library()
     header = (ROOT / "include" / "tofr_gpu.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(tofr_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*|uint64_t)\s+(tofr_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(F.EXPORTED_SYMBOLS), declared ^ set(F.EXPORTED_SYMBOLS)
     for name in declared:
