@@ -665,7 +665,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned em = __ballot_sync(0xffffffffu, active && !parked);
         if (!active || parked) continue;
         __syncwarp(em);
-        Frame2 Jt = tangent_frame(F, ttri);
+        // the tangent frame of the current triangle is already known (Jc, or Js
+        // for trial 0): recompute only after a re-projection ray changed it
+        Frame2 Jt = init ? Js : Jc;
+        if (!init && ttri != ctri) Jt = tangent_frame(F, ttri);
         TrialEval et = trial_eval(p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
         double fn = hypot(et.F.x, et.F.y);
         bool accept = have && (init || fn < fnorm);
@@ -775,7 +778,19 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int ptri = ts.x;
         V3 pnrm = (ts.y & 2) ? rec_pn(st, jb.item) : F.tri[ptri].n;
         double j_newton = c5.y;
-        if (occluded_n(F, pre.p1, ppos, n_any) || occluded_n(F, ppos, suf.p2, n_any)) {
+        // the two occlusion tests of shift_sample (shiftmap.hpp:765-767) as one
+        // loop around a single traversal site, so lanes stay converged
+        bool occ = false;
+        for (int r = 0; r < 2 && !occ; ++r) {
+            V3 a = r == 0 ? pre.p1 : ppos, bpt = r == 0 ? ppos : suf.p2;
+            V3 dd = bpt - a;
+            double dist = norm(dd);
+            if (dist <= 2 * F.eps_ray) continue;  // Bvh::occluded: nothing between
+            ++n_any;
+            V3 dir = dd / dist;
+            occ = trace_ray_impl(F.nodes, F.tri_isect, a, dir, F.eps_ray, dist - F.eps_ray, true).slot >= 0;
+        }
+        if (occ) {
             if (count) ctr.v[SC_OCCLUDED]++;
             out_fail(q, k);
             continue;
