@@ -107,10 +107,10 @@ KERNEL_BYTES = {
     "k_ris_finalize": ("item", 32),
     # merge stages: header reads of both sides + header write per item
     "k_temporal_prep": ("item", 16 + 16 + 16),
-    "k_temporal_apply": ("item", 3 * R_BYTES),
+    "k_temporal_apply": ("merge", 3 * R_BYTES),
     "k_spatial_prep_fwd": ("item", 16),
     "k_spatial_prep_inv": ("item", 16 + 16),
-    "k_spatial_apply": ("item", 3 * R_BYTES),
+    "k_spatial_apply": ("merge", 3 * R_BYTES),
     "k_shade_gated": ("pixel", 24 + 12 + 24),
     "k_shade_transient": ("item", 16 + 24),
     "k_gbuffer": ("pixel", GHIT_BYTES),
@@ -302,6 +302,9 @@ def run_ours(args) -> None:
         per_launch_jobs = work.get("shift_jobs", 0) / max(1, sum(v[1] for k, v in ktimes.items()
                                                                   if k == "k_shift_finish"))
         units["job"] = per_launch_jobs
+    if dom and KERNEL_BYTES.get(dom, ("", 0))[0] == "merge":  # merge-list items per apply launch
+        units["merge"] = work.get("merges", 0) / max(1, sum(v[1] for k, v in ktimes.items()
+                                                             if k.endswith("_apply")))
     if plain:  # deposits per launch (one deposit launch per frame)
         units["deposit"] = work.get("deposits", 0) / args.steps
     unit, per_unit = KERNEL_BYTES.get(dom, ("pixel", 0))

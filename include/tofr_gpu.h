@@ -240,8 +240,9 @@ int tofr_gpu_session_stream(tofr_session* ss, void** stream);
 int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t* d2h_image);
 /* device work counted since the session was created: out[0] shift jobs,
  * out[1] closest-hit rays (incl. camera rays), out[2] any-hit (shadow /
- * occlusion) rays, out[3] transient histogram deposits */
-int tofr_gpu_session_work(tofr_session* ss, uint64_t* out /* [4] */);
+ * occlusion) rays, out[3] transient histogram deposits, out[4] GRIS merges
+ * with a non-empty side (reuse merge lists) */
+int tofr_gpu_session_work(tofr_session* ss, uint64_t* out /* [5] */);
 void tofr_gpu_session_destroy(tofr_session* ss);
 
 /* launch accounting of the library's kernels (process-wide): every launch is

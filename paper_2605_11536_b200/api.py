@@ -411,10 +411,10 @@ class Session:
 
     def work(self) -> dict:
         """Device work since the session was created (waits for pending frames)."""
-        w = (C.c_uint64 * 4)()
+        w = (C.c_uint64 * 5)()
         self._r._check(self._r._lib.tofr_gpu_session_work(self.handle, w))
         return {"shift_jobs": int(w[0]), "rays_closest": int(w[1]), "rays_any": int(w[2]),
-                "deposits": int(w[3])}
+                "deposits": int(w[3]), "merges": int(w[4])}
 
     def io_bytes(self):
         h2d, d2h = C.c_uint64(), C.c_uint64()

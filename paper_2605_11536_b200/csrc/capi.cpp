@@ -1229,6 +1229,7 @@ int tofr_gpu_session_work(tofr_session* ss, uint64_t* out) {
         out[1] = w[WK_CLOSEST] + ss->camera_rays;
         out[2] = w[WK_ANY];
         out[3] = w[WK_DEPOSITS];
+        out[4] = w[WK_MERGES];
     });
 }
 

@@ -102,7 +102,7 @@ struct PathCfg {
 
 // device work counters (cumulative per session): shift jobs, closest-hit rays,
 // any-hit (shadow / occlusion) rays, transient histogram deposits
-enum : int { WK_JOBS = 0, WK_CLOSEST = 1, WK_ANY = 2, WK_DEPOSITS = 3, WK_COUNT = 4 };
+enum : int { WK_JOBS = 0, WK_CLOSEST = 1, WK_ANY = 2, WK_DEPOSITS = 3, WK_MERGES = 4, WK_COUNT = 5 };
 
 #if defined(__CUDACC__)
 // warp-aggregated add of a per-lane count (all lanes of the warp must call it)

@@ -142,13 +142,17 @@ __device__ __forceinline__ uint32_t queue_append(const ShiftQueue& q, bool want,
 
 // Warp-aggregated append to the merge list (items whose merge needs a sample:
 // at least one side non-empty); count in q.ctl[3].  All lanes must call it.
-__device__ __forceinline__ void mlist_append(const WaveScratch& ws, bool want, uint32_t item) {
+__device__ __forceinline__ void mlist_append(const WaveScratch& ws, bool want, uint32_t item,
+                                             unsigned long long* work) {
     unsigned m = __ballot_sync(0xffffffffu, want);
     if (!m) return;
     int lane = threadIdx.x & 31;
     int leader = __ffs(m) - 1;
     uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&ws.q.ctl[3], uint32_t(__popc(m)));
+    if (lane == leader) {
+        base = atomicAdd(&ws.q.ctl[3], uint32_t(__popc(m)));
+        if (work) atomicAdd(&work[WK_MERGES], (unsigned long long)__popc(m));
+    }
     base = __shfl_sync(0xffffffffu, base, leader);
     if (want) ws.mlist[base + __popc(m & ((1u << lane) - 1))] = item;
 }
@@ -998,7 +1002,7 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
             job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
             ws.map_b[i] = ki;
         }
-        mlist_append(ws, merge, uint32_t(i));
+        mlist_append(ws, merge, uint32_t(i), cfg.work);
     }
 }
 
@@ -1111,7 +1115,7 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
             job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
             ws.map_b[i] = k;
         }
-        mlist_append(ws, merge, uint32_t(i));
+        mlist_append(ws, merge, uint32_t(i), cfg.work);
     }
 }
 
@@ -1158,16 +1162,18 @@ __global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate
 // queue control and launchers
 
 // op 0: empty queue; op 1: mark the end (the next batch starts after it);
-// op 2: rewind to the mark.
+// op 2: rewind to the mark; op 3: mark the end, the current batch continues.
 __global__ void k_queue_ctl(uint32_t* ctl, int op) {
     if (op == 0) {
         ctl[0] = ctl[1] = ctl[2] = 0;
     } else if (op == 1) {
         ctl[2] = ctl[1];
         ctl[0] = ctl[1];
-    } else {
+    } else if (op == 2) {
         ctl[0] = ctl[2];
         ctl[1] = ctl[2];
+    } else {
+        ctl[2] = ctl[1];
     }
     ctl[3] = 0;  // merge list of the batch
 }
@@ -1237,14 +1243,16 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
         KScope ks("k_queue_ctl", s);
         k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
     }
+    // The forward shifts of every neighbour and the inverse shifts of neighbour 0
+    // (from the pass input) are independent: one shift batch.  Inverse shifts
+    // of neighbour j > 0 need merge j - 1 and replace the previous inverse batch.
     {
         KScope ks("k_spatial_prep_fwd", s);
         k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
     }
-    run_shifts(F, F, g, g, src, dst, ws.q, cfg, ctr, q, s);
     {
         KScope ks("k_queue_ctl", s);
-        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 1);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 3);
     }
     for (int j = 0; j < sp.neighbors; ++j) {
         if (j > 0) {
@@ -1255,7 +1263,7 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
             KScope ks("k_spatial_prep_inv", s);
             k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
         }
-        run_shifts(F, F, g, g, src, dst, ws.q, cfg, nullptr, q, s);
+        run_shifts(F, F, g, g, src, dst, ws.q, cfg, ctr, q, s);
         {
             KScope ks("k_spatial_apply", s);
             k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);

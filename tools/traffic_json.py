@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""profiles/traffic.json from full ncu captures: {"<workload>:<kernel>": dram bytes
+(read + write) of the captured launch}.  bench.py reports it as roofline.traffic.
+
+    python tools/traffic_json.py gpurun_out/<tag>/full_<wl>_<kernel>.ncu-rep ...
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+out_path = Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
+data = json.loads(out_path.read_text()) if out_path.exists() else {}
+for rep in sys.argv[1:]:
+    m = re.match(r"full_([^_]+)_(.+)\.ncu-rep$", Path(rep).name)
+    if not m:
+        continue
+    wl, kernel = m.group(1), m.group(2)
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(txt)))
+    hdr, units, row = r[0], r[1], r[2]
+    d, u = dict(zip(hdr, row)), dict(zip(hdr, units))
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        tot += float(d[k].replace(",", "")) * UNIT.get(u[k], 1)
+    data[f"{wl}:{kernel}"] = round(tot)
+    print(wl, kernel, f"{tot / 1e6:.1f} MB")
+out_path.write_text(json.dumps(data, indent=1, sort_keys=True) + "\n")
