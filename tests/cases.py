@@ -97,3 +97,26 @@ REFERENCE_CASES = {
     "ref_cornell": (lambda: scenes.bundled("cornell", 32), 0.0, gate(10.0, 0.5), 16, 5, 6),
     "ref_doppler": (lambda: scenes.bundled("boxes_doppler", 24), 4.0, gate(12.0, 0.5), 8, 9, 8),
 }
+
+# BASELINE.json configurations at their full sizes: the oracle renders
+# them on all host threads in seconds per frame; C2(ii) needs 84 GB in the
+# reference layout and is covered by the plain C2(i) run plus the small
+# transient cases above.
+FULL_CASES = {
+    "full_c3_boxes_doppler_1080p": (lambda: scenes.bundled("boxes_doppler", 1920, 1080),
+                                    RenderConfig(gate=gate(12.0, 0.041), m_init=1, temporal=True, spatial_passes=1,
+                                                 spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6,
+                                                 frames=3, seed=1), "gated"),
+    "full_c3w_cornell_wide_1080p": (lambda: scenes.bundled("cornell_wide", 1920, 1080),
+                                    RenderConfig(gate=gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1,
+                                                 spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6,
+                                                 frames=2, seed=1), "gated"),
+    "full_c1_cornell_256": (lambda: scenes.bundled("cornell", 256, 256),
+                            RenderConfig(gate=gate(10.0, 0.0866), m_init=1, temporal=True, spatial_passes=1,
+                                         spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, frames=4,
+                                         seed=1), "gated"),
+    "full_c2p_cornell_512_256bins": (lambda: scenes.bundled("cornell", 512, 512),
+                                     RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0,
+                                                  hist_bin_width=0.046875, m_init=1, max_depth=6, frames=2, seed=1),
+                                     "plain"),
+}

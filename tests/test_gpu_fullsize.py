@@ -1,0 +1,97 @@
+"""Full-size parity (BASELINE configs at 1080p / 512^2 x 256 bins) and
+bit-identity of the wavefront pipeline with the per-reservoir kernels.
+
+* GPU vs the CPU oracle on the exact bench configurations: >= 99.9% of pixels
+  within 1e-4 relative (north star), shift counters within 0.1%, plain
+  deposit counts bit-exact.
+* The wavefront reuse engine / path-tree state machine (default) against the
+  per-item kernels (TOFR_REUSE=legacy TOFR_TRACE=legacy) in a separate
+  process: identical arithmetic, so images and counters must be bit-identical.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from tests.cases import CASES, FULL_CASES
+from tests.parity import summary
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+KEYS = ("attempts", "newton_ok", "newton_failed", "occluded", "jac_clamped", "replay_failed", "iterations",
+        "solves", "success")
+
+
+def _render(renderer, table, name):
+    build, cfg, kind = table[name]
+    sd = build()
+    fn = {"gated": renderer.render_gated, "plain": renderer.render_transient_plain,
+          "transient": renderer.render_transient}[kind]
+    return sd, cfg, kind, fn(sd, cfg)
+
+
+def _totals(stats):
+    tot = {k: 0 for k in KEYS}
+    for fs in stats:
+        for stage in ("temporal", "spatial", "bin"):
+            for k in KEYS:
+                tot[k] += fs[stage][k]
+    return tot
+
+
+@pytest.mark.parametrize("name", sorted(FULL_CASES))
+def test_full_size_parity(renderer, ref, name):
+    sd, cfg, kind, g = _render(renderer, FULL_CASES, name)
+    rs = ref.RefScene(sd)
+    r = {"gated": ref.render_gated, "plain": ref.render_transient_plain, "transient": ref.render_transient}[kind](
+        rs, cfg)
+    s = summary(g.image, r.image)
+    print(name, s)
+    assert r.image.max() > 0
+    assert s["within"] >= 0.999, s
+    if kind == "plain":
+        assert np.array_equal(g.hist.count, r.hist.count), "bin indexing differs from the oracle"
+    else:
+        tg, tr = _totals(g.stats), _totals(r.stats)
+        print(name, tg, tr)
+        for k in KEYS:
+            assert abs(tg[k] - tr[k]) <= max(2, 1e-3 * tr[k]), (k, tg, tr)
+
+
+_CHILD = r"""
+import json, sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from tests.cases import CASES, FULL_CASES
+from paper_2605_11536_b200.api import Renderer
+table = FULL_CASES if sys.argv[2] in FULL_CASES else CASES
+build, cfg, kind = table[sys.argv[2]]
+r = Renderer(0)
+fn = {"gated": r.render_gated, "plain": r.render_transient_plain, "transient": r.render_transient}[kind]
+out = fn(build(), cfg)
+np.save(sys.argv[3], out.image)
+stats = [{st: {k: int(v) for k, v in fs[st].items() if isinstance(v, (int, np.integer))}
+          for st in ("temporal", "spatial", "bin")} for fs in out.stats] if out.stats else []
+print(json.dumps(stats))
+"""
+
+
+@pytest.mark.parametrize("name", ["full_c3_boxes_doppler_1080p", "full_c1_cornell_256", "mirror_replay",
+                                  "transient_full", "doppler_scene_reuse"])
+def test_wavefront_bit_identical_to_per_item_kernels(tmp_path, name):
+    outs = []
+    for tag, extra in (("wave", {}), ("legacy", {"TOFR_REUSE": "legacy", "TOFR_TRACE": "legacy"})):
+        env = {**os.environ, **extra}
+        f = tmp_path / f"{tag}.npy"
+        p = subprocess.run([sys.executable, "-c", _CHILD, str(ROOT), name, str(f)], capture_output=True, text=True,
+                           env=env, timeout=900)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append((np.load(f), json.loads(p.stdout.strip().splitlines()[-1])))
+    (a, sa), (b, sb) = outs
+    assert np.array_equal(a, b), summary(a, b)
+    assert sa == sb
