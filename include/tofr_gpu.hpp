@@ -247,6 +247,11 @@ inline RenderOutput render_gated(const SceneDef& def, const RenderConfig& cfg) {
     return detail::run(tofr_gpu_render_gated, "render_gated", def, cfg, false);
 }
 
+// render_doppler (pipeline.hpp:573-578): the gated pipeline on the path velocity
+inline RenderOutput render_doppler(const SceneDef& def, const RenderConfig& cfg) {
+    return detail::run(tofr_gpu_render_doppler, "render_doppler", def, cfg, false);
+}
+
 inline RenderOutput render_transient(const SceneDef& def, const RenderConfig& cfg) {
     return detail::run(tofr_gpu_render_transient, "render_transient", def, cfg, true);
 }

@@ -4,7 +4,7 @@ the C ABI of libtofr_b200.so.
     render_gated(scene, cfg)            -> RenderOutput   (pipeline.hpp:323)
     render_transient(scene, cfg)        -> RenderOutput   (pipeline.hpp:396)
     render_transient_plain(scene, cfg)  -> RenderOutput   (pipeline.hpp:531)
-    render_doppler(scene, cfg)          -> raises NotImplementedError (not built)
+    render_doppler(scene, cfg)          -> RenderOutput   (pipeline.hpp:574, velocity gate)
     reference_render(scene, frame, gate, spp, seed, max_depth) -> (mean, se)
 
 `scene` is a SceneDef (scenes.py), a path to a .scn file, or a Scene handle.
@@ -269,7 +269,9 @@ class Renderer:
         return self._render("tofr_gpu_render_gated", scene, cfg, False)
 
     def render_doppler(self, scene, cfg: RenderConfig) -> RenderOutput:
-        raise NotImplementedError("render_doppler (velocity gates) is not built in this round")
+        """render_gated with the gate read as a Doppler (path-velocity) gate:
+        centre/width in Hz, carrier cfg.gate.f0 (pipeline.hpp:573-578)."""
+        return self._render("tofr_gpu_render_doppler", scene, cfg, False)
 
     def render_transient(self, scene, cfg: RenderConfig) -> RenderOutput:
         return self._render("tofr_gpu_render_transient", scene, cfg, True)

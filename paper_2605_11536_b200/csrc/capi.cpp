@@ -303,8 +303,20 @@ void check_config(const tofr_render_config* c) {
     if (!c) throw ScopeError(TOFR_ERR_INVALID, "null config");
     if (c->max_depth < 1 || c->max_depth > 64) throw ScopeError(TOFR_ERR_INVALID, "max_depth out of range");
     if (c->frames < 0) throw ScopeError(TOFR_ERR_INVALID, "frames < 0");
-    if (c->gate_kind != TOFR_GATE_LENGTH)
-        throw ScopeError(TOFR_ERR_UNSUPPORTED, "velocity (Doppler) gates are not built yet");
+    if (c->gate_kind == TOFR_GATE_VELOCITY) {
+        // Doppler gates (render_doppler, pipeline.hpp:573-578): the gated image
+        // pipeline on the path velocity; built on the wavefront kernels
+        if (c->mode == TOFR_MODE_TRANSIENT)
+            throw ScopeError(TOFR_ERR_UNSUPPORTED, "velocity gates apply to gated rendering only");
+        if (!(c->gate_f0 != 0)) throw ScopeError(TOFR_ERR_INVALID, "velocity gate needs a carrier f0");
+        for (const char* var : {"TOFR_REUSE", "TOFR_TRACE"}) {
+            const char* e = std::getenv(var);
+            if (e && std::strcmp(e, "legacy") == 0)
+                throw ScopeError(TOFR_ERR_UNSUPPORTED, "velocity gates need the wavefront kernels (unset TOFR_REUSE / TOFR_TRACE)");
+        }
+    } else if (c->gate_kind != TOFR_GATE_LENGTH) {
+        throw ScopeError(TOFR_ERR_INVALID, "unknown gate kind");
+    }
 }
 
 enum SessionKind { KIND_RESTIR = 0, KIND_PLAIN = 1, KIND_BARE = 2 };
@@ -520,9 +532,17 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     const FrameView& F = s->slot[sl].view;
     GHit* g_local = s->slot[sl].gbuf.as<GHit>();
     const GHit* g = rows_base<GHit>(s->slot[sl].gbuf, s->r0, s->W);
+    // gate of this frame (RenderConfig::gate_at) in constraint units
+    // (GateSpec::ccenter / cwidth: Hz / f0 for velocity gates)
+    const bool vel = c.gate_kind == TOFR_GATE_VELOCITY;
     double center = c.gate_center + c.gate_step * f;
     double width = c.gate_width;
+    if (vel) {
+        center = center / c.gate_f0;
+        width = width / c.gate_f0;
+    }
     PathCfg pc = path_cfg(c, center, width, s->scene);
+    pc.gate_vel = vel ? 1 : 0;
     pc.work = s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 2;
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
@@ -559,7 +579,9 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                           rows_base<uint32_t>(s->hist_count, s->y0, pr), q, stream);
         for (int i = 1; i < 6; ++i) cudaEventRecord(ev[i], stream);
     } else {
-        InitParams ip{c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
+        // the ellipsoidal and shrink initializers apply to length gates only; velocity
+        // gates fall back to plain RIS (pipeline.hpp:110, :130)
+        InitParams ip{vel ? int(INIT_DIRECT) : c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
         ResStore cur = store_of(s, s->res[s->cur]);
         if (s->transient)
             launch_init_transient(F, bd, g, pc, ip, h, f, cur, q, stream);
@@ -612,7 +634,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
             launch_shade_transient(cur, bd, s->W, h, rows_base<double>(s->hist, s->y0, size_t(s->W) * s->B * 3),
                                    stream);
         else
-            launch_shade_gated(cur, bd, s->W, center, width, rows_base<double>(s->image, s->y0, size_t(s->W) * 3),
+            launch_shade_gated(cur, bd, s->W, center, width, pc.gate_vel, rows_base<double>(s->image, s->y0, size_t(s->W) * 3),
                                rows_base<double>(s->accum, s->y0, size_t(s->W) * 3), stream);
         // a moving camera reprojects across band edges: give the next
         // frame's temporal stage the neighbours' final reservoirs too
@@ -986,12 +1008,14 @@ int tofr_gpu_render_gated(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_
     });
 }
 
+// render_doppler (pipeline.hpp:573-578): render_gated with the velocity gate
 int tofr_gpu_render_doppler(tofr_gpu* ctx, const tofr_scene* s, const tofr_render_config* cfg, tofr_output* out) {
-    (void)s;
-    (void)cfg;
-    (void)out;
     return guard(ctx, [&] {
-        throw ScopeError(TOFR_ERR_UNSUPPORTED, "render_doppler (velocity gates) is not built yet");
+        if (!cfg) throw ScopeError(TOFR_ERR_INVALID, "null config");
+        tofr_render_config c = *cfg;
+        c.gate_kind = TOFR_GATE_VELOCITY;
+        if (c.mode == TOFR_MODE_TRANSIENT) throw ScopeError(TOFR_ERR_INVALID, "render_doppler is a gated mode");
+        render_loop(ctx, s, &c, out, false);
     });
 }
 

@@ -571,6 +571,24 @@ HFrame build_frame(const HScene& def, double frame) {
             f.tris.push_back(w);
         }
         if (obj.track.moving_at(frame)) f.geo_motion = 1;
+        // velocity_field (scene.hpp:318-335)
+        GVel gv;
+        std::memset(&gv, 0, sizeof(gv));
+        if (obj.track.animated()) {
+            double fmin = obj.track.keys.front().frame, fmax = obj.track.keys.back().frame;
+            double lo = std::max(fmin, frame - 1.0), hi = std::min(fmax, frame + 1.0);
+            if (hi <= lo) lo = hi = frame;
+            if (hi > lo) {
+                HPose pf = obj.track.pose_at(frame), pp = obj.track.pose_at(hi), pm = obj.track.pose_at(lo);
+                double inv = 1.0 / ((hi - lo) * def.dt_frame);
+                M3 rf_t = transpose(quat_matrix(pf.q));
+                M3 dr = (quat_matrix(pp.q) - quat_matrix(pm.q)) * inv;
+                gv.A = dr * rf_t;
+                gv.c = (pp.t - pm.t) * inv - gv.A * pf.t;
+                gv.moving = 1;
+            }
+        }
+        f.obj_vel.push_back(gv);
     }
     if (f.tris.empty()) throw std::runtime_error("bvh: empty mesh");
     for (const HTri& t : f.tris)
@@ -598,6 +616,14 @@ HFrame build_frame(const HScene& def, double frame) {
     f.cam.tan_half = std::tan(def.camera.fov_y / 2);
     f.cam.w = def.camera.width;
     f.cam.h = def.camera.height;
+    if (def.camera.track.size() > 1) {  // central difference on the camera position track
+        double lo = std::max(def.camera.track.front().first, frame - 1.0);
+        double hi = std::min(def.camera.track.back().first, frame + 1.0);
+        if (hi > lo) {
+            V3 pp = def.camera.pose_at(hi).position, pm = def.camera.pose_at(lo).position;
+            f.cam_vel = (pp - pm) / ((hi - lo) * def.dt_frame);
+        }
+    }
 
     std::memset(&f.light, 0, sizeof(f.light));
     f.light.pos = def.light.position;
@@ -716,6 +742,8 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
     off = align(off + nt * sizeof(GTriInfo));
     p.off_mats = off;
     off = align(off + mats.size() * sizeof(GMat));
+    p.off_vel = off;
+    off = align(off + f.obj_vel.size() * sizeof(GVel));
     p.blob.assign(off, 0);
     std::memcpy(p.blob.data() + p.off_nodes, nodes.data(), nn * sizeof(GNode));
     std::memcpy(p.blob.data() + p.off_aux, aux.data(), nn * sizeof(GNodeAux));
@@ -723,6 +751,7 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
     std::memcpy(p.blob.data() + p.off_tri_id, tri_id.data(), nt * sizeof(int));
     std::memcpy(p.blob.data() + p.off_tri, info.data(), nt * sizeof(GTriInfo));
     std::memcpy(p.blob.data() + p.off_mats, mats.data(), mats.size() * sizeof(GMat));
+    if (!f.obj_vel.empty()) std::memcpy(p.blob.data() + p.off_vel, f.obj_vel.data(), f.obj_vel.size() * sizeof(GVel));
 
     FrameView& v = p.view;
     std::memset(&v, 0, sizeof(v));
@@ -736,6 +765,8 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
     v.eps_ray = f.eps_ray;
     v.diag = f.diag;
     v.frame_id = frame_id;
+    v.n_obj = int(f.obj_vel.size());
+    v.cam_vel = f.cam_vel;
     return p;
 }
 
@@ -747,6 +778,7 @@ FrameView rebase_view(const PackedFrame& p, const unsigned char* base) {
     v.tri_id = reinterpret_cast<const int*>(base + p.off_tri_id);
     v.tri = reinterpret_cast<const GTriInfo*>(base + p.off_tri);
     v.mats = reinterpret_cast<const GMat*>(base + p.off_mats);
+    v.vel = reinterpret_cast<const GVel*>(base + p.off_vel);
     return v;
 }
 

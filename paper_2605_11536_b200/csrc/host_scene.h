@@ -107,7 +107,7 @@ struct HNode {
 // back to back in one allocation so a frame upload is a single copy.
 struct PackedFrame {
     std::vector<unsigned char> blob;
-    size_t off_nodes = 0, off_aux = 0, off_isect = 0, off_tri_id = 0, off_tri = 0, off_mats = 0;
+    size_t off_nodes = 0, off_aux = 0, off_isect = 0, off_tri_id = 0, off_tri = 0, off_mats = 0, off_vel = 0;
     FrameView view;  // pointers are offsets until rebased
 };
 
@@ -122,6 +122,8 @@ struct HFrame {
     GLightSub lsub;
     int geo_motion = 0;
     int max_depth = 0;  // deepest root-to-leaf path (for sanity checks)
+    std::vector<GVel> obj_vel;  // velocity_field per object (scene.hpp:318-335)
+    V3 cam_vel{0, 0, 0};
 };
 
 // Builds the snapshot for `frame` (scene.hpp:479-548).  Throws

@@ -80,6 +80,15 @@ struct GLightSub {  // scene.hpp:433-440
     double chain_len;
 };
 
+// Affine velocity field v(x) = A x + c of one object at one frame
+// (VelocityField, scene.hpp:308-335); zero when the object does not move.
+struct GVel {
+    M3 A;
+    V3 c;
+    int moving;
+    int pad;
+};
+
 // One frame snapshot as seen by the kernels (SceneFrame, scene.hpp:443-471).
 struct FrameView {
     const GNode* nodes;
@@ -95,8 +104,18 @@ struct FrameView {
     GLightSub lsub;
     double eps_ray, diag;
     int frame_id;  // identity of the snapshot (Domain::frame pointer compare)
-    int pad;
+    int n_obj;
+    const GVel* vel;  // per object (n_obj)
+    V3 cam_vel;       // central difference of the camera track (scene.hpp:508-513)
 };
+
+// SceneFrame::velocity_at (scene.hpp:457-460): A * world + c, or 0
+TOFR_HD V3 velocity_at(const FrameView& f, int obj, const V3& p) {
+    if (obj < 0 || obj >= f.n_obj) return splat(0);
+    const GVel& v = f.vel[obj];
+    if (!v.moving) return splat(0);
+    return v.A * p + v.c;
+}
 
 // ---------------------------------------------------------------------------
 // intersection

@@ -197,7 +197,7 @@ __device__ void init_pixel(const FrameView& F, const PathCfg& cfg, const InitPar
             ms.phat_src_of_dst =
                 luminance(inv.f) * gate_w(ip.center, ip.width * ip.shrink_k, inv.len) * ijac;
     }
-    gris_merge(out, rough, ms, fwd, ip.center, ip.width, cfg.m_cap, pick);
+    gris_merge(out, rough, ms, fwd, fwd.len, ip.center, ip.width, cfg.m_cap, pick);
 }
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_temporal(FrameView Fc,
         }
         uint64_t pix = uint64_t(py) * W + px;
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
-        int which = gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        int which = gris_merge(dst, src, ms, mapped, mapped.len, dc, dw, cfg.m_cap, rng);
         if (which == 2)
             res_store(cur, it, dst);
         else  // in place: the kept sample and its p-hat are already stored
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_spatial(FrameView F, B
                     if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
                         ms.phat_src_of_dst = luminance(inv.f) * gate_w(dc, dw, inv.len) * jac;
                 }
-                gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+                gris_merge(out, src, ms, mapped, mapped.len, dc, dw, cfg.m_cap, rng);
             }
         }
         res_store_result(dst_grid, it, out);
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB)
             if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
                 ms.phat_src_of_dst = luminance(inv.f) * gate_w(dc, dw, inv.len) * jac;
         }
-        int which = gris_merge(out, src, ms, mapped.y, dc, dw, cfg.m_cap, rng);
+        int which = gris_merge(out, src, ms, mapped.y, mapped.y.len, dc, dw, cfg.m_cap, rng);
         if (which == 2) {
             res_load_rec(sc.mapped, e, out.y);
             res_store(dst_grid, it, out);
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_binreuse(FrameView F, 
                 if (shift_sample(out.y, dd, sd, cfg, nullptr, inv, jac))
                     ms.phat_src_of_dst = luminance(inv.f) * gate_w(sc, dw, inv.len) * jac;
             }
-            gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+            gris_merge(out, src, ms, mapped, mapped.len, dc, dw, cfg.m_cap, rng);
         }
         res_store_result(dst_grid, it, out);
     }
@@ -760,20 +760,23 @@ __global__ void k_cost_scatter(const uint8_t* cls, size_t n, uint32_t* counts, u
 // ---------------------------------------------------------------------------
 // final shading (ris.hpp:108-111)
 
-__device__ __forceinline__ V3 shade_item(const ResStore& s, size_t i, double c, double w) {
+// final_shading (ris.hpp:108-111): f * (W * gate weight of the sample's
+// length, or of its path velocity for Doppler gates)
+__device__ __forceinline__ V3 shade_item(const ResStore& s, size_t i, double c, double w, int gate_vel = 0) {
     double W, M;
     int has;
     res_load_hdr(s, i, W, M, has);
     if (!has || W <= 0) return splat(0);
     double2 c1 = ld2(s, 1, i), c2 = ld2(s, 2, i), c3 = ld2(s, 3, i);
     V3 f{c2.x, c2.y, c3.x};
-    return f * (W * gate_w(c, w, c1.y));
+    double gv = gate_vel ? ld2(s, 22, i).x : c1.y;
+    return f * (W * gate_w(c, w, gv));
 }
 
-__global__ void k_shade_gated(ResStore cur, int p0, int p1, double center, double width, double* image,
-                              double* accum) {
+__global__ void k_shade_gated(ResStore cur, int p0, int p1, double center, double width, int gate_vel,
+                              double* image, double* accum) {
     for (int p = p0 + blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += gridDim.x * blockDim.x) {
-        V3 v = shade_item(cur, size_t(p), center, width);
+        V3 v = shade_item(cur, size_t(p), center, width, gate_vel);
         image[3 * size_t(p) + 0] = v.x;
         image[3 * size_t(p) + 1] = v.y;
         image[3 * size_t(p) + 2] = v.z;
@@ -1149,13 +1152,14 @@ void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const Pa
     }
 }
 
-void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
-                        double* accum, cudaStream_t s) {
+void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, int gate_vel,
+                        double* image, double* accum, cudaStream_t s) {
     size_t n = band_pixels(bd, W);
     if (!n) return;
     {
         KScope ks("k_shade_gated", s);
-        k_shade_gated<<<grid_for(n, 256), 256, 0, s>>>(cur, bd.y0 * W, bd.y1 * W, center, width, image, accum);
+        k_shade_gated<<<grid_for(n, 256), 256, 0, s>>>(cur, bd.y0 * W, bd.y1 * W, center, width, gate_vel, image,
+                                                                 accum);
     }
 }
 

@@ -73,7 +73,7 @@ struct SpatialParams {
 // run the shifts (k_shift_solve: record, prefix, suffix and the Newton solve;
 // k_shift_finish: occlusion, Jacobian, rebuild); the stage's merge kernel then
 // reads the per-job outputs.
-constexpr int kJobChunks = 13;
+constexpr int kJobChunks = 14;
 enum : uint32_t {
     JOB_REC1 = 1u,    // source record lives in store 1 (else store 0)
     JOB_SRC1 = 2u,    // source domain is frame 1 (else frame 0)
@@ -152,8 +152,8 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
                      int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, unsigned long long* q,
                      cudaStream_t s);
-void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, double* image,
-                        double* accum, cudaStream_t s);
+void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, double width, int gate_vel,
+                        double* image, double* accum, cudaStream_t s);
 void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
                             cudaStream_t s);
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,

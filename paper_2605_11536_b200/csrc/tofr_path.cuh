@@ -42,14 +42,16 @@ struct Rec {
     V3 p, pn;
     int ptri;
     V3 p2, n2;
-    int m2;
+    int m2, obj2;
     V3 wo2, suffix_f;
     double suffix_len;
+    double prefix_u, suffix_u;  // path-velocity terms (Doppler gates)
 };
 
-struct Sample {  // PathSample (transport.hpp:172-179) without pdf/u
+struct Sample {  // PathSample (transport.hpp:172-179) without pdf
     V3 f;
     double len;
+    double u;  // path velocity (transport.hpp:73-80)
     int depth;
     Rec rec;
 };
@@ -73,6 +75,9 @@ TOFR_HD void rec_clear(Rec& r) {
     r.p2 = splat(0);
     r.n2 = splat(0);
     r.m2 = -1;
+    r.obj2 = -1;
+    r.prefix_u = 0;
+    r.suffix_u = 0;
     r.wo2 = splat(0);
     r.suffix_f = splat(1);
     r.suffix_len = 0;
@@ -96,6 +101,7 @@ struct PathCfg {
     double jac_min, jac_max;
     double m_cap;
     uint64_t seed;
+    int gate_vel;  // velocity (Doppler) gate: the gated quantity is u, gate centre/width in u units
     int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
     unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
 };
@@ -155,13 +161,21 @@ struct WalkV {
     int tri, mat;
     uint32_t lane;
     int pad;
+    V3 vel;       // velocity of the vertex (velocity_at)
+    double u_in;  // path velocity of the segments camera .. this vertex
 };
 
 struct Cand {
     V3 f;
     double len, pdf;
+    double u;
     int depth;
 };
+
+// the gated quantity of a sample: path length, or path velocity (Doppler)
+__host__ __device__ __forceinline__ double gate_value(int gate_vel, double len, double u) {
+    return gate_vel ? u : len;
+}
 
 // Inputs for building a record lazily: walk history plus the optional
 // ellipsoidal insert q acting as vertex d+1.
@@ -198,6 +212,7 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
     const WalkV& pv1 = rs_vert(s, k - 1);
     r.prefix_pdf = pv1.pdf;
     r.prefix_len = pv1.len;
+    r.prefix_u = pv1.u_in;
     r.prefix_fw = pv1.fw;
     r.p1 = pv1.p;
     r.tri1 = pv1.tri;
@@ -214,10 +229,13 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
             r.skind = SK_LIGHT;
             r.p2 = F.light.pos;
             r.suffix_len = 0;
+            r.suffix_u = 0;
         } else {
             r.skind = SK_LIGHTSUB;
             r.p2 = F.lsub.pos;
             r.suffix_len = F.lsub.chain_len;
+            V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
+            r.suffix_u = dot(vs, F.lsub.wo_light);
         }
         return;
     }
@@ -227,12 +245,13 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
     r.p2 = pv2.p;
     r.n2 = pv2.n;
     r.m2 = pv2.mat;
+    r.obj2 = F.tri[pv2.tri].obj;
     V3 succ = (k + 1 == last) ? (wide ? F.light.pos : F.lsub.pos) : rs_vert(s, k + 2).p;
     r.wo2 = normalize(succ - pv2.p);
 
     V3 tail = splat(1);
-    double tail_len = 0;
-    V3 prev_p = pv2.p, prev_n = pv2.n;
+    double tail_len = 0, tail_u = 0;
+    V3 prev_p = pv2.p, prev_n = pv2.n, prev_vel = pv2.vel;
     for (int i = k + 2; i <= last; ++i) {
         const WalkV& w = rs_vert(s, i);
         V3 wdir = normalize(w.p - prev_p);
@@ -243,8 +262,10 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
             tail = tail * (wm.kind == MAT_MIRROR ? wm.albedo : eval_bsdf(wm, w.n, -wdir, out));
         }
         tail_len += norm(w.p - prev_p);
+        tail_u += dot(prev_vel - w.vel, wdir);
         prev_p = w.p;
         prev_n = w.n;
+        prev_vel = w.vel;
     }
     const WalkV& lastv = rs_vert(s, last);
     if (wide) {
@@ -256,6 +277,7 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
         if (k + 2 <= last) tail = tail * eval_bsdf(F.mats[lastv.mat], lastv.n, lastv.wi, ls.dir);
         tail = tail * (fabs(dot(lastv.n, ls.dir)) * ls.value);
         tail_len += ls.dist;
+        tail_u += dot(lastv.vel, ls.dir);
     } else {
         V3 dvec = F.lsub.pos - lastv.p;
         double dist = norm(dvec);
@@ -264,9 +286,12 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
         V3 f_s = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -wto, F.lsub.wo_light);
         tail = tail * (geom_term(lastv.p, lastv.n, F.lsub.pos, F.lsub.n) * f_s * F.lsub.power);
         tail_len += dist + F.lsub.chain_len;
+        V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
+        tail_u += dot(lastv.vel - vs, wto) + dot(vs, F.lsub.wo_light);
     }
     r.suffix_f = tail;
     r.suffix_len = tail_len;
+    r.suffix_u = tail_u;
 }
 
 // NEE completion at vertex d (Tracer::emit_nee, transport.hpp:280-328).
@@ -288,6 +313,7 @@ __device__ void emit_nee(const FrameView& F, const PathCfg& cfg, const WalkV* v,
         V3 f_at = eval_bsdf(m, x.n, x.wi, ls.dir);
         double cos_v = fabs(dot(x.n, ls.dir));
         c.f = x.fw * f_at * (cos_v) * ls.value;
+        c.u = x.u_in + dot(x.vel, ls.dir);
         c.depth = d + 1;
     } else {
         if (!F.lsub.valid) return;
@@ -302,6 +328,8 @@ __device__ void emit_nee(const FrameView& F, const PathCfg& cfg, const WalkV* v,
         V3 f_s = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -wto, F.lsub.wo_light);
         double g = geom_term(x.p, x.n, F.lsub.pos, F.lsub.n);
         c.f = x.fw * f_at * g * f_s * F.lsub.power;
+        V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
+        c.u = x.u_in + dot(x.vel - vs, wto) + dot(vs, F.lsub.wo_light);
         c.depth = d + 1;
     }
     if (c.len <= 0) return;
@@ -334,6 +362,8 @@ __device__ void trace_tree(const FrameView& F, const PathCfg& cfg, int px, int p
     v[1].pdf = 1;
     v[1].len = g.t;
     v[1].lane = 0;
+    v[1].vel = velocity_at(F, ti.obj, v[1].p);
+    v[1].u_in = dot(F.cam_vel - v[1].vel, d0);
     for (int d = 1; d + 1 <= cfg.max_depth && d < kMaxVerts - 1; ++d) {
         const GMat& m = F.mats[v[d].mat];
         if (m.kind != MAT_MIRROR) {
@@ -362,6 +392,8 @@ __device__ void trace_tree(const FrameView& F, const PathCfg& cfg, int px, int p
         double cos_w = fabs(dot(w.n, bs.wo));
         w.pdf = v[d].pdf * surv * bs.pdf * cos_w / (nh.t * nh.t);
         w.len = v[d].len + nh.t;
+        w.vel = velocity_at(F, wt.obj, w.p);
+        w.u_in = v[d].u_in + dot(v[d].vel - w.vel, bs.wo);
     }
 }
 
@@ -392,7 +424,7 @@ struct SurfPt {
 
 struct Prefix {  // BaseShiftResult (shiftmap.hpp:448-454)
     int ok;
-    double pdf, len;
+    double pdf, len, u;
     V3 fw, p1, n1, wi1;
     int tri1, m1;
 };
@@ -608,6 +640,8 @@ static __device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec,
     V3 wi = -d0;
     V3 fw = splat(1);
     double pdf = 1, len = g.t;
+    V3 vel = velocity_at(F, F.tri[tri].obj, pos);
+    double u = dot(F.cam_vel - vel, d0);
     bool rp2 = false;
     bool rp = F.mats[mat].reconnectable;
     for (int i = 1; i <= rec.k - 2; ++i) {
@@ -628,11 +662,14 @@ static __device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec,
         double cos_w = fabs(dot(nt.n, bs.wo));
         pdf = pdf * (surv * bs.pdf * cos_w / (nh.t * nh.t));
         len += nh.t;
+        V3 nvel = velocity_at(F, nt.obj, nh.pos);
+        u += dot(vel - nvel, bs.wo);
         pos = nh.pos;
         n = nt.n;
         tri = nh.tri;
         mat = nt.mat;
         wi = -bs.wo;
+        vel = nvel;
         rp2 = rp;
         rp = nm.reconnectable;
     }
@@ -642,6 +679,7 @@ static __device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec,
     out.ok = 1;
     out.pdf = pdf;
     out.len = len;
+    out.u = u;
     out.fw = fw;
     out.p1 = pos;
     out.n1 = n;
@@ -654,6 +692,8 @@ static __device__ __noinline__ Prefix base_shift(const Dom& dom, const Rec& rec,
 struct Suffix {
     V3 p2, n2;
     double len;
+    double u;  // suffix path velocity
+    V3 v2;     // velocity of the p2 endpoint
     int ok;
 };
 
@@ -885,8 +925,9 @@ struct MergeShift {
 // Merges `src` (mapped into dst's domain as `mapped`) into dst.  Returns the
 // selected input: 0 none (dst is now empty), 1 dst's own sample (kept, only W
 // and M change), 2 the mapped source sample.
+// `mapped_gv` is the mapped sample's gated quantity (length, or path velocity).
 __device__ __forceinline__ int gris_merge(Res& dst, const Res& src, const MergeShift& ms, const Sample& mapped,
-                           double dst_center, double dst_width, double m_cap, Rng& rng) {
+                           double mapped_gv, double dst_center, double dst_width, double m_cap, Rng& rng) {
     double Mc = dst.M, Ms = src.M;
     double w_sum = 0;
     int which = 0;
@@ -900,7 +941,7 @@ __device__ __forceinline__ int gris_merge(Res& dst, const Res& src, const MergeS
         merge_update(w_sum, which, 1, m_c * pc * dst.W, rng);
     }
     if (!res_empty(src) && ms.valid && ms.jac > 0) {
-        py = luminance(mapped.f) * gate_w(dst_center, dst_width, mapped.len);
+        py = luminance(mapped.f) * gate_w(dst_center, dst_width, mapped_gv);
         if (py > 0) {
             double num = Ms * src.phat / ms.jac;
             double den = Mc * py + num;

@@ -1,6 +1,6 @@
 // tofr_store.cuh -- reservoir grids in HBM.
 //
-// A reservoir is 22 x 16 B chunks (352 B).  Grids are chunk-major: chunk c of
+// A reservoir is 24 x 16 B chunks (384 B).  Grids are chunk-major: chunk c of
 // item i lives at base[c * stride + i], so when a warp touches 32 consecutive
 // items every 128-bit load/store instruction moves 512 contiguous bytes
 // (fully coalesced).  Readers that only need the header (confidence M,
@@ -11,9 +11,11 @@
 //   1: phat, len                9: wi1.x, wi1.y       17: wo2.y, wo2.z
 //   2: f.x, f.y                10: wi1.z, p.x         18: suffix_f.x, .y
 //   3: f.z, suffix_len         11: p.y, p.z           19: suffix_f.z, {m2, -}
-//   4: {has,valid,k,nl,skind,depth,-,-}, tri1, ptri
+//   4: {has,valid,k,nl,skind,depth,-,-}, tri1, ptri     19.y: {m2, obj2}
 //   5: prefix_pdf, prefix_len  12: pn.x, pn.y         20: lane_key, ctr[0..3]
 //   6: prefix_fw.x, .y         13: pn.z, p2.x         21: ctr[4..9], -
+//                                                     22: u, prefix_u
+//                                                     23: suffix_u, -
 //   7: prefix_fw.z, p1.x       14: p2.y, p2.z
 //                              15: n2.x, n2.y
 #pragma once
@@ -22,7 +24,7 @@
 
 namespace tofr_b200 {
 
-constexpr int kResChunks = 22;
+constexpr int kResChunks = 24;
 
 struct ResStore {
     double2* base;
@@ -147,7 +149,12 @@ __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y) {
         int2 mi;
         memcpy(&mi, &c.y, 8);
         q.m2 = mi.x;
+        q.obj2 = mi.y;
     }
+    c = ld2(s, 22, i);
+    y.u = c.x;
+    q.prefix_u = c.y;
+    q.suffix_u = ld2(s, 23, i).x;
     if (q.n_lanes > 0) {
         c = ld2(s, 20, i);
         memcpy(&q.lane_key, &c.x, 8);
@@ -215,9 +222,11 @@ __device__ inline void res_store(const ResStore& s, size_t i, const Res& r) {
     st2(s, 17, i, q.wo2.y, q.wo2.z);
     st2(s, 18, i, q.suffix_f.x, q.suffix_f.y);
     double m2d;
-    int2 mi = make_int2(q.m2, 0);
+    int2 mi = make_int2(q.m2, q.obj2);
     memcpy(&m2d, &mi, 8);
     st2(s, 19, i, q.suffix_f.z, m2d);
+    st2(s, 22, i, r.y.u, q.prefix_u);
+    st2(s, 23, i, q.suffix_u, 0.0);
     if (q.n_lanes > 0) {
         double a, b;
         memcpy(&a, &q.lane_key, 8);

@@ -45,6 +45,7 @@ namespace tofr_b200 {
 struct GatedSink {
     ResStore cur;
     double center, width, inv;
+    int vel;  // velocity (Doppler) gate: the gated quantity is the path velocity u
     double w_sum, phat;
     int has;
     Rng pick;
@@ -58,9 +59,9 @@ struct GatedSink {
     }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
-    __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ bool wants(double len, double u) const { return gate_w(center, width, gate_value(vel, len, u)) > 0; }
     __device__ void emit(const FrameView& F, const Cand& c, double mis, const RecSrc& rs) {
-        double p = luminance(c.f) * gate_w(center, width, c.len);
+        double p = luminance(c.f) * gate_w(center, width, gate_value(vel, c.len, c.u));
         if (p <= 0 || !(c.pdf > 0)) return;
         double w = mis * inv * p / c.pdf;
         if (!isfinite(w) || w < 0) return;
@@ -74,6 +75,7 @@ struct GatedSink {
             r.phat = p;
             r.y.f = c.f;
             r.y.len = c.len;
+            r.y.u = c.u;
             r.y.depth = c.depth;
             build_record(F, rs, r.y.rec);
             res_store(cur, item, r);
@@ -102,7 +104,7 @@ struct BinsSink {
     }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
-    __device__ bool wants(double len) const {
+    __device__ bool wants(double len, double) const {
         int b = bin_of(h, len);
         return b >= 0 && gate_w(bin_center(h, b), h.bw, len) > 0;
     }
@@ -126,6 +128,7 @@ struct BinsSink {
             r.phat = p;
             r.y.f = c.f;
             r.y.len = c.len;
+            r.y.u = c.u;
             r.y.depth = c.depth;
             build_record(F, rs, r.y.rec);
             res_store(st, i, r);
@@ -146,7 +149,7 @@ struct PlainSink2 {
     __device__ void begin(const PathCfg&, uint64_t, uint64_t, size_t p, int) { base = p * size_t(h.bins); }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
-    __device__ bool wants(double len) const { return bin_of(h, len) >= 0; }
+    __device__ bool wants(double len, double) const { return bin_of(h, len) >= 0; }
     __device__ void emit(const FrameView&, const Cand& c, double mis, const RecSrc&) {
         if (!(c.pdf > 0)) return;
         V3 val = c.f * (mis / c.pdf / m_init);
@@ -182,7 +185,7 @@ struct RefSink2 {
         sum = sum + est;
         sum2 = sum2 + est * est;
     }
-    __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ bool wants(double len, double) const { return gate_w(center, width, len) > 0; }
     __device__ void emit(const FrameView&, const Cand& c, double mis, const RecSrc&) {
         double w = gate_w(center, width, c.len);
         if (w > 0 && c.pdf > 0) est = est + c.f * (mis * w / c.pdf);
@@ -206,7 +209,7 @@ struct RefSink2 {
 
 enum : int { ST_IDLE = 0, ST_NEE = 1, ST_EXT = 2, ST_SHADOW = 3, ST_EXTEND = 4 };
 
-template <class Sink>
+template <class Sink, bool VEL>
 __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
     k_trace(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, int trees, uint64_t frame_key, Sink proto,
             unsigned long long* q) {
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
     WalkV x;  // current vertex (= v[d])
     Cand c;   // NEE candidate waiting for its shadow ray
     c.pdf = 0;
+    c.u = 0;
     V3 rd{0, 0, 1};
     double rtmax = 0, bs_pdf = 0, surv = 1;
     uint32_t n_closest = 0, n_any = 0;
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     LightSample ls;
                     if (!light_sample(Fs.light, x.p, ls)) continue;
                     c.len = x.len + ls.dist;
-                    if (!sk.wants(c.len)) continue;
+                    if (VEL) c.u = x.u_in + dot(x.vel, ls.dir);
+                    if (!sk.wants(c.len, c.u)) continue;
                     V3 f_at = eval_bsdf(mx, x.n, x.wi, ls.dir);
                     double cos_v = fabs(dot(x.n, ls.dir));
                     c.f = x.fw * f_at * (cos_v) * ls.value;
@@ -304,7 +309,11 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     if (dist <= eps * 2) continue;
                     V3 wto = dvec / dist;
                     c.len = x.len + dist + Fs.lsub.chain_len;
-                    if (!sk.wants(c.len)) continue;
+                    if (VEL) {
+                        V3 vs = velocity_at(Fs, Fs.lsub.obj, Fs.lsub.pos);
+                        c.u = x.u_in + dot(x.vel - vs, wto) + dot(vs, Fs.lsub.wo_light);
+                    }
+                    if (!sk.wants(c.len, c.u)) continue;
                     V3 f_at = eval_bsdf(mx, x.n, x.wi, wto);
                     V3 f_s = eval_bsdf(Fs.mats[Fs.lsub.mat], Fs.lsub.n, -wto, Fs.lsub.wo_light);
                     double gg = geom_term(x.p, x.n, Fs.lsub.pos, Fs.lsub.n);
@@ -351,6 +360,8 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     x.pdf = 1;
                     x.len = g.t;
                     x.lane = 0;
+                    x.vel = VEL ? velocity_at(Fs, ti.obj, x.p) : splat(0);
+                    x.u_in = VEL ? dot(Fs.cam_vel - x.vel, d0) : 0.0;
                     v[1] = x;
                     d = 1;
                     state = ST_NEE;
@@ -416,6 +427,8 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                 double cos_w = fabs(dot(w.n, rd));
                 w.pdf = x.pdf * surv * bs_pdf * cos_w / (th.t * th.t);
                 w.len = x.len + th.t;
+                w.vel = VEL ? velocity_at(Fs, wt.obj, w.p) : splat(0);
+                w.u_in = VEL ? x.u_in + dot(x.vel - w.vel, rd) : 0.0;
                 ++d;
                 v[d] = w;
                 x = w;
@@ -441,17 +454,17 @@ __global__ void k_ris_finalize(ResStore st, size_t i0, size_t i1) {
 // ---------------------------------------------------------------------------
 // launchers
 
-template <class Sink>
+template <class Sink, bool VEL = false>
 static void launch_trace(const char* kname, const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
                          int trees, uint64_t frame_key, const Sink& sk, unsigned long long* q, cudaStream_t s) {
     size_t n = size_t(bd.y1 - bd.y0) * F.cam.w;
     if (!n) return;
     size_t sm = frame_smem_bytes(F);
     cudaMemsetAsync(q, 0, sizeof(unsigned long long), s);
-    const void* kf = reinterpret_cast<const void*>(k_trace<Sink>);
+    const void* kf = reinterpret_cast<const void*>(k_trace<Sink, VEL>);
     {
         KScope ks(kname, s);
-        k_trace<Sink><<<persistent_grid(kf, 128, sm, n), 128, sm, s>>>(F, bd, g, cfg, trees, frame_key, sk, q);
+        k_trace<Sink, VEL><<<persistent_grid(kf, 128, sm, n), 128, sm, s>>>(F, bd, g, cfg, trees, frame_key, sk, q);
     }
 }
 
@@ -463,7 +476,11 @@ void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const
     sk.center = center;
     sk.width = width;
     sk.inv = 1.0 / m_init;
-    launch_trace("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+    sk.vel = cfg.gate_vel;
+    if (cfg.gate_vel)
+        launch_trace<GatedSink, true>("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+    else
+        launch_trace<GatedSink, false>("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
 }
 
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,

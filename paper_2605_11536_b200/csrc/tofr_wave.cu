@@ -202,6 +202,7 @@ __device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const Res
     pre.wi1 = V3{c9.x, c9.y, c10.x};
     pre.tri1 = tri1;
     pre.m1 = F.tri[tri1].mat;
+    pre.u = ld2(s, 22, i).y;
     return pre;
 }
 
@@ -220,6 +221,7 @@ __device__ __forceinline__ Prefix gbuffer_prefix(const FrameView& F, const GHit*
     out.len = g.t;
     out.fw = splat(1);
     out.p1 = F.cam.pos + d0 * g.t;
+    out.u = dot(F.cam_vel - velocity_at(F, F.tri[g.tri].obj, out.p1), d0);
     out.n1 = F.tri[g.tri].n;
     out.wi1 = -d0;
     out.tri1 = g.tri;
@@ -255,6 +257,7 @@ __device__ __forceinline__ void replay_put(const ShiftQueue& q, uint32_t k, cons
     int2 to = make_int2(p.ok ? p.tri1 : -1, p.ok);
     memcpy(&c12.y, &to, 8);
     jst(q, 12, k, c12);
+    jst(q, 13, k, make_double2(p.u, 0.0));
 }
 __device__ __forceinline__ Prefix replay_get(const FrameView& F, const ShiftQueue& q, uint32_t k) {
     Prefix p;
@@ -272,6 +275,7 @@ __device__ __forceinline__ Prefix replay_get(const FrameView& F, const ShiftQueu
     p.tri1 = to.x;
     p.n1 = F.tri[p.tri1].n;  // hybrid_base_shift: n = the hit triangle's normal
     p.m1 = F.tri[p.tri1].mat;
+    p.u = jld(q, 13, k).x;
     return p;
 }
 
@@ -293,16 +297,25 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
         s.p2 = rec_p2(st, item);
         s.n2 = rec_n2(st, item);
         s.len = ld2(st, 3, item).y;
+        s.u = ld2(st, 23, item).x;
+        int2 mo;
+        double m19 = ld2(st, 19, item).y;
+        memcpy(&mo, &m19, 8);
+        s.v2 = velocity_at(F, mo.y, s.p2);  // obj2
         s.ok = 1;
     } else if (skind == SK_LIGHT) {
         s.p2 = F.light.pos;
         s.len = 0;
+        s.u = 0;
+        s.v2 = splat(0);
         s.ok = 1;
     } else {
         if (!F.lsub.valid) return s;
         s.p2 = F.lsub.pos;
         s.n2 = F.lsub.n;
         s.len = F.lsub.chain_len;
+        s.v2 = velocity_at(F, F.lsub.obj, F.lsub.pos);
+        s.u = dot(s.v2, F.lsub.wo_light);
         s.ok = 1;
     }
     return s;
@@ -435,6 +448,71 @@ __device__ __forceinline__ LcEval lc_eval(const V3& p1, const V3& p2, const V3& 
     return r;
 }
 
+// Velocity (Doppler) constraint field, LocalConstraint in velocity mode
+// (shiftmap.hpp:28-122): u(p) = (v1 - v(p)).r1 + (v(p) - v2).r2 with v the rigid
+// velocity field of the object p sits on (bound per evaluation point).
+struct VelField {
+    V3 v1, v2;
+};
+
+__device__ __forceinline__ V3 transpose_mul(const M3& A, const V3& v) {
+    return V3{A.m[0][0] * v.x + A.m[1][0] * v.y + A.m[2][0] * v.z,
+              A.m[0][1] * v.x + A.m[1][1] * v.y + A.m[2][1] * v.z,
+              A.m[0][2] * v.x + A.m[1][2] * v.y + A.m[2][2] * v.z};
+}
+
+// detail::vel_term_grad / vel_term_hess (shiftmap.hpp:52-76)
+__device__ __forceinline__ V3 vel_term_grad(const V3& p, const V3& a, const V3& cvec, double s_r, double alpha,
+                                            const M3& V, bool moving) {
+    V3 e = p - a;
+    double l = norm(e);
+    V3 n = e / l;
+    M3 P = m3_identity() - m3_outer(n, n);
+    V3 g = (P * cvec) * (s_r / l);
+    if (moving) g = g + transpose_mul(V, n) * (alpha * s_r);
+    return g;
+}
+__device__ __forceinline__ M3 vel_term_hess(const V3& p, const V3& a, const V3& cvec, double s_r, double alpha,
+                                            const M3& V, bool moving) {
+    V3 e = p - a;
+    double l = norm(e);
+    V3 n = e / l;
+    M3 P = m3_identity() - m3_outer(n, n);
+    V3 Pc = P * cvec;
+    M3 h = (P * (-dot(n, cvec)) - m3_outer(n, Pc) - m3_outer(Pc, n)) * (s_r / (l * l));
+    if (moving) {
+        M3 PV = P * V;
+        h = h + (PV + transpose(PV)) * (alpha * s_r / l);
+    }
+    return h;
+}
+
+// value, world gradient and projected Hessian of the velocity field at p,
+// bound to object `obj`'s velocity field
+__device__ __noinline__ LcEval vel_eval(const FrameView* Fp, int obj, VelField vf, V3 p1, V3 p2, V3 p, Frame2 J,
+                                        bool with_hess) {
+    const FrameView& F = *Fp;
+    bool moving = obj >= 0 && obj < F.n_obj && F.vel[obj].moving;
+    M3 A = moving ? F.vel[obj].A : m3_zero();
+    V3 c = moving ? F.vel[obj].c : splat(0);
+    V3 v = moving ? A * p + c : splat(0);
+    LcEval r;
+    r.val = dot(vf.v1 - v, normalize(p - p1)) + dot(v - vf.v2, normalize(p2 - p));
+    r.grad = vel_term_grad(p, p1, vf.v1 - v, +1, -1, A, moving) + vel_term_grad(p, p2, v - vf.v2, -1, +1, A, moving);
+    r.hess = M2{0, 0, 0, 0};
+    if (with_hess)
+        r.hess = project_sym(J, vel_term_hess(p, p1, vf.v1 - v, +1, -1, A, moving) +
+                                    vel_term_hess(p, p2, v - vf.v2, -1, +1, A, moving));
+    return r;
+}
+
+template <bool VEL>
+__device__ __forceinline__ LcEval field_eval(const FrameView& F, int obj, const VelField& vf, const V3& p1,
+                                             const V3& p2, const V3& p, const Frame2& J, bool with_hess) {
+    if (VEL) return vel_eval(&F, obj, vf, p1, p2, p, J, with_hess);
+    return lc_eval(p1, p2, p, J, with_hess);
+}
+
 struct StartTerms {
     V3 g3s;     // gradient at the start point
     V2 gs;      // ... in the start frame
@@ -442,10 +520,11 @@ struct StartTerms {
     M2 Hs;      // projected Hessian at the start point (gauge != FIXED)
 };
 
-__device__ __forceinline__ StartTerms start_terms(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
-                                                  int gauge) {
+template <bool VEL>
+__device__ __forceinline__ StartTerms start_terms(const FrameView& F, int obj, const VelField& vf, const V3& p1,
+                                                  const V3& p2, const V3& ps, const Frame2& Js, int gauge) {
     StartTerms t;
-    LcEval e = lc_eval(p1, p2, ps, Js, gauge != GAUGE_FIXED);
+    LcEval e = field_eval<VEL>(F, obj, vf, p1, p2, ps, Js, gauge != GAUGE_FIXED);
     t.g3s = e.grad;
     t.gs = to_local(Js, e.grad);
     t.lvs = e.val;
@@ -460,11 +539,12 @@ struct TrialEval {
     double ngrad;    // |grad_cur|
 };
 
-__device__ __forceinline__ TrialEval trial_eval(const V3& p1, const V3& p2, const V3& ps, const Frame2& Js,
-                                                const StartTerms& st, const V3& pc, const Frame2& Jc, double delta,
-                                                int gauge) {
+template <bool VEL>
+__device__ __forceinline__ TrialEval trial_eval(const FrameView& F, int obj, const VelField& vf, const V3& p1,
+                                                const V3& p2, const V3& ps, const Frame2& Js, const StartTerms& st,
+                                                const V3& pc, const Frame2& Jc, double delta, int gauge) {
     TrialEval r;
-    LcEval e = lc_eval(p1, p2, pc, Jc, gauge != GAUGE_FIXED);
+    LcEval e = field_eval<VEL>(F, obj, vf, p1, p2, pc, Jc, gauge != GAUGE_FIXED);
     V2 gc = to_local(Jc, e.grad);
     r.ngrad = norm(gc);
     V3 disp = pc - ps;
@@ -532,6 +612,7 @@ __global__ void __launch_bounds__(128)
 // ---------------------------------------------------------------------------
 // solve: checks, prefix, suffix, Newton (newton_solve, shiftmap.hpp:314-378)
 
+template <bool VEL>
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     k_shift_solve(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                   ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
@@ -559,6 +640,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     bool cn_rec = true;  // current point's normal = the record's pn
     Frame2 Js{{1, 0, 0}, {0, 1, 0}}, Jc{{1, 0, 0}, {0, 1, 0}};
     StartTerms stt;
+    VelField vf{{0, 0, 0}, {0, 0, 0}};  // velocity gates only
     double delta = 0, tol = 0, fnorm = 0, scale = 1;
     V2 step{0, 0};
     int iter = 0, bt = 0;
@@ -614,14 +696,18 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                         } else {
                             p1 = pre.p1;
                             p2 = suf.p2;
-                            double src_len = ld2(st, 1, jb.item).y;
+                            // full-path constraint, local two-segment target (length or velocity)
+                            double src_total = VEL ? ld2(st, 22, jb.item).x : ld2(st, 1, jb.item).y;
+                            double prefix_part = VEL ? pre.u : pre.len;
+                            double suffix_part = VEL ? suf.u : suf.len;
                             double gate_delta = jb.dc - jb.sc;
-                            double target_local = src_len + gate_delta - pre.len - suf.len;
-                            delta = target_local - lc_value(p1, p2, spos);
+                            double target_local = src_total + gate_delta - prefix_part - suffix_part;
+                            if (VEL) vf = VelField{velocity_at(F, F.tri[pre.tri1].obj, pre.p1), suf.v2};
                             tol = 0.01 * jb.dw;
                             if (count) SCTR(SC_SOLVES, 1);
                             Js = tangent_frame(F, stri);
-                            stt = start_terms(p1, p2, spos, Js, cfg.gauge);
+                            stt = start_terms<VEL>(F, F.tri[stri].obj, vf, p1, p2, spos, Js, cfg.gauge);
+                            delta = target_local - stt.lvs;  // field value at the start point
                             // trial 0 evaluates the start point itself
                             cpos = spos;
                             ctri = stri;
@@ -673,7 +759,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         // for trial 0): recompute only after a re-projection ray changed it
         Frame2 Jt = init ? Js : Jc;
         if (!init && ttri != ctri) Jt = tangent_frame(F, ttri);
-        TrialEval et = trial_eval(p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
+        TrialEval et = trial_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
         double fn = hypot(et.F.x, et.F.y);
         bool accept = have && (init || fn < fnorm);
         bool fin = false, conv = false;
@@ -743,6 +829,7 @@ __device__ __forceinline__ bool occluded_n(const FrameView& F, const V3& a, cons
 
 __device__ __forceinline__ void out_fail(const ShiftQueue& q, uint32_t k) { st2(q.out, 0, k, 0.0, 0.0); }
 
+template <bool VEL>
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     k_shift_finish(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                    ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
@@ -814,9 +901,15 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         bool ok = !(l1 <= 2 * F.eps_ray) && !(l2 <= 2 * F.eps_ray);
         V3 f = splat(0);
         int m2 = -1;
+        double u_total = 0;
         if (ok) {
             V3 u1 = d1 / l1;
             V3 u2 = d2 / l2;
+            V3 pvel = splat(0);
+            if (VEL) {
+                pvel = velocity_at(F, F.tri[ptri].obj, ppos);
+                u_total = pre.u + dot(velocity_at(F, F.tri[pre.tri1].obj, pre.p1) - pvel, u1);
+            }
             const GMat& m1 = F.mats[pre.m1];
             f = pre.fw * eval_bsdf(m1, pre.n1, pre.wi1, u1) * geom_term(pre.p1, pre.n1, ppos, pnrm);
             const GMat& mp = F.mats[F.tri[ptri].mat];
@@ -838,6 +931,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 V3 fs = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -u2, F.lsub.wo_light);
                 f = f * (geom_term(ppos, pnrm, F.lsub.pos, F.lsub.n) * fs * F.lsub.power);
             }
+            if (VEL) u_total += dot(pvel - suf.v2, u2) + suf.u;
             ok = finite3(f);
         }
         if (!ok) {
@@ -846,9 +940,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             continue;
         }
         double len = pre.len + l1 + l2 + suf.len;
-        if (count && gate_w(jb.dc, jb.dw, len) > 0 && luminance(f) > 0) ctr.v[SC_SUCCESS]++;
+        double gv = gate_value(VEL, len, u_total);
+        if (count && gate_w(jb.dc, jb.dw, gv) > 0 && luminance(f) > 0) ctr.v[SC_SUCCESS]++;
         if (!(jb.meta & JOB_FULL)) {  // inverse shift: p-hat of the source gate times |J|
-            st2(q.out, 0, k, luminance(f) * gate_w(jb.dc, jb.dw, len) * jac, 1.0);
+            st2(q.out, 0, k, luminance(f) * gate_w(jb.dc, jb.dw, gv) * jac, 1.0);
             continue;
         }
         // mapped record (rebuild_sample's record update, stored as res_store would)
@@ -886,8 +981,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         }
         __stcg(&o.base[15 * o.stride + k], c15);
         __stcg(&o.base[16 * o.stride + k], c16);
-        for (int c = 17; c < (mt.nl > 0 ? kResChunks : 20); ++c)
+        for (int c = 17; c < (mt.nl > 0 ? 22 : 20); ++c)
             __stcg(&o.base[size_t(c) * o.stride + k], ld2(st, c, jb.item));
+        st2(o, 22, k, u_total, pre.u);
+        st2(o, 23, k, mt.skind == SK_LIGHTSUB ? suf.u : ld2(st, 23, jb.item).x, 0.0);
     }
     work_add(cfg.work, WK_ANY, n_any);
     ctr_flush(ctr, ctr_out);
@@ -895,6 +992,16 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 
 // ---------------------------------------------------------------------------
 // merge-side helpers
+
+// chunks [from, 24) of record i -> record j, without the replay lanes (20-21)
+// unless the record has lanes
+__device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const ResStore& dst, size_t j, int from,
+                                            int n_lanes) {
+    for (int c = from; c < kResChunks; ++c) {
+        if ((c == 20 || c == 21) && n_lanes <= 0) continue;
+        __stcg(&dst.base[size_t(c) * dst.stride + j], ld2(src, c, i));
+    }
+}
 
 // Selected mapped record (job k) -> reservoir `it` with the merge's W, M, p-hat.
 __device__ __forceinline__ void put_mapped(const ResStore& o, uint32_t k, const ResStore& dst, size_t it, double W,
@@ -904,8 +1011,7 @@ __device__ __forceinline__ void put_mapped(const ResStore& o, uint32_t k, const 
     double2 c4 = ld2(o, 4, k);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    int nc = mt.nl > 0 ? kResChunks : 20;
-    for (int c = 2; c < nc; ++c) __stcg(&dst.base[size_t(c) * dst.stride + it], ld2(o, c, k));
+    copy_chunks(o, k, dst, it, 2, mt.nl);
 }
 
 // Reservoir copy src[it] -> dst[it] with a new W, M (sample and p-hat kept).
@@ -914,8 +1020,7 @@ __device__ __forceinline__ void copy_res(const ResStore& src, const ResStore& ds
     double2 c4 = ld2(src, 4, it);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    int nc = mt.nl > 0 ? kResChunks : 20;
-    for (int c = 1; c < nc; ++c) __stcg(&dst.base[size_t(c) * dst.stride + it], ld2(src, c, it));
+    copy_chunks(src, it, dst, it, 1, mt.nl);
 }
 
 // header (W, M, has, p-hat) of a reservoir
@@ -924,15 +1029,17 @@ __device__ __forceinline__ void res_head_phat(const ResStore& s, size_t i, Res& 
     if (r.has) r.phat = ld2(s, 1, i).x;
 }
 
-// forward-shift output of job k: ok, Jacobian, mapped f and length
-__device__ __forceinline__ void fwd_output(const ShiftQueue& q, uint32_t k, MergeShift& ms, Sample& mapped) {
+// forward-shift output of job k: ok, Jacobian, mapped f and gate value
+// (length, or path velocity for Doppler gates)
+__device__ __forceinline__ void fwd_output(const ShiftQueue& q, uint32_t k, int gate_vel, MergeShift& ms,
+                                           Sample& mapped, double& gv) {
     if (k == kNoJob) return;
     double2 o0 = ld2(q.out, 0, k);
     if (!(o0.y > 0)) return;
     ms.valid = 1;
     ms.jac = o0.x;
-    double2 o1 = ld2(q.out, 1, k), o2 = ld2(q.out, 2, k), o3 = ld2(q.out, 3, k);
-    mapped.len = o1.y;
+    double2 o2 = ld2(q.out, 2, k), o3 = ld2(q.out, 3, k);
+    gv = gate_vel ? ld2(q.out, 22, k).x : ld2(q.out, 1, k).y;
     mapped.f = V3{o2.x, o2.y, o3.x};
 }
 
@@ -1025,12 +1132,13 @@ __global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int f
         gate_of(cg, b, dc, dw);
         MergeShift ms{0, 1.0, 0.0};
         Sample mapped;
+        double mgv = 0;
         uint32_t kf = src.has ? ws.map_a[i] : kNoJob;
-        fwd_output(ws.q, kf, ms, mapped);
+        fwd_output(ws.q, kf, cfg.gate_vel, ms, mapped, mgv);
         ms.phat_src_of_dst = inv_output(ws.q, dst.has ? ws.map_b[i] : kNoJob);
         uint64_t pix = uint64_t(py) * W + px;
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
-        int which = gris_merge(dst, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        int which = gris_merge(dst, src, ms, mapped, mgv, dc, dw, cfg.m_cap, rng);
         if (which == 2)
             put_mapped(ws.q.out, kf, cur, it, dst.W, dst.M, dst.phat);
         else  // in place: the kept sample and its p-hat are already stored
@@ -1142,12 +1250,13 @@ __global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate
         gate_of(gate, b, dc, dw);
         MergeShift ms{0, 1.0, 0.0};
         Sample mapped;
+        double mgv = 0;
         uint32_t kf = src.has ? ws.map_a[size_t(j) * n + i] : kNoJob;
-        fwd_output(ws.q, kf, ms, mapped);
+        fwd_output(ws.q, kf, cfg.gate_vel, ms, mapped, mgv);
         ms.phat_src_of_dst = inv_output(ws.q, out.has ? ws.map_b[i] : kNoJob);
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(pass * 131 + b), 10);
         if (j > 0) rng.ctr = ws.rng_ctr[i];
-        int which = gris_merge(out, src, ms, mapped, dc, dw, cfg.m_cap, rng);
+        int which = gris_merge(out, src, ms, mapped, mgv, dc, dw, cfg.m_cap, rng);
         if (which == 2)
             put_mapped(ws.q.out, kf, dst_grid, it, out.W, out.M, out.phat);
         else if (which == 1 && j == 0)
@@ -1199,16 +1308,19 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
                              s>>>(F0, F1, g0, g1, st0, st1, q, cfg, wq);
         }
     }
+    // length-gate and velocity-gate (Doppler) instantiations
+    auto solve = cfg.gate_vel ? k_shift_solve<true> : k_shift_solve<false>;
+    auto finish = cfg.gate_vel ? k_shift_finish<true> : k_shift_finish<false>;
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_solve", s);
-        k_shift_solve<<<persistent_grid(reinterpret_cast<const void*>(k_shift_solve), 128, sm, cap_jobs), 128, sm, s>>>(
+        solve<<<persistent_grid(reinterpret_cast<const void*>(solve), 128, sm, cap_jobs), 128, sm, s>>>(
             F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
     }
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_finish", s);
-        k_shift_finish<<<persistent_grid(reinterpret_cast<const void*>(k_shift_finish), 128, sm, cap_jobs), 128, sm, s>>>(
+        finish<<<persistent_grid(reinterpret_cast<const void*>(finish), 128, sm, cap_jobs), 128, sm, s>>>(
             F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
     }
 }

@@ -92,6 +92,26 @@ CASES = {
                                                spatial_neighbors=2, spatial_radius=3, seed=7), "transient"),
 }
 
+# Doppler (velocity) gates: render_doppler, pipeline.hpp:573-578 -- the gated
+# pipeline on the path velocity u (receding big box ~ -0.1, approaching small
+# box > 0, static geometry 0 in boxes_doppler, f0 = 1 Hz so shift = u)
+def vgate(c, w, f0=1.0):
+    return GateSpec(F.GATE_VELOCITY, c, w, f0)
+
+
+CASES.update({
+    "doppler_receding": (lambda: scenes.bundled("boxes_doppler", 48),
+                         RenderConfig(gate=vgate(-0.09, 0.04), m_init=2, temporal=True, spatial_passes=1,
+                                      spatial_neighbors=3, spatial_radius=8, frames=3, frame0=2), "doppler"),
+    "doppler_approaching": (lambda: scenes.bundled("boxes_doppler", 48),
+                            RenderConfig(gate=vgate(0.06, 0.06), m_init=2, temporal=True, spatial_passes=1,
+                                         spatial_neighbors=3, spatial_radius=8, frames=3, frame0=5), "doppler"),
+    "doppler_wide_f0": (lambda: scenes.bundled("boxes_doppler", 40),
+                        RenderConfig(gate=vgate(-0.1, 0.4, 2.0), m_init=2, temporal=True, spatial_passes=2,
+                                     spatial_neighbors=3, spatial_radius=6, frames=3, gate_step=0.01, frame0=1),
+                        "doppler"),
+})
+
 REFERENCE_CASES = {
     "ref_cornell_wide": (lambda: scenes.bundled("cornell_wide", 32), 0.0, gate(6.0, 0.5), 16, 3, 6),
     "ref_cornell": (lambda: scenes.bundled("cornell", 32), 0.0, gate(10.0, 0.5), 16, 5, 6),

@@ -28,6 +28,9 @@ def _run(renderer, ref, name):
     if kind == "gated":
         g = renderer.render_gated(sd, cfg)
         r = ref.render_gated(rs, cfg)
+    elif kind == "doppler":  # the reference's render_doppler is render_gated with the velocity gate
+        g = renderer.render_doppler(sd, cfg)
+        r = ref.render_gated(rs, cfg)
     elif kind == "plain":
         g = renderer.render_transient_plain(sd, cfg)
         r = ref.render_transient_plain(rs, cfg)
@@ -60,7 +63,7 @@ def test_plain_deposit_counts_exact(renderer, ref, name):
 
 
 @pytest.mark.parametrize("name", ["c1_cornell", "wide_reuse", "doppler_scene_reuse", "mirror_replay",
-                                  "transient_full"])
+                                  "transient_full", "doppler_receding", "doppler_wide_f0"])
 def test_shift_counters(renderer, ref, name):
     """ShiftCounts per stage and frame (integer) equal the oracle's."""
     g, r = _run(renderer, ref, name)
