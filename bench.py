@@ -57,6 +57,11 @@ WORKLOADS = {
            RenderConfig(gate=_gate(12.0, 0.041), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
                         spatial_radius=10, m_cap=20, max_depth=6, seed=1),
            "C3: boxes_doppler 1920x1080 gated tau=12.0 dtau=0.041, m_init 1, temporal + 1x3 spatial r10"),
+    "c3d": ("boxes_doppler", 1920, 1080,
+            RenderConfig(gate=GateSpec(F.GATE_VELOCITY, -0.09, 0.04, 1.0), m_init=1, temporal=True, spatial_passes=1,
+                         spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+            "C3 Doppler: boxes_doppler 1920x1080 velocity gate -0.09 +- 0.02 Hz (f0 1 Hz: receding box), m_init 1, "
+            "temporal + 1x3 spatial r10 (render_doppler)"),
     "c3w": ("cornell_wide", 1920, 1080,
             RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
                          spatial_radius=10, m_cap=20, max_depth=6, seed=1),

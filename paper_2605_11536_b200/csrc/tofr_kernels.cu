@@ -111,7 +111,7 @@ struct RisSink {
             win->f = c.f;
             win->len = c.len;
             win->depth = c.depth;
-            build_record(*F, rs, win->rec);
+            build_record<false>(*F, rs, win->rec);
             has = 1;
             phat = p;
         }
@@ -260,7 +260,7 @@ struct BinSink {
             r.y.f = c.f;
             r.y.len = c.len;
             r.y.depth = c.depth;
-            build_record(*F, rs, r.y.rec);
+            build_record<false>(*F, rs, r.y.rec);
             res_store(st, i, r);
         }
     }

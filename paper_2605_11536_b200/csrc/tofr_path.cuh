@@ -161,6 +161,11 @@ struct WalkV {
     int tri, mat;
     uint32_t lane;
     int pad;
+};
+
+// Velocity history of a walk (Doppler gates only; kept apart from WalkV so the
+// length-gate kernels do not carry it)
+struct WalkVel {
     V3 vel;       // velocity of the vertex (velocity_at)
     double u_in;  // path velocity of the segments camera .. this vertex
 };
@@ -184,13 +189,21 @@ struct RecSrc {
     int d;
     const WalkV* q;
     uint64_t lane_key;
+    const WalkVel* wv;  // velocity history (null: no velocity terms)
 };
+
+__device__ inline WalkVel rs_vel(const RecSrc& s, int i) {
+    if (!s.wv || (s.q && i == s.d + 1)) return WalkVel{splat(0), 0.0};
+    return s.wv[i];
+}
 
 __device__ inline const WalkV& rs_vert(const RecSrc& s, int i) {
     return (s.q && i == s.d + 1) ? *s.q : s.v[i];
 }
 
-// build_record (transport.hpp:448-582), Length subset
+// build_record (transport.hpp:448-582); VEL adds the path-velocity terms
+// (prefix_u, suffix_u, obj2) of Doppler gates
+template <bool VEL>
 static __device__ __noinline__ void build_record(const FrameView& F, const RecSrc& s, Rec& r) {
     rec_clear(r);
     int last = s.q ? s.d + 1 : s.d;
@@ -212,7 +225,7 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
     const WalkV& pv1 = rs_vert(s, k - 1);
     r.prefix_pdf = pv1.pdf;
     r.prefix_len = pv1.len;
-    r.prefix_u = pv1.u_in;
+    if (VEL) r.prefix_u = rs_vel(s, k - 1).u_in;
     r.prefix_fw = pv1.fw;
     r.p1 = pv1.p;
     r.tri1 = pv1.tri;
@@ -234,8 +247,7 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
             r.skind = SK_LIGHTSUB;
             r.p2 = F.lsub.pos;
             r.suffix_len = F.lsub.chain_len;
-            V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
-            r.suffix_u = dot(vs, F.lsub.wo_light);
+            if (VEL) r.suffix_u = dot(velocity_at(F, F.lsub.obj, F.lsub.pos), F.lsub.wo_light);
         }
         return;
     }
@@ -245,13 +257,13 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
     r.p2 = pv2.p;
     r.n2 = pv2.n;
     r.m2 = pv2.mat;
-    r.obj2 = F.tri[pv2.tri].obj;
+    if (VEL) r.obj2 = F.tri[pv2.tri].obj;
     V3 succ = (k + 1 == last) ? (wide ? F.light.pos : F.lsub.pos) : rs_vert(s, k + 2).p;
     r.wo2 = normalize(succ - pv2.p);
 
     V3 tail = splat(1);
     double tail_len = 0, tail_u = 0;
-    V3 prev_p = pv2.p, prev_n = pv2.n, prev_vel = pv2.vel;
+    V3 prev_p = pv2.p, prev_n = pv2.n, prev_vel = VEL ? rs_vel(s, k + 1).vel : splat(0);
     for (int i = k + 2; i <= last; ++i) {
         const WalkV& w = rs_vert(s, i);
         V3 wdir = normalize(w.p - prev_p);
@@ -262,10 +274,13 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
             tail = tail * (wm.kind == MAT_MIRROR ? wm.albedo : eval_bsdf(wm, w.n, -wdir, out));
         }
         tail_len += norm(w.p - prev_p);
-        tail_u += dot(prev_vel - w.vel, wdir);
+        if (VEL) {
+            V3 wvel = rs_vel(s, i).vel;
+            tail_u += dot(prev_vel - wvel, wdir);
+            prev_vel = wvel;
+        }
         prev_p = w.p;
         prev_n = w.n;
-        prev_vel = w.vel;
     }
     const WalkV& lastv = rs_vert(s, last);
     if (wide) {
@@ -277,7 +292,7 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
         if (k + 2 <= last) tail = tail * eval_bsdf(F.mats[lastv.mat], lastv.n, lastv.wi, ls.dir);
         tail = tail * (fabs(dot(lastv.n, ls.dir)) * ls.value);
         tail_len += ls.dist;
-        tail_u += dot(lastv.vel, ls.dir);
+        if (VEL) tail_u += dot(rs_vel(s, last).vel, ls.dir);
     } else {
         V3 dvec = F.lsub.pos - lastv.p;
         double dist = norm(dvec);
@@ -286,8 +301,10 @@ static __device__ __noinline__ void build_record(const FrameView& F, const RecSr
         V3 f_s = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -wto, F.lsub.wo_light);
         tail = tail * (geom_term(lastv.p, lastv.n, F.lsub.pos, F.lsub.n) * f_s * F.lsub.power);
         tail_len += dist + F.lsub.chain_len;
-        V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
-        tail_u += dot(lastv.vel - vs, wto) + dot(vs, F.lsub.wo_light);
+        if (VEL) {
+            V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
+            tail_u += dot(rs_vel(s, last).vel - vs, wto) + dot(vs, F.lsub.wo_light);
+        }
     }
     r.suffix_f = tail;
     r.suffix_len = tail_len;
@@ -313,7 +330,7 @@ __device__ void emit_nee(const FrameView& F, const PathCfg& cfg, const WalkV* v,
         V3 f_at = eval_bsdf(m, x.n, x.wi, ls.dir);
         double cos_v = fabs(dot(x.n, ls.dir));
         c.f = x.fw * f_at * (cos_v) * ls.value;
-        c.u = x.u_in + dot(x.vel, ls.dir);
+        c.u = 0;  // legacy per-item trace: length gates only
         c.depth = d + 1;
     } else {
         if (!F.lsub.valid) return;
@@ -328,8 +345,7 @@ __device__ void emit_nee(const FrameView& F, const PathCfg& cfg, const WalkV* v,
         V3 f_s = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -wto, F.lsub.wo_light);
         double g = geom_term(x.p, x.n, F.lsub.pos, F.lsub.n);
         c.f = x.fw * f_at * g * f_s * F.lsub.power;
-        V3 vs = velocity_at(F, F.lsub.obj, F.lsub.pos);
-        c.u = x.u_in + dot(x.vel - vs, wto) + dot(vs, F.lsub.wo_light);
+        c.u = 0;
         c.depth = d + 1;
     }
     if (c.len <= 0) return;
@@ -362,8 +378,6 @@ __device__ void trace_tree(const FrameView& F, const PathCfg& cfg, int px, int p
     v[1].pdf = 1;
     v[1].len = g.t;
     v[1].lane = 0;
-    v[1].vel = velocity_at(F, ti.obj, v[1].p);
-    v[1].u_in = dot(F.cam_vel - v[1].vel, d0);
     for (int d = 1; d + 1 <= cfg.max_depth && d < kMaxVerts - 1; ++d) {
         const GMat& m = F.mats[v[d].mat];
         if (m.kind != MAT_MIRROR) {
@@ -392,8 +406,6 @@ __device__ void trace_tree(const FrameView& F, const PathCfg& cfg, int px, int p
         double cos_w = fabs(dot(w.n, bs.wo));
         w.pdf = v[d].pdf * surv * bs.pdf * cos_w / (nh.t * nh.t);
         w.len = v[d].len + nh.t;
-        w.vel = velocity_at(F, wt.obj, w.p);
-        w.u_in = v[d].u_in + dot(v[d].vel - w.vel, bs.wo);
     }
 }
 

@@ -90,7 +90,8 @@ __device__ __forceinline__ void res_load_value(const ResStore& s, size_t i, Res&
 }
 
 // chunks 4-21: the reconnection record (+ depth)
-__device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y) {
+// `vel`: also the path-velocity terms (chunks 22-23; Doppler gates only)
+__device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y, bool vel = false) {
     double2 c;
     Rec& q = y.rec;
     Meta m = ld_meta(s, i);
@@ -151,10 +152,15 @@ __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y) {
         q.m2 = mi.x;
         q.obj2 = mi.y;
     }
-    c = ld2(s, 22, i);
-    y.u = c.x;
-    q.prefix_u = c.y;
-    q.suffix_u = ld2(s, 23, i).x;
+    if (vel) {
+        c = ld2(s, 22, i);
+        y.u = c.x;
+        q.prefix_u = c.y;
+        q.suffix_u = ld2(s, 23, i).x;
+    } else {
+        y.u = 0;
+        q.prefix_u = q.suffix_u = 0;
+    }
     if (q.n_lanes > 0) {
         c = ld2(s, 20, i);
         memcpy(&q.lane_key, &c.x, 8);
@@ -200,7 +206,7 @@ __device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& 
     st2(s, 4, i, v.x, v.y);
 }
 
-__device__ inline void res_store(const ResStore& s, size_t i, const Res& r) {
+__device__ inline void res_store(const ResStore& s, size_t i, const Res& r, bool vel = false) {
     const Rec& q = r.y.rec;
     st2(s, 0, i, r.W, r.M);
     st2(s, 1, i, r.phat, r.y.len);
@@ -225,8 +231,10 @@ __device__ inline void res_store(const ResStore& s, size_t i, const Res& r) {
     int2 mi = make_int2(q.m2, q.obj2);
     memcpy(&m2d, &mi, 8);
     st2(s, 19, i, q.suffix_f.z, m2d);
-    st2(s, 22, i, r.y.u, q.prefix_u);
-    st2(s, 23, i, q.suffix_u, 0.0);
+    if (vel) {
+        st2(s, 22, i, r.y.u, q.prefix_u);
+        st2(s, 23, i, q.suffix_u, 0.0);
+    }
     if (q.n_lanes > 0) {
         double a, b;
         memcpy(&a, &q.lane_key, 8);

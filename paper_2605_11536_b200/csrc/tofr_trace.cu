@@ -25,6 +25,8 @@
 // gated reference (transport.hpp:591-617).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #define TOFR_OUTLINE_MATH 0
 
 #include "ktime.h"
@@ -42,10 +44,11 @@ namespace tofr_b200 {
 
 // RIS into the pixel's gated reservoir; the winning sample's record is written
 // to the grid when it wins, chunk 0 (W, M) when the pixel is done.
+// VEL: velocity (Doppler) gate, the gated quantity is the path velocity u
+template <bool VEL>
 struct GatedSink {
     ResStore cur;
     double center, width, inv;
-    int vel;  // velocity (Doppler) gate: the gated quantity is the path velocity u
     double w_sum, phat;
     int has;
     Rng pick;
@@ -59,9 +62,9 @@ struct GatedSink {
     }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
-    __device__ bool wants(double len, double u) const { return gate_w(center, width, gate_value(vel, len, u)) > 0; }
+    __device__ bool wants(double len, double u) const { return gate_w(center, width, VEL ? u : len) > 0; }
     __device__ void emit(const FrameView& F, const Cand& c, double mis, const RecSrc& rs) {
-        double p = luminance(c.f) * gate_w(center, width, gate_value(vel, c.len, c.u));
+        double p = luminance(c.f) * gate_w(center, width, VEL ? c.u : c.len);
         if (p <= 0 || !(c.pdf > 0)) return;
         double w = mis * inv * p / c.pdf;
         if (!isfinite(w) || w < 0) return;
@@ -77,8 +80,8 @@ struct GatedSink {
             r.y.len = c.len;
             r.y.u = c.u;
             r.y.depth = c.depth;
-            build_record(F, rs, r.y.rec);
-            res_store(cur, item, r);
+            build_record<VEL>(F, rs, r.y.rec);
+            res_store(cur, item, r, VEL);
             has = 1;
             phat = p;
         }
@@ -130,7 +133,7 @@ struct BinsSink {
             r.y.len = c.len;
             r.y.u = c.u;
             r.y.depth = c.depth;
-            build_record(F, rs, r.y.rec);
+            build_record<false>(F, rs, r.y.rec);
             res_store(st, i, r);
         }
     }
@@ -237,6 +240,9 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
     uint64_t pix = 0;
     Rng rng{0, 0};
     WalkV x;  // current vertex (= v[d])
+    WalkVel vv[VEL ? kMaxVerts : 1];  // velocity history (Doppler gates)
+    V3 xvel{0, 0, 0};                 // current vertex velocity and path velocity so far
+    double xu = 0;
     Cand c;   // NEE candidate waiting for its shadow ray
     c.pdf = 0;
     c.u = 0;
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     LightSample ls;
                     if (!light_sample(Fs.light, x.p, ls)) continue;
                     c.len = x.len + ls.dist;
-                    if (VEL) c.u = x.u_in + dot(x.vel, ls.dir);
+                    if (VEL) c.u = xu + dot(xvel, ls.dir);
                     if (!sk.wants(c.len, c.u)) continue;
                     V3 f_at = eval_bsdf(mx, x.n, x.wi, ls.dir);
                     double cos_v = fabs(dot(x.n, ls.dir));
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     c.len = x.len + dist + Fs.lsub.chain_len;
                     if (VEL) {
                         V3 vs = velocity_at(Fs, Fs.lsub.obj, Fs.lsub.pos);
-                        c.u = x.u_in + dot(x.vel - vs, wto) + dot(vs, Fs.lsub.wo_light);
+                        c.u = xu + dot(xvel - vs, wto) + dot(vs, Fs.lsub.wo_light);
                     }
                     if (!sk.wants(c.len, c.u)) continue;
                     V3 f_at = eval_bsdf(mx, x.n, x.wi, wto);
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                 V3 dd = lp - x.p;
                 double dist = norm(dd);
                 if (dist <= 2 * eps) {  // never occluded
-                    RecSrc rs{v, d, nullptr, rng.key};
+                    RecSrc rs{v, d, nullptr, rng.key, VEL ? vv : nullptr};
                     sk.emit(Fs, c, 1.0, rs);
                     continue;
                 }
@@ -360,9 +366,12 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     x.pdf = 1;
                     x.len = g.t;
                     x.lane = 0;
-                    x.vel = VEL ? velocity_at(Fs, ti.obj, x.p) : splat(0);
-                    x.u_in = VEL ? dot(Fs.cam_vel - x.vel, d0) : 0.0;
                     v[1] = x;
+                    if (VEL) {
+                        xvel = velocity_at(Fs, ti.obj, x.p);
+                        xu = dot(Fs.cam_vel - xvel, d0);
+                        vv[1] = WalkVel{xvel, xu};
+                    }
                     d = 1;
                     state = ST_NEE;
                     continue;
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
         // ---- consume
         if (state == ST_SHADOW) {
             if (th.slot < 0) {
-                RecSrc rs{v, d, nullptr, rng.key};
+                RecSrc rs{v, d, nullptr, rng.key, VEL ? vv : nullptr};
                 sk.emit(Fs, c, 1.0, rs);
             }
             state = ST_EXT;
@@ -427,11 +436,15 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                 double cos_w = fabs(dot(w.n, rd));
                 w.pdf = x.pdf * surv * bs_pdf * cos_w / (th.t * th.t);
                 w.len = x.len + th.t;
-                w.vel = VEL ? velocity_at(Fs, wt.obj, w.p) : splat(0);
-                w.u_in = VEL ? x.u_in + dot(x.vel - w.vel, rd) : 0.0;
                 ++d;
                 v[d] = w;
                 x = w;
+                if (VEL) {
+                    V3 wvel = velocity_at(Fs, wt.obj, w.p);
+                    xu = xu + dot(xvel - wvel, rd);
+                    xvel = wvel;
+                    vv[d] = WalkVel{xvel, xu};
+                }
                 state = ST_NEE;
             }
         }
@@ -471,16 +484,18 @@ static void launch_trace(const char* kname, const FrameView& F, const Band& bd, 
 void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
                         double center, double width, int frame_idx, ResStore cur, unsigned long long* q,
                         cudaStream_t s) {
-    GatedSink sk;
-    sk.cur = cur;
-    sk.center = center;
-    sk.width = width;
-    sk.inv = 1.0 / m_init;
-    sk.vel = cfg.gate_vel;
+    auto run = [&](auto sk, auto vel) {
+        sk.cur = cur;
+        sk.center = center;
+        sk.width = width;
+        sk.inv = 1.0 / m_init;
+        launch_trace<decltype(sk), decltype(vel)::value>("k_trace_gated", F, bd, g, cfg, m_init,
+                                                         uint64_t(frame_idx), sk, q, s);
+    };
     if (cfg.gate_vel)
-        launch_trace<GatedSink, true>("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+        run(GatedSink<true>{}, std::true_type{});
     else
-        launch_trace<GatedSink, false>("k_trace_gated", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
+        run(GatedSink<false>{}, std::false_type{});
 }
 
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,

@@ -189,7 +189,8 @@ __device__ __forceinline__ V3 rec_suffix_f(const ResStore& s, size_t i, int& m2)
 }
 
 // stored_prefix (identity shift: same pixel and frame), from the store
-__device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const ResStore& s, size_t i, int tri1) {
+__device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const ResStore& s, size_t i, int tri1,
+                                                   bool vel) {
     Prefix pre;
     double2 c5 = ld2(s, 5, i), c6 = ld2(s, 6, i), c7 = ld2(s, 7, i), c8 = ld2(s, 8, i), c9 = ld2(s, 9, i),
             c10 = ld2(s, 10, i);
@@ -202,13 +203,13 @@ __device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const Res
     pre.wi1 = V3{c9.x, c9.y, c10.x};
     pre.tri1 = tri1;
     pre.m1 = F.tri[tri1].mat;
-    pre.u = ld2(s, 22, i).y;
+    pre.u = vel ? ld2(s, 22, i).y : 0.0;
     return pre;
 }
 
 // hybrid_base_shift for k = 2 (shiftmap.hpp:459-528 with no replayed bounce):
 // the prefix is the destination pixel's primary hit.
-__device__ __forceinline__ Prefix gbuffer_prefix(const FrameView& F, const GHit* gbuf, int px, int py) {
+__device__ __forceinline__ Prefix gbuffer_prefix(const FrameView& F, const GHit* gbuf, int px, int py, bool vel) {
     Prefix out;
     out.ok = 0;
     GHit g = gbuf[size_t(py) * F.cam.w + px];
@@ -221,7 +222,7 @@ __device__ __forceinline__ Prefix gbuffer_prefix(const FrameView& F, const GHit*
     out.len = g.t;
     out.fw = splat(1);
     out.p1 = F.cam.pos + d0 * g.t;
-    out.u = dot(F.cam_vel - velocity_at(F, F.tri[g.tri].obj, out.p1), d0);
+    out.u = vel ? dot(F.cam_vel - velocity_at(F, F.tri[g.tri].obj, out.p1), d0) : 0.0;
     out.n1 = F.tri[g.tri].n;
     out.wi1 = -d0;
     out.tri1 = g.tri;
@@ -282,14 +283,16 @@ __device__ __forceinline__ Prefix replay_get(const FrameView& F, const ShiftQueu
 // prefix of the destination path: stored (identity), the primary hit (k = 2)
 // or the replayed bounces computed by k_shift_replay (k > 2)
 __device__ __forceinline__ Prefix job_prefix(const FrameView& F, const GHit* gbuf, const Job& jb, bool identity,
-                                             const ResStore& st, const Meta& mt, const ShiftQueue& q, uint32_t k) {
-    if (identity) return stored_prefix_at(F, st, jb.item, mt.tri1);
-    if (mt.k == 2) return gbuffer_prefix(F, gbuf, jb.dpx, jb.dpy);
+                                             const ResStore& st, const Meta& mt, const ShiftQueue& q, uint32_t k,
+                                             bool vel) {
+    if (identity) return stored_prefix_at(F, st, jb.item, mt.tri1, vel);
+    if (mt.k == 2) return gbuffer_prefix(F, gbuf, jb.dpx, jb.dpy, vel);
     return replay_get(F, q, k);
 }
 
 // suffix_geometry (shiftmap.hpp:546-575)
-__device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore& st, size_t item, int skind) {
+__device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore& st, size_t item, int skind,
+                                             bool vel) {
     Suffix s;
     s.ok = 0;
     s.n2 = splat(0);
@@ -297,11 +300,15 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
         s.p2 = rec_p2(st, item);
         s.n2 = rec_n2(st, item);
         s.len = ld2(st, 3, item).y;
-        s.u = ld2(st, 23, item).x;
-        int2 mo;
-        double m19 = ld2(st, 19, item).y;
-        memcpy(&mo, &m19, 8);
-        s.v2 = velocity_at(F, mo.y, s.p2);  // obj2
+        s.u = 0;
+        s.v2 = splat(0);
+        if (vel) {
+            s.u = ld2(st, 23, item).x;
+            int2 mo;
+            double m19 = ld2(st, 19, item).y;
+            memcpy(&mo, &m19, 8);
+            s.v2 = velocity_at(F, mo.y, s.p2);  // obj2
+        }
         s.ok = 1;
     } else if (skind == SK_LIGHT) {
         s.p2 = F.light.pos;
@@ -314,8 +321,8 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
         s.p2 = F.lsub.pos;
         s.n2 = F.lsub.n;
         s.len = F.lsub.chain_len;
-        s.v2 = velocity_at(F, F.lsub.obj, F.lsub.pos);
-        s.u = dot(s.v2, F.lsub.wo_light);
+        s.v2 = vel ? velocity_at(F, F.lsub.obj, F.lsub.pos) : splat(0);
+        s.u = vel ? dot(s.v2, F.lsub.wo_light) : 0.0;
         s.ok = 1;
     }
     return s;
@@ -678,11 +685,11 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     Suffix suf;
                     if (ok) {
                         bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
-                        pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, job);
+                        pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, job, VEL);
                         ok = pre.ok;
                     }
                     if (ok) {
-                        suf = job_suffix(F, st, jb.item, mt.skind);
+                        suf = job_suffix(F, st, jb.item, mt.skind, VEL);
                         ok = suf.ok;
                     }
                     if (!ok) {
@@ -862,8 +869,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         Meta mt = ld_meta(st, jb.item);
         bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
         bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
-        Prefix pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, k);
-        Suffix suf = job_suffix(F, st, jb.item, mt.skind);
+        Prefix pre = job_prefix(F, dsel ? g1 : g0, jb, identity, st, mt, q, k, VEL);
+        Suffix suf = job_suffix(F, st, jb.item, mt.skind, VEL);
         double2 c4 = jld(q, 4, k), c5 = jld(q, 5, k);
         V3 ppos{c4.x, c4.y, c5.x};
         int ptri = ts.x;
@@ -983,8 +990,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         __stcg(&o.base[16 * o.stride + k], c16);
         for (int c = 17; c < (mt.nl > 0 ? 22 : 20); ++c)
             __stcg(&o.base[size_t(c) * o.stride + k], ld2(st, c, jb.item));
-        st2(o, 22, k, u_total, pre.u);
-        st2(o, 23, k, mt.skind == SK_LIGHTSUB ? suf.u : ld2(st, 23, jb.item).x, 0.0);
+        if (VEL) {
+            st2(o, 22, k, u_total, pre.u);
+            st2(o, 23, k, mt.skind == SK_LIGHTSUB ? suf.u : ld2(st, 23, jb.item).x, 0.0);
+        }
     }
     work_add(cfg.work, WK_ANY, n_any);
     ctr_flush(ctr, ctr_out);
@@ -996,8 +1005,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 // chunks [from, 24) of record i -> record j, without the replay lanes (20-21)
 // unless the record has lanes
 __device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const ResStore& dst, size_t j, int from,
-                                            int n_lanes) {
-    for (int c = from; c < kResChunks; ++c) {
+                                            int n_lanes, bool vel) {
+    for (int c = from; c < (vel ? kResChunks : 22); ++c) {
         if ((c == 20 || c == 21) && n_lanes <= 0) continue;
         __stcg(&dst.base[size_t(c) * dst.stride + j], ld2(src, c, i));
     }
@@ -1005,22 +1014,23 @@ __device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const
 
 // Selected mapped record (job k) -> reservoir `it` with the merge's W, M, p-hat.
 __device__ __forceinline__ void put_mapped(const ResStore& o, uint32_t k, const ResStore& dst, size_t it, double W,
-                                           double M, double phat) {
+                                           double M, double phat, bool vel) {
     st2(dst, 0, it, W, M);
     st2(dst, 1, it, phat, ld2(o, 1, k).y);
     double2 c4 = ld2(o, 4, k);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    copy_chunks(o, k, dst, it, 2, mt.nl);
+    copy_chunks(o, k, dst, it, 2, mt.nl, vel);
 }
 
 // Reservoir copy src[it] -> dst[it] with a new W, M (sample and p-hat kept).
-__device__ __forceinline__ void copy_res(const ResStore& src, const ResStore& dst, size_t it, double W, double M) {
+__device__ __forceinline__ void copy_res(const ResStore& src, const ResStore& dst, size_t it, double W, double M,
+                                         bool vel) {
     st2(dst, 0, it, W, M);
     double2 c4 = ld2(src, 4, it);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    copy_chunks(src, it, dst, it, 1, mt.nl);
+    copy_chunks(src, it, dst, it, 1, mt.nl, vel);
 }
 
 // header (W, M, has, p-hat) of a reservoir
@@ -1140,7 +1150,7 @@ __global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int f
         Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(b), 8);
         int which = gris_merge(dst, src, ms, mapped, mgv, dc, dw, cfg.m_cap, rng);
         if (which == 2)
-            put_mapped(ws.q.out, kf, cur, it, dst.W, dst.M, dst.phat);
+            put_mapped(ws.q.out, kf, cur, it, dst.W, dst.M, dst.phat, cfg.gate_vel);
         else  // in place: the kept sample and its p-hat are already stored
             res_store_w(cur, it, dst.W, dst.M);
     }
@@ -1203,7 +1213,7 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
                 if (j == 0) {  // the output starts as the pass input
                     double2 c0 = ld2(src_grid, 0, it);
                     if (c0.x > 0)
-                        copy_res(src_grid, dst_grid, it, c0.x, c0.y);
+                        copy_res(src_grid, dst_grid, it, c0.x, c0.y, cfg.gate_vel);
                     else
                         res_store_w(dst_grid, it, 0.0, c0.y);
                     if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
@@ -1258,9 +1268,9 @@ __global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate
         if (j > 0) rng.ctr = ws.rng_ctr[i];
         int which = gris_merge(out, src, ms, mapped, mgv, dc, dw, cfg.m_cap, rng);
         if (which == 2)
-            put_mapped(ws.q.out, kf, dst_grid, it, out.W, out.M, out.phat);
+            put_mapped(ws.q.out, kf, dst_grid, it, out.W, out.M, out.phat, cfg.gate_vel);
         else if (which == 1 && j == 0)
-            copy_res(src_grid, dst_grid, it, out.W, out.M);
+            copy_res(src_grid, dst_grid, it, out.W, out.M, cfg.gate_vel);
         else  // kept in place (j > 0) or empty
             res_store_w(dst_grid, it, out.W, out.M);
         if (j + 1 < sp.neighbors) ws.rng_ctr[i] = rng.ctr;
