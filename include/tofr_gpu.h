@@ -254,6 +254,9 @@ uint64_t tofr_gpu_kernel_launches(void);
 int tofr_gpu_kernel_times(char* names, int32_t name_len, double* total_ms, uint64_t* launches, int32_t cap);
 void tofr_gpu_kernel_times_reset(void);
 
+/* FNV-1a 64 of a byte buffer (image.hpp:90-97; manifest output hashes) */
+uint64_t tofr_fnv1a64(const void* data, uint64_t n);
+
 /* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit
  * (Bvh::intersect_min) -> t, tri; mode 1 = occluded(a = o, b = d) -> tri = 0/1 */
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* s, double frame, const double* rays, int32_t n,

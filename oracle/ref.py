@@ -70,6 +70,9 @@ def lib():
         L.ref_neighbor_offsets.restype = None
         L.ref_initial_sampling.argtypes = [vp, P(F.RenderConfigC), C.c_int] + [P(C.c_double)] * 4 + \
             [P(C.c_int), P(C.c_int), C.c_char_p, C.c_size_t]
+        L.ref_compute_metrics.argtypes = [P(C.c_double), P(C.c_double), C.c_int, C.c_int, P(C.c_double),
+                                          P(C.c_double)]
+        L.ref_compute_metrics.restype = None
         _lib = L
     return _lib
 
@@ -220,3 +223,55 @@ def initial_sampling(scene: RefScene, cfg: RenderConfig, frame_idx: int):
     _check(lib().ref_initial_sampling(scene.h, C.byref(c), frame_idx, _dptr(W), _dptr(M), _dptr(ph), _dptr(ln),
                                       _iptr(has), _iptr(k), err, 512), err)
     return {"W": W, "M": M, "phat": ph, "len": ln, "has": has, "k": k}
+
+
+def compute_metrics(est: np.ndarray, refimg: np.ndarray):
+    """The reference's compute_metrics (pipeline.hpp:588-607): (mape, relmse)."""
+    est = np.ascontiguousarray(est, dtype=np.float64)
+    refimg = np.ascontiguousarray(refimg, dtype=np.float64)
+    h, w = est.shape[:2]
+    mape, relmse = C.c_double(), C.c_double()
+    lib().ref_compute_metrics(_dptr(est), _dptr(refimg), w, h, C.byref(mape), C.byref(relmse))
+    return mape.value, relmse.value
+
+
+def _tool(*args, stdin: str | None = None) -> str:
+    """oracle/_ref/ref_tool: the reference's stream-based writers in their own
+    process (libstdc++ streams inside the ctypes-loaded library are not safe
+    next to this interpreter's runtime)."""
+    import subprocess
+    exe = LIB.parent / "ref_tool"
+    if not exe.exists():
+        raise RuntimeError(f"{exe} missing (build with `make -C oracle`)")
+    r = subprocess.run([str(exe), *map(str, args)], input=stdin, capture_output=True, text=True, check=True)
+    return r.stdout
+
+
+def write_image(img: np.ndarray, pfm_path: str, txt_path: str) -> None:
+    """write_pfm + write_text_matrix (image.hpp:41-82) of the reference."""
+    import tempfile
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    with tempfile.NamedTemporaryFile(suffix=".f64") as f:
+        f.write(img.tobytes())
+        f.flush()
+        _tool("write_image", f.name, img.shape[1], img.shape[0], pfm_path, txt_path)
+
+
+def hash_file(path: str) -> int:
+    """hash_file (image.hpp:99-106) of the reference."""
+    return int(_tool("hash", path).strip())
+
+
+def stats_lines(stats: list) -> str:
+    """stats_lines (pipeline.hpp:612-633) of the reference for the given
+    per-frame counters and timings."""
+    keys = ("attempts", "newton_ok", "newton_failed", "occluded", "jac_clamped", "replay_failed", "iterations",
+            "solves", "success")
+    rows = []
+    for fs in stats:
+        row = [str(fs["frame"]), repr(float(fs["t_init"])), repr(float(fs["t_shade"]))]
+        for st in ("temporal", "spatial", "bin"):
+            row += [str(int(fs[st][k])) for k in keys] + [repr(float(fs[st]["seconds"]))]
+        rows.append(" ".join(row))
+    return _tool("stats_lines", stdin="\n".join(rows) + "\n")
+

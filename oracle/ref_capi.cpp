@@ -362,4 +362,16 @@ int ref_initial_sampling(ref_scene* s, const tofr_render_config* c, int frame_id
     });
 }
 
+// compute_metrics (pipeline.hpp:588-607) on two W x H x 3 images
+void ref_compute_metrics(const double* est, const double* refimg, int w, int h, double* mape, double* relmse) {
+    Image a(w, h), b(w, h);
+    for (size_t i = 0; i < size_t(w) * h; ++i) {
+        a.px[i] = {est[3 * i], est[3 * i + 1], est[3 * i + 2]};
+        b.px[i] = {refimg[3 * i], refimg[3 * i + 1], refimg[3 * i + 2]};
+    }
+    Metrics m = compute_metrics(a, b);
+    *mape = m.mape;
+    *relmse = m.relmse;
+}
+
 }  // extern "C"

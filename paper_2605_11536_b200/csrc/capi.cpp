@@ -1273,6 +1273,16 @@ int tofr_gpu_kernel_times(char* names, int32_t name_len, double* total_ms, uint6
     return kt_read(names, name_len, total_ms, launches, cap);
 }
 
+uint64_t tofr_fnv1a64(const void* data, uint64_t n) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
 void tofr_gpu_kernel_times_reset(void) {
     kt_collect();
     kt_reset();

@@ -158,6 +158,48 @@ class SceneDef:
         return d, keep
 
 
+def to_scn(sd: SceneDef) -> str:
+    """Scene description text (scene_io.hpp grammar) of a SceneDef, for the
+    CLI.  Rotated pose keys are not expressible from a quaternion here and
+    raise ValueError; translation tracks and static scenes round-trip."""
+    g = lambda v: format(float(v), ".17g")  # noqa: E731
+    v3 = lambda t: " ".join(g(x) for x in t)  # noqa: E731
+    cam = sd.camera
+    lines = ["camera {", f"  position {v3(cam.base.position)}", f"  forward {v3(cam.base.forward)}",
+             f"  up {v3(cam.base.up)}", f"  fov_deg {g(cam.fov_y * 180.0 / KPI)}",
+             f"  resolution {cam.width} {cam.height}"]
+    if cam.track:
+        lines.append("  track {")
+        for fr, p in cam.track:
+            lines.append(f"    frame {g(fr)} position {v3(p.position)} forward {v3(p.forward)} up {v3(p.up)}")
+        lines.append("  }")
+    lines += ["}", f"dt_frame {g(sd.dt_frame)}"]
+    kinds = {F.MAT_DIFFUSE: "diffuse", F.MAT_GLOSSY: "glossy", F.MAT_MIRROR: "mirror"}
+    for i, m in enumerate(sd.materials):
+        lines.append(f"material m{i} {{ kind {kinds[m.kind]} albedo {v3(m.albedo)} roughness {g(m.roughness)} }}")
+    L = sd.light
+    lines += ["light {", f"  regime {'wide' if L.regime == F.LIGHT_WIDE else 'collimated'}",
+              f"  position {v3(L.position)}", f"  direction {v3(L.direction)}",
+              f"  cone_deg {g(L.cone_half_angle * 180.0 / KPI)}", f"  intensity {v3(L.intensity)}", "}"]
+    for i, o in enumerate(sd.objects):
+        lines.append(f"object {o.name or f'o{i}'} {{")
+        cur = None
+        for (a, b, c, m) in o.tris:
+            if m != cur:
+                lines.append(f"  material m{m}")
+                cur = m
+            lines.append(f"  tri {v3(a)}   {v3(b)}   {v3(c)}")
+        if o.track:
+            lines.append("  track {")
+            for k in o.track:
+                if tuple(k.q) != (1.0, 0.0, 0.0, 0.0):
+                    raise ValueError("to_scn: rotated pose keys are not supported")
+                lines.append(f"    frame {g(k.frame)} translate {v3(k.t)}")
+            lines.append("  }")
+        lines.append("}")
+    return "\n".join(lines) + "\n"
+
+
 # ---------------------------------------------------------------------------
 # test-suite builders (test_scenes.hpp:17-101)
 
