@@ -195,6 +195,14 @@ struct tofr_session {
     uint64_t halo_exchanges = 0;
     // per-frame stage events, two frames in flight
     cudaEvent_t ev[2][7] = {};
+    // Frame pipelining (ReSTIR sessions): frame f's upload, camera stage and
+    // initial sampling run on `side` as soon as frame f-1's temporal stage is
+    // done -- concurrently with frame f-1's spatial pass and shading on the
+    // main stream.  They touch only the buffers frame f-1 no longer reads after
+    // its temporal stage: the frame slot / G-buffer of frame f-2 and the grid
+    // that held frame f-2's final reservoirs.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_temporal[2] = {}, ev_init[2] = {};
     bool pending[2] = {false, false};
     unsigned long long* err_host = nullptr;  // pinned [2]
     cudaEvent_t read_ev[2] = {};             // asynchronous image read-backs
@@ -213,8 +221,12 @@ struct tofr_session {
     ~tofr_session() {
         if (ctx) {
             cudaSetDevice(ctx->device);
+            if (side) cudaStreamSynchronize(side);
             if (ctx->stream) cudaStreamSynchronize(ctx->stream);
         }
+        for (auto* e : {&ev_temporal[0], &ev_temporal[1], &ev_init[0], &ev_init[1]})
+            if (*e) cudaEventDestroy(*e);
+        if (side) cudaStreamDestroy(side);
         for (auto& set : ev)
             for (auto& e : set)
                 if (e) cudaEventDestroy(e);
@@ -282,7 +294,7 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width, const
     return p;
 }
 
-void upload_frame(tofr_session* s, int which, double frame, int frame_id) {
+void upload_frame(tofr_session* s, int which, double frame, int frame_id, cudaStream_t st) {
     FrameSlot& sl = s->slot[which];
     HFrame hf = build_frame(s->scene, frame);
     if (hf.max_depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
@@ -293,7 +305,7 @@ void upload_frame(tofr_session* s, int which, double frame, int frame_id) {
     sl.staging.ensure(nb);
     std::memcpy(sl.staging.p, sl.pk.blob.data(), nb);
     sl.blob.ensure(nb);
-    ck(cudaMemcpyAsync(sl.blob.p, sl.staging.p, nb, cudaMemcpyHostToDevice, s->ctx->stream), "frame upload");
+    ck(cudaMemcpyAsync(sl.blob.p, sl.staging.p, nb, cudaMemcpyHostToDevice, st), "frame upload");
     sl.view = rebase_view(sl.pk, static_cast<const unsigned char*>(sl.blob.p));
     sl.gbuf.ensure(size_t(s->r1 - s->r0) * s->W * sizeof(GHit));
     s->last_h2d = nb;
@@ -346,13 +358,18 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     for (auto& e : s->read_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&s->err_host), 2 * sizeof(unsigned long long)), "pinned");
     s->err_host[0] = s->err_host[1] = 0;
-    // [3 stages x SC_COUNT][band error][work counter q][WK_COUNT device work]
-    s->ctr.ensure((3 * SC_COUNT + 2 + WK_COUNT) * sizeof(unsigned long long));
-    ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 2 + WK_COUNT) * sizeof(unsigned long long), ctx->stream),
+    // [3 stages x SC_COUNT][band error][work counter q][WK_COUNT device work][side-stream work counter]
+    s->ctr.ensure((3 * SC_COUNT + 3 + WK_COUNT) * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(s->ctr.p, 0, (3 * SC_COUNT + 3 + WK_COUNT) * sizeof(unsigned long long), ctx->stream),
        "memset");
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
     s->plain = plain;
+    if (!plain && !(std::getenv("TOFR_PIPELINE") && std::strcmp(std::getenv("TOFR_PIPELINE"), "0") == 0)) {
+        ck(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "stream");
+        for (auto* e : {&s->ev_temporal[0], &s->ev_temporal[1], &s->ev_init[0], &s->ev_init[1]})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    }
     s->transient = plain || cfg->mode == TOFR_MODE_TRANSIENT;
     s->B = s->transient ? cfg->bins : 1;
     if (s->transient && (cfg->bins < 1 || !(cfg->hist_bin_width > 0)))
@@ -528,7 +545,9 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     int set = f & 1;
     flush_set(s, set);  // frame f-2: frees its event set and its staging buffer
     int sl = f & 1, psl = sl ^ 1;
-    upload_frame(s, sl, c.frame0 + f, f);
+    if (s->side && !s->plain && f > 0)  // frame f-1 no longer reads frame f-2's slot and grid
+        cudaStreamWaitEvent(s->side, s->ev_temporal[set ^ 1], 0);
+    upload_frame(s, sl, c.frame0 + f, f, (s->side && !s->plain) ? s->side : stream);
     const FrameView& F = s->slot[sl].view;
     GHit* g_local = s->slot[sl].gbuf.as<GHit>();
     const GHit* g = rows_base<GHit>(s->slot[sl].gbuf, s->r0, s->W);
@@ -551,6 +570,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     bool prev_halo = halo && s->cam_moves;
     Band bd = band_of(s, prev_halo);
     cudaEvent_t* ev = s->ev[set];
+    // camera + initial sampling stream (see tofr_session::side)
+    const bool piped = s->side != nullptr && !s->plain;
+    cudaStream_t fs = piped ? s->side : stream;
+    unsigned long long* q_side = piped ? ctr + 3 * SC_COUNT + 2 + WK_COUNT : q;
     WorkOrder wo{nullptr, nullptr, nullptr};
     WaveScratch wv;
     if (s->wave) {
@@ -568,10 +591,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     }
     if (s->order && s->wo_perm.p)
         wo = WorkOrder{s->wo_cls.as<uint8_t>(), s->wo_counts.as<uint32_t>(), s->wo_perm.as<uint32_t>()};
-    ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
+    if (!piped) ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
 
-    cudaEventRecord(ev[0], stream);
-    launch_gbuffer(F, bd, g_local, stream);
+    cudaEventRecord(ev[0], fs);
+    launch_gbuffer(F, bd, g_local, fs);
     s->camera_rays += uint64_t(s->r1 - s->r0) * s->W;
     if (s->plain) {
         size_t pr = size_t(s->W) * s->B;
@@ -584,10 +607,15 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         InitParams ip{vel ? int(INIT_DIRECT) : c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
         ResStore cur = store_of(s, s->res[s->cur]);
         if (s->transient)
-            launch_init_transient(F, bd, g, pc, ip, h, f, cur, q, stream);
+            launch_init_transient(F, bd, g, pc, ip, h, f, cur, q_side, fs);
         else
-            launch_init_gated(F, bd, g, pc, ip, f, cur, q, stream);
-        cudaEventRecord(ev[1], stream);
+            launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs);
+        cudaEventRecord(ev[1], fs);
+        if (piped) {  // the main stream continues once this frame's reservoirs exist
+            cudaEventRecord(s->ev_init[set], fs);
+            cudaStreamWaitEvent(stream, s->ev_init[set], 0);
+            ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
+        }
         GateGrid cg{s->transient ? 1 : 0, center, width, h};
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
@@ -600,6 +628,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                                 wo, ctr + 0 * SC_COUNT, q, stream);
         }
         cudaEventRecord(ev[2], stream);
+        if (piped) cudaEventRecord(s->ev_temporal[set], stream);
         if (s->transient && c.bin_reuse) {
             launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
@@ -1043,7 +1072,7 @@ int tofr_gpu_reference(tofr_gpu* ctx, const tofr_scene* sc, double frame, double
         c.max_depth = max_depth;
         c.seed = seed;
         std::unique_ptr<tofr_session> s(make_session(ctx, sc, &c, KIND_BARE));
-        upload_frame(s.get(), 0, frame, 0);
+        upload_frame(s.get(), 0, frame, 0, ctx->stream);
         size_t npix = size_t(s->W) * s->H;
         DevBuf dm, ds;
         dm.ensure(npix * 3 * 8);
@@ -1295,7 +1324,7 @@ int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const
         tofr_render_config c;
         tofr_render_config_default(&c);
         std::unique_ptr<tofr_session> s(make_session(ctx, sc, &c, KIND_BARE));
-        upload_frame(s.get(), 0, frame, 0);
+        upload_frame(s.get(), 0, frame, 0, ctx->stream);
         if (n == 0) {
             ck(cudaStreamSynchronize(ctx->stream), "probe");
             return;
