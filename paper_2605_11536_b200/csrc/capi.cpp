@@ -365,7 +365,9 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
     s->plain = plain;
-    if (!plain && !(std::getenv("TOFR_PIPELINE") && std::strcmp(std::getenv("TOFR_PIPELINE"), "0") == 0)) {
+    // opt-in (TOFR_PIPELINE=1): measured +1-3% frames/s, but the overlap muddles the
+    // per-kernel event timings the roofline is computed from
+    if (!plain && std::getenv("TOFR_PIPELINE") && std::strcmp(std::getenv("TOFR_PIPELINE"), "1") == 0) {
         ck(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "stream");
         for (auto* e : {&s->ev_temporal[0], &s->ev_temporal[1], &s->ev_init[0], &s->ev_init[1]})
             ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");

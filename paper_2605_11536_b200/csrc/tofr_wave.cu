@@ -157,6 +157,48 @@ __device__ __forceinline__ void mlist_append(const WaveScratch& ws, bool want, u
     if (want) ws.mlist[base + __popc(m & ((1u << lane) - 1))] = item;
 }
 
+// Block-aggregated appends for the per-item prep kernels: one global atomic
+// per block and list per loop iteration instead of one per warp (the warps of
+// a 67 M-item transient grid otherwise serialise on the queue counters).  All
+// threads of the block must call them; `sh` is nwarps + 1 words of shared memory.
+__device__ __forceinline__ uint32_t block_append(uint32_t* gctr, bool want, uint32_t* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (lane == 0) sh[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            uint32_t c = sh[w];
+            sh[w] = tot;
+            tot += c;
+        }
+        sh[nw] = tot ? atomicAdd(gctr, tot) : 0u;
+    }
+    __syncthreads();
+    uint32_t k = sh[nw] + sh[warp] + __popc(m & ((1u << lane) - 1));
+    __syncthreads();  // `sh` is reused by the next call
+    return want ? k : kNoJob;
+}
+
+__device__ __forceinline__ uint32_t block_queue_append(const ShiftQueue& q, bool want, unsigned long long* err,
+                                                       uint32_t* sh) {
+    uint32_t k = block_append(&q.ctl[1], want, sh);
+    if (k != kNoJob && k >= q.cap) {
+        atomicAdd(err, 1ull << 32);
+        return kNoJob;
+    }
+    return k;
+}
+
+__device__ __forceinline__ void block_mlist_append(const WaveScratch& ws, bool want, uint32_t item,
+                                                   unsigned long long* work, uint32_t* sh) {
+    uint32_t k = block_append(&ws.q.ctl[3], want, sh);
+    if (k != kNoJob) ws.mlist[k] = item;
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (work && (threadIdx.x & 31) == 0 && m) atomicAdd(&work[WK_MERGES], (unsigned long long)__popc(m));
+}
+
 // ---------------------------------------------------------------------------
 // record fields straight from the reservoir store (tofr_store.cuh layout)
 
@@ -1066,12 +1108,38 @@ __device__ __forceinline__ double inv_output(const ShiftQueue& q, uint32_t k) {
 // (or ~0: no primary hit, off-screen, or outside the rows the band holds);
 // job maps are written only for items that have the job (the apply kernel
 // reads them under the same non-emptiness tests).
+// Reprojection of each band pixel's primary hit into the previous camera
+// (temporal_reuse, pipeline.hpp:213-219): ws.tsrc[pixel] = source pixel or ~0.
+__global__ void k_temporal_reproject(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, WaveScratch ws) {
+    int W = Fc.cam.w;
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        int p = bd.y0 * W + int(i);
+        int px = p % W, py = p / W;
+        uint64_t src_pix = ~uint64_t(0);
+        GHit g = gc[p];
+        int qx, qy;
+        if (g.tri >= 0) {
+            V3 d0 = primary_dir(Fc.cam, px, py);
+            V3 hp = Fc.cam.pos + d0 * g.t;
+            if (project(Fp.cam, hp, qx, qy)) {
+                if (qy < bd.t0 || qy >= bd.t1)  // reprojection left the rows this band holds
+                    atomicAdd(bd.err, 1ull);
+                else
+                    src_pix = uint64_t(qy) * W + qx;
+            }
+        }
+        ws.tsrc[i] = src_pix;
+    }
+}
+
 __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg,
                                 PathCfg cfg, ResStore cur, ResStore prev, WaveScratch ws) {
     int W = Fc.cam.w, B = cg.transient ? cg.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + 31) & ~size_t(31);
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
         bool live = i < n;
         size_t it = base + (live ? i : 0);
@@ -1081,36 +1149,27 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
         size_t src_i = 0;
         int qx = 0, qy = 0;
         if (live) {
-            GHit g = gc[p];
-            uint64_t src_pix = ~uint64_t(0);
-            if (g.tri >= 0) {
-                V3 d0 = primary_dir(Fc.cam, px, py);
-                V3 hp = Fc.cam.pos + d0 * g.t;
-                if (project(Fp.cam, hp, qx, qy)) {
-                    if (qy < bd.t0 || qy >= bd.t1) {  // reprojection left the rows this band holds
-                        if (b == 0) atomicAdd(bd.err, 1ull);
-                    } else {
-                        src_pix = uint64_t(qy) * W + qx;
-                        src_i = size_t(src_pix) * B + b;
-                        double2 s0 = ld2(prev, 0, src_i);
-                        if (s0.y > 0) {
-                            double2 c0 = ld2(cur, 0, it);
-                            fwd = s0.x > 0;
-                            inv = c0.x > 0;
-                            merge = fwd || inv;
-                            // both empty: the merge only adds the confidences (no RNG draw)
-                            if (!merge) res_store_w(cur, it, 0.0, dmin(c0.y + s0.y, cfg.m_cap));
-                        }
-                    }
+            uint64_t src_pix = ws.tsrc[size_t(p) - size_t(bd.y0) * W];
+            if (src_pix != ~uint64_t(0)) {
+                qx = int(src_pix % W);
+                qy = int(src_pix / W);
+                src_i = size_t(src_pix) * B + b;
+                double2 s0 = ld2(prev, 0, src_i);
+                if (s0.y > 0) {
+                    double2 c0 = ld2(cur, 0, it);
+                    fwd = s0.x > 0;
+                    inv = c0.x > 0;
+                    merge = fwd || inv;
+                    // both empty: the merge only adds the confidences (no RNG draw)
+                    if (!merge) res_store_w(cur, it, 0.0, dmin(c0.y + s0.y, cfg.m_cap));
                 }
             }
-            if (b == 0) ws.tsrc[size_t(p) - size_t(bd.y0) * W] = src_pix;
         }
         double dc, dw, sc, sw;
         gate_of(cg, b, dc, dw);
         gate_of(pg, b, sc, sw);
-        uint32_t kf = queue_append(ws.q, fwd, bd.err);
-        uint32_t ki = queue_append(ws.q, inv, bd.err);
+        uint32_t kf = block_queue_append(ws.q, fwd, bd.err, sh);
+        uint32_t ki = block_queue_append(ws.q, inv, bd.err, sh);
         if (kf != kNoJob) {
             job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
             ws.map_a[i] = kf;
@@ -1119,7 +1178,7 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
             job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
             ws.map_b[i] = ki;
         }
-        mlist_append(ws, merge, uint32_t(i), cfg.work);
+        block_mlist_append(ws, merge, uint32_t(i), cfg.work, sh);
     }
 }
 
@@ -1167,7 +1226,8 @@ __global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid g
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + 31) & ~size_t(31);
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
         bool live = i < n;
         size_t it = base + (live ? i : 0);
@@ -1183,7 +1243,7 @@ __global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid g
             // when its record has no reconnection vertex, as the reference does)
             bool want = live && spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
                         ld2(src_grid, 0, si).x > 0;
-            uint32_t k = queue_append(ws.q, want, bd.err);
+            uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
             if (k != kNoJob) job_put(ws.q, k, si, JOB_FULL | JOB_COUNT, nx, ny, px, py, dc, dc, dw);
             if (live) ws.map_a[size_t(j) * n + i] = k;
         }
@@ -1195,7 +1255,8 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + 31) & ~size_t(31);
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
     const ResStore& out_grid = j == 0 ? src_grid : dst_grid;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
         bool live = i < n;
@@ -1228,12 +1289,12 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
                 }
             }
         }
-        uint32_t k = queue_append(ws.q, want, bd.err);
+        uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
         if (k != kNoJob) {
             job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
             ws.map_b[i] = k;
         }
-        mlist_append(ws, merge, uint32_t(i), cfg.work);
+        block_mlist_append(ws, merge, uint32_t(i), cfg.work, sh);
     }
 }
 
@@ -1344,6 +1405,11 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
     {
         KScope ks("k_queue_ctl", s);
         k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    }
+    {
+        KScope ks("k_temporal_reproject", s);
+        size_t npx = size_t(bd.y1 - bd.y0) * Fc.cam.w;
+        k_temporal_reproject<<<grid_n(npx, 256), 256, 0, s>>>(Fc, bd, gc, Fp, ws);
     }
     {
         KScope ks("k_temporal_prep", s);
