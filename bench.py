@@ -288,6 +288,19 @@ def run_ours(args) -> None:
     shift_stats = {k: {n: st[k][n] for n in ("attempts", "solves", "iterations", "newton_ok", "occluded",
                                               "success")} for k in ("temporal", "spatial")}
 
+    # per-frame latency (C5): frames stepped one at a time, device
+    # time of each frame from its own events (submit -> last kernel)
+    latency = None
+    if args.latency_frames > 0:
+        lat = []
+        for _ in range(args.latency_frames):
+            sess.step(stats=True)
+            tot, _ = sess.sess.last_ms()
+            lat.append(tot)
+        lat_all = parallel.gather_floats(lat, group) if ws > 1 else lat
+        latency = {"frames": len(lat), "p50_ms": float(np.percentile(lat_all, 50)),
+                   "p99_ms": float(np.percentile(lat_all, 99)), "max_ms": float(np.max(lat_all))}
+
     # e2e through the public API: step + image read-back to pinned host memory
     parallel.barrier(group)
     e2e_s = sess.run_e2e(args.steps)
@@ -351,6 +364,7 @@ def run_ours(args) -> None:
             "mpaths_per_s": w * h * cfg.m_init * fps / 1e6,
             "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},
             "shift_stats_one_frame": shift_stats,
+            "frame_latency": latency,
             "e2e": {"value": frames / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
@@ -381,7 +395,11 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-frames", type=int, default=-1,
+                    help="frames stepped one at a time for p50/p99 frame latency (default: 30 for c5, else 0)")
     args = ap.parse_args()
+    if args.latency_frames < 0:
+        args.latency_frames = 30 if args.workload == "c5" else 0
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -63,6 +63,18 @@ def max_over_ranks(x: float, group) -> float:
     return float(t.item())
 
 
+def gather_floats(xs: list, group) -> list:
+    """All ranks' per-frame values (frame latency is the max over the bands
+    of the same frame, so the lists are reduced elementwise with MAX)."""
+    if group is None:
+        return list(xs)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x) for x in xs], dtype=torch.float64, device=_dev(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t.cpu().tolist()
+
+
 class HaloExchanger:
     """Swaps halo rows with the upper (rank-1) and lower (rank+1) neighbour.
 

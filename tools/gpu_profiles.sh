@@ -26,6 +26,7 @@ cap() {  # workload kernel skip
 }
 cap c3 k_shift_solve 15
 cap c3 k_trace 3
+cap c3w k_trace 3
 cap c3w k_shift_solve 15
 cap c3w k_shift_finish 15
 cap c2r k_temporal_prep 3
