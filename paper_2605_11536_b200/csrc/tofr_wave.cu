@@ -778,6 +778,49 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             break;
         }
 
+        // ---- tail phase: once the queue is drained, idle lanes help the lowest
+        // busy lane by evaluating the rest of its halving ladder (scale/2, /4, ...)
+        // speculatively in the same round.  The trials of a ladder depend only on
+        // the current point and step, so taking the first accepted one in ladder
+        // order (and counting the rejections before it) is the sequential
+        // newton_solve; the serial critical path of long solves shrinks instead.
+        bool tail = false, helper = false;
+        int owner = 0, hk = 0, K = 0;
+        {
+            unsigned idle = __ballot_sync(0xffffffffu, exhausted);
+            unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked);
+            if (idle && cand) {
+                tail = true;
+                owner = __ffs(cand) - 1;
+                int obt = __shfl_sync(0xffffffffu, bt, owner);
+                K = min(__popc(idle), 8 - obt);
+                int rank = __popc(idle & ((1u << lane) - 1)) + 1;
+                helper = exhausted && rank <= K;
+                hk = helper ? rank : 0;
+#define TOFR_BORROW(x)                                          \
+    {                                                           \
+        auto t_ = __shfl_sync(0xffffffffu, (x), owner);         \
+        if (helper) (x) = t_;                                   \
+    }
+#define TOFR_BORROW3(v) TOFR_BORROW(v.x) TOFR_BORROW(v.y) TOFR_BORROW(v.z)
+                TOFR_BORROW(dsel) TOFR_BORROW(ctri) TOFR_BORROW(cn_rec) TOFR_BORROW(scale) TOFR_BORROW(delta)
+                TOFR_BORROW(fnorm) TOFR_BORROW(step.x) TOFR_BORROW(step.y)
+                TOFR_BORROW3(cpos) TOFR_BORROW3(spos) TOFR_BORROW3(p1) TOFR_BORROW3(p2)
+                TOFR_BORROW3(Jc.t) TOFR_BORROW3(Jc.b) TOFR_BORROW3(Js.t) TOFR_BORROW3(Js.b)
+                TOFR_BORROW3(stt.g3s) TOFR_BORROW(stt.gs.x) TOFR_BORROW(stt.gs.y) TOFR_BORROW(stt.lvs)
+                TOFR_BORROW(stt.Hs.a) TOFR_BORROW(stt.Hs.b) TOFR_BORROW(stt.Hs.c) TOFR_BORROW(stt.Hs.d)
+                if (VEL) {
+                    TOFR_BORROW3(vf.v1) TOFR_BORROW3(vf.v2)
+                }
+#undef TOFR_BORROW3
+#undef TOFR_BORROW
+                if (helper) {
+                    init = false;
+                    for (int k = 0; k < hk; ++k) scale *= 0.5;
+                }
+            }
+        }
+
         // ---- one Newton trial (trial 0 = the initial evaluation at the start point)
         const FrameView& F = sF[dsel];
         V3 tpos = cpos + to_world(Jc, step * scale);  // plane point
@@ -786,11 +829,16 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         if (init) tpos = spos;
         // A plane point outside the current triangle needs re-projection rays
         // (reproject_to_mesh).  Such lanes park until TOFR_RAYBATCH lanes of the
-        // warp need rays (or no other lane can proceed) and then trace together.
-        if (active && !parked && !init && !in_triangle(F, ctri, tpos)) parked = true;
+        // warp need rays (or no other lane can proceed) and then trace together;
+        // in the tail phase rays are traced at once.
+        bool part = (active && !parked) || helper;
+        bool need_ray = part && !init && !in_triangle(F, ctri, tpos);
+        if (need_ray && !tail && active) parked = true;
         unsigned pm = __ballot_sync(0xffffffffu, parked);
         unsigned rm = __ballot_sync(0xffffffffu, active && !parked);
-        if (parked && (__popc(pm) >= TOFR_RAYBATCH || rm == 0)) {
+        bool trace_now = (parked && (tail || __popc(pm) >= TOFR_RAYBATCH || rm == 0)) || (tail && need_ray);
+        if (trace_now) {
+            if (parked) tpos = cpos + to_world(Jc, step * scale);
             SurfR r = reproject_rays(&F, ctri, tpos, p1);
             n_rays += uint32_t(r.rays);
             have = r.ok;
@@ -801,8 +849,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             }
             parked = false;
         }
-        unsigned em = __ballot_sync(0xffffffffu, active && !parked);
-        if (!active || parked) continue;
+        unsigned em = __ballot_sync(0xffffffffu, (active && !parked) || helper);
+        if (!((active && !parked) || helper)) continue;
         __syncwarp(em);
         // the tangent frame of the current triangle is already known (Jc, or Js
         // for trial 0): recompute only after a re-projection ray changed it
@@ -811,6 +859,32 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         TrialEval et = trial_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
         double fn = hypot(et.F.x, et.F.y);
         bool accept = have && (init || fn < fnorm);
+        if (tail) {
+            // the owner takes the first accepted trial of its ladder
+            unsigned hm = __ballot_sync(em, helper && accept);
+            int src = hm ? __ffs(hm) - 1 : owner;
+#define TOFR_TAKE(x)                                \
+    {                                               \
+        auto t_ = __shfl_sync(em, (x), src);        \
+        if (take) (x) = t_;                         \
+    }
+#define TOFR_TAKE3(v) TOFR_TAKE(v.x) TOFR_TAKE(v.y) TOFR_TAKE(v.z)
+            bool take = lane == owner && !accept && hm != 0;
+            TOFR_TAKE3(tpos) TOFR_TAKE(ttri) TOFR_TAKE(tn_rec) TOFR_TAKE3(Jt.t) TOFR_TAKE3(Jt.b)
+            TOFR_TAKE(et.F.x) TOFR_TAKE(et.F.y) TOFR_TAKE(et.dFp.a) TOFR_TAKE(et.dFp.b) TOFR_TAKE(et.dFp.c)
+            TOFR_TAKE(et.dFp.d) TOFR_TAKE(et.det_dF) TOFR_TAKE(et.ngrad) TOFR_TAKE(fn)
+#undef TOFR_TAKE3
+#undef TOFR_TAKE
+            if (lane == owner && !accept) {
+                if (hm) {
+                    accept = true;  // helper ladder trial accepted (bt is reset below)
+                } else {
+                    bt += K;  // K more rejected halvings; the owner's own rejection follows
+                    for (int k = 0; k < K; ++k) scale *= 0.5;
+                }
+            }
+            if (helper) continue;  // helpers only evaluate
+        }
         bool fin = false, conv = false;
         double jac = 0;
         if (accept) {
