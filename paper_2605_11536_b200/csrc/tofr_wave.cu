@@ -784,19 +784,31 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         // the current point and step, so taking the first accepted one in ladder
         // order (and counting the rejections before it) is the sequential
         // newton_solve; the serial critical path of long solves shrinks instead.
-        bool tail = false, helper = false;
-        int owner = 0, hk = 0, K = 0;
+        bool tail = false, helper = false, own = false;
+        int owner = lane, hk = 0, K = 0;
+        unsigned group = 1u << lane;
         {
             unsigned idle = __ballot_sync(0xffffffffu, exhausted);
             unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked);
             if (idle && cand) {
+                // idle lanes are dealt out in rank order, H to each busy lane
                 tail = true;
-                owner = __ffs(cand) - 1;
+                const int nc = __popc(cand);
+                const int H = min(8, max(1, __popc(idle) / nc));
+                const int r = __popc(idle & ((1u << lane) - 1));
+                const int j = r / H;
+                if (exhausted && j < nc) {
+                    unsigned m = cand;
+                    for (int q = 0; q < j; ++q) m &= m - 1;
+                    owner = __ffs(m) - 1;
+                }
                 int obt = __shfl_sync(0xffffffffu, bt, owner);
-                K = min(__popc(idle), 8 - obt);
-                int rank = __popc(idle & ((1u << lane) - 1)) + 1;
-                helper = exhausted && rank <= K;
-                hk = helper ? rank : 0;
+                hk = r % H + 1;
+                helper = exhausted && j < nc && hk <= 8 - obt;
+                if (!helper) owner = lane, hk = 0;
+                group = __match_any_sync(0xffffffffu, owner);
+                own = !helper && __popc(group) > 1;
+                K = own ? __popc(group) - 1 : 0;
 #define TOFR_BORROW(x)                                          \
     {                                                           \
         auto t_ = __shfl_sync(0xffffffffu, (x), owner);         \
@@ -860,23 +872,23 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         double fn = hypot(et.F.x, et.F.y);
         bool accept = have && (init || fn < fnorm);
         if (tail) {
-            // the owner takes the first accepted trial of its ladder
+            // each owner takes the first accepted trial of its ladder
             unsigned hm = __ballot_sync(em, helper && accept);
-            int src = hm ? __ffs(hm) - 1 : owner;
+            int src = (own && (group & hm)) ? __ffs(group & hm) - 1 : lane;
 #define TOFR_TAKE(x)                                \
     {                                               \
         auto t_ = __shfl_sync(em, (x), src);        \
         if (take) (x) = t_;                         \
     }
 #define TOFR_TAKE3(v) TOFR_TAKE(v.x) TOFR_TAKE(v.y) TOFR_TAKE(v.z)
-            bool take = lane == owner && !accept && hm != 0;
+            bool take = own && !accept && (group & hm) != 0;
             TOFR_TAKE3(tpos) TOFR_TAKE(ttri) TOFR_TAKE(tn_rec) TOFR_TAKE3(Jt.t) TOFR_TAKE3(Jt.b)
             TOFR_TAKE(et.F.x) TOFR_TAKE(et.F.y) TOFR_TAKE(et.dFp.a) TOFR_TAKE(et.dFp.b) TOFR_TAKE(et.dFp.c)
             TOFR_TAKE(et.dFp.d) TOFR_TAKE(et.det_dF) TOFR_TAKE(et.ngrad) TOFR_TAKE(fn)
 #undef TOFR_TAKE3
 #undef TOFR_TAKE
-            if (lane == owner && !accept) {
-                if (hm) {
+            if (own && !accept) {
+                if (group & hm) {
                     accept = true;  // helper ladder trial accepted (bt is reset below)
                 } else {
                     bt += K;  // K more rejected halvings; the owner's own rejection follows
