@@ -43,6 +43,10 @@
 #endif
 // lanes needing re-projection rays a warp collects before it traces them
 #ifndef TOFR_RAYBATCH
+// 1: lanes waiting for a refill help too (measured slower: it disables ray parking)
+#ifndef TOFR_HELP_IDLE
+#define TOFR_HELP_IDLE 0
+#endif
 #define TOFR_RAYBATCH 8
 #endif
 
@@ -788,7 +792,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int owner = lane, hk = 0, K = 0;
         unsigned group = 1u << lane;
         {
-            unsigned idle = __ballot_sync(0xffffffffu, exhausted);
+            const bool free_lane = TOFR_HELP_IDLE ? !active : exhausted;
+            unsigned idle = __ballot_sync(0xffffffffu, free_lane);
             unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked);
             if (idle && cand) {
                 // idle lanes are dealt out in rank order, H to each busy lane
@@ -797,14 +802,14 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 const int H = min(8, max(1, __popc(idle) / nc));
                 const int r = __popc(idle & ((1u << lane) - 1));
                 const int j = r / H;
-                if (exhausted && j < nc) {
+                if (free_lane && j < nc) {
                     unsigned m = cand;
                     for (int q = 0; q < j; ++q) m &= m - 1;
                     owner = __ffs(m) - 1;
                 }
                 int obt = __shfl_sync(0xffffffffu, bt, owner);
                 hk = r % H + 1;
-                helper = exhausted && j < nc && hk <= 8 - obt;
+                helper = free_lane && j < nc && hk <= 8 - obt;
                 if (!helper) owner = lane, hk = 0;
                 group = __match_any_sync(0xffffffffu, owner);
                 own = !helper && __popc(group) > 1;
