@@ -243,6 +243,11 @@ def run_ours(args) -> None:
     ws, rank, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    # TOFR_DIST_BACKEND=gloo: host-staged halo transport, several ranks may
+    # share one GPU (plumbing test of the N > 1 path on a one-GPU box)
+    backend = os.environ.get("TOFR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     from paper_2605_11536_b200 import parallel
     from paper_2605_11536_b200.api import Renderer
@@ -250,7 +255,10 @@ def run_ours(args) -> None:
     group = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     scene_name, w, h, cfg, desc = WORKLOADS[args.workload]
     plain = args.workload in PLAIN

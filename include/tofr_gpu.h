@@ -257,6 +257,11 @@ void tofr_gpu_kernel_times_reset(void);
 /* FNV-1a 64 of a byte buffer (image.hpp:90-97; manifest output hashes) */
 uint64_t tofr_fnv1a64(const void* data, uint64_t n);
 
+/* self-test of the device's shared-reciprocal FP64 division against the
+ * compiler's a / b on n random V3 / scalar quotients: *mismatches = quotients
+ * whose bits differ (0 expected) */
+int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
+
 /* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit
  * (Bvh::intersect_min) -> t, tri; mode 1 = occluded(a = o, b = d) -> tri = 0/1 */
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* s, double frame, const double* rays, int32_t n,

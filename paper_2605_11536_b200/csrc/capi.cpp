@@ -1319,6 +1319,18 @@ void tofr_gpu_kernel_times_reset(void) {
     kt_reset();
 }
 
+int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    return guard(ctx, [&] {
+        if (!ctx || !mismatches) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");
+        DevBuf d;
+        d.ensure(8);
+        ck(cudaMemsetAsync(d.p, 0, 8, ctx->stream), "memset");
+        launch_selftest_div(n, seed, d.as<unsigned long long>(), ctx->stream);
+        ck(cudaMemcpyAsync(mismatches, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        ck(cudaStreamSynchronize(ctx->stream), "selftest");
+    });
+}
+
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const double* rays, int32_t n,
                         int32_t mode, double* out_t, int32_t* out_tri) {
     return guard(ctx, [&] {

@@ -955,6 +955,48 @@ __global__ void k_probe_rays(FrameView F, const double* rays, int n, int mode, d
     }
 }
 
+// Self-test of the shared-reciprocal division (v3_div_shared / ddiv_by,
+// tofr_core.h) against the compiler's a / b: counts quotients whose bits
+// differ.  Operands: raw 64-bit patterns (every exponent, subnormals, inf, NaN)
+// for odd k, and geometry-range values (|a| < 2^20, |b| in [2^-30, 2^30]) for
+// even k; the three numerators of a V3 share one divisor.
+__device__ __forceinline__ uint64_t st_mix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad) {
+    unsigned long long local = 0;
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t h = st_mix(seed ^ (k * 0x2545f4914f6cdd1dull));
+        double a[3], b;
+        if (k & 1) {
+            b = __longlong_as_double((long long)st_mix(h));
+            for (int j = 0; j < 3; ++j) a[j] = __longlong_as_double((long long)st_mix(h + 1 + j));
+        } else {
+            uint64_t hb = st_mix(h);
+            double m = 1.0 + double(hb >> 12) * 0x1p-52;
+            b = ldexp(m, int((hb & 63) - 30)) * ((hb >> 7) & 1 ? -1.0 : 1.0);
+            for (int j = 0; j < 3; ++j) {
+                uint64_t ha = st_mix(h + 1 + j);
+                a[j] = (double(ha >> 11) * 0x1p-53 * 2.0 - 1.0) * ldexp(1.0, int(ha & 31) - 10);
+            }
+        }
+        V3 q = v3_div_shared(V3{a[0], a[1], a[2]}, b);
+        double ref[3] = {a[0] / b, a[1] / b, a[2] / b};
+        double got[3] = {q.x, q.y, q.z};
+        for (int j = 0; j < 3; ++j)
+            local += __double_as_longlong(got[j]) != __double_as_longlong(ref[j]);
+    }
+    if (local) atomicAdd(bad, local);
+}
+
+void launch_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s) {
+    KScope ks("k_selftest_div", s);
+    k_selftest_div<<<148 * 8, 256, 0, s>>>(n, seed, bad);
+}
+
 // ---------------------------------------------------------------------------
 // halo staging (row-band sharding): one 16 B chunk per thread, coalesced on
 // both sides

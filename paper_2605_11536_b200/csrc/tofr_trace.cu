@@ -28,6 +28,7 @@
 #include <type_traits>
 
 #define TOFR_OUTLINE_MATH 0
+#define TOFR_SHARED_DIV 0
 
 #include "ktime.h"
 #include "tofr_kcommon.cuh"

@@ -804,6 +804,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 const int j = r / H;
                 if (free_lane && j < nc) {
                     unsigned m = cand;
+                    #pragma unroll 1
                     for (int q = 0; q < j; ++q) m &= m - 1;
                     owner = __ffs(m) - 1;
                 }
@@ -833,6 +834,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 #undef TOFR_BORROW
                 if (helper) {
                     init = false;
+                    #pragma unroll 1
                     for (int k = 0; k < hk; ++k) scale *= 0.5;
                 }
             }
@@ -897,6 +899,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     accept = true;  // helper ladder trial accepted (bt is reset below)
                 } else {
                     bt += K;  // K more rejected halvings; the owner's own rejection follows
+                    #pragma unroll 1
                     for (int k = 0; k < K; ++k) scale *= 0.5;
                 }
             }

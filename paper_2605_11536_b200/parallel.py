@@ -107,7 +107,9 @@ class HaloExchanger:
         self.calls += 1
         if not ops:
             return
-        if self.stream is not None:
+        if self.stream is not None and dist.get_backend(self.group) != "nccl":
+            self._host_staged(ops)
+        elif self.stream is not None:
             # NCCL waits on the session stream (the pack kernels) and the
             # session stream waits on NCCL (the unpack kernels follow)
             with torch.cuda.stream(self.stream):
@@ -116,6 +118,21 @@ class HaloExchanger:
         else:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+
+
+    def _host_staged(self, ops) -> None:
+        """Device buffers over a host-only backend (gloo): wait for the pack
+        kernels, exchange host copies, copy the received rows back."""
+        import torch
+        import torch.distributed as dist
+        self.stream.synchronize()
+        host = [op.tensor.cpu() for op in ops]
+        for r in dist.batch_isend_irecv([dist.P2POp(op.op, h, op.peer, self.group) for op, h in zip(ops, host)]):
+            r.wait()
+        with torch.cuda.stream(self.stream):
+            for op, h in zip(ops, host):
+                if op.op is dist.irecv:
+                    op.tensor.copy_(h)
 
 
 class _DevBytes:
