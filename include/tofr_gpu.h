@@ -243,6 +243,10 @@ int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t
  * occlusion) rays, out[3] transient histogram deposits, out[4] GRIS merges
  * with a non-empty side (reuse merge lists) */
 int tofr_gpu_session_work(tofr_session* ss, uint64_t* out /* [5] */);
+/* sparse transient grids: pool rows currently held by each of the three
+ * reservoir grids (rows_used[3]) and the rows per grid (*rows_cap; 0 = the
+ * session's grids are dense).  Waits for the frames in flight. */
+int tofr_gpu_session_pool(tofr_session* ss, uint64_t* rows_used, uint64_t* rows_cap);
 void tofr_gpu_session_destroy(tofr_session* ss);
 
 /* launch accounting of the library's kernels (process-wide): every launch is

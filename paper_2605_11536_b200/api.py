@@ -418,6 +418,14 @@ class Session:
         return {"shift_jobs": int(w[0]), "rays_closest": int(w[1]), "rays_any": int(w[2]),
                 "deposits": int(w[3]), "merges": int(w[4])}
 
+    def pool(self) -> dict:
+        """Sparse transient grids: pool rows held per grid now and rows per grid
+        (cap 0: dense grids).  Waits for pending frames."""
+        used = (C.c_uint64 * 3)()
+        cap = C.c_uint64()
+        self._r._check(self._r._lib.tofr_gpu_session_pool(self.handle, used, C.byref(cap)))
+        return {"rows_used": [int(x) for x in used], "rows_cap": int(cap.value)}
+
     def io_bytes(self):
         h2d, d2h = C.c_uint64(), C.c_uint64()
         self._r._check(self._r._lib.tofr_gpu_session_io_bytes(self.handle, C.byref(h2d), C.byref(d2h)))

@@ -179,6 +179,11 @@ struct tofr_session {
     FrameSlot slot[2];
     DevBuf res[3];
     int cur = 0, prev = 1, spare = 2;
+    // sparse transient grids (tofr_store.cuh): slot map per grid, pool rows
+    // handed out per grid ([3] u32), pool rows per grid (+2 reserved rows)
+    bool sparse = false;
+    size_t pool_rows = 0;
+    DevBuf res_slot[3], res_rows;
     DevBuf image, accum, hist, hist_count;  // owned rows only
     DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag + work counter
     DevBuf send_lo, send_hi, recv_lo, recv_hi;
@@ -242,6 +247,8 @@ struct tofr_session {
             sl.gbuf.release();
         }
         for (auto& r : res) r.release();
+        for (auto& r : res_slot) r.release();
+        res_rows.release();
         for (DevBuf* b : {&image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
@@ -254,7 +261,24 @@ namespace {
 // Global-indexed views of band-local buffers (see Band in tofr_kernels.h).
 ResStore store_of(const tofr_session* s, const DevBuf& b) {
     size_t items = s->items_stored();
-    return ResStore{b.as<double2>() - ptrdiff_t(size_t(s->r0) * s->W * s->B), items};
+    ptrdiff_t off = ptrdiff_t(size_t(s->r0) * s->W * s->B);
+    if (!s->sparse) return ResStore{b.as<double2>() - off, items};
+    int k = int(&b - &s->res[0]);
+    ResStore st{b.as<double2>() - off, s->pool_rows + 2};
+    st.slot = s->res_slot[k].as<uint32_t>() - off;
+    // chunk planes 1..23 follow the header plane; plane c at pool + c * stride
+    st.pool = b.as<double2>() + items - ptrdiff_t(st.stride);
+    st.rows = s->res_rows.as<unsigned int>() + k;
+    st.err = s->ctr.as<unsigned long long>() + 3 * SC_COUNT;
+    return st;
+}
+
+// a sparse grid about to be rewritten (new frame's init, spatial / bin-reuse
+// output): every reservoir loses its pool row
+void reset_store(tofr_session* s, int k, cudaStream_t st) {
+    if (!s->sparse) return;
+    ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, s->items_stored() * sizeof(uint32_t), st), "memset");
+    ck(cudaMemsetAsync(s->res_rows.as<unsigned int>() + k, 0, sizeof(unsigned int), st), "memset");
 }
 template <class T>
 T* rows_base(const DevBuf& b, int row0, size_t per_row) {
@@ -387,7 +411,34 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         s->has_temporal = cfg->temporal ? 1 : 0;
         s->has_bin = (s->transient && cfg->bin_reuse) ? 1 : 0;
         s->has_spatial = cfg->spatial_passes > 0 ? 1 : 0;
-        size_t rb = s->items_stored() * kResChunks * 16;
+        size_t items = s->items_stored();
+        size_t rb = items * kResChunks * 16;
+        {
+            // transient grids are mostly empty reservoirs: header plane + a pool
+            // of sample rows (TOFR_SPARSE=0: dense).  Pool = TOFR_POOL_FRAC of
+            // the items (default 0.25), or all of them while that is small.
+            const char* sp = std::getenv("TOFR_SPARSE");
+            s->sparse = s->transient && !(sp && sp[0] == '0');
+            if (s->sparse) {
+                double frac = 0.25;
+                if (const char* pf = std::getenv("TOFR_POOL_FRAC")) frac = std::atof(pf);
+                size_t rows = size_t(double(items) * frac) + 1;
+                const size_t small = (size_t(2) << 30) / ((kResChunks - 1) * 16);
+                if (rows < small) rows = small;
+                if (rows > items) rows = items;
+                if (const char* pr = std::getenv("TOFR_POOL_ROWS")) rows = size_t(std::strtoull(pr, nullptr, 10));
+                if (rows > 0xfffffff0ull) rows = 0xfffffff0ull;
+                s->pool_rows = rows;
+                rb = items * 16 + (kResChunks - 1) * (rows + 2) * 16;
+                for (int k = 0; k < 3; ++k)
+                    if (k < 2 || s->has_bin || s->has_spatial) {
+                        s->res_slot[k].ensure(items * sizeof(uint32_t));
+                        ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, items * sizeof(uint32_t), ctx->stream), "memset");
+                    }
+                s->res_rows.ensure(4 * sizeof(unsigned int));
+                ck(cudaMemsetAsync(s->res_rows.p, 0, 4 * sizeof(unsigned int), ctx->stream), "memset");
+            }
+        }
         s->res[0].ensure(rb);
         s->res[1].ensure(rb);
         if (s->has_bin || s->has_spatial) s->res[2].ensure(rb);
@@ -502,6 +553,10 @@ void flush_set(tofr_session* s, int set) {
         s->stage_tot[i] += ms[i];
     }
     s->tot_frames++;
+    if (s->err_host[set] & kErrPool)
+        throw ScopeError(TOFR_ERR_OOM,
+                         "transient reservoir pool full: more non-empty reservoirs than TOFR_POOL_FRAC of the grid "
+                         "(raise it, or TOFR_SPARSE=0)");
     if (s->err_host[set] >> 32)
         throw ScopeError(TOFR_ERR_OOM,
                          "reuse shift queue overflow: more shifts than TOFR_WAVE_CAP jobs in one stage (raise it, or "
@@ -607,6 +662,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         // the ellipsoidal and shrink initializers apply to length gates only; velocity
         // gates fall back to plain RIS (pipeline.hpp:110, :130)
         InitParams ip{vel ? int(INIT_DIRECT) : c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
+        reset_store(s, s->cur, fs);
         ResStore cur = store_of(s, s->res[s->cur]);
         if (s->transient)
             launch_init_transient(F, bd, g, pc, ip, h, f, cur, q_side, fs);
@@ -632,6 +688,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         cudaEventRecord(ev[2], stream);
         if (piped) cudaEventRecord(s->ev_temporal[set], stream);
         if (s->transient && c.bin_reuse) {
+            reset_store(s, s->spare, stream);
             launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur]);
@@ -640,6 +697,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
         for (int pass = 0; pass < c.spatial_passes; ++pass) {
             if (halo) exchange_halo(s, cur, pass);
+            reset_store(s, s->spare, stream);
             SpatialScratch scr;
             const SpatialScratch* scp = nullptr;
             if (s->phased) {
@@ -1271,6 +1329,17 @@ int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t
     if (h2d_per_step) *h2d_per_step = ss->last_h2d;
     if (d2h_image) *d2h_image = uint64_t(ss->owned_pixels()) * 3 * sizeof(double);
     return TOFR_OK;
+}
+
+int tofr_gpu_session_pool(tofr_session* ss, uint64_t* rows_used, uint64_t* rows_cap) {
+    if (!ss || !rows_used || !rows_cap) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        unsigned int r[3] = {0, 0, 0};
+        if (ss->sparse) ck(cudaMemcpy(r, ss->res_rows.p, sizeof(r), cudaMemcpyDeviceToHost), "pool");
+        for (int k = 0; k < 3; ++k) rows_used[k] = r[k];
+        *rows_cap = ss->sparse ? ss->pool_rows : 0;
+    });
 }
 
 int tofr_gpu_session_work(tofr_session* ss, uint64_t* out) {

@@ -1005,15 +1005,28 @@ __global__ void k_halo_pack(ResStore grid, size_t item0, size_t n, double2* buf)
     size_t total = n * kResChunks;
     for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
         size_t c = j / n, i = j % n;
-        buf[j] = __ldcg(&grid.base[c * grid.stride + item0 + i]);
+        // sparse stores: the sample chunks of an empty reservoir are never read (zeros go out)
+        bool live = c == 0 || grid.slot == nullptr || ld2(grid, 0, item0 + i).x > 0;
+        buf[j] = live ? ld2(grid, int(c), item0 + i) : make_double2(0.0, 0.0);
     }
+}
+
+// sparse stores: pool rows for the non-empty reservoirs that arrive (one
+// thread per item, before the chunk-parallel copy)
+__global__ void k_halo_alloc(ResStore grid, size_t item0, size_t n, const double2* buf) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        if (__ldcg(&buf[i]).x > 0) res_row_w(grid, item0 + i);
 }
 
 __global__ void k_halo_unpack(ResStore grid, size_t item0, size_t n, const double2* buf) {
     size_t total = n * kResChunks;
     for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
         size_t c = j / n, i = j % n;
-        __stcg(&grid.base[c * grid.stride + item0 + i], __ldcg(&buf[j]));
+        double2 v = __ldcg(&buf[j]);
+        if (c == 0)
+            __stcg(&grid.base[item0 + i], v);
+        else if (grid.slot == nullptr || __ldcg(&buf[i]).x > 0)
+            st2r(grid, int(c), res_row(grid, item0 + i), v);
     }
 }
 
@@ -1272,6 +1285,10 @@ void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf,
 void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s) {
     if (!n_items) return;
     {
+        if (grid.slot) {
+            KScope ka("k_halo_alloc", s);
+            k_halo_alloc<<<grid_for(n_items, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+        }
         KScope ks("k_halo_unpack", s);
         k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
     }

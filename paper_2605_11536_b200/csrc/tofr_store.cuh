@@ -26,18 +26,75 @@ namespace tofr_b200 {
 
 constexpr int kResChunks = 24;
 
+// Dense store (gated grids, scratch planes): chunk c of item i at
+// base[c * stride + i].
+//
+// Sparse store (transient grids, TOFR_SPARSE): the header plane (chunk 0:
+// W, M) stays dense, base[i], but chunks 1..23 live in a pool of rows that
+// only non-empty reservoirs occupy: chunk c of item i at
+// pool[c * stride + slot[i]] (stride = pool rows + 2).  A W x H x B transient
+// grid is mostly empty reservoirs (92% at C2), so the pool is a fraction of the
+// dense grid.  A reservoir gets its row the first time a sample chunk is
+// written to it (one atomic on the grid's row counter) and keeps it until the
+// grid is recycled for another frame or pass (slot map reset to kNoSlot,
+// counter to 0: reset_sparse_store).  Rows stride-1 (all zero: what an
+// empty reservoir reads) and stride-2 (where writes go once the pool is full;
+// raises kErrPool in the band error word) are never handed out.  One thread
+// writes a given item of a grid at a time (every writer owns its items), so a
+// row is allocated once.
+constexpr uint32_t kNoSlot = 0xffffffffu;
+constexpr unsigned long long kErrPool = 1ull << 62;
+
 struct ResStore {
     double2* base;
-    size_t stride;  // items per chunk plane
+    size_t stride;                       // dense: items per chunk plane; sparse: pool rows + 2
+    uint32_t* slot = nullptr;            // sparse: item -> pool row (global item index)
+    double2* pool = nullptr;             // sparse: chunk planes 1..23 (pool[c * stride + row])
+    unsigned int* rows = nullptr;        // sparse: rows handed out
+    unsigned long long* err = nullptr;   // sparse: band error word (kErrPool on overflow)
 };
 
 #if defined(__CUDACC__)
 
+// pool row of item i for reading chunks >= 1 (the zero row when it has none)
+__device__ __forceinline__ size_t res_row(const ResStore& s, size_t i) {
+    if (s.slot == nullptr) return i;
+    uint32_t r = __ldcg(&s.slot[i]);
+    return r == kNoSlot ? s.stride - 1 : size_t(r);
+}
+// pool row of item i for writing chunks >= 1 (allocated on first use)
+__device__ __forceinline__ size_t res_row_w(const ResStore& s, size_t i) {
+    if (s.slot == nullptr) return i;
+    uint32_t r = __ldcg(&s.slot[i]);
+    if (r == kNoSlot) {
+        r = atomicAdd(s.rows, 1u);
+        if (size_t(r) >= s.stride - 2) {
+            atomicOr(s.err, kErrPool);
+            return s.stride - 2;
+        }
+        __stcg(&s.slot[i], r);
+    }
+    return r;
+}
+__device__ __forceinline__ double2* res_planes(const ResStore& s) { return s.slot ? s.pool : s.base; }
+
+// chunk c >= 1 at a known row
+__device__ __forceinline__ double2 ld2r(const ResStore& s, int c, size_t row) {
+    return __ldcg(&res_planes(s)[size_t(c) * s.stride + row]);
+}
+__device__ __forceinline__ void st2r(const ResStore& s, int c, size_t row, double2 v) {
+    __stcg(&res_planes(s)[size_t(c) * s.stride + row], v);
+}
+
 __device__ __forceinline__ double2 ld2(const ResStore& s, int c, size_t i) {
-    return __ldcg(&s.base[size_t(c) * s.stride + i]);
+    if (c == 0) return __ldcg(&s.base[i]);
+    return ld2r(s, c, res_row(s, i));
 }
 __device__ __forceinline__ void st2(const ResStore& s, int c, size_t i, double a, double b) {
-    __stcg(&s.base[size_t(c) * s.stride + i], make_double2(a, b));
+    if (c == 0)
+        __stcg(&s.base[i], make_double2(a, b));
+    else
+        st2r(s, c, res_row_w(s, i), make_double2(a, b));
 }
 
 struct Meta {
@@ -45,6 +102,12 @@ struct Meta {
     int tri1, ptri;
 };
 
+__device__ __forceinline__ Meta ld_meta_r(const ResStore& s, size_t row) {
+    double2 v = ld2r(s, 4, row);
+    Meta m;
+    memcpy(&m, &v, 16);
+    return m;
+}
 __device__ __forceinline__ Meta ld_meta(const ResStore& s, size_t i) {
     double2 v = ld2(s, 4, i);
     Meta m;
@@ -78,13 +141,14 @@ __device__ __forceinline__ void res_load_head(const ResStore& s, size_t i, Res& 
 // chunks 1-3: phat, len, f, suffix_len (what a merge reads of a candidate)
 __device__ __forceinline__ void res_load_value(const ResStore& s, size_t i, Res& r) {
     double2 c;
-    c = ld2(s, 1, i);
+    const size_t row = res_row(s, i);
+    c = ld2r(s, 1, row);
     r.phat = c.x;
     r.y.len = c.y;
-    c = ld2(s, 2, i);
+    c = ld2r(s, 2, row);
     r.y.f.x = c.x;
     r.y.f.y = c.y;
-    c = ld2(s, 3, i);
+    c = ld2r(s, 3, row);
     r.y.f.z = c.x;
     r.y.rec.suffix_len = c.y;
 }
@@ -94,7 +158,8 @@ __device__ __forceinline__ void res_load_value(const ResStore& s, size_t i, Res&
 __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y, bool vel = false) {
     double2 c;
     Rec& q = y.rec;
-    Meta m = ld_meta(s, i);
+    const size_t row = res_row(s, i);
+    Meta m = ld_meta_r(s, row);
     q.valid = m.valid;
     q.k = m.k == 255 ? -1 : int(m.k);
     q.n_lanes = m.nl;
@@ -102,49 +167,49 @@ __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y, bool
     y.depth = m.depth;
     q.tri1 = m.tri1;
     q.ptri = m.ptri;
-    c = ld2(s, 5, i);
+    c = ld2r(s, 5, row);
     q.prefix_pdf = c.x;
     q.prefix_len = c.y;
-    c = ld2(s, 6, i);
+    c = ld2r(s, 6, row);
     q.prefix_fw.x = c.x;
     q.prefix_fw.y = c.y;
-    c = ld2(s, 7, i);
+    c = ld2r(s, 7, row);
     q.prefix_fw.z = c.x;
     q.p1.x = c.y;
-    c = ld2(s, 8, i);
+    c = ld2r(s, 8, row);
     q.p1.y = c.x;
     q.p1.z = c.y;
-    c = ld2(s, 9, i);
+    c = ld2r(s, 9, row);
     q.wi1.x = c.x;
     q.wi1.y = c.y;
-    c = ld2(s, 10, i);
+    c = ld2r(s, 10, row);
     q.wi1.z = c.x;
     q.p.x = c.y;
-    c = ld2(s, 11, i);
+    c = ld2r(s, 11, row);
     q.p.y = c.x;
     q.p.z = c.y;
-    c = ld2(s, 12, i);
+    c = ld2r(s, 12, row);
     q.pn.x = c.x;
     q.pn.y = c.y;
-    c = ld2(s, 13, i);
+    c = ld2r(s, 13, row);
     q.pn.z = c.x;
     q.p2.x = c.y;
-    c = ld2(s, 14, i);
+    c = ld2r(s, 14, row);
     q.p2.y = c.x;
     q.p2.z = c.y;
-    c = ld2(s, 15, i);
+    c = ld2r(s, 15, row);
     q.n2.x = c.x;
     q.n2.y = c.y;
-    c = ld2(s, 16, i);
+    c = ld2r(s, 16, row);
     q.n2.z = c.x;
     q.wo2.x = c.y;
-    c = ld2(s, 17, i);
+    c = ld2r(s, 17, row);
     q.wo2.y = c.x;
     q.wo2.z = c.y;
-    c = ld2(s, 18, i);
+    c = ld2r(s, 18, row);
     q.suffix_f.x = c.x;
     q.suffix_f.y = c.y;
-    c = ld2(s, 19, i);
+    c = ld2r(s, 19, row);
     q.suffix_f.z = c.x;
     {
         int2 mi;
@@ -153,19 +218,19 @@ __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y, bool
         q.obj2 = mi.y;
     }
     if (vel) {
-        c = ld2(s, 22, i);
+        c = ld2r(s, 22, row);
         y.u = c.x;
         q.prefix_u = c.y;
-        q.suffix_u = ld2(s, 23, i).x;
+        q.suffix_u = ld2r(s, 23, row).x;
     } else {
         y.u = 0;
         q.prefix_u = q.suffix_u = 0;
     }
     if (q.n_lanes > 0) {
-        c = ld2(s, 20, i);
+        c = ld2r(s, 20, row);
         memcpy(&q.lane_key, &c.x, 8);
         memcpy(&q.lane_ctr[0], &c.y, 8);
-        c = ld2(s, 21, i);
+        c = ld2r(s, 21, row);
         memcpy(&q.lane_ctr[4], &c, 12);
     } else {
         q.lane_key = 0;
@@ -189,7 +254,7 @@ __device__ __forceinline__ void res_load_all(const ResStore& s, size_t i, Res& r
     res_load_rec(s, i, r.y);
 }
 
-__device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& r) {
+__device__ __forceinline__ void st_meta_r(const ResStore& s, size_t row, const Res& r) {
     Meta m;
     const Rec& q = r.y.rec;
     m.has = (unsigned char)(r.has ? 1 : 0);
@@ -203,46 +268,48 @@ __device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& 
     m.ptri = q.ptri;
     double2 v;
     memcpy(&v, &m, 16);
-    st2(s, 4, i, v.x, v.y);
+    st2r(s, 4, row, v);
 }
+__device__ __forceinline__ void st_meta(const ResStore& s, size_t i, const Res& r) { st_meta_r(s, res_row_w(s, i), r); }
 
 __device__ inline void res_store(const ResStore& s, size_t i, const Res& r, bool vel = false) {
     const Rec& q = r.y.rec;
     st2(s, 0, i, r.W, r.M);
-    st2(s, 1, i, r.phat, r.y.len);
-    st2(s, 2, i, r.y.f.x, r.y.f.y);
-    st2(s, 3, i, r.y.f.z, q.suffix_len);
-    st_meta(s, i, r);
-    st2(s, 5, i, q.prefix_pdf, q.prefix_len);
-    st2(s, 6, i, q.prefix_fw.x, q.prefix_fw.y);
-    st2(s, 7, i, q.prefix_fw.z, q.p1.x);
-    st2(s, 8, i, q.p1.y, q.p1.z);
-    st2(s, 9, i, q.wi1.x, q.wi1.y);
-    st2(s, 10, i, q.wi1.z, q.p.x);
-    st2(s, 11, i, q.p.y, q.p.z);
-    st2(s, 12, i, q.pn.x, q.pn.y);
-    st2(s, 13, i, q.pn.z, q.p2.x);
-    st2(s, 14, i, q.p2.y, q.p2.z);
-    st2(s, 15, i, q.n2.x, q.n2.y);
-    st2(s, 16, i, q.n2.z, q.wo2.x);
-    st2(s, 17, i, q.wo2.y, q.wo2.z);
-    st2(s, 18, i, q.suffix_f.x, q.suffix_f.y);
+    const size_t row = res_row_w(s, i);
+    st2r(s, 1, row, make_double2(r.phat, r.y.len));
+    st2r(s, 2, row, make_double2(r.y.f.x, r.y.f.y));
+    st2r(s, 3, row, make_double2(r.y.f.z, q.suffix_len));
+    st_meta_r(s, row, r);
+    st2r(s, 5, row, make_double2(q.prefix_pdf, q.prefix_len));
+    st2r(s, 6, row, make_double2(q.prefix_fw.x, q.prefix_fw.y));
+    st2r(s, 7, row, make_double2(q.prefix_fw.z, q.p1.x));
+    st2r(s, 8, row, make_double2(q.p1.y, q.p1.z));
+    st2r(s, 9, row, make_double2(q.wi1.x, q.wi1.y));
+    st2r(s, 10, row, make_double2(q.wi1.z, q.p.x));
+    st2r(s, 11, row, make_double2(q.p.y, q.p.z));
+    st2r(s, 12, row, make_double2(q.pn.x, q.pn.y));
+    st2r(s, 13, row, make_double2(q.pn.z, q.p2.x));
+    st2r(s, 14, row, make_double2(q.p2.y, q.p2.z));
+    st2r(s, 15, row, make_double2(q.n2.x, q.n2.y));
+    st2r(s, 16, row, make_double2(q.n2.z, q.wo2.x));
+    st2r(s, 17, row, make_double2(q.wo2.y, q.wo2.z));
+    st2r(s, 18, row, make_double2(q.suffix_f.x, q.suffix_f.y));
     double m2d;
     int2 mi = make_int2(q.m2, q.obj2);
     memcpy(&m2d, &mi, 8);
-    st2(s, 19, i, q.suffix_f.z, m2d);
+    st2r(s, 19, row, make_double2(q.suffix_f.z, m2d));
     if (vel) {
-        st2(s, 22, i, r.y.u, q.prefix_u);
-        st2(s, 23, i, q.suffix_u, 0.0);
+        st2r(s, 22, row, make_double2(r.y.u, q.prefix_u));
+        st2r(s, 23, row, make_double2(q.suffix_u, 0.0));
     }
     if (q.n_lanes > 0) {
         double a, b;
         memcpy(&a, &q.lane_key, 8);
         memcpy(&b, &q.lane_ctr[0], 8);
-        st2(s, 20, i, a, b);
+        st2r(s, 20, row, make_double2(a, b));
         double2 t = make_double2(0, 0);
         memcpy(&t, &q.lane_ctr[4], 12);
-        st2(s, 21, i, t.x, t.y);
+        st2r(s, 21, row, t);
     }
 }
 

@@ -1122,10 +1122,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             c15 = make_double2(F.lsub.n.x, F.lsub.n.y);
             c16.x = F.lsub.n.z;
         }
-        __stcg(&o.base[15 * o.stride + k], c15);
-        __stcg(&o.base[16 * o.stride + k], c16);
-        for (int c = 17; c < (mt.nl > 0 ? 22 : 20); ++c)
-            __stcg(&o.base[size_t(c) * o.stride + k], ld2(st, c, jb.item));
+        st2r(o, 15, k, c15);
+        st2r(o, 16, k, c16);
+        {
+            const size_t sr = res_row(st, jb.item);
+            for (int c = 17; c < (mt.nl > 0 ? 22 : 20); ++c) st2r(o, c, k, ld2r(st, c, sr));
+        }
         if (VEL) {
             st2(o, 22, k, u_total, pre.u);
             st2(o, 23, k, mt.skind == SK_LIGHTSUB ? suf.u : ld2(st, 23, jb.item).x, 0.0);
@@ -1142,9 +1144,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 // unless the record has lanes
 __device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const ResStore& dst, size_t j, int from,
                                             int n_lanes, bool vel) {
+    const size_t ri = res_row(src, i), rj = res_row_w(dst, j);
     for (int c = from; c < (vel ? kResChunks : 22); ++c) {
         if ((c == 20 || c == 21) && n_lanes <= 0) continue;
-        __stcg(&dst.base[size_t(c) * dst.stride + j], ld2(src, c, i));
+        st2r(dst, c, rj, ld2r(src, c, ri));
     }
 }
 

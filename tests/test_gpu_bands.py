@@ -35,6 +35,10 @@ CASES = {
     "doppler_animated": (lambda: scenes.bundled("boxes_doppler", 40),
                          RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True,
                                       spatial_passes=1, spatial_neighbors=4, spatial_radius=6, frames=3)),
+    "transient_sparse": (lambda: scenes.bundled("cornell", 40),
+                         RenderConfig(mode=F.MODE_TRANSIENT, bins=24, hist_t0=8.0, hist_bin_width=0.5, m_init=2,
+                                      temporal=True, spatial_passes=2, spatial_neighbors=3, spatial_radius=4,
+                                      frames=3)),
     "moving_camera": (lambda: _moving_camera(40),
                       RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1, temporal=True,
                                    spatial_passes=1, spatial_neighbors=3, spatial_radius=4, frames=3)),

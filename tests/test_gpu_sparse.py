@@ -1,0 +1,99 @@
+"""Sparse transient reservoir grids (tofr_store.cuh): a dense header plane
+plus a pool of sample rows that only non-empty reservoirs hold.  The storage
+layout must not change a single bit of the output: every transient
+configuration (temporal, spatial, bin reuse, row bands with halo exchange,
+the per-item legacy kernels) renders identically with TOFR_SPARSE=0 (dense
+grids), the pool accounting is exact, and a full pool raises an error instead
+of corrupting reservoirs."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2605_11536_b200 import _ffi as F
+from paper_2605_11536_b200 import scenes
+from paper_2605_11536_b200.api import RenderConfig, Renderer, TofrError
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(**kw):
+    base = dict(mode=F.MODE_TRANSIENT, bins=48, hist_t0=8.0, hist_bin_width=0.25, m_init=2, frames=3,
+                temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=4.0, seed=3)
+    base.update(kw)
+    return RenderConfig(**base)
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        for k, v in self.kv.items():
+            os.environ[k] = v
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+CASES = {
+    "temporal_spatial": ("cornell", _cfg()),
+    "bin_reuse": ("cornell_wide", _cfg(hist_t0=3.0, bin_reuse=True, spatial_passes=2)),
+    "animated": ("boxes_doppler", _cfg(hist_t0=7.0, hist_bin_width=0.5, max_depth=8)),
+}
+
+
+def _render(scene, cfg, **env):
+    with _env(**env):
+        out = Renderer(0).render_transient(scenes.bundled(scene, 36), cfg)
+    return out
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_sparse_equals_dense(name):
+    scene, cfg = CASES[name]
+    dense = _render(scene, cfg, TOFR_SPARSE="0")
+    sparse = _render(scene, cfg, TOFR_SPARSE="1")
+    assert dense.hist.rgb.max() > 0
+    assert np.array_equal(sparse.hist.rgb, dense.hist.rgb)
+    assert np.array_equal(sparse.image, dense.image)
+    for a, b in zip(sparse.stats, dense.stats):
+        for stage in ("temporal", "spatial", "bin"):
+            da = {k: v for k, v in a[stage].items() if k != "seconds"}
+            db = {k: v for k, v in b[stage].items() if k != "seconds"}
+            assert da == db, stage
+
+
+def test_sparse_equals_dense_legacy_kernels():
+    scene, cfg = CASES["bin_reuse"]
+    dense = _render(scene, cfg, TOFR_SPARSE="0", TOFR_REUSE="legacy", TOFR_TRACE="legacy")
+    sparse = _render(scene, cfg, TOFR_SPARSE="1", TOFR_REUSE="legacy", TOFR_TRACE="legacy")
+    assert np.array_equal(sparse.hist.rgb, dense.hist.rgb)
+
+
+def test_pool_rows_count_nonempty_reservoirs():
+    """After a frame the current grid holds exactly one pool row per
+    reservoir that was ever non-empty in it: at least the non-empty ones."""
+    scene, cfg = "cornell", _cfg(spatial_passes=0)
+    with _env(TOFR_SPARSE="1"):
+        r = Renderer(0)
+        s = r.session(scenes.bundled(scene, 36), cfg)
+        for _ in range(3):
+            s.step(stats=False)
+        pool = s.pool()
+    assert pool["rows_cap"] > 0
+    assert max(pool["rows_used"]) > 0
+    assert max(pool["rows_used"]) <= pool["rows_cap"]
+
+
+def test_pool_overflow_raises():
+    scene, cfg = CASES["temporal_spatial"]
+    with pytest.raises(TofrError, match="pool"):
+        _render(scene, cfg, TOFR_SPARSE="1", TOFR_POOL_ROWS="16")
