@@ -86,9 +86,19 @@ WORKLOADS = {
             RenderConfig(mode=F.MODE_TRANSIENT, bins=1024, hist_t0=7.0, hist_bin_width=0.01953125, m_init=1,
                          max_depth=8, seed=1),
             "C4 (plain): boxes_doppler 1920x1080 transient 1024 bins [7,27), depth 8, trace + histogram deposits"),
+    "c4r": ("boxes_doppler", 1920, 1080,
+            RenderConfig(mode=F.MODE_TRANSIENT, bins=1024, hist_t0=7.0, hist_bin_width=0.01953125, m_init=1,
+                         max_depth=8, temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=10,
+                         m_cap=20, seed=1),
+            "C4 (reservoirs): boxes_doppler 1920x1080 transient 1024 bins [7,27), depth 8, render_transient "
+            "temporal + 1x3 spatial r10 per bin, row bands with reservoir halo exchange"),
 }
 
-PLAIN = {"c2p", "c4p"}  # render_transient_plain workloads; the others are ReSTIR sessions
+PLAIN = {"c2p", "c4p"}
+# workloads that do not fit one GPU whole: at N = 1 one GPU renders the band of
+# rank EMULATE_RANK of an EMULATE_WORLD-way split (per-GPU share of that job;
+# its halo rows arrive empty, no transfer), labelled in `config`
+BAND_ONLY = {"c4r": (8, 4)}  # render_transient_plain workloads; the others are ReSTIR sessions
 
 # Algorithmic HBM bytes per unit of work of each kernel (
 # R = 224 B compact reservoir).  Units are counted on the device
@@ -212,6 +222,10 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     scene_name, w, h, cfg, desc = WORKLOADS[args.workload]
+    if args.workload in BAND_ONLY:
+        print(json.dumps({"impl": "reference", "unavailable": "the reference's render_transient needs 1.3 TB of "
+                                                               "reservoirs per grid at this size (SURVEY 8d)"}))
+        return
     for _ in range(args.warmup):
         cpu_reference_sample(args.workload, 1)
     secs, frames, cores = 0.0, 0, 1
@@ -264,7 +278,13 @@ def run_ours(args) -> None:
     plain = args.workload in PLAIN
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
-    sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
+    emulated = None
+    if ws == 1 and args.workload in BAND_ONLY:
+        emulated = BAND_ONLY[args.workload]
+        sess = parallel.BandSession(r, sd, cfg, rank=emulated[1], world=emulated[0], group=None, plain=plain,
+                                    emulate=True)
+    else:
+        sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
     for _ in range(args.warmup):
         sess.step()
     sess.sync()
@@ -314,6 +334,11 @@ def run_ours(args) -> None:
     e2e_s = sess.run_e2e(args.steps)
     e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
     h2d, d2h = sess.io_bytes()
+    pool_info = None
+    if not plain and cfg.mode == F.MODE_TRANSIENT:
+        p = sess.sess.pool()
+        pool_info = {"rows_used_max": max(p["rows_used"]), "rows_cap": p["rows_cap"],
+                     "rows_per_owned_item": max(p["rows_used"]) / max(1, sess.owned_pixels() * cfg.bins)}
 
     # roofline of the dominant kernel: algorithmic bytes per launch / average
     # launch duration (CUDA events on the session stream, timed region above)
@@ -351,7 +376,11 @@ def run_ours(args) -> None:
     t_s = t_max * 1e-3
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload in BAND_ONLY:
+        cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
+               "sample": "not run: the reference's render_transient holds 2.12 G reservoirs of 624 B (1.3 TB per "
+                         "grid) at this size (SURVEY 8d)"}
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             c = cpu_reference_sample(args.workload, 2)
             cpu = {"value": c["frames"] / c["seconds"], "unit": "frames/s", "cores": c["cores"],
@@ -367,9 +396,12 @@ def run_ours(args) -> None:
             "warmup": args.warmup, "ms_per_step": t_max / frames, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "scene": scene_name, "resolution": f"{w}x{h}",
-                       "parallelism": f"rowband{ws}" if ws > 1 else "single",
+                       "parallelism": (f"rowband{emulated[0]}: the band of rank {emulated[1]} (rows "
+                                       f"{sess.y0}-{sess.y1} + {sess.halo}-row halos) on one GPU, halo rows "
+                                       f"not transferred; value = that band's frames/s"
+                                       if emulated else (f"rowband{ws}" if ws > 1 else "single")),
                        "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
-            "mpaths_per_s": w * h * cfg.m_init * fps / 1e6,
+            "mpaths_per_s": (sess.owned_pixels() if emulated else w * h) * cfg.m_init * fps / 1e6,
             "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},
             "shift_stats_one_frame": shift_stats,
             "frame_latency": latency,
@@ -383,6 +415,7 @@ def run_ours(args) -> None:
                          "note": "FP64 latency/divergence-bound shift and trace kernels: HBM fraction is small "
                                  "by construction (SURVEY 8d); see rays_per_s and kernel_ms"},
             "kernel_ms_per_step": kernel_ms,
+            "reservoir_pool": pool_info,
             "rays_per_s": rays / t_s if t_s > 0 else None,
             "shift_jobs_per_s": work.get("shift_jobs", 0) / t_s if (t_s > 0 and work) else None,
             "cpu_baseline": cpu,

@@ -183,6 +183,8 @@ struct tofr_session {
     // handed out per grid ([3] u32), pool rows per grid (+2 reserved rows)
     bool sparse = false;
     size_t pool_rows = 0;
+    unsigned int* occ_host = nullptr;  // pinned [2][3]: pool rows per grid at the end of a frame
+    size_t occ_seen = 0;               // largest of them over the frames flushed so far
     DevBuf res_slot[3], res_rows;
     DevBuf image, accum, hist, hist_count;  // owned rows only
     DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag + work counter
@@ -238,6 +240,7 @@ struct tofr_session {
         for (auto& e : read_ev)
             if (e) cudaEventDestroy(e);
         if (err_host) cudaFreeHost(err_host);
+        if (occ_host) cudaFreeHost(occ_host);
         release_buffers();
         if (ctx && --ctx->live_sessions == 0 && ctx->closing) release_ctx(ctx);
     }
@@ -275,6 +278,38 @@ ResStore store_of(const tofr_session* s, const DevBuf& b) {
 
 // a sparse grid about to be rewritten (new frame's init, spatial / bin-reuse
 // output): every reservoir loses its pool row
+// Row batches of a wavefront reuse stage: the shift queue holds wv_cap jobs and
+// a stage makes at most `per` jobs per item, so batches of at most
+// wv_cap / per items can never overflow it (exact, no occupancy estimate; a
+// transient grid whose worst case exceeds the queue pays one queue fill per
+// batch).
+int wave_batches(const tofr_session* s, size_t per) {
+    size_t items = s->owned_pixels() * s->B;
+    size_t rows = size_t(s->y1 - s->y0);
+    size_t per_row = items / std::max<size_t>(1, rows);
+    size_t rows_fit = s->wv_cap / std::max<size_t>(1, per * per_row);
+    if (rows_fit == 0) throw ScopeError(TOFR_ERR_OOM, "reuse shift queue smaller than one image row (raise TOFR_WAVE_CAP)");
+    return int((rows + rows_fit - 1) / rows_fit);
+}
+template <class Fn>
+void for_row_batches(const Band& bd, int nb, Fn&& fn) {
+    int rows = (bd.y1 - bd.y0 + nb - 1) / nb;  // <= rows_fit of wave_batches
+    for (int y = bd.y0; y < bd.y1; y += rows) {
+        Band sb = bd;
+        sb.y0 = y;
+        sb.y1 = std::min(bd.y1, y + rows);
+        fn(sb);
+    }
+}
+
+// payload rows a compacted (sparse) halo of n items carries: the pool's share
+size_t halo_cap(const tofr_session* s, size_t n) {
+    if (!s->sparse || !n) return 0;
+    double frac = double(s->pool_rows) / double(std::max<size_t>(1, s->items_stored()));
+    size_t cap = size_t(double(n) * frac) + 4096;
+    return std::min(n, cap);
+}
+
 void reset_store(tofr_session* s, int k, cudaStream_t st) {
     if (!s->sparse) return;
     ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, s->items_stored() * sizeof(uint32_t), st), "memset");
@@ -415,16 +450,22 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         size_t rb = items * kResChunks * 16;
         {
             // transient grids are mostly empty reservoirs: header plane + a pool
-            // of sample rows (TOFR_SPARSE=0: dense).  Pool = TOFR_POOL_FRAC of
-            // the items (default 0.25), or all of them while that is small.
+            // of sample rows (TOFR_SPARSE=0: dense).  Pool rows per grid: one per
+            // item while the three pools fit in 55% of the free memory, else what
+            // fits (TOFR_POOL_FRAC: that fraction of the items instead).
             const char* sp = std::getenv("TOFR_SPARSE");
             s->sparse = s->transient && !(sp && sp[0] == '0');
             if (s->sparse) {
-                double frac = 0.25;
-                if (const char* pf = std::getenv("TOFR_POOL_FRAC")) frac = std::atof(pf);
-                size_t rows = size_t(double(items) * frac) + 1;
-                const size_t small = (size_t(2) << 30) / ((kResChunks - 1) * 16);
-                if (rows < small) rows = small;
+                const size_t row_bytes = (kResChunks - 1) * 16;
+                size_t rows = items;
+                size_t fr = 0, tot = 0;
+                if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+                    size_t ngrid = (s->has_bin || s->has_spatial) ? 3 : 2;
+                    size_t fit = size_t(double(fr) * 0.55) / ngrid;
+                    fit = fit > items * 20 ? (fit - items * 20) / row_bytes : 0;
+                    rows = std::min(rows, std::max<size_t>(fit, 1024));
+                }
+                if (const char* pf = std::getenv("TOFR_POOL_FRAC")) rows = size_t(double(items) * std::atof(pf)) + 1;
                 if (rows > items) rows = items;
                 if (const char* pr = std::getenv("TOFR_POOL_ROWS")) rows = size_t(std::strtoull(pr, nullptr, 10));
                 if (rows > 0xfffffff0ull) rows = 0xfffffff0ull;
@@ -435,6 +476,8 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                         s->res_slot[k].ensure(items * sizeof(uint32_t));
                         ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, items * sizeof(uint32_t), ctx->stream), "memset");
                     }
+                ck(cudaMallocHost(reinterpret_cast<void**>(&s->occ_host), 6 * sizeof(unsigned int)), "pinned");
+                std::memset(s->occ_host, 0, 6 * sizeof(unsigned int));
                 s->res_rows.ensure(4 * sizeof(unsigned int));
                 ck(cudaMemsetAsync(s->res_rows.p, 0, 4 * sizeof(unsigned int), ctx->stream), "memset");
             }
@@ -457,7 +500,15 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             if (s->wave) {
                 size_t per = wave_jobs_per_item(s->has_spatial ? cfg->spatial_neighbors : 0);
                 size_t cap = per * own_items;
+                // 64 M jobs (38 GB) when a quarter of the free memory holds them, else 32 M;
+                // larger stages run in row batches (wave_batches)
                 size_t limit = size_t(32) << 20;
+                {
+                    size_t fr = 0, tot = 0;
+                    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
+                        fr / 4 > (size_t(64) << 20) * (kJobChunks + kResChunks) * 16)
+                        limit = size_t(64) << 20;
+                }
                 if (const char* cl = std::getenv("TOFR_WAVE_CAP")) limit = size_t(std::strtoull(cl, nullptr, 10));
                 if (cap > limit) cap = limit;
                 if (cap > 0xfffffff0ull) cap = 0xfffffff0ull;
@@ -507,8 +558,11 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             ck(cudaMemsetAsync(s->accum.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
             ck(cudaMemsetAsync(s->image.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
         }
-        size_t per_row = size_t(s->W) * s->B * kResChunks * 16;
-        size_t lo = size_t(s->y0 - s->r0) * per_row, hi = size_t(s->r1 - s->y1) * per_row;
+        size_t per_row_items = size_t(s->W) * s->B;
+        size_t lo = halo_bytes(size_t(s->y0 - s->r0) * per_row_items, halo_cap(s.get(), size_t(s->y0 - s->r0) * per_row_items),
+                               s->sparse);
+        size_t hi = halo_bytes(size_t(s->r1 - s->y1) * per_row_items, halo_cap(s.get(), size_t(s->r1 - s->y1) * per_row_items),
+                               s->sparse);
         if (lo) {
             s->send_lo.ensure(lo);
             s->recv_lo.ensure(lo);
@@ -553,6 +607,8 @@ void flush_set(tofr_session* s, int set) {
         s->stage_tot[i] += ms[i];
     }
     s->tot_frames++;
+    if (s->sparse)
+        for (int k = 0; k < 3; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[3 * set + k]);
     if (s->err_host[set] & kErrPool)
         throw ScopeError(TOFR_ERR_OOM,
                          "transient reservoir pool full: more non-empty reservoirs than TOFR_POOL_FRAC of the grid "
@@ -582,13 +638,13 @@ void exchange_halo(tofr_session* s, ResStore g, int pass) {
     cudaStream_t st = s->ctx->stream;
     size_t per_row = size_t(s->W) * s->B;
     size_t lo = size_t(s->y0 - s->r0) * per_row, hi = size_t(s->r1 - s->y1) * per_row;
-    launch_halo_pack(g, size_t(s->y0) * per_row, lo, s->send_lo.as<double2>(), st);
-    launch_halo_pack(g, size_t(s->y1) * per_row - hi, hi, s->send_hi.as<double2>(), st);
+    launch_halo_pack(g, size_t(s->y0) * per_row, lo, s->send_lo.as<double2>(), halo_cap(s, lo), st);
+    launch_halo_pack(g, size_t(s->y1) * per_row - hi, hi, s->send_hi.as<double2>(), halo_cap(s, hi), st);
     ck(cudaGetLastError(), "halo pack");
     int rc = s->xfn(s->xuser, pass);
     if (rc != 0) throw ScopeError(TOFR_ERR_CUDA, "halo exchange callback failed");
-    launch_halo_unpack(g, size_t(s->r0) * per_row, lo, s->recv_lo.as<double2>(), st);
-    launch_halo_unpack(g, size_t(s->y1) * per_row, hi, s->recv_hi.as<double2>(), st);
+    launch_halo_unpack(g, size_t(s->r0) * per_row, lo, s->recv_lo.as<double2>(), halo_cap(s, lo), st);
+    launch_halo_unpack(g, size_t(s->y1) * per_row, hi, s->recv_hi.as<double2>(), halo_cap(s, hi), st);
     ck(cudaGetLastError(), "halo unpack");
     s->halo_exchanges++;
 }
@@ -679,8 +735,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
             if (s->wave)
-                launch_temporal_wave(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur,
-                                     store_of(s, s->res[s->prev]), wv, ctr + 0 * SC_COUNT, q, stream);
+                for_row_batches(bd, wave_batches(s, 2), [&](const Band& sb) {
+                    launch_temporal_wave(F, sb, g, s->slot[psl].view, gp, pc, cg, pg, f, cur,
+                                         store_of(s, s->res[s->prev]), wv, ctr + 0 * SC_COUNT, q, stream);
+                });
             else
                 launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
                                 wo, ctr + 0 * SC_COUNT, q, stream);
@@ -710,8 +768,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                 scp = &scr;
             }
             if (s->wave && sp.neighbors > 0 && sp.radius > 0)
-                launch_spatial_wave(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wv,
-                                    ctr + 1 * SC_COUNT, q, stream);
+                for_row_batches(bd, wave_batches(s, wave_jobs_per_item(sp.neighbors)), [&](const Band& sb) {
+                    launch_spatial_wave(F, sb, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wv,
+                                        ctr + 1 * SC_COUNT, q, stream);
+                });
             else
                 launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
                                ctr + 1 * SC_COUNT, q, stream);
@@ -734,6 +794,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     ck(cudaMemcpyAsync(&s->err_host[set], ctr + 3 * SC_COUNT, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        stream),
        "flag");
+    if (s->sparse)
+        ck(cudaMemcpyAsync(s->occ_host + 3 * set, s->res_rows.p, 3 * sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                           stream),
+           "occupancy");
     cudaEventRecord(ev[6], stream);
     ck(cudaGetLastError(), "kernel launch");
     s->pending[set] = true;

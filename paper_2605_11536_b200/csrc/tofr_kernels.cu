@@ -1005,28 +1005,76 @@ __global__ void k_halo_pack(ResStore grid, size_t item0, size_t n, double2* buf)
     size_t total = n * kResChunks;
     for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
         size_t c = j / n, i = j % n;
-        // sparse stores: the sample chunks of an empty reservoir are never read (zeros go out)
-        bool live = c == 0 || grid.slot == nullptr || ld2(grid, 0, item0 + i).x > 0;
-        buf[j] = live ? ld2(grid, int(c), item0 + i) : make_double2(0.0, 0.0);
+        buf[j] = __ldcg(&grid.base[c * grid.stride + item0 + i]);
     }
-}
-
-// sparse stores: pool rows for the non-empty reservoirs that arrive (one
-// thread per item, before the chunk-parallel copy)
-__global__ void k_halo_alloc(ResStore grid, size_t item0, size_t n, const double2* buf) {
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-        if (__ldcg(&buf[i]).x > 0) res_row_w(grid, item0 + i);
 }
 
 __global__ void k_halo_unpack(ResStore grid, size_t item0, size_t n, const double2* buf) {
     size_t total = n * kResChunks;
     for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < total; j += size_t(gridDim.x) * blockDim.x) {
         size_t c = j / n, i = j % n;
-        double2 v = __ldcg(&buf[j]);
-        if (c == 0)
-            __stcg(&grid.base[item0 + i], v);
-        else if (grid.slot == nullptr || __ldcg(&buf[i]).x > 0)
-            st2r(grid, int(c), res_row(grid, item0 + i), v);
+        __stcg(&grid.base[c * grid.stride + item0 + i], __ldcg(&buf[j]));
+    }
+}
+
+// Sparse grids travel compacted (HaloLayout): the dense header plane of the
+// halo rows, then only the non-empty reservoirs' sample rows with their item
+// offsets.  Rows are handed out warp-aggregated so consecutive lanes write
+// consecutive payload rows (coalesced chunk planes).
+struct HaloLayout {
+    unsigned int* count;  // payload rows
+    double2* hdr;         // n headers
+    uint32_t* idx;        // cap item offsets
+    double2* pl;          // chunk c (1..23) of payload row r at pl[(c - 1) * cap + r]
+    size_t cap;
+};
+__device__ __forceinline__ HaloLayout halo_layout(double2* buf, size_t n, size_t cap) {
+    HaloLayout h;
+    h.count = reinterpret_cast<unsigned int*>(buf);
+    h.hdr = buf + 1;
+    h.idx = reinterpret_cast<uint32_t*>(buf + 1 + n);
+    h.pl = buf + 1 + n + (cap * 4 + 15) / 16;
+    h.cap = cap;
+    return h;
+}
+
+__global__ void k_halo_pack_sparse(ResStore grid, size_t item0, size_t n, double2* buf, size_t cap) {
+    HaloLayout h = halo_layout(buf, n, cap);
+    const int lane = threadIdx.x & 31;
+    size_t n_round = (n + 31) / 32 * 32;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += size_t(gridDim.x) * blockDim.x) {
+        bool live = i < n;
+        double2 c0 = live ? __ldcg(&grid.base[item0 + i]) : make_double2(0.0, 0.0);
+        if (live) __stcg(&h.hdr[i], c0);
+        bool ne = live && c0.x > 0;
+        unsigned m = __ballot_sync(0xffffffffu, ne);
+        unsigned r0 = 0;
+        if (m && lane == __ffs(m) - 1) r0 = atomicAdd(h.count, unsigned(__popc(m)));
+        r0 = __shfl_sync(0xffffffffu, r0, __ffs(m ? m : 1u) - 1);
+        if (!ne) continue;
+        size_t r = r0 + __popc(m & ((1u << lane) - 1));
+        if (r >= cap) {
+            atomicOr(grid.err, kErrPool);
+            continue;
+        }
+        __stcg(&h.idx[r], uint32_t(i));
+        const size_t row = res_row(grid, item0 + i);
+        for (int c = 1; c < kResChunks; ++c) __stcg(&h.pl[size_t(c - 1) * cap + r], ld2r(grid, c, row));
+    }
+}
+
+__global__ void k_halo_unpack_hdr(ResStore grid, size_t item0, size_t n, const double2* buf, size_t cap) {
+    HaloLayout h = halo_layout(const_cast<double2*>(buf), n, cap);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        __stcg(&grid.base[item0 + i], __ldcg(&h.hdr[i]));
+}
+
+__global__ void k_halo_unpack_rows(ResStore grid, size_t item0, size_t n, const double2* buf, size_t cap) {
+    HaloLayout h = halo_layout(const_cast<double2*>(buf), n, cap);
+    size_t cnt = min(size_t(__ldcg(h.count)), cap);
+    for (size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x; r < cnt; r += size_t(gridDim.x) * blockDim.x) {
+        const size_t row = res_row_w(grid, item0 + __ldcg(&h.idx[r]));
+        for (int c = 1; c < kResChunks; ++c) st2r(grid, c, row, __ldcg(&h.pl[size_t(c - 1) * cap + r]));
     }
 }
 
@@ -1274,24 +1322,37 @@ void launch_hist_image(const double* hist, const Band& bd, int W, int B, double 
     }
 }
 
-void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s) {
-    if (!n_items) return;
-    {
-        KScope ks("k_halo_pack", s);
-        k_halo_pack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
-    }
+size_t halo_bytes(size_t n_items, size_t cap, bool sparse) {
+    if (!n_items) return 0;
+    if (!sparse) return n_items * kResChunks * 16;
+    return 16 + n_items * 16 + (cap * 4 + 15) / 16 * 16 + (kResChunks - 1) * cap * 16;
 }
 
-void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s) {
+void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, size_t cap, cudaStream_t s) {
     if (!n_items) return;
-    {
-        if (grid.slot) {
-            KScope ka("k_halo_alloc", s);
-            k_halo_alloc<<<grid_for(n_items, 256), 256, 0, s>>>(grid, item0, n_items, buf);
-        }
-        KScope ks("k_halo_unpack", s);
-        k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+    if (grid.slot) {
+        cudaMemsetAsync(buf, 0, 16, s);
+        KScope ks("k_halo_pack_sparse", s);
+        k_halo_pack_sparse<<<grid_for(n_items, 256), 256, 0, s>>>(grid, item0, n_items, buf, cap);
+        return;
     }
+    KScope ks("k_halo_pack", s);
+    k_halo_pack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
+}
+void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, size_t cap,
+                        cudaStream_t s) {
+    if (!n_items) return;
+    if (grid.slot) {
+        {
+            KScope ks("k_halo_unpack_hdr", s);
+            k_halo_unpack_hdr<<<grid_for(n_items, 256), 256, 0, s>>>(grid, item0, n_items, buf, cap);
+        }
+        KScope ks("k_halo_unpack_rows", s);
+        k_halo_unpack_rows<<<grid_for(cap, 256), 256, 0, s>>>(grid, item0, n_items, buf, cap);
+        return;
+    }
+    KScope ks("k_halo_unpack", s);
+    k_halo_unpack<<<grid_for(n_items * kResChunks, 256), 256, 0, s>>>(grid, item0, n_items, buf);
 }
 
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,

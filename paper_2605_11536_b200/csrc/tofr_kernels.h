@@ -167,8 +167,12 @@ void launch_hist_image(const double* hist, const Band& bd, int W, int B, double 
                        cudaStream_t s);
 // halo staging: rows [a, b) of a global-indexed grid <-> a contiguous buffer
 // laid out chunk-major ([kResChunks][(b - a) * W * B] x 16 B)
-void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, cudaStream_t s);
-void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, cudaStream_t s);
+// halo rows of a grid: dense grids as n_items x 24 chunks; sparse grids
+// compacted (headers + the non-empty reservoirs' rows, at most `cap` of them)
+size_t halo_bytes(size_t n_items, size_t cap, bool sparse);
+void launch_halo_pack(ResStore grid, size_t item0, size_t n_items, double2* buf, size_t cap, cudaStream_t s);
+void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const double2* buf, size_t cap,
+                        cudaStream_t s);
 void launch_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s);
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
                        cudaStream_t s);

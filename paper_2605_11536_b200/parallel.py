@@ -153,7 +153,11 @@ def _wrap(ptr: int, nbytes: int, device):
 class BandSession:
     """A session rendering one row band of every frame (the whole frame when world == 1)."""
 
-    def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None, plain: bool = False):
+    def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None, plain: bool = False,
+                 emulate: bool = False):
+        """emulate: render band `rank` of a `world`-way split alone (no process
+        group): the halo exchange is a no-op, so halo rows hold empty
+        reservoirs -- the per-GPU work of that split, for one-GPU measurement."""
         import torch
         self.r = renderer
         self.cfg = cfg
@@ -164,11 +168,14 @@ class BandSession:
         halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if (world > 1 and not plain) else 0
         if world > 1 and min(band_rows(H, world, g)[1] - band_rows(H, world, g)[0] for g in range(world)) < halo:
             raise ValueError(f"{world} bands of a {H}-row image are thinner than the {halo}-row halo")
+        self.halo = halo
         self.sess = renderer.session(scene_def, cfg, band=(self.y0, self.y1, halo), plain=plain)
         self.W, self.H = self.sess.width, self.sess.height
         self.stream = torch.cuda.ExternalStream(self.sess.stream_ptr())
         self.exchanger = None
-        if world > 1 and halo > 0:
+        if emulate and halo > 0:
+            self.sess.set_halo_exchange(lambda pass_: None)
+        elif world > 1 and halo > 0:
             hb = self.sess.halo_buffers()
             dev = torch.device("cuda", torch.cuda.current_device())
             self.exchanger = HaloExchanger(rank, world, group, _wrap(hb["send_lo"], hb["bytes_lo"], dev),

@@ -97,3 +97,32 @@ def test_pool_overflow_raises():
     scene, cfg = CASES["temporal_spatial"]
     with pytest.raises(TofrError, match="pool"):
         _render(scene, cfg, TOFR_SPARSE="1", TOFR_POOL_ROWS="16")
+
+
+# ---------------------------------------------------------------------------
+# row batches: a reuse stage whose shifts exceed the job queue runs over row
+# ranges of the band, one queue fill each (capi.cpp wave_batches).  Items are
+# independent within a stage, so batching must not change a bit.
+
+def test_gated_row_batches_equal_one_batch():
+    from paper_2605_11536_b200.api import GateSpec
+    sd = scenes.bundled("cornell", 48)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=2, temporal=True, spatial_passes=2,
+                       spatial_neighbors=3, spatial_radius=5, frames=3, seed=5)
+    one = Renderer(0).render_gated(sd, cfg)
+    with _env(TOFR_WAVE_CAP="1500"):  # 4 jobs x 2304 items -> 7 batches
+        many = Renderer(0).render_gated(sd, cfg)
+    assert one.image.max() > 0
+    assert np.array_equal(many.image, one.image)
+    for a, b in zip(many.stats, one.stats):
+        for stage in ("temporal", "spatial"):
+            assert {k: v for k, v in a[stage].items() if k != "seconds"} == \
+                   {k: v for k, v in b[stage].items() if k != "seconds"}
+
+
+def test_transient_row_batches_equal_one_batch():
+    scene, cfg = CASES["temporal_spatial"]
+    cfg = RenderConfig(**{**cfg.__dict__, "frames": 5})
+    one = _render(scene, cfg, TOFR_SPARSE="1")
+    many = _render(scene, cfg, TOFR_SPARSE="1", TOFR_WAVE_CAP="20000")
+    assert np.array_equal(many.hist.rgb, one.hist.rgb)
