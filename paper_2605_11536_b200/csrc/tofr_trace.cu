@@ -43,6 +43,12 @@ namespace tofr_b200 {
 // ---------------------------------------------------------------------------
 // sinks
 
+// gated grids are never sparse: a store view the compiler knows is dense
+__device__ __forceinline__ ResStore dense(ResStore s) {
+    s.slot = nullptr;
+    return s;
+}
+
 // RIS into the pixel's gated reservoir; the winning sample's record is written
 // to the grid when it wins, chunk 0 (W, M) when the pixel is done.
 // VEL: velocity (Doppler) gate, the gated quantity is the path velocity u
@@ -82,14 +88,14 @@ struct GatedSink {
             r.y.u = c.u;
             r.y.depth = c.depth;
             build_record<VEL>(F, rs, r.y.rec);
-            res_store(cur, item, r, VEL);
+            res_store(dense(cur), item, r, VEL);
             has = 1;
             phat = p;
         }
     }
     __device__ void end() {
         double W = (has && phat > 0) ? w_sum / phat : 0;
-        res_store_w(cur, item, W, 1.0);
+        res_store_w(dense(cur), item, W, 1.0);
     }
     __device__ void flush(unsigned long long*) {}
 };

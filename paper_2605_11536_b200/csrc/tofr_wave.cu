@@ -665,10 +665,14 @@ __global__ void __launch_bounds__(128)
 // ---------------------------------------------------------------------------
 // solve: checks, prefix, suffix, Newton (newton_solve, shiftmap.hpp:314-378)
 
-template <bool VEL>
+// SP: the grids may be sparse (transient); !SP instantiations (gated grids)
+// see slot == nullptr at compile time and drop the slot-map branches.
+template <bool VEL, bool SP>
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     k_shift_solve(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                   ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
+    if (!SP) st0.slot = st1.slot = nullptr;
+    q.out.slot = nullptr;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ FrameView sF[2];
     stage_two(F0, F1, sF, smem);
@@ -972,10 +976,12 @@ __device__ __forceinline__ bool occluded_n(const FrameView& F, const V3& a, cons
 
 __device__ __forceinline__ void out_fail(const ShiftQueue& q, uint32_t k) { st2(q.out, 0, k, 0.0, 0.0); }
 
-template <bool VEL>
+template <bool VEL, bool SP>
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     k_shift_finish(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                    ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
+    if (!SP) st0.slot = st1.slot = nullptr;
+    q.out.slot = nullptr;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ FrameView sF[2];
     stage_two(F0, F1, sF, smem);
@@ -1477,8 +1483,11 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
         }
     }
     // length-gate and velocity-gate (Doppler) instantiations
-    auto solve = cfg.gate_vel ? k_shift_solve<true> : k_shift_solve<false>;
-    auto finish = cfg.gate_vel ? k_shift_finish<true> : k_shift_finish<false>;
+    // velocity gates are gated-only (dense grids)
+    const bool sp = st0.slot != nullptr || st1.slot != nullptr;
+    auto solve = cfg.gate_vel ? k_shift_solve<true, false> : (sp ? k_shift_solve<false, true> : k_shift_solve<false, false>);
+    auto finish = cfg.gate_vel ? k_shift_finish<true, false>
+                               : (sp ? k_shift_finish<false, true> : k_shift_finish<false, false>);
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_solve", s);
