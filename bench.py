@@ -278,13 +278,15 @@ def run_ours(args) -> None:
     plain = args.workload in PLAIN
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
-    emulated = None
-    if ws == 1 and args.workload in BAND_ONLY:
-        emulated = BAND_ONLY[args.workload]
-        sess = parallel.BandSession(r, sd, cfg, rank=emulated[1], world=emulated[0], group=None, plain=plain,
-                                    emulate=True)
-    else:
-        sess = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
+    emulated = BAND_ONLY[args.workload] if (ws == 1 and args.workload in BAND_ONLY) else None
+
+    def new_session():
+        if emulated:
+            return parallel.BandSession(r, sd, cfg, rank=emulated[1], world=emulated[0], group=None, plain=plain,
+                                        emulate=True)
+        return parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
+
+    sess = new_session()
     for _ in range(args.warmup):
         sess.step()
     sess.sync()
@@ -329,22 +331,30 @@ def run_ours(args) -> None:
         latency = {"frames": len(lat), "p50_ms": float(np.percentile(lat_all, 50)),
                    "p99_ms": float(np.percentile(lat_all, 99)), "max_ms": float(np.max(lat_all))}
 
-    # e2e through the public API: step + image read-back to pinned host memory
-    parallel.barrier(group)
-    e2e_s = sess.run_e2e(args.steps)
-    e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
-    h2d, d2h = sess.io_bytes()
     pool_info = None
     if not plain and cfg.mode == F.MODE_TRANSIENT:
         p = sess.sess.pool()
         pool_info = {"rows_used_max": max(p["rows_used"]), "rows_cap": p["rows_cap"],
                      "rows_per_owned_item": max(p["rows_used"]) / max(1, sess.owned_pixels() * cfg.bins)}
 
+    # e2e through the public API: step + image read-back to pinned host memory,
+    # on a fresh session over the same frames as the device-timed run (W warm-up
+    # frames, then K): transient reservoir grids fill up frame by frame, so
+    # later frames cost more and would not compare
+    band_px = sess.owned_pixels()
+    sess.sess.close()
+    sess = new_session()
+    for _ in range(args.warmup):
+        sess.step()
+    parallel.barrier(group)
+    e2e_s = sess.run_e2e(args.steps)
+    e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
+    h2d, d2h = sess.io_bytes()
+
     # roofline of the dominant kernel: algorithmic bytes per launch / average
     # launch duration (CUDA events on the session stream, timed region above)
     avg = [x / args.steps for x in stage_tot]
     names = ["init", "temporal", "bin", "spatial", "shade"]
-    band_px = sess.owned_pixels()
     items = band_px * (cfg.bins if cfg.mode == F.MODE_TRANSIENT or plain else 1)
     dom = max(ktimes, key=lambda k: ktimes[k][0]) if ktimes else None
     work = {k: work1[k] - work0[k] for k in work1} if work1 else {}

@@ -444,11 +444,15 @@ class Session:
         import torch
         torch.cuda.ExternalStream(self.stream_ptr()).synchronize()
 
+    def close(self) -> None:
+        """Free the session's device memory now (waits for its frames)."""
+        if self.handle:
+            self._r._lib.tofr_gpu_session_destroy(self.handle)
+            self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                self._r._lib.tofr_gpu_session_destroy(self.handle)
-                self.handle = None
+            self.close()
         except Exception:
             pass
 

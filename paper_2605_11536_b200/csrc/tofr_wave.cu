@@ -573,18 +573,6 @@ struct StartTerms {
     M2 Hs;      // projected Hessian at the start point (gauge != FIXED)
 };
 
-template <bool VEL>
-__device__ __forceinline__ StartTerms start_terms(const FrameView& F, int obj, const VelField& vf, const V3& p1,
-                                                  const V3& p2, const V3& ps, const Frame2& Js, int gauge) {
-    StartTerms t;
-    LcEval e = field_eval<VEL>(F, obj, vf, p1, p2, ps, Js, gauge != GAUGE_FIXED);
-    t.g3s = e.grad;
-    t.gs = to_local(Js, e.grad);
-    t.lvs = e.val;
-    t.Hs = e.hess;
-    return t;
-}
-
 struct TrialEval {
     V2 F;
     M2 dFp;
@@ -592,12 +580,10 @@ struct TrialEval {
     double ngrad;    // |grad_cur|
 };
 
-template <bool VEL>
-__device__ __forceinline__ TrialEval trial_eval(const FrameView& F, int obj, const VelField& vf, const V3& p1,
-                                                const V3& p2, const V3& ps, const Frame2& Js, const StartTerms& st,
+// the trial half given the field evaluation e at the trial point pc
+__device__ __forceinline__ TrialEval trial_from(const LcEval& e, const V3& ps, const Frame2& Js, const StartTerms& st,
                                                 const V3& pc, const Frame2& Jc, double delta, int gauge) {
     TrialEval r;
-    LcEval e = field_eval<VEL>(F, obj, vf, p1, p2, pc, Jc, gauge != GAUGE_FIXED);
     V2 gc = to_local(Jc, e.grad);
     r.ngrad = norm(gc);
     V3 disp = pc - ps;
@@ -628,6 +614,17 @@ __device__ __forceinline__ TrialEval trial_eval(const FrameView& F, int obj, con
     r.dFp = M2{gc.x, gc.y, row_c.x, row_c.y};
     r.det_dF = det(M2{-st.gs.x, -st.gs.y, -row_s.x, -row_s.y});
     return r;
+}
+
+// Trial 0 evaluates the start point itself, which is where the start-point
+// terms come from (gradient, length and projected Hessian at the start point:
+// the same field evaluation), so one evaluation serves both: the start terms
+// are taken from it and the trial continues from it.
+__device__ __forceinline__ void start_from(const LcEval& e, const Frame2& Js, StartTerms& t) {
+    t.g3s = e.grad;
+    t.gs = to_local(Js, e.grad);
+    t.lvs = e.val;
+    t.Hs = e.hess;
 }
 
 // ---------------------------------------------------------------------------
@@ -763,8 +760,9 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             tol = 0.01 * jb.dw;
                             if (count) SCTR(SC_SOLVES, 1);
                             Js = tangent_frame(F, stri);
-                            stt = start_terms<VEL>(F, F.tri[stri].obj, vf, p1, p2, spos, Js, cfg.gauge);
-                            delta = target_local - stt.lvs;  // field value at the start point
+                            // start terms and delta = target - (field at the start
+                            // point) come with trial 0 (start_from)
+                            delta = target_local;
                             // trial 0 evaluates the start point itself
                             cpos = spos;
                             ctri = stri;
@@ -879,7 +877,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         // for trial 0): recompute only after a re-projection ray changed it
         Frame2 Jt = init ? Js : Jc;
         if (!init && ttri != ctri) Jt = tangent_frame(F, ttri);
-        TrialEval et = trial_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
+        LcEval ev = field_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, tpos, Jt, cfg.gauge != GAUGE_FIXED);
+        if (init) {
+            start_from(ev, Js, stt);
+            delta = delta - stt.lvs;  // field value at the start point
+        }
+        TrialEval et = trial_from(ev, spos, Js, stt, tpos, Jt, delta, cfg.gauge);
         double fn = hypot(et.F.x, et.F.y);
         bool accept = have && (init || fn < fnorm);
         if (tail) {
