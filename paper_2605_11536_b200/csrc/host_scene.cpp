@@ -726,6 +726,11 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
         info[i].leaf = f.leaf_of[i];
     }
     for (int j = 0; j < nt; ++j) info[f.tri_order[j]].leaf_slot = j;
+    std::vector<Frame2> tframe(nt);
+    for (int i = 0; i < nt; ++i) {
+        const HTri& t = f.tris[i];
+        tframe[i] = tangent_frame_of(t.n, t.v1 - t.v0, t.v2 - t.v0);
+    }
     std::vector<GMat> mats = device_materials(s);
 
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -744,7 +749,10 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
     off = align(off + mats.size() * sizeof(GMat));
     p.off_vel = off;
     off = align(off + f.obj_vel.size() * sizeof(GVel));
+    p.off_tframe = off;
+    off = align(off + nt * sizeof(Frame2));
     p.blob.assign(off, 0);
+    std::memcpy(p.blob.data() + p.off_tframe, tframe.data(), nt * sizeof(Frame2));
     std::memcpy(p.blob.data() + p.off_nodes, nodes.data(), nn * sizeof(GNode));
     std::memcpy(p.blob.data() + p.off_aux, aux.data(), nn * sizeof(GNodeAux));
     std::memcpy(p.blob.data() + p.off_isect, isect.data(), nt * sizeof(GTriIsect));
@@ -779,6 +787,7 @@ FrameView rebase_view(const PackedFrame& p, const unsigned char* base) {
     v.tri = reinterpret_cast<const GTriInfo*>(base + p.off_tri);
     v.mats = reinterpret_cast<const GMat*>(base + p.off_mats);
     v.vel = reinterpret_cast<const GVel*>(base + p.off_vel);
+    v.tframe = reinterpret_cast<const Frame2*>(base + p.off_tframe);
     return v;
 }
 

@@ -107,7 +107,8 @@ struct HNode {
 // back to back in one allocation so a frame upload is a single copy.
 struct PackedFrame {
     std::vector<unsigned char> blob;
-    size_t off_nodes = 0, off_aux = 0, off_isect = 0, off_tri_id = 0, off_tri = 0, off_mats = 0, off_vel = 0;
+    size_t off_nodes = 0, off_aux = 0, off_isect = 0, off_tri_id = 0, off_tri = 0, off_mats = 0, off_vel = 0,
+           off_tframe = 0;
     FrameView view;  // pointers are offsets until rebased
 };
 

@@ -106,6 +106,7 @@ struct FrameView {
     int frame_id;  // identity of the snapshot (Domain::frame pointer compare)
     int n_obj;
     const GVel* vel;  // per object (n_obj)
+    const Frame2* tframe;  // tangent_frame per triangle id
     V3 cam_vel;       // central difference of the camera track (scene.hpp:508-513)
 };
 

@@ -136,21 +136,8 @@ __device__ __forceinline__ const GTriIsect& tri_geo(const FrameView& F, int id) 
     return F.tri_isect[F.tri[id].leaf_slot];
 }
 
-// tangent_frame (geometry.hpp:51-63)
-__device__ inline Frame2 tangent_frame(const FrameView& F, int id) {
-    const GTriIsect& g = tri_geo(F, id);
-    V3 n = F.tri[id].n;
-    V3 e = g.e1;
-    V3 t = e - n * dot(n, e);
-    double l = norm(t);
-    if (l < 1e-12) {
-        e = g.e2;
-        t = e - n * dot(n, e);
-        l = norm(t);
-    }
-    t = t / l;
-    return Frame2{t, cross(n, t)};
-}
+// tangent_frame (geometry.hpp:51-63): precomputed per triangle (tangent_frame_of)
+__device__ __forceinline__ Frame2 tangent_frame(const FrameView& F, int id) { return F.tframe[id]; }
 
 // ---------------------------------------------------------------------------
 // path-tree walk (Tracer::trace_tree, transport.hpp:224-275)

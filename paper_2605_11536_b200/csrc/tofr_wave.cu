@@ -692,7 +692,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     V3 p1{0, 0, 0}, p2{0, 0, 0}, spos{0, 0, 0}, cpos{0, 0, 0};
     int stri = 0, ctri = 0;
     bool cn_rec = true;  // current point's normal = the record's pn
-    Frame2 Js{{1, 0, 0}, {0, 1, 0}}, Jc{{1, 0, 0}, {0, 1, 0}};
+    // tangent frames are per-triangle lookups (FrameView::tframe): the start
+    // point's is tframe[stri], the current point's tframe[ctri]
     StartTerms stt;
     VelField vf{{0, 0, 0}, {0, 0, 0}};  // velocity gates only
     double delta = 0, tol = 0, fnorm = 0, scale = 1;
@@ -759,7 +760,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             if (VEL) vf = VelField{velocity_at(F, F.tri[pre.tri1].obj, pre.p1), suf.v2};
                             tol = 0.01 * jb.dw;
                             if (count) SCTR(SC_SOLVES, 1);
-                            Js = tangent_frame(F, stri);
                             // start terms and delta = target - (field at the start
                             // point) come with trial 0 (start_from)
                             delta = target_local;
@@ -767,7 +767,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             cpos = spos;
                             ctri = stri;
                             cn_rec = true;
-                            Jc = Js;
                             step = V2{0, 0};
                             scale = 1.0;
                             iter = 0;
@@ -826,7 +825,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 TOFR_BORROW(dsel) TOFR_BORROW(ctri) TOFR_BORROW(cn_rec) TOFR_BORROW(scale) TOFR_BORROW(delta)
                 TOFR_BORROW(fnorm) TOFR_BORROW(step.x) TOFR_BORROW(step.y)
                 TOFR_BORROW3(cpos) TOFR_BORROW3(spos) TOFR_BORROW3(p1) TOFR_BORROW3(p2)
-                TOFR_BORROW3(Jc.t) TOFR_BORROW3(Jc.b) TOFR_BORROW3(Js.t) TOFR_BORROW3(Js.b)
+                TOFR_BORROW(stri)
                 TOFR_BORROW3(stt.g3s) TOFR_BORROW(stt.gs.x) TOFR_BORROW(stt.gs.y) TOFR_BORROW(stt.lvs)
                 TOFR_BORROW(stt.Hs.a) TOFR_BORROW(stt.Hs.b) TOFR_BORROW(stt.Hs.c) TOFR_BORROW(stt.Hs.d)
                 if (VEL) {
@@ -844,7 +843,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
 
         // ---- one Newton trial (trial 0 = the initial evaluation at the start point)
         const FrameView& F = sF[dsel];
-        V3 tpos = cpos + to_world(Jc, step * scale);  // plane point
+        V3 tpos = cpos + to_world(F.tframe[ctri], step * scale);  // plane point
         int ttri = ctri;
         bool tn_rec = cn_rec, have = true;
         if (init) tpos = spos;
@@ -859,7 +858,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned rm = __ballot_sync(0xffffffffu, active && !parked);
         bool trace_now = (parked && (tail || __popc(pm) >= TOFR_RAYBATCH || rm == 0)) || (tail && need_ray);
         if (trace_now) {
-            if (parked) tpos = cpos + to_world(Jc, step * scale);
+            if (parked) tpos = cpos + to_world(F.tframe[ctri], step * scale);
             SurfR r = reproject_rays(&F, ctri, tpos, p1);
             n_rays += uint32_t(r.rays);
             have = r.ok;
@@ -873,10 +872,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned em = __ballot_sync(0xffffffffu, (active && !parked) || helper);
         if (!((active && !parked) || helper)) continue;
         __syncwarp(em);
-        // the tangent frame of the current triangle is already known (Jc, or Js
-        // for trial 0): recompute only after a re-projection ray changed it
-        Frame2 Jt = init ? Js : Jc;
-        if (!init && ttri != ctri) Jt = tangent_frame(F, ttri);
+        const Frame2 Jt = F.tframe[ttri];
+        const Frame2 Js = F.tframe[stri];
         LcEval ev = field_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, tpos, Jt, cfg.gauge != GAUGE_FIXED);
         if (init) {
             start_from(ev, Js, stt);
@@ -896,7 +893,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     }
 #define TOFR_TAKE3(v) TOFR_TAKE(v.x) TOFR_TAKE(v.y) TOFR_TAKE(v.z)
             bool take = own && !accept && (group & hm) != 0;
-            TOFR_TAKE3(tpos) TOFR_TAKE(ttri) TOFR_TAKE(tn_rec) TOFR_TAKE3(Jt.t) TOFR_TAKE3(Jt.b)
+            TOFR_TAKE3(tpos) TOFR_TAKE(ttri) TOFR_TAKE(tn_rec)
             TOFR_TAKE(et.F.x) TOFR_TAKE(et.F.y) TOFR_TAKE(et.dFp.a) TOFR_TAKE(et.dFp.b) TOFR_TAKE(et.dFp.c)
             TOFR_TAKE(et.dFp.d) TOFR_TAKE(et.det_dF) TOFR_TAKE(et.ngrad) TOFR_TAKE(fn)
 #undef TOFR_TAKE3
@@ -920,7 +917,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             cpos = tpos;
             cn_rec = tn_rec;
             ctri = ttri;
-            Jc = Jt;
             fnorm = fn;
             if (fabs(et.F.x) <= tol && fabs(et.F.y) <= tol) {
                 double dc = det(et.dFp);

@@ -1,4 +1,4 @@
-O=gpurun_out/s4g; mkdir -p $O
+O=gpurun_out/${TAG:-s4g}; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
 for wl in c3 c3w c2r c1; do
   timeout 400 python bench.py --workload $wl --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_$wl.json 2> $O/bench_$wl.err
