@@ -43,11 +43,11 @@
 #endif
 // lanes needing re-projection rays a warp collects before it traces them
 #ifndef TOFR_RAYBATCH
+#define TOFR_RAYBATCH 8
+#endif
 // 1: lanes waiting for a refill help too (measured slower: it disables ray parking)
 #ifndef TOFR_HELP_IDLE
 #define TOFR_HELP_IDLE 0
-#endif
-#define TOFR_RAYBATCH 8
 #endif
 
 namespace tofr_b200 {
