@@ -22,11 +22,13 @@ for rep in sys.argv[1:]:
     wl, kernel = m.group(1), m.group(2)
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(txt)))
-    hdr, units, row = r[0], r[1], r[2]
-    d, u = dict(zip(hdr, row)), dict(zip(hdr, units))
+    hdr, units, rows = r[0], r[1], r[2:]
+    u = dict(zip(hdr, units))
     tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        tot += float(d[k].replace(",", "")) * UNIT.get(u[k], 1)
-    data[f"{wl}:{kernel}"] = round(tot)
+    for row in rows:  # every captured launch: the average per launch
+        d = dict(zip(hdr, row))
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k].replace(",", "")) * UNIT.get(u[k], 1)
+    data[f"{wl}:{kernel}"] = round(tot / max(1, len(rows)))
     print(wl, kernel, f"{tot / 1e6:.1f} MB")
 out_path.write_text(json.dumps(data, indent=1, sort_keys=True) + "\n")
