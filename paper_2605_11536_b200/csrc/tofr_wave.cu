@@ -1017,22 +1017,17 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int ptri = ts.x;
         V3 pnrm = (ts.y & 2) ? rec_pn(st, jb.item) : F.tri[ptri].n;
         double j_newton = c5.y;
-        // The two connection segments.  Bvh::occluded (the two occlusion tests of
-        // shift_sample, shiftmap.hpp:765-767) and rebuild_sample compute the same
-        // differences, lengths and directions: computed once here.
-        const V3 d1 = ppos - pre.p1;
-        const double l1 = norm(d1);
-        const V3 d2 = suf.p2 - ppos;
-        const double l2 = norm(d2);
-        const V3 u1 = d1 / l1, u2 = d2 / l2;
-        // one loop around a single traversal site, so lanes stay converged
+        // the two occlusion tests of shift_sample (shiftmap.hpp:765-767) as one
+        // loop around a single traversal site, so lanes stay converged
         bool occ = false;
         for (int r = 0; r < 2 && !occ; ++r) {
-            const double dist = r == 0 ? l1 : l2;
+            V3 a = r == 0 ? pre.p1 : ppos, bpt = r == 0 ? ppos : suf.p2;
+            V3 dd = bpt - a;
+            double dist = norm(dd);
             if (dist <= 2 * F.eps_ray) continue;  // Bvh::occluded: nothing between
             ++n_any;
-            occ = trace_ray_impl(F.nodes, F.tri_isect, r == 0 ? pre.p1 : ppos, r == 0 ? u1 : u2, F.eps_ray,
-                                 dist - F.eps_ray, true).slot >= 0;
+            V3 dir = dd / dist;
+            occ = trace_ray_impl(F.nodes, F.tri_isect, a, dir, F.eps_ray, dist - F.eps_ray, true).slot >= 0;
         }
         if (occ) {
             if (count) ctr.v[SC_OCCLUDED]++;
@@ -1047,11 +1042,17 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             continue;
         }
         // rebuild_sample
+        V3 d1 = ppos - pre.p1;
+        double l1 = norm(d1);
+        V3 d2 = suf.p2 - ppos;
+        double l2 = norm(d2);
         bool ok = !(l1 <= 2 * F.eps_ray) && !(l2 <= 2 * F.eps_ray);
         V3 f = splat(0);
         int m2 = -1;
         double u_total = 0;
         if (ok) {
+            V3 u1 = d1 / l1;
+            V3 u2 = d2 / l2;
             V3 pvel = splat(0);
             if (VEL) {
                 pvel = velocity_at(F, F.tri[ptri].obj, ppos);

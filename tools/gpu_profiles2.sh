@@ -26,10 +26,16 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --workload c4r --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_summary.py launches $O/launches_c4r.csv > $O/launches_c4r_summary.txt 2>&1
 # full captures: <workload> <file tag = library kernel name> <ncu regex> <skip> <count>
+# (reports are ~5 MB per launch and gpurun brings back <= 64 MiB: each one is
+# summarised on the box -- metrics, DRAM traffic, hot source lines -- then dropped)
 cap() {
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$3" -s $4 -c $5 -o $O/full_$1_$2 \
       python bench.py --workload $1 --steps 2 --warmup 4 --no-cpu-baseline > $O/ncu_full_$1_$2.log 2>&1
   python tools/ncu_summary.py full $O/full_$1_$2.ncu-rep > $O/full_$1_$2.txt 2>&1
+  python tools/traffic_json.py --out $O/traffic.json $O/full_$1_$2.ncu-rep >> $O/traffic.log 2>&1
+  ncu -i $O/full_$1_$2.ncu-rep --page source --print-source cuda,sass --csv --launch-count 1 > /tmp/src.csv 2>/dev/null
+  python tools/ncu_lines.py /tmp/src.csv 30 > $O/lines_$1_$2.txt 2>&1
+  rm -f $O/full_$1_$2.ncu-rep
 }
 cap c3 k_shift_solve '^k_shift_solve' 16 4
 cap c3 k_trace_gated '^k_trace' 4 1
@@ -41,3 +47,7 @@ cap c2r k_temporal_apply '^k_temporal_apply' 8 2
 cap c2r k_temporal_prep '^k_temporal_prep' 8 2
 cap c4p k_hist_plain '^k_hist_plain' 4 1
 ls $O
+# one raw report kept for inspection (one steady-state launch of the headline's dominant kernel)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^k_shift_solve' -s 17 -c 1 \
+    -o $O/keep_c3_k_shift_solve python bench.py --workload c3 --steps 2 --warmup 4 --no-cpu-baseline > /dev/null 2>&1
+du -sh $O

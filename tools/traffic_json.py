@@ -2,7 +2,7 @@
 """profiles/traffic.json from full ncu captures: {"<workload>:<kernel>": dram bytes
 (read + write) of the captured launch}.  bench.py reports it as roofline.traffic.
 
-    python tools/traffic_json.py gpurun_out/<tag>/full_<wl>_<kernel>.ncu-rep ...
+    python tools/traffic_json.py [--out traffic.json] gpurun_out/<tag>/full_<wl>_<kernel>.ncu-rep ...
 """
 import csv
 import io
@@ -13,9 +13,12 @@ import sys
 from pathlib import Path
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+args = sys.argv[1:]
 out_path = Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
+if args[:1] == ["--out"]:
+    out_path, args = Path(args[1]), args[2:]
 data = json.loads(out_path.read_text()) if out_path.exists() else {}
-for rep in sys.argv[1:]:
+for rep in args:
     m = re.match(r"full_([^_]+)_(.+)\.ncu-rep$", Path(rep).name)
     if not m:
         continue
