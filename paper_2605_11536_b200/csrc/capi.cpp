@@ -212,7 +212,13 @@ struct tofr_session {
     cudaEvent_t ev_temporal[2] = {}, ev_init[2] = {};
     bool pending[2] = {false, false};
     unsigned long long* err_host = nullptr;  // pinned [2]
-    cudaEvent_t read_ev[2] = {};             // asynchronous image read-backs
+    cudaEvent_t read_ev[2] = {};             // asynchronous image read-backs (on copy_stream)
+    // read-back slots: the frame's image is staged on the device (a D2D copy, or
+    // the transient histogram sum written there directly) on the session stream,
+    // then copied to the host on copy_stream, overlapping the next frames' kernels
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t staged_ev[2] = {};
+    DevBuf read_stage[2];
     int f = 0;
     double prev_center = 0, prev_width = 0;
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -239,6 +245,12 @@ struct tofr_session {
                 if (e) cudaEventDestroy(e);
         for (auto& e : read_ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : staged_ev)
+            if (e) cudaEventDestroy(e);
+        if (copy_stream) {
+            cudaStreamSynchronize(copy_stream);
+            cudaStreamDestroy(copy_stream);
+        }
         if (err_host) cudaFreeHost(err_host);
         if (occ_host) cudaFreeHost(occ_host);
         release_buffers();
@@ -252,7 +264,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (auto& r : res_slot) r.release();
         res_rows.release();
-        for (DevBuf* b : {&image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+        for (DevBuf* b : {&read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
@@ -415,6 +427,8 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     for (auto& set : s->ev)
         for (auto& e : set) ck(cudaEventCreate(&e), "event");
     for (auto& e : s->read_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : s->staged_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking), "stream");
     ck(cudaMallocHost(reinterpret_cast<void**>(&s->err_host), 2 * sizeof(unsigned long long)), "pinned");
     s->err_host[0] = s->err_host[1] = 0;
     // [3 stages x SC_COUNT][band error][work counter q][WK_COUNT device work][side-stream work counter]
@@ -1277,26 +1291,31 @@ int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats) {
 }
 
 namespace {
-void enqueue_image(tofr_session* ss, double* image) {
-    if (ss->transient) {
-        // wide-band image of the histogram accumulated so far, / frames
-        size_t npix = ss->owned_pixels();
-        ss->image.ensure(npix * 3 * sizeof(double));
-        Band bd = band_of(ss, false);
-        double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
-        launch_hist_image(rows_base<double>(ss->hist, ss->y0, size_t(ss->W) * ss->B * 3), bd, ss->W, ss->B, scale,
-                          rows_base<double>(ss->image, ss->y0, size_t(ss->W) * 3), ss->ctx->stream);
-        ck(cudaGetLastError(), "hist image");
-    }
-    ck(cudaMemcpyAsync(image, ss->image.p, ss->owned_pixels() * 24, cudaMemcpyDeviceToHost, ss->ctx->stream), "d2h");
-}
 }  // namespace
 
 int tofr_gpu_session_read_image_async(tofr_session* ss, double* pinned_image, int32_t slot) {
     if (!ss || !pinned_image || slot < 0 || slot > 1) return TOFR_ERR_INVALID;
     return guard(ss->ctx, [&] {
-        enqueue_image(ss, pinned_image);
-        ck(cudaEventRecord(ss->read_ev[slot], ss->ctx->stream), "event");
+        cudaStream_t st = ss->ctx->stream;
+        size_t bytes = ss->owned_pixels() * 24;
+        DevBuf& stage = ss->read_stage[slot];
+        stage.ensure(bytes);
+        // the slot's previous host copy must be done before its staging buffer is rewritten
+        ck(cudaStreamWaitEvent(st, ss->read_ev[slot], 0), "wait");
+        if (ss->transient) {
+            // wide-band image of the histogram accumulated so far, / frames
+            Band bd = band_of(ss, false);
+            double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+            launch_hist_image(rows_base<double>(ss->hist, ss->y0, size_t(ss->W) * ss->B * 3), bd, ss->W, ss->B,
+                              scale, rows_base<double>(stage, ss->y0, size_t(ss->W) * 3), st);
+            ck(cudaGetLastError(), "hist image");
+        } else {
+            ck(cudaMemcpyAsync(stage.p, ss->image.p, bytes, cudaMemcpyDeviceToDevice, st), "d2d");
+        }
+        ck(cudaEventRecord(ss->staged_ev[slot], st), "event");
+        ck(cudaStreamWaitEvent(ss->copy_stream, ss->staged_ev[slot], 0), "wait");
+        ck(cudaMemcpyAsync(pinned_image, stage.p, bytes, cudaMemcpyDeviceToHost, ss->copy_stream), "d2h");
+        ck(cudaEventRecord(ss->read_ev[slot], ss->copy_stream), "event");
     });
 }
 
