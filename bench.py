@@ -292,22 +292,28 @@ def run_ours(args) -> None:
     sess.sync()
     parallel.barrier(group)
 
-    # timed region: per-kernel CUDA events (library launch accounting, on the
-    # session stream), exact launch count and device work counters around it
+    # timed region (value): K frames between CUDA events on the session stream,
+    # exact launch count and device work counters around it; no per-kernel
+    # instrumentation (its events between launches cost ~10% of a gated frame)
     clk = ClockSampler(local) if rank == 0 else None
     stage_tot = [0.0] * 6
-    F.kernel_times(reset=True)
-    F.kernel_timing(True)
     work0 = sess.work()
     l0 = F.kernel_launches()
     t_ms = sess.timed_steps(args.steps, stage_tot)
     launches = F.kernel_launches() - l0
     work1 = sess.work()
-    F.kernel_timing(False)
-    ktimes = F.kernel_times(reset=True)
     clocks = clk.stop() if clk else None
     t_max = parallel.max_over_ranks(t_ms, group)
     frames = args.steps
+    # the next K frames again with every launch bracketed by CUDA events: the
+    # per-kernel times and the roofline's launch durations / units
+    F.kernel_times(reset=True)
+    F.kernel_timing(True)
+    work0k = sess.work()
+    sess.timed_steps(args.steps, [0.0] * 6)
+    work1k = sess.work()
+    F.kernel_timing(False)
+    ktimes = F.kernel_times(reset=True)
     fps = frames / (t_max * 1e-3)
 
     # shift counters of one more (synchronous) frame: the work behind the time
@@ -339,15 +345,13 @@ def run_ours(args) -> None:
 
     # e2e through the public API: step + image read-back to pinned host memory,
     # on a fresh session over the same frames as the device-timed run (W warm-up
-    # frames, then K): transient reservoir grids fill up frame by frame, so
-    # later frames cost more and would not compare
+    # frames of the same loop, untimed, then K timed): transient reservoir grids
+    # fill up frame by frame, so later frames cost more and would not compare
     band_px = sess.owned_pixels()
     sess.sess.close()
     sess = new_session()
-    for _ in range(args.warmup):
-        sess.step()
     parallel.barrier(group)
-    e2e_s = sess.run_e2e(args.steps)
+    e2e_s = sess.run_e2e(args.steps, warm=args.warmup)
     e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
     h2d, d2h = sess.io_bytes()
 
@@ -357,7 +361,7 @@ def run_ours(args) -> None:
     names = ["init", "temporal", "bin", "spatial", "shade"]
     items = band_px * (cfg.bins if cfg.mode == F.MODE_TRANSIENT or plain else 1)
     dom = max(ktimes, key=lambda k: ktimes[k][0]) if ktimes else None
-    work = {k: work1[k] - work0[k] for k in work1} if work1 else {}
+    work = {k: work1k[k] - work0k[k] for k in work1k} if work1k else {}  # the instrumented frames
     units = {"pixel": band_px, "item": items}
     if dom and KERNEL_BYTES.get(dom, ("", 0))[0] == "job":
         per_launch_jobs = work.get("shift_jobs", 0) / max(1, sum(v[1] for k, v in ktimes.items()
@@ -382,7 +386,8 @@ def run_ours(args) -> None:
         except Exception:
             traffic = None
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
-    rays = (work.get("rays_closest", 0) + work.get("rays_any", 0)) if work else 0
+    workv = {k: work1[k] - work0[k] for k in work1} if work1 else {}  # the value frames
+    rays = (workv.get("rays_closest", 0) + workv.get("rays_any", 0)) if workv else 0
     t_s = t_max * 1e-3
 
     cpu = None
@@ -427,7 +432,7 @@ def run_ours(args) -> None:
             "kernel_ms_per_step": kernel_ms,
             "reservoir_pool": pool_info,
             "rays_per_s": rays / t_s if t_s > 0 else None,
-            "shift_jobs_per_s": work.get("shift_jobs", 0) / t_s if (t_s > 0 and work) else None,
+            "shift_jobs_per_s": workv.get("shift_jobs", 0) / t_s if (t_s > 0 and workv) else None,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clocks,

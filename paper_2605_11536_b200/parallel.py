@@ -220,25 +220,33 @@ class BandSession:
                                        pin_memory=True).numpy()
         return self.sess.read_image(self._pinned)
 
-    def run_e2e(self, k: int) -> float:
+    def run_e2e(self, k: int, warm: int = 0) -> float:
         """k frames through the public API, each frame's image read back to
         pinned host memory (double-buffered: frame f's copy overlaps frame
-        f+1's kernels; every copy has landed when this returns).  Wall seconds."""
+        f+1's kernels; every copy has landed when this returns).  `warm` frames
+        of the same loop run first, untimed, so the clock starts on a running
+        pipeline (steady state).  Wall seconds of the k frames."""
         import time
         import torch
         bufs = [torch.empty((self.y1 - self.y0, self.W, 3), dtype=torch.float64, pin_memory=True).numpy()
                 for _ in range(2)]
         self.sync()
-        t0 = time.perf_counter()
-        for f in range(k):
+
+        def frame(g):
             self.sess.step(stats=False)
-            if f >= 2:
-                self.sess.wait_read(f & 1)  # the buffer written two frames ago is free again
-            self.sess.read_image_async(bufs[f & 1], f & 1)
-        for f in range(max(0, k - 2), k):
-            self.sess.wait_read(f & 1)
+            if g >= 2:
+                self.sess.wait_read(g & 1)  # the buffer written two frames ago is free again
+            self.sess.read_image_async(bufs[g & 1], g & 1)
+
+        for g in range(warm):
+            frame(g)
+        t0 = time.perf_counter()
+        for g in range(warm, warm + k):
+            frame(g)
+        for g in range(max(0, warm + k - 2), warm + k):
+            self.sess.wait_read(g & 1)
         dt = time.perf_counter() - t0
-        self.last_e2e_image = bufs[(k - 1) & 1]
+        self.last_e2e_image = bufs[(warm + k - 1) & 1]
         return dt
 
     def gather_image(self) -> np.ndarray | None:

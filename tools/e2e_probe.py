@@ -46,3 +46,12 @@ for f in range(k):
 sess.sync()
 tot = time.perf_counter() - t0
 print(wl, f"steps only {k / tot:.1f} fps, host step {hs / k * 1e3:.3f} ms/frame")
+# pure host enqueue cost: the GPU is idle when each step starts
+hs = []
+for f in range(k):
+    sess.sync()
+    a = time.perf_counter()
+    sess.sess.step(stats=False)
+    hs.append(time.perf_counter() - a)
+sess.sync()
+print(wl, f"host enqueue per step (idle GPU): median {np.median(hs) * 1e3:.3f} ms, max {max(hs) * 1e3:.3f} ms")
