@@ -39,7 +39,7 @@
 #endif
 // idle lanes a warp of k_shift_solve collects before it refills them
 #ifndef TOFR_REFILL
-#define TOFR_REFILL 16
+#define TOFR_REFILL 12
 #endif
 // lanes needing re-projection rays a warp collects before it traces them
 #ifndef TOFR_RAYBATCH
