@@ -144,19 +144,28 @@ class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
     def __init__(self, index: int):
+        # started before the warm-up (nvidia-smi needs ~0.1-0.3 s to produce its
+        # first line); only the samples inside mark()..stop() are kept
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        self.t0 = None
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def mark(self) -> None:
+        """Start of the timed region."""
+        self.t0 = time.time()
+
     def stop(self) -> dict:
+        import datetime
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
         self.p.terminate()
         self.p.wait()
         self.f.flush()
@@ -167,6 +176,9 @@ class ClockSampler:
         for r in rows:
             r = [x.strip() for x in r]
             try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self.t0 is not None and not (self.t0 <= ts <= t1):
+                    continue
                 sm.append(float(r[1]))
                 mx = float(r[2])
             except (ValueError, IndexError):
@@ -174,8 +186,15 @@ class ClockSampler:
             for nm, v in zip(names, r[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if not sm and rows:  # unparsable timestamps: every sample of the run
+            self.t0 = None
+            raw = [x for x in rows if len(x) > 2]
+            vals = [float(x[1]) for x in raw if x[1].strip().replace(".", "", 1).isdigit()]
+            out.update({"sm_mhz": statistics.median(vals) if vals else None, "samples": len(vals),
+                        "window": "whole run (timestamps unparsable)"})
+        return out
 
 
 def dist_env():
@@ -287,6 +306,7 @@ def run_ours(args) -> None:
         return parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
 
     sess = new_session()
+    clk = ClockSampler(local) if rank == 0 else None
     for _ in range(args.warmup):
         sess.step()
     sess.sync()
@@ -295,14 +315,14 @@ def run_ours(args) -> None:
     # timed region (value): K frames between CUDA events on the session stream,
     # exact launch count and device work counters around it; no per-kernel
     # instrumentation (its events between launches cost ~10% of a gated frame)
-    clk = ClockSampler(local) if rank == 0 else None
+    if clk:
+        clk.mark()
     stage_tot = [0.0] * 6
     work0 = sess.work()
     l0 = F.kernel_launches()
     t_ms = sess.timed_steps(args.steps, stage_tot)
     launches = F.kernel_launches() - l0
     work1 = sess.work()
-    clocks = clk.stop() if clk else None
     t_max = parallel.max_over_ranks(t_ms, group)
     frames = args.steps
     # the next K frames again with every launch bracketed by CUDA events: the
@@ -314,6 +334,8 @@ def run_ours(args) -> None:
     work1k = sess.work()
     F.kernel_timing(False)
     ktimes = F.kernel_times(reset=True)
+    # clocks over both passes (the GPU is under load throughout)
+    clocks = clk.stop() if clk else None
     fps = frames / (t_max * 1e-3)
 
     # shift counters of one more (synchronous) frame: the work behind the time
