@@ -183,6 +183,7 @@ struct tofr_session {
     // handed out per grid ([3] u32), pool rows per grid (+2 reserved rows)
     bool sparse = false;
     size_t pool_rows = 0;
+    int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
     unsigned int* occ_host = nullptr;  // pinned [2][3]: pool rows per grid at the end of a frame
     size_t occ_seen = 0;               // largest of them over the frames flushed so far
     DevBuf res_slot[3], res_rows;
@@ -285,6 +286,7 @@ ResStore store_of(const tofr_session* s, const DevBuf& b) {
     st.pool = b.as<double2>() + items - ptrdiff_t(st.stride);
     st.rows = s->res_rows.as<unsigned int>() + k;
     st.err = s->ctr.as<unsigned long long>() + 3 * SC_COUNT;
+    st.planes = s->pool_planes;
     return st;
 }
 
@@ -470,7 +472,14 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             const char* sp = std::getenv("TOFR_SPARSE");
             s->sparse = s->transient && !(sp && sp[0] == '0');
             if (s->sparse) {
-                const size_t row_bytes = (kResChunks - 1) * 16;
+                // records of scenes without non-reconnectable materials never carry
+                // replay lanes (k = 2), and transient gates are length gates: the
+                // pool holds chunks 1-19 only
+                bool lanes = false;
+                for (const HMaterial& m : sc->s.materials)
+                    if (!m.reconnectable()) lanes = true;
+                s->pool_planes = lanes ? kResChunks : 20;
+                const size_t row_bytes = size_t(s->pool_planes - 1) * 16;
                 size_t rows = items;
                 size_t fr = 0, tot = 0;
                 if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
@@ -484,7 +493,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 if (const char* pr = std::getenv("TOFR_POOL_ROWS")) rows = size_t(std::strtoull(pr, nullptr, 10));
                 if (rows > 0xfffffff0ull) rows = 0xfffffff0ull;
                 s->pool_rows = rows;
-                rb = items * 16 + (kResChunks - 1) * (rows + 2) * 16;
+                rb = items * 16 + size_t(s->pool_planes - 1) * (rows + 2) * 16;
                 for (int k = 0; k < 3; ++k)
                     if (k < 2 || s->has_bin || s->has_spatial) {
                         s->res_slot[k].ensure(items * sizeof(uint32_t));

@@ -1059,7 +1059,7 @@ __global__ void k_halo_pack_sparse(ResStore grid, size_t item0, size_t n, double
         }
         __stcg(&h.idx[r], uint32_t(i));
         const size_t row = res_row(grid, item0 + i);
-        for (int c = 1; c < kResChunks; ++c) __stcg(&h.pl[size_t(c - 1) * cap + r], ld2r(grid, c, row));
+        for (int c = 1; c < grid.planes; ++c) __stcg(&h.pl[size_t(c - 1) * cap + r], ld2r(grid, c, row));
     }
 }
 
@@ -1074,7 +1074,7 @@ __global__ void k_halo_unpack_rows(ResStore grid, size_t item0, size_t n, const 
     size_t cnt = min(size_t(__ldcg(h.count)), cap);
     for (size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x; r < cnt; r += size_t(gridDim.x) * blockDim.x) {
         const size_t row = res_row_w(grid, item0 + __ldcg(&h.idx[r]));
-        for (int c = 1; c < kResChunks; ++c) st2r(grid, c, row, __ldcg(&h.pl[size_t(c - 1) * cap + r]));
+        for (int c = 1; c < grid.planes; ++c) st2r(grid, c, row, __ldcg(&h.pl[size_t(c - 1) * cap + r]));
     }
 }
 

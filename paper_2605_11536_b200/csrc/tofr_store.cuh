@@ -52,6 +52,10 @@ struct ResStore {
     double2* pool = nullptr;             // sparse: chunk planes 1..23 (pool[c * stride + row])
     unsigned int* rows = nullptr;        // sparse: rows handed out
     unsigned long long* err = nullptr;   // sparse: band error word (kErrPool on overflow)
+    // chunk planes held (header included): a sparse pool drops the replay-lane
+    // and velocity chunks (20-23) when no record can have them (no
+    // non-reconnectable material, length gates): 20
+    int planes = kResChunks;
 };
 
 #if defined(__CUDACC__)

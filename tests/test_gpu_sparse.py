@@ -44,15 +44,24 @@ class _env:
 
 
 CASES = {
+    # mirror box: records with replay lanes (k > 2), pools keep all 24 chunk planes
+    "mirror_lanes": ("mirror", _cfg(hist_t0=3.0, hist_bin_width=0.5, max_depth=8)),
     "temporal_spatial": ("cornell", _cfg()),
     "bin_reuse": ("cornell_wide", _cfg(hist_t0=3.0, bin_reuse=True, spatial_passes=2)),
     "animated": ("boxes_doppler", _cfg(hist_t0=7.0, hist_bin_width=0.5, max_depth=8)),
 }
 
 
+def _scene(name):
+    if name == "mirror":
+        from tests.cases import mirror_box
+        return mirror_box(36)
+    return scenes.bundled(name, 36)
+
+
 def _render(scene, cfg, **env):
     with _env(**env):
-        out = Renderer(0).render_transient(scenes.bundled(scene, 36), cfg)
+        out = Renderer(0).render_transient(_scene(scene), cfg)
     return out
 
 
@@ -84,7 +93,7 @@ def test_pool_rows_count_nonempty_reservoirs():
     scene, cfg = "cornell", _cfg(spatial_passes=0)
     with _env(TOFR_SPARSE="1"):
         r = Renderer(0)
-        s = r.session(scenes.bundled(scene, 36), cfg)
+        s = r.session(_scene(scene), cfg)
         for _ in range(3):
             s.step(stats=False)
         pool = s.pool()
