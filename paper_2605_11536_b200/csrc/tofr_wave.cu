@@ -45,6 +45,9 @@
 #ifndef TOFR_RAYBATCH
 #define TOFR_RAYBATCH 8
 #endif
+#ifndef TOFR_SOLVE_REVERSE
+#define TOFR_SOLVE_REVERSE 0
+#endif
 // 1: lanes waiting for a refill help too (measured slower: it disables ray parking)
 #ifndef TOFR_HELP_IDLE
 #define TOFR_HELP_IDLE 0
@@ -719,7 +722,9 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 if (kk >= j1) {
                     exhausted = true;
                 } else {
-                    job = uint32_t(kk);
+                    // TOFR_SOLVE_REVERSE: take the queue from its end (order A/B;
+                    // every job's result is independent of the order)
+                    job = TOFR_SOLVE_REVERSE ? uint32_t(j1 - 1 - (kk - j0)) : uint32_t(kk);
                     Job jb = job_get(q, job);
                     dsel = (jb.meta & JOB_DST1) ? 1 : 0;
                     const FrameView& F = sF[dsel];
