@@ -298,12 +298,29 @@ def run_ours(args) -> None:
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
     emulated = BAND_ONLY[args.workload] if (ws == 1 and args.workload in BAND_ONLY) else None
+    # N > 1: bands of equal cost, not equal rows (the lit region of a frame is
+    # not spread evenly over the rows): rank 0 renders the first frames whole,
+    # weighs the rows by their lit pixels, and broadcasts the split
+    bands = None
+    if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "1") != "0":
+        import torch.distributed as dist
+        obj = [None]
+        if rank == 0:
+            probe = parallel.BandSession(r, sd, cfg, plain=plain)
+            for _ in range(2):
+                probe.step()
+            weights = parallel.row_weights(probe.read_image_host())
+            probe.sess.close()
+            halo = parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes) if not plain else 0
+            obj = [parallel.balanced_bands(weights, ws, max(1, halo))]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        bands = obj[0]
 
     def new_session():
         if emulated:
             return parallel.BandSession(r, sd, cfg, rank=emulated[1], world=emulated[0], group=None, plain=plain,
                                         emulate=True)
-        return parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain)
+        return parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain, bands=bands)
 
     sess = new_session()
     clk = ClockSampler(local) if rank == 0 else None
@@ -436,7 +453,8 @@ def run_ours(args) -> None:
                        "parallelism": (f"rowband{emulated[0]}: the band of rank {emulated[1]} (rows "
                                        f"{sess.y0}-{sess.y1} + {sess.halo}-row halos) on one GPU, halo rows "
                                        f"not transferred; value = that band's frames/s"
-                                       if emulated else (f"rowband{ws}" if ws > 1 else "single")),
+                                       if emulated else (f"rowband{ws}" + (f" (cost-balanced rows {bands})" if bands
+                                                                           else "") if ws > 1 else "single")),
                        "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
             "mpaths_per_s": (sess.owned_pixels() if emulated else w * h) * cfg.m_init * fps / 1e6,
             "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},

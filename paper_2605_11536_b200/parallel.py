@@ -32,6 +32,35 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
     return y0, y0 + base + (1 if rank < rem else 0)
 
 
+def row_weights(image: np.ndarray, base: float = 0.05) -> np.ndarray:
+    """Per-row cost proxy from a rendered frame ([H, W, 3]): pixels with a
+    non-zero estimate carry the reservoir / shift work, every pixel a little
+    (camera ray, empty merges)."""
+    lit = (np.asarray(image) > 0).any(axis=2).sum(axis=1).astype(np.float64)
+    return lit + base * image.shape[1]
+
+
+def balanced_bands(weights, world: int, min_rows: int = 1) -> list:
+    """Contiguous row bands [y0, y1) of about equal total weight (cuts at the
+    prefix-sum quantiles), each at least max(1, min_rows) rows."""
+    w = np.asarray(weights, dtype=np.float64)
+    H = len(w)
+    m = max(1, int(min_rows))
+    if world <= 1:
+        return [(0, H)]
+    if world * m > H:
+        raise ValueError(f"{world} bands of at least {m} rows do not fit {H} rows")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for g in range(1, world):
+        y = int(np.searchsorted(cum, cum[-1] * g / world))
+        y = max(y, cuts[-1] + m)              # at least m rows in the band above
+        y = min(y, H - (world - g) * m)       # room for the bands below
+        cuts.append(y)
+    cuts.append(H)
+    return [(cuts[g], cuts[g + 1]) for g in range(world)]
+
+
 def halo_rows(radius: float, passes: int = 1) -> int:
     """Rows a spatial pass may read beyond a band: neighbor_offset rounds
     rr*sin(th) with rr < radius (pipeline.hpp:232-239), so |dy| <= ceil(radius).
@@ -154,19 +183,22 @@ class BandSession:
     """A session rendering one row band of every frame (the whole frame when world == 1)."""
 
     def __init__(self, renderer, scene_def, cfg, rank: int = 0, world: int = 1, group=None, plain: bool = False,
-                 emulate: bool = False):
+                 emulate: bool = False, rows=None, bands=None):
         """emulate: render band `rank` of a `world`-way split alone (no process
         group): the halo exchange is a no-op, so halo rows hold empty
-        reservoirs -- the per-GPU work of that split, for one-GPU measurement."""
+        reservoirs -- the per-GPU work of that split, for one-GPU measurement.
+        bands: the split as [(y0, y1)] per rank (default: equal bands,
+        band_rows); rows: this rank's band alone (emulation)."""
         import torch
         self.r = renderer
         self.cfg = cfg
         self.plain = plain
         self.rank, self.world, self.group = rank, world, group
         H = scene_def.camera.height
-        self.y0, self.y1 = band_rows(H, world, rank)
+        self.bands = list(bands) if bands else [band_rows(H, world, g) for g in range(world)]
+        self.y0, self.y1 = rows if rows else self.bands[rank]
         halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if (world > 1 and not plain) else 0
-        if world > 1 and min(band_rows(H, world, g)[1] - band_rows(H, world, g)[0] for g in range(world)) < halo:
+        if world > 1 and min(b[1] - b[0] for b in self.bands) < halo:
             raise ValueError(f"{world} bands of a {H}-row image are thinner than the {halo}-row halo")
         self.halo = halo
         self.sess = renderer.session(scene_def, cfg, band=(self.y0, self.y1, halo), plain=plain)
@@ -257,16 +289,14 @@ class BandSession:
         if self.world == 1:
             return band.numpy()
         dev = _dev(self.group)
-        hmax = max(band_rows(self.H, self.world, g)[1] - band_rows(self.H, self.world, g)[0]
-                   for g in range(self.world))
+        hmax = max(b[1] - b[0] for b in self.bands)
         pad = torch.zeros((hmax, self.W, 3), dtype=torch.float64, device=dev)
         pad[: band.shape[0]] = band.to(dev)
         parts = [torch.empty_like(pad) for _ in range(self.world)]
         dist.all_gather(parts, pad, group=self.group)
         if self.rank != 0:
             return None
-        rows = [parts[g][: band_rows(self.H, self.world, g)[1] - band_rows(self.H, self.world, g)[0]]
-                for g in range(self.world)]
+        rows = [parts[g][: self.bands[g][1] - self.bands[g][0]] for g in range(self.world)]
         return torch.cat(rows).cpu().numpy()
 
     def io_bytes(self):

@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import restate as RS
-from paper_2605_11536_b200.parallel import HaloExchanger, band_rows, halo_rows
+from paper_2605_11536_b200.parallel import HaloExchanger, balanced_bands, band_rows, halo_rows, row_weights
 
 
 def test_band_rows_partition():
@@ -30,6 +30,27 @@ def test_band_rows_partition():
                 assert a[1] == b[0]
             sizes = [b - a for a, b in rows]
             assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_balanced_bands_partition(world):
+    """Cost-balanced bands (bench.py at N > 1): contiguous, covering, at least
+    the halo thick, and no band heavier than an equal-row split's heaviest."""
+    rng = np.random.default_rng(world)
+    H, halo = 1080, 10
+    img = np.zeros((H, 64, 3))
+    img[300:700, :40] = rng.random((400, 40, 3))  # a lit block in the middle rows
+    w = row_weights(img)
+    bands = balanced_bands(w, world, halo)
+    assert bands[0][0] == 0 and bands[-1][1] == H and len(bands) == world
+    for a, b in zip(bands, bands[1:]):
+        assert a[1] == b[0]
+    assert min(b - a for a, b in bands) >= (halo if world > 1 else 1)
+    cost = lambda bs: max(w[a:b].sum() for a, b in bs)  # noqa: E731
+    equal = [band_rows(H, world, g) for g in range(world)]
+    assert cost(bands) <= cost(equal) + 1e-9
+    if world == 8:
+        assert cost(bands) < 0.75 * cost(equal)
 
 
 @pytest.mark.parametrize("radius", [0.5, 1.0, 3.0, 5.5, 10.0])
