@@ -298,9 +298,10 @@ def run_ours(args) -> None:
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
     emulated = BAND_ONLY[args.workload] if (ws == 1 and args.workload in BAND_ONLY) else None
-    # N > 1: bands of equal cost, not equal rows (the lit region of a frame is
-    # not spread evenly over the rows): rank 0 renders the first frames whole,
-    # weighs the rows by their lit pixels, and broadcasts the split
+    # N > 1: bands of equal cost, not equal rows (the shift work of a frame is
+    # far from even over the rows: C3's bottom eighth holds half of it): rank 0
+    # renders the first frames whole, weighs the rows by their device-counted
+    # shift cost and lit pixels, and broadcasts the split
     bands = None
     if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "1") != "0":
         import torch.distributed as dist
@@ -309,7 +310,13 @@ def run_ours(args) -> None:
             probe = parallel.BandSession(r, sd, cfg, plain=plain)
             for _ in range(2):
                 probe.step()
-            weights = parallel.row_weights(probe.read_image_host())
+            cost = None
+            if not plain:
+                probe.sess.row_cost(True)
+                for _ in range(2):
+                    probe.step()
+                cost = probe.sess.row_cost(False)
+            weights = parallel.row_weights(probe.read_image_host(), cost)
             probe.sess.close()
             halo = parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes) if not plain else 0
             obj = [parallel.balanced_bands(weights, ws, max(1, halo))]

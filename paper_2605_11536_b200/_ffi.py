@@ -145,6 +145,7 @@ def _declare(lib) -> None:
     lib.tofr_gpu_session_destroy.restype = None
     lib.tofr_gpu_session_work.argtypes = [vp, P(C.c_uint64)]
     lib.tofr_gpu_session_pool.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
+    lib.tofr_gpu_session_row_cost.argtypes = [vp, C.c_int32, P(C.c_uint64)]
     lib.tofr_gpu_kernel_timing.argtypes = [C.c_int32]
     lib.tofr_gpu_kernel_launches.argtypes = []
     lib.tofr_gpu_kernel_launches.restype = C.c_uint64
@@ -172,7 +173,7 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_last_ms", "tofr_gpu_session_io_bytes", "tofr_gpu_session_stream",
     "tofr_gpu_session_create_band", "tofr_gpu_session_band", "tofr_gpu_session_set_halo_exchange",
     "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
-    "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_pool", "tofr_gpu_session_destroy",
+    "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_pool", "tofr_gpu_session_row_cost", "tofr_gpu_session_destroy",
     "tofr_gpu_kernel_timing", "tofr_gpu_kernel_launches", "tofr_gpu_kernel_times", "tofr_gpu_kernel_times_reset",
     "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )

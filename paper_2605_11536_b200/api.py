@@ -426,6 +426,14 @@ class Session:
         self._r._check(self._r._lib.tofr_gpu_session_pool(self.handle, used, C.byref(cap)))
         return {"rows_used": [int(x) for x in used], "rows_cap": int(cap.value)}
 
+    def row_cost(self, enable: bool):
+        """Per-image-row shift cost counted since the last enable (numpy u64,
+        image height), then counting on (enable) or off."""
+        out = np.zeros(self.height, dtype=np.uint64)
+        self._r._check(self._r._lib.tofr_gpu_session_row_cost(self.handle, int(enable),
+                                                              out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
     def io_bytes(self):
         h2d, d2h = C.c_uint64(), C.c_uint64()
         self._r._check(self._r._lib.tofr_gpu_session_io_bytes(self.handle, C.byref(h2d), C.byref(d2h)))

@@ -184,6 +184,8 @@ struct tofr_session {
     bool sparse = false;
     size_t pool_rows = 0;
     int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
+    DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
+    bool row_cost_on = false;
     unsigned int* occ_host = nullptr;  // pinned [2][3]: pool rows per grid at the end of a frame
     size_t occ_seen = 0;               // largest of them over the frames flushed so far
     DevBuf res_slot[3], res_rows;
@@ -265,7 +267,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (auto& r : res_slot) r.release();
         res_rows.release();
-        for (DevBuf* b : {&read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+        for (DevBuf* b : {&row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
@@ -699,6 +701,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     PathCfg pc = path_cfg(c, center, width, s->scene);
     pc.gate_vel = vel ? 1 : 0;
     pc.work = s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 2;
+    pc.row_cost = s->row_cost_on ? s->row_cost.as<unsigned int>() : nullptr;
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
     unsigned long long* q = ctr + 3 * SC_COUNT + 1;  // persistent-kernel work counter (stream-ordered reuse)
@@ -1421,6 +1424,24 @@ int tofr_gpu_session_io_bytes(tofr_session* ss, uint64_t* h2d_per_step, uint64_t
     if (h2d_per_step) *h2d_per_step = ss->last_h2d;
     if (d2h_image) *d2h_image = uint64_t(ss->owned_pixels()) * 3 * sizeof(double);
     return TOFR_OK;
+}
+
+int tofr_gpu_session_row_cost(tofr_session* ss, int32_t enable, uint64_t* out) {
+    if (!ss) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        flush_all(ss);
+        size_t H = size_t(ss->H);
+        if (out) {
+            std::vector<unsigned int> h(H, 0);
+            if (ss->row_cost.p) ck(cudaMemcpy(h.data(), ss->row_cost.p, H * 4, cudaMemcpyDeviceToHost), "row cost");
+            for (size_t y = 0; y < H; ++y) out[y] = h[y];
+        }
+        if (enable) {
+            ss->row_cost.ensure(H * 4);
+            ck(cudaMemset(ss->row_cost.p, 0, H * 4), "memset");
+        }
+        ss->row_cost_on = enable != 0;
+    });
 }
 
 int tofr_gpu_session_pool(tofr_session* ss, uint64_t* rows_used, uint64_t* rows_cap) {

@@ -104,6 +104,10 @@ struct PathCfg {
     int gate_vel;  // velocity (Doppler) gate: the gated quantity is u, gate centre/width in u units
     int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
     unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
+    // per-image-row shift cost (Newton trials + setup of the jobs whose
+    // destination lies in the row; null = off): the load-balancing probe of
+    // multi-GPU row bands (tofr_gpu_session_row_cost)
+    unsigned int* row_cost;
 };
 
 // device work counters (cumulative per session): shift jobs, closest-hit rays,

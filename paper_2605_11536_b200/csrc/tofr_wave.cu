@@ -702,6 +702,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     double delta = 0, tol = 0, fnorm = 0, scale = 1;
     V2 step{0, 0};
     int iter = 0, bt = 0;
+    uint32_t trials = 0;  // trials of the current job (row-cost probe)
+    int drow = 0;
 
     for (;;) {
         // ---- refill: idle lanes take the next jobs (one atomic per warp), but only
@@ -731,6 +733,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
                     count = (jb.meta & JOB_COUNT) != 0;
                     if (count) SCTR(SC_ATTEMPTS, 1);
+                    drow = jb.dpy;
+                    trials = 0;
                     Meta mt = ld_meta(st, jb.item);
                     bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
                     bool ok = mt.valid && !(!same_frame && mt.skind == SK_SURFACE && F.geo_motion);
@@ -916,6 +920,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         }
         bool fin = false, conv = false;
         double jac = 0;
+        ++trials;
         if (accept) {
             if (!init) ++iter;
             init = false;
@@ -941,6 +946,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             scale *= 0.5;
         }
         if (fin) {
+            if (cfg.row_cost) atomicAdd(&cfg.row_cost[drow], trials + 4u);  // + setup and finish
             if (count) SCTR(SC_ITERATIONS, iter);
             if (conv && !F.mats[F.tri[ctri].mat].reconnectable) {
                 if (count) {

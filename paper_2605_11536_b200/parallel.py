@@ -32,12 +32,17 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
     return y0, y0 + base + (1 if rank < rem else 0)
 
 
-def row_weights(image: np.ndarray, base: float = 0.05) -> np.ndarray:
-    """Per-row cost proxy from a rendered frame ([H, W, 3]): pixels with a
-    non-zero estimate carry the reservoir / shift work, every pixel a little
-    (camera ray, empty merges)."""
+def row_weights(image: np.ndarray, shift_cost=None, base: float = 0.05, lit_cost: float = 2.0) -> np.ndarray:
+    """Per-row cost of a rendered frame ([H, W, 3]): the shift work counted on
+    the device (Newton trials + setup per shift job, by destination row:
+    Session.row_cost), the path trees of pixels with a non-zero estimate
+    (lit_cost trial-equivalents each) and a little for every pixel (camera
+    ray, empty merges)."""
     lit = (np.asarray(image) > 0).any(axis=2).sum(axis=1).astype(np.float64)
-    return lit + base * image.shape[1]
+    w = lit_cost * lit + base * image.shape[1]
+    if shift_cost is not None:
+        w = w + np.asarray(shift_cost, dtype=np.float64)
+    return w
 
 
 def balanced_bands(weights, world: int, min_rows: int = 1) -> list:

@@ -33,7 +33,11 @@ full = parallel.BandSession(r, sd, cfg)
 for _ in range(3):
     full.step()
 t_full = full.timed_steps(20, [0.0] * 6) / 20
-weights = parallel.row_weights(full.read_image_host())
+full.sess.row_cost(True)
+for _ in range(2):
+    full.step()
+cost = full.sess.row_cost(False)
+weights = parallel.row_weights(full.read_image_host(), cost)
 full.sess.close()
 eq = run([parallel.band_rows(h, n, g) for g in range(n)])
 bal_rows = parallel.balanced_bands(weights, n, parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes))
