@@ -298,12 +298,15 @@ def run_ours(args) -> None:
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
     emulated = BAND_ONLY[args.workload] if (ws == 1 and args.workload in BAND_ONLY) else None
-    # N > 1: bands of equal cost, not equal rows (the shift work of a frame is
-    # far from even over the rows: C3's bottom eighth holds half of it): rank 0
-    # renders the first frames whole, weighs the rows by their device-counted
-    # shift cost and lit pixels, and broadcasts the split
+    # N > 1, TOFR_BALANCE=1: bands of equal estimated cost instead of equal rows
+    # (rank 0 renders the first frames whole, weighs the rows by their
+    # device-counted shift cost and lit pixels, and broadcasts the split).  Off
+    # by default: emulated on one GPU (tools/band_probe2.py) it did not beat
+    # equal bands -- a C3 band's frame time is dominated by a ~1 ms latency floor
+    # (the serial Newton chains that end each shift batch), not by its share
+    # of the work
     bands = None
-    if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "1") != "0":
+    if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "0") == "1":
         import torch.distributed as dist
         obj = [None]
         if rank == 0:
