@@ -184,6 +184,9 @@ struct tofr_session {
     bool sparse = false;
     size_t pool_rows = 0;
     int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
+    // solve / finish overlap (ShiftQueue::done, ShiftOverlap; TOFR_OVERLAP=0 disables)
+    DevBuf wv_done, wv_fin_ctr;
+    uint32_t ov_epoch = 0;
     DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
     bool row_cost_on = false;
     unsigned int* occ_host = nullptr;  // pinned [2][3]: pool rows per grid at the end of a frame
@@ -250,6 +253,7 @@ struct tofr_session {
             if (e) cudaEventDestroy(e);
         for (auto& e : staged_ev)
             if (e) cudaEventDestroy(e);
+
         if (copy_stream) {
             cudaStreamSynchronize(copy_stream);
             cudaStreamDestroy(copy_stream);
@@ -267,7 +271,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (auto& r : res_slot) r.release();
         res_rows.release();
-        for (DevBuf* b : {&row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+        for (DevBuf* b : {&wv_done, &wv_fin_ctr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
@@ -546,6 +550,12 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
                 s->wv_mlist.ensure(own_items * sizeof(uint32_t));
+                const char* ovs = std::getenv("TOFR_OVERLAP");
+                if (!(ovs && ovs[0] == '0')) {
+                    s->wv_done.ensure(cap * sizeof(uint32_t));
+                    ck(cudaMemsetAsync(s->wv_done.p, 0, cap * sizeof(uint32_t), ctx->stream), "memset");
+                    s->wv_fin_ctr.ensure(16);
+                }
             }
         }
         const char* ord = std::getenv("TOFR_ORDER");
@@ -727,6 +737,11 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         wv.tsrc = s->wv_tsrc.as<uint64_t>();
         wv.rng_ctr = s->wv_rng.as<uint64_t>();
         wv.mlist = s->wv_mlist.as<uint32_t>();
+        if (s->wv_done.p) {
+            wv.q.done = s->wv_done.as<uint32_t>();
+            wv.ov.fin_ctr = s->wv_fin_ctr.as<unsigned long long>();
+            wv.ov.epoch = &s->ov_epoch;
+        }
     }
     if (s->order && s->wo_perm.p)
         wo = WorkOrder{s->wo_cls.as<uint8_t>(), s->wo_counts.as<uint32_t>(), s->wo_perm.as<uint32_t>()};

@@ -91,6 +91,17 @@ struct ShiftQueue {
     // shift succeeded.  JOB_FULL jobs also get the mapped record in chunks 1-21.
     ResStore out;
     uint32_t* ctl;  // [0] first job of the current batch, [1] end, [2] mark, [3] merge-list length
+    // solve -> finish overlap (TOFR_OVERLAP): the solve marks job k done with
+    // the batch's epoch after its hand-off is written; the finish, running
+    // concurrently on a second stream, waits for the mark (null: no overlap)
+    uint32_t* done = nullptr;
+    uint32_t epoch = 0;
+};
+
+// host side of the solve / finish overlap
+struct ShiftOverlap {
+    unsigned long long* fin_ctr = nullptr;  // the finish kernel's work counter (null: no overlap)
+    uint32_t* epoch = nullptr;              // host counter of shift batches
 };
 
 struct WaveScratch {
@@ -100,6 +111,7 @@ struct WaveScratch {
     uint64_t* tsrc;     // temporal: reprojected source pixel of each band pixel, or ~0
     uint64_t* rng_ctr;  // spatial: lane-10 RNG position per item
     uint32_t* mlist;    // items whose merge has a non-empty side (count in q.ctl[3])
+    ShiftOverlap ov;    // host only
 };
 
 // jobs per item a stage can enqueue (capacity planning)

@@ -124,6 +124,20 @@ __device__ __forceinline__ void sol_put(const ShiftQueue& q, uint32_t k, const V
     int2 ts = make_int2(tri, status);
     memcpy(&c6.y, &ts, 8);
     jst(q, 6, k, c6);
+    if (q.done) {  // publish: hand-off first, then the mark (release)
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(q.done + k), "r"(q.epoch) : "memory");
+    }
+}
+// finish side: wait until the solve of job k has published its hand-off
+__device__ __forceinline__ void sol_wait(const ShiftQueue& q, uint32_t k) {
+    if (!q.done) return;
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(q.done + k) : "memory");
+        if (v == q.epoch) break;
+        __nanosleep(64);
+    }
 }
 __device__ __forceinline__ void sol_fail(const ShiftQueue& q, uint32_t k) { sol_put(q, k, splat(0), -1, 0.0, 0); }
 
@@ -704,6 +718,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     int iter = 0, bt = 0;
     uint32_t trials = 0;  // trials of the current job (row-cost probe)
     int drow = 0;
+    bool pdl_fired = false;
 
     for (;;) {
         // ---- refill: idle lanes take the next jobs (one atomic per warp), but only
@@ -790,6 +805,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         if (__all_sync(0xffffffffu, exhausted)) {
             work_add(cfg.work, WK_CLOSEST, n_rays);
             break;
+        }
+        // the queue is drained (every job is in a resident warp's hands): let
+        // the dependent finish grid launch (PDL; a no-op without it)
+        if (q.done && __any_sync(0xffffffffu, exhausted) && lane == 0 && !pdl_fired) {
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            pdl_fired = true;
         }
 
         // ---- tail phase: once the queue is drained, idle lanes help the lowest
@@ -1006,6 +1027,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     if (blockIdx.x == 0 && threadIdx.x == 0 && cfg.work && njobs) atomicAdd(&cfg.work[WK_JOBS], (unsigned long long)njobs);
     TOFR_FOR_ITEMS(i, njobs, wq) {
         uint32_t k = j0 + uint32_t(i);
+        sol_wait(q, k);
         double2 c6 = jld(q, 6, k);
         int2 ts;
         memcpy(&ts, &c6.y, 8);
@@ -1479,8 +1501,8 @@ static int grid_n(size_t n, int block) {
 }
 
 static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0, const GHit* g1, ResStore st0,
-                       ResStore st1, const ShiftQueue& q, const PathCfg& cfg, unsigned long long* ctr,
-                       unsigned long long* wq, cudaStream_t s) {
+                       ResStore st1, ShiftQueue q, const ShiftOverlap& ov, const PathCfg& cfg,
+                       unsigned long long* ctr, unsigned long long* wq, cudaStream_t s) {
     bool same = F1.nodes == F0.nodes && F1.tri_isect == F0.tri_isect;
     size_t sm = frame_smem_bytes(F0) + (same ? 0 : frame_smem_bytes(F1));
     size_t cap_jobs = q.cap;
@@ -1498,17 +1520,40 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
     auto solve = cfg.gate_vel ? k_shift_solve<true, false> : (sp ? k_shift_solve<false, true> : k_shift_solve<false, false>);
     auto finish = cfg.gate_vel ? k_shift_finish<true, false>
                                : (sp ? k_shift_finish<false, true> : k_shift_finish<false, false>);
+    // Overlap (programmatic dependent launch): every solve CTA triggers the
+    // finish launch once its warps find the job queue drained, so the finish
+    // grid starts with the solve's tail and fills the SMs it leaves idle (its
+    // CTAs start as solve CTAs retire).  The finish does not wait for the solve
+    // grid: it takes each job once the solve has published that job's hand-off
+    // (ShiftQueue::done, release / acquire).  Every job has been handed to a
+    // resident solve warp before the finish can launch: no deadlock.
+    const bool overlap = ov.fin_ctr && q.done;
+    if (overlap)
+        q.epoch = ++*ov.epoch;
+    else
+        q.done = nullptr;
+    unsigned long long* fq = overlap ? ov.fin_ctr : wq;
     cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
+    if (overlap) cudaMemsetAsync(fq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_solve", s);
         solve<<<persistent_grid(reinterpret_cast<const void*>(solve), 128, sm, cap_jobs), 128, sm, s>>>(
             F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
     }
-    cudaMemsetAsync(wq, 0, sizeof(unsigned long long), s);
+    if (!overlap) cudaMemsetAsync(fq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_finish", s);
-        finish<<<persistent_grid(reinterpret_cast<const void*>(finish), 128, sm, cap_jobs), 128, sm, s>>>(
-            F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(unsigned(persistent_grid(reinterpret_cast<const void*>(finish), 128, sm, cap_jobs)));
+        lc.blockDim = dim3(128);
+        lc.dynamicSmemBytes = sm;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = overlap ? 1 : 0;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaLaunchKernelEx(&lc, finish, F0, F1, g0, g1, st0, st1, q, cfg, ctr, fq);
     }
 }
 
@@ -1531,7 +1576,7 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
         KScope ks("k_temporal_prep", s);
         k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
     }
-    run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, cfg, ctr, q, s);
+    run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, ws.ov, cfg, ctr, q, s);
     {
         KScope ks("k_temporal_apply", s);
         k_temporal_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cfg, frame_idx, cur, prev, ws);
@@ -1567,7 +1612,7 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
             KScope ks("k_spatial_prep_inv", s);
             k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
         }
-        run_shifts(F, F, g, g, src, dst, ws.q, cfg, ctr, q, s);
+        run_shifts(F, F, g, g, src, dst, ws.q, ws.ov, cfg, ctr, q, s);
         {
             KScope ks("k_spatial_apply", s);
             k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
