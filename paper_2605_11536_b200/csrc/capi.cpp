@@ -184,7 +184,7 @@ struct tofr_session {
     bool sparse = false;
     size_t pool_rows = 0;
     int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
-    // solve / finish overlap (ShiftQueue::done, ShiftOverlap; TOFR_OVERLAP=0 disables)
+    // solve / finish overlap (ShiftQueue::done, ShiftOverlap; opt-in TOFR_OVERLAP=1)
     DevBuf wv_done, wv_fin_ctr;
     uint32_t ov_epoch = 0;
     DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
@@ -550,8 +550,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
                 s->wv_mlist.ensure(own_items * sizeof(uint32_t));
+                // opt-in (TOFR_OVERLAP=1): measured 2-7% slower -- the finish warps
+                // take issue slots from the tail's serial Newton chains
                 const char* ovs = std::getenv("TOFR_OVERLAP");
-                if (!(ovs && ovs[0] == '0')) {
+                if (ovs && ovs[0] == '1') {
                     s->wv_done.ensure(cap * sizeof(uint32_t));
                     ck(cudaMemsetAsync(s->wv_done.p, 0, cap * sizeof(uint32_t), ctx->stream), "memset");
                     s->wv_fin_ctr.ensure(16);
