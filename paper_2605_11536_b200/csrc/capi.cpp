@@ -185,7 +185,7 @@ struct tofr_session {
     size_t pool_rows = 0;
     int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
     // solve / finish overlap (ShiftQueue::done, ShiftOverlap; opt-in TOFR_OVERLAP=1)
-    DevBuf wv_done, wv_fin_ctr;
+    DevBuf wv_done, wv_fin_ctr, wv_nbr;
     uint32_t ov_epoch = 0;
     DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
     bool row_cost_on = false;
@@ -271,7 +271,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (auto& r : res_slot) r.release();
         res_rows.release();
-        for (DevBuf* b : {&wv_done, &wv_fin_ctr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+        for (DevBuf* b : {&wv_done, &wv_fin_ctr, &wv_nbr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
@@ -550,6 +550,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
                 s->wv_mlist.ensure(own_items * sizeof(uint32_t));
+                s->wv_nbr.ensure(std::max<size_t>(1, nj) * s->owned_pixels() * sizeof(uint32_t));
                 // opt-in (TOFR_OVERLAP=1): measured 2-7% slower -- the finish warps
                 // take issue slots from the tail's serial Newton chains
                 const char* ovs = std::getenv("TOFR_OVERLAP");
@@ -739,6 +740,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         wv.tsrc = s->wv_tsrc.as<uint64_t>();
         wv.rng_ctr = s->wv_rng.as<uint64_t>();
         wv.mlist = s->wv_mlist.as<uint32_t>();
+        wv.nbr = s->wv_nbr.as<uint32_t>();
         if (s->wv_done.p) {
             wv.q.done = s->wv_done.as<uint32_t>();
             wv.ov.fin_ctr = s->wv_fin_ctr.as<unsigned long long>();

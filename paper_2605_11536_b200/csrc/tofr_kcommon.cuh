@@ -107,6 +107,29 @@ __device__ __forceinline__ bool spatial_neighbor(const Band& bd, int W, int H, i
     return c0.y > 0;
 }
 
+// neighbor_offset of (pixel, j) packed for the per-pass offset cache: dx in the
+// low 16 bits, dy in the high 16 (|dx|, |dy| <= radius)
+__device__ __forceinline__ uint32_t pack_offset(int dx, int dy) {
+    return (uint32_t(uint16_t(int16_t(dx)))) | (uint32_t(uint16_t(int16_t(dy))) << 16);
+}
+// spatial_neighbor with the offset taken from the cache
+__device__ __forceinline__ bool spatial_neighbor_at(const Band& bd, int W, int H, int B, int px, int py, int b,
+                                                    uint32_t off, const ResStore& src_grid, int& nx, int& ny,
+                                                    size_t& si) {
+    int dx = int(int16_t(uint16_t(off & 0xffffu))), dy = int(int16_t(uint16_t(off >> 16)));
+    nx = px + dx;
+    ny = py + dy;
+    if (nx == px && ny == py) return false;
+    if (nx < 0 || nx >= W || ny < 0 || ny >= H) return false;
+    if (ny < bd.r0 || ny >= bd.r1) {  // beyond the exchanged halo
+        atomicAdd(bd.err, 1ull);
+        return false;
+    }
+    si = (size_t(ny) * W + nx) * B + b;
+    double2 c0 = ld2(src_grid, 0, si);
+    return c0.y > 0;
+}
+
 __device__ __forceinline__ uint64_t spatial_rot_key(uint64_t pix, int pass, uint64_t seed, int frame_idx) {
     return mix64(pix * 1315423911u + (unsigned)(pass * 2654435761u) + seed + uint64_t(frame_idx) * 97);
 }

@@ -111,6 +111,7 @@ struct WaveScratch {
     uint64_t* tsrc;     // temporal: reprojected source pixel of each band pixel, or ~0
     uint64_t* rng_ctr;  // spatial: lane-10 RNG position per item
     uint32_t* mlist;    // items whose merge has a non-empty side (count in q.ctl[3])
+    uint32_t* nbr;      // spatial: neighbor_offset of (j, band pixel) for the pass [N * pixels]
     ShiftOverlap ov;    // host only
 };
 

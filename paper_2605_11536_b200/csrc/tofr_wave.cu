@@ -1356,6 +1356,24 @@ __global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int f
 // of the running output and the merge (the running output and the lane-10 RNG
 // position stay in HBM between neighbours; same draws in the same order).
 
+// neighbor_offset (pipeline.hpp:232-239) of every band pixel and neighbour for
+// this pass: the offsets depend on the pixel alone, so the prep and merge
+// kernels of every item (and every bin) read them instead of re-evaluating
+// the rotation hash and sin / cos
+__global__ void k_spatial_offsets(Band bd, int W, PathCfg cfg, SpatialParams sp, int pass, int frame_idx,
+                                  WaveScratch ws) {
+    size_t npx = size_t(bd.y1 - bd.y0) * W;
+    for (size_t lp = blockIdx.x * size_t(blockDim.x) + threadIdx.x; lp < npx; lp += size_t(gridDim.x) * blockDim.x) {
+        size_t p = size_t(bd.y0) * W + lp;
+        uint64_t rk = spatial_rot_key(uint64_t(p), pass, cfg.seed, frame_idx);
+        for (int j = 0; j < sp.neighbors; ++j) {
+            int dx, dy;
+            neighbor_offset(j, sp.neighbors, sp.radius, rk, dx, dy);
+            ws.nbr[size_t(j) * npx + lp] = pack_offset(dx, dy);
+        }
+    }
+}
+
 __global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
                                    int frame_idx, ResStore src_grid, WaveScratch ws) {
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
@@ -1370,13 +1388,14 @@ __global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid g
         int px = p % W, py = p / W;
         double dc, dw;
         gate_of(gate, b, dc, dw);
-        uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
+        const size_t npx = size_t(bd.y1 - bd.y0) * W, lp = size_t(p) - size_t(bd.y0) * W;
         for (int j = 0; j < sp.neighbors; ++j) {
             int nx = 0, ny = 0;
             size_t si = 0;
             // every non-empty neighbour is a forward shift attempt (counted even
             // when its record has no reconnection vertex, as the reference does)
-            bool want = live && spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
+            bool want = live &&
+                        spatial_neighbor_at(bd, W, H, B, px, py, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx, ny, si) &&
                         ld2(src_grid, 0, si).x > 0;
             uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
             if (k != kNoJob) job_put(ws.q, k, si, JOB_FULL | JOB_COUNT, nx, ny, px, py, dc, dc, dw);
@@ -1404,8 +1423,8 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
         size_t si = 0;
         bool want = false, merge = false;
         if (live) {
-            uint64_t rk = spatial_rot_key(uint64_t(py) * W + px, pass, cfg.seed, frame_idx);
-            if (!spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si)) {
+            const size_t npx = size_t(bd.y1 - bd.y0) * W, lp = size_t(p) - size_t(bd.y0) * W;
+            if (!spatial_neighbor_at(bd, W, H, B, px, py, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx, ny, si)) {
                 if (j == 0) {  // the output starts as the pass input
                     double2 c0 = ld2(src_grid, 0, it);
                     if (c0.x > 0)
@@ -1443,10 +1462,10 @@ __global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate
         int p = int(it / B), b = int(it % B);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
-        uint64_t rk = spatial_rot_key(pix, pass, cfg.seed, frame_idx);
         int nx, ny;
         size_t si = 0;
-        spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si);
+        const size_t npx = size_t(bd.y1 - bd.y0) * W, lp = size_t(p) - size_t(bd.y0) * W;
+        spatial_neighbor_at(bd, W, H, B, px, py, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx, ny, si);
         Res out, src;
         res_load_head(j == 0 ? src_grid : dst_grid, it, out);
         res_load_head(src_grid, si, src);
@@ -1595,6 +1614,11 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
     // The forward shifts of every neighbour and the inverse shifts of neighbour 0
     // (from the pass input) are independent: one shift batch.  Inverse shifts
     // of neighbour j > 0 need merge j - 1 and replace the previous inverse batch.
+    {
+        KScope ks("k_spatial_offsets", s);
+        size_t npx = size_t(bd.y1 - bd.y0) * F.cam.w;
+        k_spatial_offsets<<<grid_n(npx, 256), 256, 0, s>>>(bd, F.cam.w, cfg, sp, pass, frame_idx, ws);
+    }
     {
         KScope ks("k_spatial_prep_fwd", s);
         k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
