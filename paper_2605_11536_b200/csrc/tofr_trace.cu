@@ -28,7 +28,10 @@
 #include <type_traits>
 
 #define TOFR_OUTLINE_MATH 0
-#define TOFR_SHARED_DIV 0
+#ifndef TOFR_TRACE_SHARED_DIV
+#define TOFR_TRACE_SHARED_DIV 0
+#endif
+#define TOFR_SHARED_DIV TOFR_TRACE_SHARED_DIV
 
 #include "ktime.h"
 #include "tofr_kcommon.cuh"

@@ -75,3 +75,21 @@ def test_gated_session_equals_render_gated():
     for a, b in zip(stats, ref.stats):
         assert a["spatial"]["attempts"] == b["spatial"]["attempts"]
         assert a["temporal"]["success"] == b["temporal"]["success"]
+
+
+@pytest.mark.parametrize("mode", ["gated", "transient"])
+def test_spatial_radius_zero_is_a_no_op(mode):
+    """test_pipeline.cpp:132-145: a spatial pass of radius 0 only meets the
+    pixel itself (skipped), so it leaves every reservoir as it was."""
+    sd = scenes.bundled("cornell", 32)
+    base = dict(m_init=2, temporal=True, frames=3, seed=5)
+    if mode == "gated":
+        base["gate"] = GateSpec(F.GATE_LENGTH, 10.0, 0.4, 1.0)
+    else:
+        base.update(mode=F.MODE_TRANSIENT, bins=24, hist_t0=8.0, hist_bin_width=0.5)
+    r = Renderer(0)
+    render = r.render_gated if mode == "gated" else r.render_transient
+    off = render(sd, RenderConfig(**base, spatial_passes=0))
+    zero = render(sd, RenderConfig(**base, spatial_passes=1, spatial_neighbors=3, spatial_radius=0.0))
+    assert off.image.max() > 0
+    assert np.array_equal(zero.image, off.image)

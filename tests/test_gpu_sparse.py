@@ -135,3 +135,11 @@ def test_transient_row_batches_equal_one_batch():
     one = _render(scene, cfg, TOFR_SPARSE="1")
     many = _render(scene, cfg, TOFR_SPARSE="1", TOFR_WAVE_CAP="20000")
     assert np.array_equal(many.hist.rgb, one.hist.rgb)
+
+
+def test_queue_smaller_than_a_row_raises():
+    """A shift queue that cannot hold one image row's worst case is refused
+    up front (row batches need at least one row)."""
+    scene, cfg = CASES["temporal_spatial"]
+    with pytest.raises(TofrError, match="smaller than one image row"):
+        _render(scene, cfg, TOFR_WAVE_CAP="10")
