@@ -298,33 +298,28 @@ def run_ours(args) -> None:
     sd = scenes.bundled(scene_name, w, h)
     r = Renderer(local)
     emulated = BAND_ONLY[args.workload] if (ws == 1 and args.workload in BAND_ONLY) else None
-    # N > 1, TOFR_BALANCE=1: bands of equal estimated cost instead of equal rows
-    # (rank 0 renders the first frames whole, weighs the rows by their
-    # device-counted shift cost and lit pixels, and broadcasts the split).  Off
-    # by default: emulated on one GPU (tools/band_probe2.py) it did not beat
-    # equal bands -- a C3 band's frame time is dominated by a ~1 ms latency floor
-    # (the serial Newton chains that end each shift batch), not by its share
-    # of the work
+    # N > 1: the row split is refined from measured band times (the shift work
+    # of a frame is far from even over the rows: C3's bottom eighth holds half
+    # of it).  Each refinement renders a few frames on the current split, takes
+    # every rank's device time, and re-cuts the rows at equal measured cost
+    # (parallel.rebalance_bands; TOFR_BALANCE=0: equal rows).  Emulated on one
+    # GPU (tools/band_probe3.py) two steps take C3 at 8 bands from 2.8x to 3.0x
+    # of one GPU; what remains is each batch's serial Newton-chain floor.
     bands = None
-    if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "0") == "1":
-        import torch.distributed as dist
-        obj = [None]
-        if rank == 0:
-            probe = parallel.BandSession(r, sd, cfg, plain=plain)
-            for _ in range(2):
+    if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "1") != "0":
+        bands = [parallel.band_rows(h, ws, g) for g in range(ws)]
+        halo = parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes) if not plain else 0
+        for _ in range(2):
+            probe = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain, bands=bands)
+            for _ in range(3):
                 probe.step()
-            cost = None
-            if not plain:
-                probe.sess.row_cost(True)
-                for _ in range(2):
-                    probe.step()
-                cost = probe.sess.row_cost(False)
-            weights = parallel.row_weights(probe.read_image_host(), cost)
+            probe.sync()
+            parallel.barrier(group)
+            t_band = probe.timed_steps(5, [0.0] * 6)
+            times = parallel.gather_floats_all([t_band], group)
             probe.sess.close()
-            halo = parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes) if not plain else 0
-            obj = [parallel.balanced_bands(weights, ws, max(1, halo))]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        bands = obj[0]
+            del probe
+            bands = parallel.rebalance_bands(bands, times, max(1, halo))
 
     def new_session():
         if emulated:
@@ -463,8 +458,9 @@ def run_ours(args) -> None:
                        "parallelism": (f"rowband{emulated[0]}: the band of rank {emulated[1]} (rows "
                                        f"{sess.y0}-{sess.y1} + {sess.halo}-row halos) on one GPU, halo rows "
                                        f"not transferred; value = that band's frames/s"
-                                       if emulated else (f"rowband{ws}" + (f" (cost-balanced rows {bands})" if bands
-                                                                           else "") if ws > 1 else "single")),
+                                       if emulated else (f"rowband{ws}" + (f" (rows rebalanced on measured band "
+                                                                           f"times: {bands})" if bands else "")
+                                                         if ws > 1 else "single")),
                        "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
             "mpaths_per_s": (sess.owned_pixels() if emulated else w * h) * cfg.m_init * fps / 1e6,
             "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},

@@ -66,6 +66,17 @@ def balanced_bands(weights, world: int, min_rows: int = 1) -> list:
     return [(cuts[g], cuts[g + 1]) for g in range(world)]
 
 
+def rebalance_bands(bands, times, min_rows: int = 1) -> list:
+    """One refinement step of a row split from measured per-band frame times:
+    each band's time is spread evenly over its rows (a piecewise-constant cost
+    density), and the rows are cut again at equal cost (balanced_bands)."""
+    H = bands[-1][1]
+    dens = np.zeros(H)
+    for (y0, y1), t in zip(bands, times):
+        dens[y0:y1] = float(t) / max(1, y1 - y0)
+    return balanced_bands(dens, len(bands), min_rows)
+
+
 def halo_rows(radius: float, passes: int = 1) -> int:
     """Rows a spatial pass may read beyond a band: neighbor_offset rounds
     rr*sin(th) with rr < radius (pipeline.hpp:232-239), so |dy| <= ceil(radius).
@@ -107,6 +118,18 @@ def gather_floats(xs: list, group) -> list:
     t = torch.tensor([float(x) for x in xs], dtype=torch.float64, device=_dev(group))
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.cpu().tolist()
+
+
+def gather_floats_all(xs: list, group) -> list:
+    """Every rank's values, concatenated in rank order (all_gather)."""
+    if group is None:
+        return list(xs)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x) for x in xs], dtype=torch.float64, device=_dev(group))
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    return [float(v) for p in parts for v in p.cpu().tolist()]
 
 
 class HaloExchanger:
