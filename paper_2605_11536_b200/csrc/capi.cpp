@@ -446,9 +446,11 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if (kind == KIND_BARE) return s.release();
     bool plain = kind == KIND_PLAIN;
     s->plain = plain;
-    // opt-in (TOFR_PIPELINE=1): measured +1-3% frames/s, but the overlap muddles the
-    // per-kernel event timings the roofline is computed from
-    if (!plain && std::getenv("TOFR_PIPELINE") && std::strcmp(std::getenv("TOFR_PIPELINE"), "1") == 0) {
+    // on by default (TOFR_PIPELINE=0: off): +0.2-3.5% frames/s, bit-identical
+    // (test_pipelined_frames_equal_serial); the per-kernel event times of a
+    // pipelined run overlap
+    const char* pipe_env = std::getenv("TOFR_PIPELINE");
+    if (!plain && !(pipe_env && pipe_env[0] == '0')) {
         ck(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking), "stream");
         for (auto* e : {&s->ev_temporal[0], &s->ev_temporal[1], &s->ev_init[0], &s->ev_init[1]})
             ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");

@@ -93,3 +93,23 @@ def test_spatial_radius_zero_is_a_no_op(mode):
     zero = render(sd, RenderConfig(**base, spatial_passes=1, spatial_neighbors=3, spatial_radius=0.0))
     assert off.image.max() > 0
     assert np.array_equal(zero.image, off.image)
+
+
+@pytest.mark.parametrize("name", ["gated", "transient"])
+def test_pipelined_frames_equal_serial(name, monkeypatch):
+    """Pipelined sessions (the default) run the camera and initial sampling of
+    frame f on a side stream while frame f-1 finishes: the frames must equal
+    those of one stream (TOFR_PIPELINE=0)."""
+    sd = scenes.bundled("boxes_doppler", 40)
+    if name == "gated":
+        cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True,
+                           spatial_passes=1, spatial_neighbors=3, spatial_radius=5, frames=4)
+    else:
+        cfg = _transient_cfg(hist_t0=7.0, hist_bin_width=0.5, temporal=True, spatial_passes=1,
+                             spatial_neighbors=3, spatial_radius=4, frames=4)
+    render = Renderer(0).render_gated if name == "gated" else Renderer(0).render_transient
+    got = render(sd, cfg)
+    monkeypatch.setenv("TOFR_PIPELINE", "0")
+    ref = render(sd, cfg)
+    assert ref.image.max() > 0
+    assert np.array_equal(got.image, ref.image)
