@@ -189,7 +189,11 @@ struct tofr_session {
     uint32_t ov_epoch = 0;
     DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
     bool row_cost_on = false;
-    unsigned int* occ_host = nullptr;  // pinned [2][3]: pool rows per grid at the end of a frame
+    // res_rows block (32 B): u32 rows handed out per grid [3], pad, u64 sticky
+    // pool-overflow word (kErrPool; never reset: frames in flight share the
+    // per-frame error word, and a full pool is fatal); occ_host: pinned copy of
+    // the block per frame set [2][8 u32]
+    unsigned int* occ_host = nullptr;
     size_t occ_seen = 0;               // largest of them over the frames flushed so far
     DevBuf res_slot[3], res_rows;
     DevBuf image, accum, hist, hist_count;  // owned rows only
@@ -291,7 +295,7 @@ ResStore store_of(const tofr_session* s, const DevBuf& b) {
     // chunk planes 1..23 follow the header plane; plane c at pool + c * stride
     st.pool = b.as<double2>() + items - ptrdiff_t(st.stride);
     st.rows = s->res_rows.as<unsigned int>() + k;
-    st.err = s->ctr.as<unsigned long long>() + 3 * SC_COUNT;
+    st.err = reinterpret_cast<unsigned long long*>(s->res_rows.as<unsigned char>() + 16);
     st.planes = s->pool_planes;
     return st;
 }
@@ -507,10 +511,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                         s->res_slot[k].ensure(items * sizeof(uint32_t));
                         ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, items * sizeof(uint32_t), ctx->stream), "memset");
                     }
-                ck(cudaMallocHost(reinterpret_cast<void**>(&s->occ_host), 6 * sizeof(unsigned int)), "pinned");
-                std::memset(s->occ_host, 0, 6 * sizeof(unsigned int));
-                s->res_rows.ensure(4 * sizeof(unsigned int));
-                ck(cudaMemsetAsync(s->res_rows.p, 0, 4 * sizeof(unsigned int), ctx->stream), "memset");
+                ck(cudaMallocHost(reinterpret_cast<void**>(&s->occ_host), 16 * sizeof(unsigned int)), "pinned");
+                std::memset(s->occ_host, 0, 16 * sizeof(unsigned int));
+                s->res_rows.ensure(32);
+                ck(cudaMemsetAsync(s->res_rows.p, 0, 32, ctx->stream), "memset");
             }
         }
         s->res[0].ensure(rb);
@@ -648,8 +652,10 @@ void flush_set(tofr_session* s, int set) {
     }
     s->tot_frames++;
     if (s->sparse)
-        for (int k = 0; k < 3; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[3 * set + k]);
-    if (s->err_host[set] & kErrPool)
+        for (int k = 0; k < 3; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[8 * set + k]);
+    unsigned long long pool_err = 0;
+    if (s->sparse) std::memcpy(&pool_err, s->occ_host + 8 * set + 4, 8);
+    if ((s->err_host[set] | pool_err) & kErrPool)
         throw ScopeError(TOFR_ERR_OOM,
                          "transient reservoir pool full: more non-empty reservoirs than TOFR_POOL_FRAC of the grid "
                          "(raise it, or TOFR_SPARSE=0)");
@@ -842,7 +848,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                        stream),
        "flag");
     if (s->sparse)
-        ck(cudaMemcpyAsync(s->occ_host + 3 * set, s->res_rows.p, 3 * sizeof(unsigned int), cudaMemcpyDeviceToHost,
+        ck(cudaMemcpyAsync(s->occ_host + 8 * set, s->res_rows.p, 32, cudaMemcpyDeviceToHost,
                            stream),
            "occupancy");
     cudaEventRecord(ev[6], stream);
