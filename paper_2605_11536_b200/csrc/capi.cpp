@@ -1069,7 +1069,20 @@ int tofr_gpu_create(const int* devices, int n_devices, tofr_gpu** out) {
     int rc = guard(ctx.get(), [&] {
         ctx->device = (devices && n_devices > 0) ? devices[0] : 0;
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-        ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        {
+            // the frame's critical path runs on this stream at the highest
+            // priority: when a pipelined session's side stream (next frame's
+            // path trees, default priority) competes for SM slots, the block
+            // scheduler serves this stream's reuse kernels first
+            // (TOFR_STREAM_PRIORITY=0: default priority)
+            int least = 0, greatest = 0;
+            const char* pe = std::getenv("TOFR_STREAM_PRIORITY");
+            bool prio = !(pe && pe[0] == '0') && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
+            if (prio)
+                ck(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, greatest), "stream");
+            else
+                ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        }
         double x[32], w[32];
         gauss_rule32(x, w);
         set_gauss_rule(x, w, ctx->stream);
