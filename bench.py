@@ -347,17 +347,6 @@ def run_ours(args) -> None:
     work1 = sess.work()
     t_max = parallel.max_over_ranks(t_ms, group)
     frames = args.steps
-    # the next K frames again with every launch bracketed by CUDA events: the
-    # per-kernel times and the roofline's launch durations / units
-    F.kernel_times(reset=True)
-    F.kernel_timing(True)
-    work0k = sess.work()
-    sess.timed_steps(args.steps, [0.0] * 6)
-    work1k = sess.work()
-    F.kernel_timing(False)
-    ktimes = F.kernel_times(reset=True)
-    # clocks over both passes (the GPU is under load throughout)
-    clocks = clk.stop() if clk else None
     fps = frames / (t_max * 1e-3)
 
     # shift counters of one more (synchronous) frame: the work behind the time
@@ -386,6 +375,33 @@ def run_ours(args) -> None:
         p = sess.sess.pool()
         pool_info = {"rows_used_max": max(p["rows_used"]), "rows_cap": p["rows_cap"],
                      "rows_per_owned_item": max(p["rows_used"]) / max(1, sess.owned_pixels() * cfg.bins)}
+    clocks = clk.stop() if clk else None  # the value frames and the stats / latency frames
+
+    # per-kernel times and the roofline's launch durations / units: the same
+    # frames (W warm-up, K timed) on a fresh session with every launch bracketed
+    # by CUDA events, and one stream (pipelined frames overlap their kernels, so
+    # an event pair would also time the wait for SM slots)
+    sess.sess.close()
+    pipe_env = os.environ.get("TOFR_PIPELINE")
+    os.environ["TOFR_PIPELINE"] = "0"
+    try:
+        sess = new_session()
+    finally:
+        if pipe_env is None:
+            os.environ.pop("TOFR_PIPELINE", None)
+        else:
+            os.environ["TOFR_PIPELINE"] = pipe_env
+    for _ in range(args.warmup):
+        sess.step()
+    sess.sync()
+    parallel.barrier(group)
+    F.kernel_times(reset=True)
+    F.kernel_timing(True)
+    work0k = sess.work()
+    sess.timed_steps(args.steps, [0.0] * 6)
+    work1k = sess.work()
+    F.kernel_timing(False)
+    ktimes = F.kernel_times(reset=True)
 
     # e2e through the public API: step + image read-back to pinned host memory,
     # on a fresh session over the same frames as the device-timed run (W warm-up
