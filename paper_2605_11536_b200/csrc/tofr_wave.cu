@@ -43,7 +43,7 @@
 #endif
 // lanes needing re-projection rays a warp collects before it traces them
 #ifndef TOFR_RAYBATCH
-#define TOFR_RAYBATCH 8
+#define TOFR_RAYBATCH 12
 #endif
 #ifndef TOFR_SOLVE_REVERSE
 #define TOFR_SOLVE_REVERSE 0
