@@ -161,6 +161,18 @@ class ClockSampler:
         """Start of the timed region."""
         self.t0 = time.time()
 
+    def wait_ready(self) -> None:
+        """Wait (up to 3 s) for nvidia-smi's first line, so that even a short
+        timed region is sampled (call before the ranks' barrier)."""
+        t_end = time.time() + 3.0
+        while self.p is not None and time.time() < t_end:
+            try:
+                if os.path.getsize(self.f.name) > 0:
+                    break
+            except OSError:
+                break
+            time.sleep(0.02)
+
     def stop(self) -> dict:
         import datetime
         if self.p is None:
@@ -332,6 +344,8 @@ def run_ours(args) -> None:
     for _ in range(args.warmup):
         sess.step()
     sess.sync()
+    if clk:
+        clk.wait_ready()
     parallel.barrier(group)
 
     # timed region (value): K frames between CUDA events on the session stream,
