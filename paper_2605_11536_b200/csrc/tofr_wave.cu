@@ -212,6 +212,52 @@ __device__ __forceinline__ uint32_t block_queue_append(const ShiftQueue& q, bool
     return k;
 }
 
+// One block-wide append of up to 2 jobs per thread to the shift queue and of
+// the item to the merge list (2 barriers + 1 instead of 3 per append): returns
+// the thread's first job slot (its jobs are consecutive), kNoJob if none or
+// the queue is full (overflow bit raised).  `sh`: 2 * nwarps + 2 words.
+__device__ __forceinline__ uint32_t block_append_jobs(const WaveScratch& ws, uint32_t njobs, bool merge,
+                                                      uint32_t item, unsigned long long* err,
+                                                      unsigned long long* work, uint32_t* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t incl = njobs;  // inclusive warp scan of the job counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned mm = __ballot_sync(0xffffffffu, merge);
+    if (lane == 0) {
+        sh[warp] = wtot;
+        sh[nw + warp] = __popc(mm);
+        if (work && mm) atomicAdd(&work[WK_MERGES], (unsigned long long)__popc(mm));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tj = 0, tm = 0;
+        for (int w = 0; w < nw; ++w) {
+            uint32_t cj = sh[w], cm = sh[nw + w];
+            sh[w] = tj;
+            sh[nw + w] = tm;
+            tj += cj;
+            tm += cm;
+        }
+        sh[2 * nw] = tj ? atomicAdd(&ws.q.ctl[1], tj) : 0u;
+        sh[2 * nw + 1] = tm ? atomicAdd(&ws.q.ctl[3], tm) : 0u;
+    }
+    __syncthreads();
+    const uint32_t k = sh[2 * nw] + sh[warp] + (incl - njobs);
+    if (merge) ws.mlist[sh[2 * nw + 1] + sh[nw + warp] + __popc(mm & ((1u << lane) - 1))] = item;
+    __syncthreads();  // `sh` is reused by the next call
+    if (!njobs) return kNoJob;
+    if (size_t(k) + njobs > ws.q.cap) {
+        atomicAdd(err, 1ull << 32);
+        return kNoJob;
+    }
+    return k;
+}
+
 __device__ __forceinline__ void block_mlist_append(const WaveScratch& ws, bool want, uint32_t item,
                                                    unsigned long long* work, uint32_t* sh) {
     uint32_t k = block_append(&ws.q.ctl[3], want, sh);
@@ -1303,8 +1349,12 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
         double dc, dw, sc, sw;
         gate_of(cg, b, dc, dw);
         gate_of(pg, b, sc, sw);
-        uint32_t kf = block_queue_append(ws.q, fwd, bd.err, sh);
-        uint32_t ki = block_queue_append(ws.q, inv, bd.err, sh);
+        // the item's jobs (forward, then inverse) and its merge-list entry in one
+        // block-wide append
+        const uint32_t k0 = block_append_jobs(ws, uint32_t(fwd) + uint32_t(inv), merge, uint32_t(i), bd.err,
+                                              cfg.work, sh);
+        const uint32_t kf = (fwd && k0 != kNoJob) ? k0 : kNoJob;
+        const uint32_t ki = (inv && k0 != kNoJob) ? k0 + uint32_t(fwd) : kNoJob;
         if (kf != kNoJob) {
             job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
             ws.map_a[i] = kf;
@@ -1313,7 +1363,6 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
             job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
             ws.map_b[i] = ki;
         }
-        block_mlist_append(ws, merge, uint32_t(i), cfg.work, sh);
     }
 }
 
@@ -1443,12 +1492,11 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
                 }
             }
         }
-        uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
+        uint32_t k = block_append_jobs(ws, uint32_t(want), merge, uint32_t(i), bd.err, cfg.work, sh);
         if (k != kNoJob) {
             job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
             ws.map_b[i] = k;
         }
-        block_mlist_append(ws, merge, uint32_t(i), cfg.work, sh);
     }
 }
 
