@@ -247,7 +247,7 @@ int tofr_gpu_session_work(tofr_session* ss, uint64_t* out /* [5] */);
  * reservoir grids (rows_used[3]) and the rows per grid (*rows_cap; 0 = the
  * session's grids are dense).  Waits for the frames in flight. */
 int tofr_gpu_session_pool(tofr_session* ss, uint64_t* rows_used, uint64_t* rows_cap);
-/* per-image-row shift cost (Newton trials + 4 per shift job, by destination
+/* per-image-row shift cost (Newton iterations + 4 per shift job, by destination
  * row), for balancing multi-GPU row bands: enable = 1 zeroes the counters and
  * counts the following frames, enable = 0 stops; out (image height entries,
  * may be null) receives the counts so far.  Waits for the frames in flight. */

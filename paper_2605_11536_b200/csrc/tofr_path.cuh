@@ -104,7 +104,7 @@ struct PathCfg {
     int gate_vel;  // velocity (Doppler) gate: the gated quantity is u, gate centre/width in u units
     int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
     unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
-    // per-image-row shift cost (Newton trials + setup of the jobs whose
+    // per-image-row shift cost (Newton iterations + 4 per job whose
     // destination lies in the row; null = off): the load-balancing probe of
     // multi-GPU row bands (tofr_gpu_session_row_cost)
     unsigned int* row_cost;
@@ -698,6 +698,7 @@ struct Suffix {
     double u;  // suffix path velocity
     V3 v2;     // velocity of the p2 endpoint
     int ok;
+    int vobj = -1;  // object whose velocity field v2 is (velocity_at(F, vobj, p2) == v2)
 };
 
 // suffix_geometry (shiftmap.hpp:546-575)

@@ -417,6 +417,7 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
             double m19 = ld2(st, 19, item).y;
             memcpy(&mo, &m19, 8);
             s.v2 = velocity_at(F, mo.y, s.p2);  // obj2
+            s.vobj = mo.y;
         }
         s.ok = 1;
     } else if (skind == SK_LIGHT) {
@@ -431,6 +432,7 @@ __device__ __forceinline__ Suffix job_suffix(const FrameView& F, const ResStore&
         s.n2 = F.lsub.n;
         s.len = F.lsub.chain_len;
         s.v2 = vel ? velocity_at(F, F.lsub.obj, F.lsub.pos) : splat(0);
+        s.vobj = F.lsub.obj;
         s.u = vel ? dot(s.v2, F.lsub.wo_light) : 0.0;
         s.ok = 1;
     }
@@ -758,12 +760,13 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     // tangent frames are per-triangle lookups (FrameView::tframe): the start
     // point's is tframe[stri], the current point's tframe[ctri]
     StartTerms stt;
-    VelField vf{{0, 0, 0}, {0, 0, 0}};  // velocity gates only
+    // velocity gates: the endpoint velocities are re-evaluated per trial from
+    // their objects (velocity_at, the same inputs: the same values) instead of
+    // held as six doubles per lane
+    int vobj1 = -1, vobj2 = -1;
     double delta = 0, tol = 0, fnorm = 0, scale = 1;
     V2 step{0, 0};
     int iter = 0, bt = 0;
-    uint32_t trials = 0;  // trials of the current job (row-cost probe)
-    int drow = 0;
     bool pdl_fired = false;
 
     for (;;) {
@@ -794,8 +797,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
                     count = (jb.meta & JOB_COUNT) != 0;
                     if (count) SCTR(SC_ATTEMPTS, 1);
-                    drow = jb.dpy;
-                    trials = 0;
                     Meta mt = ld_meta(st, jb.item);
                     bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
                     bool ok = mt.valid && !(!same_frame && mt.skind == SK_SURFACE && F.geo_motion);
@@ -827,7 +828,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             double suffix_part = VEL ? suf.u : suf.len;
                             double gate_delta = jb.dc - jb.sc;
                             double target_local = src_total + gate_delta - prefix_part - suffix_part;
-                            if (VEL) vf = VelField{velocity_at(F, F.tri[pre.tri1].obj, pre.p1), suf.v2};
+                            if (VEL) {
+                                vobj1 = F.tri[pre.tri1].obj;
+                                vobj2 = suf.vobj;
+                            }
                             tol = 0.01 * jb.dw;
                             if (count) SCTR(SC_SOLVES, 1);
                             // start terms and delta = target - (field at the start
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 TOFR_BORROW3(stt.g3s) TOFR_BORROW(stt.gs.x) TOFR_BORROW(stt.gs.y) TOFR_BORROW(stt.lvs)
                 TOFR_BORROW(stt.Hs.a) TOFR_BORROW(stt.Hs.b) TOFR_BORROW(stt.Hs.c) TOFR_BORROW(stt.Hs.d)
                 if (VEL) {
-                    TOFR_BORROW3(vf.v1) TOFR_BORROW3(vf.v2)
+                    TOFR_BORROW(vobj1) TOFR_BORROW(vobj2)
                 }
 #undef TOFR_BORROW3
 #undef TOFR_BORROW
@@ -950,6 +954,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         __syncwarp(em);
         const Frame2 Jt = F.tframe[ttri];
         const Frame2 Js = F.tframe[stri];
+        VelField vf{{0, 0, 0}, {0, 0, 0}};
+        if (VEL) vf = VelField{velocity_at(F, vobj1, p1), velocity_at(F, vobj2, p2)};
         LcEval ev = field_eval<VEL>(F, F.tri[ttri].obj, vf, p1, p2, tpos, Jt, cfg.gauge != GAUGE_FIXED);
         if (init) {
             start_from(ev, Js, stt);
@@ -987,7 +993,6 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         }
         bool fin = false, conv = false;
         double jac = 0;
-        ++trials;
         if (accept) {
             if (!init) ++iter;
             init = false;
@@ -1013,7 +1018,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             scale *= 0.5;
         }
         if (fin) {
-            if (cfg.row_cost) atomicAdd(&cfg.row_cost[drow], trials + 4u);  // + setup and finish
+            if (cfg.row_cost)  // the job's destination row: Newton iterations + setup and finish
+                atomicAdd(&cfg.row_cost[job_get(q, job).dpy], uint32_t(iter) + 4u);
             if (count) SCTR(SC_ITERATIONS, iter);
             if (conv && !F.mats[F.tri[ctri].mat].reconnectable) {
                 if (count) {
