@@ -37,6 +37,9 @@
 #ifndef TOFR_WAVE_MINB
 #define TOFR_WAVE_MINB 4
 #endif
+#ifndef TOFR_FINISH_MINB
+#define TOFR_FINISH_MINB TOFR_WAVE_MINB
+#endif
 // idle lanes a warp of k_shift_solve collects before it refills them
 #ifndef TOFR_REFILL
 #define TOFR_REFILL 12
@@ -1060,7 +1063,7 @@ __device__ __forceinline__ bool occluded_n(const FrameView& F, const V3& a, cons
 __device__ __forceinline__ void out_fail(const ShiftQueue& q, uint32_t k) { st2(q.out, 0, k, 0.0, 0.0); }
 
 template <bool VEL, bool SP>
-__global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
+__global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
     k_shift_finish(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                    ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
     if (!SP) st0.slot = st1.slot = nullptr;
