@@ -320,7 +320,8 @@ def run_ours(args) -> None:
     bands = None
     if ws > 1 and args.workload not in BAND_ONLY and os.environ.get("TOFR_BALANCE", "1") != "0":
         bands = [parallel.band_rows(h, ws, g) for g in range(ws)]
-        halo = parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes) if not plain else 0
+        halo = (parallel.halo_rows(cfg.spatial_radius, cfg.spatial_passes, parallel.motion_rows_for(sd, cfg))
+                if not plain else 0)
         for _ in range(2):
             probe = parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain, bands=bands)
             for _ in range(3):

@@ -10,7 +10,7 @@
  *       <- SceneDef construction, parse_scene, load_scene
  *          (scene.hpp:417-429, scene_io.hpp:136-313)
  *   tofr_gpu_render_gated       <- render_gated           (pipeline.hpp:323-392)
- *   tofr_gpu_render_doppler     <- render_doppler         (pipeline.hpp:574-578)  [not built: returns TOFR_ERR_UNSUPPORTED]
+ *   tofr_gpu_render_doppler     <- render_doppler         (pipeline.hpp:574-578)  (velocity gates)
  *   tofr_gpu_render_transient   <- render_transient       (pipeline.hpp:396-528)
  *   tofr_gpu_render_transient_plain <- render_transient_plain (pipeline.hpp:531-571)
  *   tofr_gpu_reference          <- reference_render       (harness.hpp:16-30)

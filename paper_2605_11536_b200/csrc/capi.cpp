@@ -187,7 +187,7 @@ struct tofr_session {
     // solve / finish overlap (ShiftQueue::done, ShiftOverlap; opt-in TOFR_OVERLAP=1)
     DevBuf wv_done, wv_fin_ctr, wv_nbr;
     uint32_t ov_epoch = 0;
-    DevBuf row_cost;               // per image row shift cost (u32), counted while row_cost_on
+    DevBuf row_cost;               // per image row shift cost (u64), counted while row_cost_on
     bool row_cost_on = false;
     // res_rows block (32 B): u32 rows handed out per grid [3], pad, u64 sticky
     // pool-overflow word (kErrPool; never reset: frames in flight share the
@@ -326,10 +326,17 @@ void for_row_batches(const Band& bd, int nb, Fn&& fn) {
     }
 }
 
-// payload rows a compacted (sparse) halo of n items carries: the pool's share
+// payload rows a compacted (sparse) halo of n items carries.  The sender's
+// send buffer and the receiver's recv buffer must agree on the layout (the
+// payload offsets depend on cap), so cap is a function of n alone -- never of
+// a rank's own pool size, which depends on its free memory and band height.
+// TOFR_HALO_FRAC (default 0.5: C4 bands peak at ~36% non-empty) must be the
+// same on every rank; a halo with more non-empty reservoirs raises "pool full".
 size_t halo_cap(const tofr_session* s, size_t n) {
     if (!s->sparse || !n) return 0;
-    double frac = double(s->pool_rows) / double(std::max<size_t>(1, s->items_stored()));
+    double frac = 0.5;
+    if (const char* hf = std::getenv("TOFR_HALO_FRAC")) frac = std::atof(hf);
+    if (!(frac > 0)) frac = 0.5;
     size_t cap = size_t(double(n) * frac) + 4096;
     return std::min(n, cap);
 }
@@ -436,6 +443,9 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if ((y0 - s->r0) > (y1 - y0) || (s->r1 - y1) > (y1 - y0))
         throw ScopeError(TOFR_ERR_INVALID, "row band thinner than its halo (use fewer ranks)");
     s->cam_moves = !sc->s.camera.track.empty();
+    if (kind == KIND_RESTIR && cfg && cfg->temporal && s->cam_moves && halo == 0 && (y0 > 0 || y1 < s->H))
+        throw ScopeError(TOFR_ERR_INVALID,
+                         "row band of a moving camera with temporal reuse needs a reprojection halo (halo > 0)");
     for (auto& set : s->ev)
         for (auto& e : set) ck(cudaEventCreate(&e), "event");
     for (auto& e : s->read_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -722,7 +732,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     PathCfg pc = path_cfg(c, center, width, s->scene);
     pc.gate_vel = vel ? 1 : 0;
     pc.work = s->ctr.as<unsigned long long>() + 3 * SC_COUNT + 2;
-    pc.row_cost = s->row_cost_on ? s->row_cost.as<unsigned int>() : nullptr;
+    pc.row_cost = s->row_cost_on ? s->row_cost.as<unsigned long long>() : nullptr;
     HistSpec h{s->B, c.hist_t0, c.hist_bin_width};
     unsigned long long* ctr = s->ctr.as<unsigned long long>();
     unsigned long long* q = ctr + 3 * SC_COUNT + 1;  // persistent-kernel work counter (stream-ordered reuse)
@@ -806,7 +816,10 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         }
         cudaEventRecord(ev[3], stream);
         SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
-        for (int pass = 0; pass < c.spatial_passes; ++pass) {
+        // no neighbours or radius 0: spatial_reuse returns its input (pipeline.hpp:246),
+        // so the passes are skipped (every rank agrees: same config)
+        const int passes = (sp.neighbors > 0 && sp.radius > 0) ? c.spatial_passes : 0;
+        for (int pass = 0; pass < passes; ++pass) {
             if (halo) exchange_halo(s, cur, pass);
             reset_store(s, s->spare, stream);
             SpatialScratch scr;
@@ -1472,13 +1485,13 @@ int tofr_gpu_session_row_cost(tofr_session* ss, int32_t enable, uint64_t* out) {
         flush_all(ss);
         size_t H = size_t(ss->H);
         if (out) {
-            std::vector<unsigned int> h(H, 0);
-            if (ss->row_cost.p) ck(cudaMemcpy(h.data(), ss->row_cost.p, H * 4, cudaMemcpyDeviceToHost), "row cost");
+            std::vector<unsigned long long> h(H, 0);
+            if (ss->row_cost.p) ck(cudaMemcpy(h.data(), ss->row_cost.p, H * 8, cudaMemcpyDeviceToHost), "row cost");
             for (size_t y = 0; y < H; ++y) out[y] = h[y];
         }
         if (enable) {
-            ss->row_cost.ensure(H * 4);
-            ck(cudaMemset(ss->row_cost.p, 0, H * 4), "memset");
+            ss->row_cost.ensure(H * 8);
+            ck(cudaMemset(ss->row_cost.p, 0, H * 8), "memset");
         }
         ss->row_cost_on = enable != 0;
     });

@@ -107,7 +107,7 @@ struct PathCfg {
     // per-image-row shift cost (Newton iterations + 4 per job whose
     // destination lies in the row; null = off): the load-balancing probe of
     // multi-GPU row bands (tofr_gpu_session_row_cost)
-    unsigned int* row_cost;
+    unsigned long long* row_cost;
 };
 
 // device work counters (cumulative per session): shift jobs, closest-hit rays,

@@ -1022,7 +1022,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         }
         if (fin) {
             if (cfg.row_cost)  // the job's destination row: Newton iterations + setup and finish
-                atomicAdd(&cfg.row_cost[job_get(q, job).dpy], uint32_t(iter) + 4u);
+                atomicAdd(&cfg.row_cost[job_get(q, job).dpy], (unsigned long long)(iter) + 4ull);
             if (count) SCTR(SC_ITERATIONS, iter);
             if (conv && !F.mats[F.tri[ctri].mat].reconnectable) {
                 if (count) {

@@ -77,13 +77,25 @@ def rebalance_bands(bands, times, min_rows: int = 1) -> list:
     return balanced_bands(dens, len(bands), min_rows)
 
 
-def halo_rows(radius: float, passes: int = 1) -> int:
-    """Rows a spatial pass may read beyond a band: neighbor_offset rounds
-    rr*sin(th) with rr < radius (pipeline.hpp:232-239), so |dy| <= ceil(radius).
-    No spatial passes -> no halo."""
-    if passes <= 0:
-        return 0
-    return int(math.ceil(max(0.0, radius)))
+# rows of reprojection margin a band keeps for a moving camera's temporal reuse
+# (project() into the previous camera, pipeline.hpp:209-229, may land outside
+# the band); a reprojection beyond it raises instead of diverging
+MOTION_HALO_ROWS = 16
+
+
+def halo_rows(radius: float, passes: int = 1, motion_rows: int = 0) -> int:
+    """Rows a band keeps on each side: a spatial pass may read |dy| <=
+    ceil(radius) rows beyond it (neighbor_offset rounds rr*sin(th) with
+    rr < radius, pipeline.hpp:232-239), and a moving camera's temporal stage
+    reprojects up to `motion_rows` rows away.  Neither -> no halo."""
+    spatial = int(math.ceil(max(0.0, radius))) if passes > 0 else 0
+    return max(spatial, int(motion_rows))
+
+
+def motion_rows_for(scene_def, cfg) -> int:
+    """MOTION_HALO_ROWS when the camera is animated and temporal reuse is on."""
+    cam = getattr(scene_def, "camera", None)
+    return MOTION_HALO_ROWS if (cfg.temporal and cam is not None and getattr(cam, "track", None)) else 0
 
 
 def barrier(group) -> None:
@@ -225,7 +237,8 @@ class BandSession:
         H = scene_def.camera.height
         self.bands = list(bands) if bands else [band_rows(H, world, g) for g in range(world)]
         self.y0, self.y1 = rows if rows else self.bands[rank]
-        halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes) if (world > 1 and not plain) else 0
+        halo = (halo_rows(cfg.spatial_radius, cfg.spatial_passes, motion_rows_for(scene_def, cfg))
+                if (world > 1 and not plain) else 0)
         if world > 1 and min(b[1] - b[0] for b in self.bands) < halo:
             raise ValueError(f"{world} bands of a {H}-row image are thinner than the {halo}-row halo")
         self.halo = halo

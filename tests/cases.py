@@ -118,11 +118,28 @@ REFERENCE_CASES = {
     "ref_doppler": (lambda: scenes.bundled("boxes_doppler", 24), 4.0, gate(12.0, 0.5), 8, 9, 8),
 }
 
-# BASELINE.json configurations at their full sizes: the oracle renders
-# them on all host threads in seconds per frame; C2(ii) needs 84 GB in the
-# reference layout and is covered by the plain C2(i) run plus the small
-# transient cases above.
+# BASELINE.json configurations at their full sizes, or -- where the
+# reference's 624 B reservoirs do not fit the GPU box's host RAM -- at the
+# largest size the oracle renders in a few minutes with the config otherwise
+# unchanged: C2(ii) at 256^2 x 256 bins (21 GB of oracle grids; 512^2 needs
+# 84 GB per pair and ~10 min per frame), C4 reservoirs at 128x72 x 1024 bins
+# (18 GB), C5 at 256^2 over 25 frames of the gate sweep.
 FULL_CASES = {
+    "full_c2r_cornell_256_256bins": (lambda: scenes.bundled("cornell", 256, 256),
+                                     RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0,
+                                                  hist_bin_width=0.046875, m_init=1, temporal=True, m_cap=20,
+                                                  max_depth=6, frames=3, seed=1), "transient"),
+    "full_c4r_doppler_128x72_1024bins": (lambda: scenes.bundled("boxes_doppler", 128, 72),
+                                         RenderConfig(mode=F.MODE_TRANSIENT, bins=1024, hist_t0=7.0,
+                                                      hist_bin_width=0.01953125, m_init=1, max_depth=8,
+                                                      temporal=True, spatial_passes=1, spatial_neighbors=3,
+                                                      spatial_radius=10, m_cap=20, frames=3, seed=1),
+                                         "transient"),
+    "full_c5_cornell_wide_256_25frames": (lambda: scenes.bundled("cornell_wide", 256, 256),
+                                          RenderConfig(gate=gate(6.0, 0.0173), gate_step=0.01, m_init=1,
+                                                       temporal=True, spatial_passes=1, spatial_neighbors=3,
+                                                       spatial_radius=10, m_cap=20, max_depth=6, frames=25,
+                                                       seed=1), "gated"),
     "full_c3_boxes_doppler_1080p": (lambda: scenes.bundled("boxes_doppler", 1920, 1080),
                                     RenderConfig(gate=gate(12.0, 0.041), m_init=1, temporal=True, spatial_passes=1,
                                                  spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6,

@@ -15,7 +15,7 @@ import pytest
 from paper_2605_11536_b200 import _ffi as F
 from paper_2605_11536_b200 import scenes
 from paper_2605_11536_b200.api import GateSpec, RenderConfig, Renderer
-from paper_2605_11536_b200.parallel import _wrap, band_rows, halo_rows
+from paper_2605_11536_b200.parallel import _wrap, band_rows, halo_rows, motion_rows_for
 
 pytestmark = pytest.mark.gpu
 
@@ -42,15 +42,20 @@ CASES = {
     "moving_camera": (lambda: _moving_camera(40),
                       RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1, temporal=True,
                                    spatial_passes=1, spatial_neighbors=3, spatial_radius=4, frames=3)),
+    # temporal reuse only: the band keeps a reprojection halo (parallel.MOTION_HALO_ROWS)
+    "moving_camera_temporal_only": (lambda: _moving_camera(48),
+                                    RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1,
+                                                 temporal=True, frames=3)),
 }
 
 
-def _render_bands(sd, cfg, world):
+def _render_bands(sd, cfg, world, bands=None):
     import torch
     H = sd.camera.height
-    halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes)
+    halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes, motion_rows_for(sd, cfg))
+    bands = bands or [band_rows(H, world, g) for g in range(world)]
     rs = [Renderer(0) for _ in range(world)]
-    ss = [rs[g].session(sd, cfg, band=(*band_rows(H, world, g), halo)) for g in range(world)]
+    ss = [rs[g].session(sd, cfg, band=(*bands[g], halo)) for g in range(world)]
     dev = torch.device("cuda", 0)
     bufs = []
     for s in ss:
@@ -105,3 +110,29 @@ def test_bands_equal_full_frame(name, world):
     got = _render_bands(sd, cfg, world)
     assert ref.max() > 0
     assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"
+
+
+def test_sparse_bands_unequal_heights_and_pools(monkeypatch):
+    """Sparse transient grids with a memory-limited pool (TOFR_POOL_FRAC < 1)
+    and unequal band heights (edge bands keep one halo, middle bands two):
+    the compacted halo layout must agree between sender and receiver."""
+    monkeypatch.setenv("TOFR_POOL_FRAC", "0.6")
+    sd = scenes.bundled("cornell", 48)
+    cfg = RenderConfig(mode=F.MODE_TRANSIENT, bins=24, hist_t0=8.0, hist_bin_width=0.5, m_init=2,
+                       temporal=True, spatial_passes=2, spatial_neighbors=3, spatial_radius=4, frames=3)
+    full = Renderer(0).session(sd, cfg)
+    for _ in range(cfg.frames):
+        full.step(stats=False)
+    ref = full.read_image()
+    got = _render_bands(sd, cfg, 3, bands=[(0, 9), (9, 35), (35, 48)])
+    assert ref.max() > 0
+    assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"
+
+
+def test_moving_camera_band_without_halo_is_rejected():
+    """A sub-band of a moving camera with temporal reuse and no halo would read
+    reprojected reservoirs outside its rows: rejected up front."""
+    sd = _moving_camera(32)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1, temporal=True, frames=2)
+    with pytest.raises(Exception, match="reprojection halo"):
+        Renderer(0).session(sd, cfg, band=(0, 16, 0))

@@ -1,9 +1,10 @@
 """Full-size parity (BASELINE configs at 1080p / 512^2 x 256 bins) and
 bit-identity of the wavefront pipeline with the per-reservoir kernels.
 
-* GPU vs the CPU oracle on the exact bench configurations: >= 99.9% of pixels
-  within 1e-4 relative (north star), shift counters within 0.1%, plain
-  deposit counts bit-exact.
+* GPU vs the CPU oracle on the bench configurations (full size, or the largest
+  size the oracle's reservoirs fit in host RAM): >= 99.9% of pixels and
+  histogram bins within 1e-4 relative (north star), histogram counts and
+  every shift counter of every frame and stage integer-equal.
 * The wavefront reuse engine / path-tree state machine (default) against the
   per-item kernels (TOFR_REUSE=legacy TOFR_TRACE=legacy) in a separate
   process: identical arithmetic, so images and counters must be bit-identical.
@@ -55,13 +56,26 @@ def test_full_size_parity(renderer, ref, name):
     print(name, s)
     assert r.image.max() > 0
     assert s["within"] >= 0.999, s
-    if kind == "plain":
-        assert np.array_equal(g.hist.count, r.hist.count), "bin indexing differs from the oracle"
-    else:
-        tg, tr = _totals(g.stats), _totals(r.stats)
-        print(name, tg, tr)
-        for k in KEYS:
-            assert abs(tg[k] - tr[k]) <= max(2, 1e-3 * tr[k]), (k, tg, tr)
+    if g.hist is not None:
+        hs = summary(g.hist.rgb, r.hist.rgb)
+        print(name, "hist", hs)
+        assert hs["within"] >= 0.999, hs
+        assert np.array_equal(g.hist.count, r.hist.count), "histogram counts differ from the oracle"
+    if kind != "plain":
+        diffs = counter_diffs(g.stats, r.stats)
+        print(name, _totals(g.stats), _totals(r.stats))
+        assert not diffs, diffs
+
+
+def counter_diffs(gs, rs) -> dict:
+    """Every ShiftCounts field of every frame and stage that differs (integer-exact bar)."""
+    out = {}
+    for f, (fg, fr) in enumerate(zip(gs, rs)):
+        for stage in ("temporal", "spatial", "bin"):
+            for k in KEYS:
+                if fg[stage][k] != fr[stage][k]:
+                    out[f"f{f}.{stage}.{k}"] = (fg[stage][k], fr[stage][k])
+    return out
 
 
 _CHILD = r"""

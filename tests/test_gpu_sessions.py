@@ -77,20 +77,27 @@ def test_gated_session_equals_render_gated():
         assert a["temporal"]["success"] == b["temporal"]["success"]
 
 
-@pytest.mark.parametrize("mode", ["gated", "transient"])
-def test_spatial_radius_zero_is_a_no_op(mode):
+@pytest.mark.parametrize("mode", ["gated", "transient", "doppler"])
+@pytest.mark.parametrize("variant", ["radius0", "neighbors0"])
+def test_spatial_radius_zero_is_a_no_op(mode, variant):
     """test_pipeline.cpp:132-145: a spatial pass of radius 0 only meets the
-    pixel itself (skipped), so it leaves every reservoir as it was."""
-    sd = scenes.bundled("cornell", 32)
+    pixel itself (skipped), and one with no neighbours merges nothing
+    (pipeline.hpp:246), so it leaves every reservoir as it was -- including
+    the velocity chunks of a Doppler reservoir."""
+    sd = scenes.bundled("boxes_doppler" if mode == "doppler" else "cornell", 32)
     base = dict(m_init=2, temporal=True, frames=3, seed=5)
     if mode == "gated":
         base["gate"] = GateSpec(F.GATE_LENGTH, 10.0, 0.4, 1.0)
+    elif mode == "doppler":
+        base.update(gate=GateSpec(F.GATE_VELOCITY, -0.09, 0.06, 1.0), frame0=2)
     else:
         base.update(mode=F.MODE_TRANSIENT, bins=24, hist_t0=8.0, hist_bin_width=0.5)
     r = Renderer(0)
-    render = r.render_gated if mode == "gated" else r.render_transient
+    render = {"gated": r.render_gated, "transient": r.render_transient, "doppler": r.render_doppler}[mode]
     off = render(sd, RenderConfig(**base, spatial_passes=0))
-    zero = render(sd, RenderConfig(**base, spatial_passes=1, spatial_neighbors=3, spatial_radius=0.0))
+    sp = dict(spatial_neighbors=3, spatial_radius=0.0) if variant == "radius0" else \
+        dict(spatial_neighbors=0, spatial_radius=5.0)
+    zero = render(sd, RenderConfig(**base, spatial_passes=2, **sp))
     assert off.image.max() > 0
     assert np.array_equal(zero.image, off.image)
 

@@ -67,6 +67,22 @@ def test_halo_covers_reference_neighbour_offsets(radius):
                     worst = max(worst, abs(dy))
     assert worst <= h
     assert halo_rows(radius, passes=0) == 0
+    # a moving camera with temporal reuse keeps a reprojection margin even without spatial passes
+    assert halo_rows(radius, passes=0, motion_rows=16) == 16
+    assert halo_rows(radius, passes=1, motion_rows=16) == max(16, h)
+
+
+def test_motion_rows_only_for_animated_cameras_with_temporal_reuse():
+    from paper_2605_11536_b200 import scenes
+    from paper_2605_11536_b200.api import RenderConfig
+    from paper_2605_11536_b200.parallel import MOTION_HALO_ROWS, motion_rows_for
+    sd = scenes.bundled("cornell_wide", 16)
+    assert motion_rows_for(sd, RenderConfig(temporal=True)) == 0
+    base = sd.camera.base
+    sd.camera.track = [(0.0, scenes.CameraPose((0.0, 0.0, 3.0), base.forward, base.up)),
+                       (10.0, scenes.CameraPose((0.0, 0.02, 3.0), base.forward, base.up))]
+    assert motion_rows_for(sd, RenderConfig(temporal=True)) == MOTION_HALO_ROWS
+    assert motion_rows_for(sd, RenderConfig(temporal=False)) == 0
 
 
 def _free_port() -> int:
