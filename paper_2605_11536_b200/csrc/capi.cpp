@@ -196,7 +196,7 @@ struct tofr_session {
     unsigned int* occ_host = nullptr;
     size_t occ_seen = 0;               // largest of them over the frames flushed so far
     DevBuf res_slot[3], res_rows;
-    DevBuf image, accum, hist, hist_count;  // owned rows only
+    DevBuf image, accum, hist;  // owned rows only (plain sessions: accum = wide-band image accumulator)
     DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag + work counter
     DevBuf send_lo, send_hi, recv_lo, recv_hi;
     DevBuf wo_cls, wo_counts, wo_perm;  // cost-ordered reuse (TOFR_ORDER=0 disables)
@@ -275,7 +275,7 @@ struct tofr_session {
         for (auto& r : res) r.release();
         for (auto& r : res_slot) r.release();
         res_rows.release();
-        for (DevBuf* b : {&wv_done, &wv_fin_ctr, &wv_nbr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &hist_count, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
+        for (DevBuf* b : {&wv_done, &wv_fin_ctr, &wv_nbr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
                           &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
             b->release();
@@ -476,10 +476,11 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if (!s->transient && cfg->m_init < 0) throw ScopeError(TOFR_ERR_INVALID, "m_init < 0");
     size_t own = s->owned_pixels() * s->B;
     if (plain) {
-        s->hist.ensure(own * 3 * sizeof(double));
-        s->hist_count.ensure(own * sizeof(uint32_t));
-        ck(cudaMemsetAsync(s->hist.p, 0, own * 3 * sizeof(double), ctx->stream), "memset");
-        ck(cudaMemsetAsync(s->hist_count.p, 0, own * sizeof(uint32_t), ctx->stream), "memset");
+        // 32 B bin records {r, g, b, count} (hist_deposit) + the wide-band image accumulator
+        s->hist.ensure(own * 4 * sizeof(double));
+        ck(cudaMemsetAsync(s->hist.p, 0, own * 4 * sizeof(double), ctx->stream), "memset");
+        s->accum.ensure(s->owned_pixels() * 3 * sizeof(double));
+        ck(cudaMemsetAsync(s->accum.p, 0, s->owned_pixels() * 3 * sizeof(double), ctx->stream), "memset");
     } else {
         s->has_temporal = cfg->temporal ? 1 : 0;
         s->has_bin = (s->transient && cfg->bin_reuse) ? 1 : 0;
@@ -774,8 +775,8 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     s->camera_rays += uint64_t(s->r1 - s->r0) * s->W;
     if (s->plain) {
         size_t pr = size_t(s->W) * s->B;
-        launch_hist_plain(F, bd, g, pc, h, c.m_init, f, rows_base<double>(s->hist, s->y0, pr * 3),
-                          rows_base<uint32_t>(s->hist_count, s->y0, pr), q, stream);
+        launch_hist_plain(F, bd, g, pc, h, c.m_init, f, rows_base<double>(s->hist, s->y0, pr * 4),
+                          rows_base<double>(s->accum, s->y0, size_t(s->W) * 3), q, stream);
         for (int i = 1; i < 6; ++i) cudaEventRecord(ev[i], stream);
     } else {
         // the ellipsoidal and shrink initializers apply to length gates only; velocity
@@ -910,6 +911,30 @@ int guard(tofr_gpu* ctx, F&& fn) {
     }
 }
 
+// Histogram of a session's owned rows in the reference's layout: rgb (3 f64 per
+// bin) and, for plain sessions, the per-bin deposit counts (de-interleaved
+// from the 32 B bin records).
+void read_hist_records(tofr_session* s, double* rgb, std::vector<int64_t>* count) {
+    size_t items = s->owned_pixels() * s->B;
+    if (!s->plain) {
+        ck(cudaMemcpy(rgb, s->hist.p, items * 24, cudaMemcpyDeviceToHost), "histogram");
+        return;
+    }
+    std::vector<double> rec(items * 4);
+    ck(cudaMemcpy(rec.data(), s->hist.p, rec.size() * 8, cudaMemcpyDeviceToHost), "histogram");
+    if (count) count->resize(items);
+    for (size_t i = 0; i < items; ++i) {
+        rgb[3 * i + 0] = rec[4 * i + 0];
+        rgb[3 * i + 1] = rec[4 * i + 1];
+        rgb[3 * i + 2] = rec[4 * i + 2];
+        if (count) {
+            uint64_t c;
+            std::memcpy(&c, &rec[4 * i + 3], 8);
+            (*count)[i] = int64_t(c);
+        }
+    }
+}
+
 // Output of a (full-frame) session in RenderOutput form (pipeline.hpp:384-391,
 // :516-527, :563-570).
 void read_outputs(tofr_session* s, const tofr_render_config* cfg, tofr_output* out, bool plain) {
@@ -934,19 +959,17 @@ void read_outputs(tofr_session* s, const tofr_render_config* cfg, tofr_output* o
     }
     size_t items = npix * s->B;
     std::vector<double> rgb(items * 3);
-    ck(cudaMemcpy(rgb.data(), s->hist.p, rgb.size() * 8, cudaMemcpyDeviceToHost), "histogram");
+    std::vector<int64_t> cnt;
+    read_hist_records(s, rgb.data(), plain ? &cnt : nullptr);
     double k = plain ? 1.0 / std::max(1, frames) : (frames > 0 ? 1.0 / double(frames) : 1.0);
     if (plain || frames > 0)
         for (double& v : rgb) v *= k;
     if (out->hist_rgb) std::memcpy(out->hist_rgb, rgb.data(), rgb.size() * 8);
     if (out->hist_count) {
-        if (plain) {
-            std::vector<uint32_t> cnt(items);
-            ck(cudaMemcpy(cnt.data(), s->hist_count.p, items * 4, cudaMemcpyDeviceToHost), "counts");
-            for (size_t i = 0; i < items; ++i) out->hist_count[i] = cnt[i];
-        } else {
+        if (plain)
+            std::memcpy(out->hist_count, cnt.data(), items * 8);
+        else
             for (size_t i = 0; i < items; ++i) out->hist_count[i] = frames;
-        }
     }
     if (out->image) {
         for (size_t p = 0; p < npix; ++p) {
@@ -1367,7 +1390,12 @@ int tofr_gpu_session_read_image_async(tofr_session* ss, double* pinned_image, in
         stage.ensure(bytes);
         // the slot's previous host copy must be done before its staging buffer is rewritten
         ck(cudaStreamWaitEvent(st, ss->read_ev[slot], 0), "wait");
-        if (ss->transient) {
+        if (ss->plain) {
+            // wide-band image accumulated by the deposits, / frames
+            double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+            launch_scale3(ss->accum.as<double>(), ss->owned_pixels(), scale, stage.as<double>(), st);
+            ck(cudaGetLastError(), "image scale");
+        } else if (ss->transient) {
             // wide-band image of the histogram accumulated so far, / frames
             Band bd = band_of(ss, false);
             double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
@@ -1392,7 +1420,13 @@ int tofr_gpu_session_wait_read(tofr_session* ss, int32_t slot) {
 int tofr_gpu_session_read_image(tofr_session* ss, double* image) {
     if (!ss || !image) return TOFR_ERR_INVALID;
     return guard(ss->ctx, [&] {
-        if (ss->transient) {
+        if (ss->plain) {
+            size_t npix = ss->owned_pixels();
+            ss->image.ensure(npix * 3 * sizeof(double));
+            double scale = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
+            launch_scale3(ss->accum.as<double>(), npix, scale, ss->image.as<double>(), ss->ctx->stream);
+            ck(cudaGetLastError(), "image scale");
+        } else if (ss->transient) {
             // wide-band image of the histogram accumulated so far, / frames
             size_t npix = ss->owned_pixels();
             ss->image.ensure(npix * 3 * sizeof(double));
@@ -1415,18 +1449,17 @@ int tofr_gpu_session_read_histogram(tofr_session* ss, double* rgb, int64_t* coun
         flush_all(ss);
         size_t items = ss->owned_pixels() * ss->B;
         double k = ss->f > 0 ? 1.0 / double(ss->f) : 1.0;
-        if (rgb) {
-            ck(cudaMemcpy(rgb, ss->hist.p, items * 24, cudaMemcpyDeviceToHost), "histogram");
+        std::vector<double> tmp;
+        if (!rgb) tmp.resize(items * 3);
+        std::vector<int64_t> cnt;
+        read_hist_records(ss, rgb ? rgb : tmp.data(), (count && ss->plain) ? &cnt : nullptr);
+        if (rgb)
             for (size_t i = 0; i < items * 3; ++i) rgb[i] *= k;
-        }
         if (count) {
-            if (ss->plain) {
-                std::vector<uint32_t> c(items);
-                ck(cudaMemcpy(c.data(), ss->hist_count.p, items * 4, cudaMemcpyDeviceToHost), "counts");
-                for (size_t i = 0; i < items; ++i) count[i] = c[i];
-            } else {
+            if (ss->plain)
+                std::memcpy(count, cnt.data(), items * 8);
+            else
                 for (size_t i = 0; i < items; ++i) count[i] = ss->f;
-            }
         }
     });
 }

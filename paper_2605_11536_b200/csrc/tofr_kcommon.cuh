@@ -32,6 +32,33 @@ __device__ __forceinline__ void stage_frame(FrameView& F, unsigned char* smem, s
 }
 
 // ---------------------------------------------------------------------------
+// plain transient deposits (TransientHistogram::deposit, transport.hpp:121-126)
+//
+// A bin is one 32 B record {r, g, b (f64), count (u64)} -- the reference's two
+// arrays (rgb Vec3 + int64 count) interleaved so a deposit touches exactly one
+// DRAM sector -- at (y*W + x)*B + b.  Deposits are L2 reductions (RED.ADD.F64
+// / RED.ADD.64): fire-and-forget, the lane never waits on the old value.  Each
+// pixel's trees run on one lane, so its deposits reach a bin in emission order
+// (same-address operations of one thread keep program order), and the f64 sums
+// equal the reference's sequential `rgb += v`.  Deposits are sparse (1-3 per
+// path tree over 256-1024 bins), so there is nothing for a shared-memory
+// private copy to combine; the pixel's wide-band image (sum over its bins,
+// pipeline.hpp:563-569) is reduced into `img` alongside (L2-resident: 50 MB at
+// 1080p), so reading the image never rescans the histogram.
+__device__ __forceinline__ void hist_deposit(double* hist, double* img, size_t bin, size_t pix, const V3& v) {
+    double* r = hist + 4 * bin;
+    atomicAdd(r + 0, v.x);
+    atomicAdd(r + 1, v.y);
+    atomicAdd(r + 2, v.z);
+    atomicAdd(reinterpret_cast<unsigned long long*>(r + 3), 1ull);
+    if (img) {
+        atomicAdd(img + 3 * pix + 0, v.x);
+        atomicAdd(img + 3 * pix + 1, v.y);
+        atomicAdd(img + 3 * pix + 2, v.z);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // shift counters: per-thread u32, summed in shared memory, one u64 atomic per
 // counter and CTA (every thread of the CTA must reach the call)
 

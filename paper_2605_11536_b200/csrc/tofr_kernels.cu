@@ -810,9 +810,9 @@ __global__ void k_hist_image(const double* hist, int p0, int p1, int B, double s
         const double* h = hist + 3 * size_t(p) * B;
         double sx = 0, sy = 0, sz = 0;
         for (int b = lane; b < B; b += 32) {
-            sx += h[3 * b + 0];
-            sy += h[3 * b + 1];
-            sz += h[3 * b + 2];
+            sx += __ldcs(&h[3 * b + 0]);
+            sy += __ldcs(&h[3 * b + 1]);
+            sz += __ldcs(&h[3 * b + 2]);
         }
         for (int o = 16; o > 0; o >>= 1) {
             sx += __shfl_down_sync(0xffffffffu, sx, o);
@@ -829,15 +829,15 @@ __global__ void k_hist_image(const double* hist, int p0, int p1, int B, double s
 
 // ---------------------------------------------------------------------------
 // trace-only transient deposits (render_transient_plain, pipeline.hpp:531-571;
-// TransientHistogram::deposit, transport.hpp:121-126).  Each thread owns its
-// pixel's B bins, so deposits are plain read-modify-writes in emission order.
+// TransientHistogram::deposit, transport.hpp:121-126): nested-loop variant
+// (TOFR_TRACE=legacy); the default is k_trace<PlainSink2> (tofr_trace.cu).
 
 struct PlainSink {
     HistSpec h;
     int m_init;
-    double* rgb;
-    uint32_t* count;
-    size_t base;
+    double* hist;
+    double* img;
+    size_t base, pix;
     uint32_t* n_dep;
     __device__ bool wants(double len) const { return bin_of(h, len) >= 0; }
     __device__ void emit(const Cand& c, double mis, const RecSrc&) {
@@ -845,18 +845,14 @@ struct PlainSink {
         V3 val = c.f * (mis / c.pdf / m_init);
         int b = bin_of(h, c.len);
         if (b < 0) return;
-        size_t i = base + b;
-        rgb[3 * i + 0] += val.x;
-        rgb[3 * i + 1] += val.y;
-        rgb[3 * i + 2] += val.z;
-        count[i] += 1;
+        hist_deposit(hist, img, base + b, pix, val);
         ++*n_dep;
     }
 };
 
 __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
-                                                    HistSpec h, int m_init, int frame_idx, double* rgb,
-                                                    uint32_t* count, unsigned long long* q) {
+                                                    HistSpec h, int m_init, int frame_idx, double* hist,
+                                                    double* img, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -870,7 +866,7 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
         int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
-        PlainSink sink{h, m_init, rgb, count, size_t(p) * h.bins, &n_dep};
+        PlainSink sink{h, m_init, hist, img, size_t(p) * h.bins, size_t(p), &n_dep};
         GHit g = gbuf[p];
         for (int s = 0; s < m_init; ++s) {
             Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
@@ -1278,22 +1274,32 @@ void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec&
 }
 
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                       int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                       int m_init, int frame_idx, double* hist, double* img, unsigned long long* q,
                        cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    // the nested-loop kernel measured faster for plain deposits (every candidate
-    // in the histogram range is traced, so its lanes stay in step); the state
-    // machine is selected with TOFR_TRACE=wave
-    if (std::getenv("TOFR_TRACE") && std::strcmp(std::getenv("TOFR_TRACE"), "wave") == 0) {
-        launch_trace_plain(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q, s);
+    // path-tree state machine (no vertex history: plain deposits build no
+    // records); the nested-loop kernel with TOFR_TRACE=legacy
+    if (trace_wave()) {
+        launch_trace_plain(F, bd, g, cfg, h, m_init, frame_idx, hist, img, q, s);
         return;
     }
     size_t sm = frame_smem_bytes(F);
     {
         KScope ks("k_hist_plain", s);
-        TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, rgb, count, q);
+        TOFR_PERSISTENT(k_hist_plain, n, sm)(F, bd, g, cfg, h, m_init, frame_idx, hist, img, q);
     }
+}
+
+// image = accumulator * scale (plain sessions keep the wide-band image per deposit)
+__global__ void k_scale3(const double* a, size_t n, double scale, double* out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        out[i] = a[i] * scale;
+}
+void launch_scale3(const double* a, size_t n_pixels, double scale, double* out, cudaStream_t s) {
+    if (!n_pixels) return;
+    KScope ks("k_scale3", s);
+    k_scale3<<<grid_for(n_pixels * 3, 256), 256, 0, s>>>(a, n_pixels * 3, scale, out);
 }
 
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,

@@ -135,8 +135,10 @@ void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const
                         cudaStream_t s);
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
                             const HistSpec& h, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s);
+// plain deposits into 32 B bin records {r, g, b, count} (hist) and the per-pixel
+// wide-band accumulator img (3 doubles per pixel; may be null)
 void launch_trace_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                        int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                        int m_init, int frame_idx, double* hist, double* img, unsigned long long* q,
                         cudaStream_t s);
 void launch_trace_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
                             double width, int spp, uint64_t frame_key, double* mean, double* se,
@@ -170,8 +172,9 @@ void launch_shade_gated(ResStore cur, const Band& bd, int W, double center, doub
 void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec& h, double* hist,
                             cudaStream_t s);
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                       int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                       int m_init, int frame_idx, double* hist, double* img, unsigned long long* q,
                        cudaStream_t s);
+void launch_scale3(const double* a, size_t n_pixels, double scale, double* out, cudaStream_t s);
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
                       double width, int spp, uint64_t frame_key, double* mean, double* se, unsigned long long* q,
                       cudaStream_t s);

@@ -151,15 +151,19 @@ struct BinsSink {
     __device__ void flush(unsigned long long*) {}
 };
 
-// TransientHistogram::deposit of every candidate (f * mis / pdf / m_init)
+// TransientHistogram::deposit of every candidate (f * mis / pdf / m_init,
+// pipeline.hpp:547-556, transport.hpp:121-126) -- see hist_deposit
 struct PlainSink2 {
     HistSpec h;
     int m_init;
-    double* rgb;
-    uint32_t* count;
-    size_t base;
+    double* hist;  // 32 B bin records (HistBin)
+    double* img;   // per-pixel wide-band accumulator (3 doubles)
+    size_t base, pix;
     uint32_t deposits;
-    __device__ void begin(const PathCfg&, uint64_t, uint64_t, size_t p, int) { base = p * size_t(h.bins); }
+    __device__ void begin(const PathCfg&, uint64_t, uint64_t, size_t p, int) {
+        base = p * size_t(h.bins);
+        pix = p;
+    }
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
     __device__ bool wants(double len, double) const { return bin_of(h, len) >= 0; }
@@ -168,11 +172,7 @@ struct PlainSink2 {
         V3 val = c.f * (mis / c.pdf / m_init);
         int b = bin_of(h, c.len);
         if (b < 0) return;
-        size_t i = base + b;
-        rgb[3 * i + 0] += val.x;
-        rgb[3 * i + 1] += val.y;
-        rgb[3 * i + 2] += val.z;
-        count[i] += 1;
+        hist_deposit(hist, img, base + b, pix, val);
         ++deposits;
     }
     __device__ void end() {}
@@ -528,13 +528,13 @@ void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, c
 }
 
 void launch_trace_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
-                        int m_init, int frame_idx, double* rgb, uint32_t* count, unsigned long long* q,
+                        int m_init, int frame_idx, double* hist, double* img, unsigned long long* q,
                         cudaStream_t s) {
     PlainSink2 sk;
     sk.h = h;
     sk.m_init = m_init;
-    sk.rgb = rgb;
-    sk.count = count;
+    sk.hist = hist;
+    sk.img = img;
     sk.deposits = 0;
     launch_trace("k_trace_plain", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
 }

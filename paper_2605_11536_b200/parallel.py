@@ -86,10 +86,13 @@ MOTION_HALO_ROWS = 16
 def halo_rows(radius: float, passes: int = 1, motion_rows: int = 0) -> int:
     """Rows a band keeps on each side: a spatial pass may read |dy| <=
     ceil(radius) rows beyond it (neighbor_offset rounds rr*sin(th) with
-    rr < radius, pipeline.hpp:232-239), and a moving camera's temporal stage
-    reprojects up to `motion_rows` rows away.  Neither -> no halo."""
-    spatial = int(math.ceil(max(0.0, radius))) if passes > 0 else 0
-    return max(spatial, int(motion_rows))
+    rr < radius, pipeline.hpp:232-239).  Without spatial passes, a moving
+    camera's temporal stage still reprojects across band edges: it keeps
+    `motion_rows` rows (the spatial halo doubles as that margin otherwise).
+    Neither -> no halo."""
+    if passes > 0:
+        return int(math.ceil(max(0.0, radius)))
+    return int(motion_rows)
 
 
 def motion_rows_for(scene_def, cfg) -> int:

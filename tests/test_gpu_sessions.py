@@ -120,3 +120,18 @@ def test_pipelined_frames_equal_serial(name, monkeypatch):
     ref = render(sd, cfg)
     assert ref.image.max() > 0
     assert np.array_equal(got.image, ref.image)
+
+
+def test_plain_deposits_are_deterministic():
+    """Plain deposits are L2 reductions; a pixel's trees run on one lane, so
+    every bin receives its deposits in emission order: two renders are bit
+    identical (and the sums are the reference's sequential rgb += v)."""
+    sd = scenes.bundled("boxes_doppler", 40)
+    cfg = _transient_cfg(bins=200, hist_t0=7.0, hist_bin_width=0.1, m_init=4, max_depth=8, frames=2)
+    r = Renderer(0)
+    a = r.render_transient_plain(sd, cfg)
+    b = r.render_transient_plain(sd, cfg)
+    assert a.hist.count.sum() > 0
+    assert np.array_equal(a.hist.rgb, b.hist.rgb)
+    assert np.array_equal(a.hist.count, b.hist.count)
+    assert np.array_equal(a.image, b.image)
