@@ -209,6 +209,17 @@ class ClockSampler:
         return out
 
 
+def kernel_profile(workload: str, kernel: str | None):
+    """profiles/kernel_profile.json entry of (workload, kernel), or None."""
+    p = ROOT / "profiles" / "kernel_profile.json"
+    if not kernel or not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(f"{workload}:{kernel}")
+    except Exception:
+        return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -340,9 +351,15 @@ def run_ours(args) -> None:
                                         emulate=True)
         return parallel.BandSession(r, sd, cfg, rank=rank, world=ws, group=group, plain=plain, bands=bands)
 
+    # steady state: a ReSTIR frame's cost depends on the reservoirs' confidence
+    # M, which saturates at m_cap after m_cap frames of temporal reuse, so the
+    # warm-up runs at least m_cap + 5 frames (frame_ms_curve shows the ramp)
+    warm = args.warmup
+    if cfg.temporal and not plain:
+        warm = max(warm, cfg.m_cap + 5)
     sess = new_session()
     clk = ClockSampler(local) if rank == 0 else None
-    for _ in range(args.warmup):
+    for _ in range(warm):
         sess.step()
     sess.sync()
     if clk:
@@ -406,7 +423,7 @@ def run_ours(args) -> None:
             os.environ.pop("TOFR_PIPELINE", None)
         else:
             os.environ["TOFR_PIPELINE"] = pipe_env
-    for _ in range(args.warmup):
+    for _ in range(warm):
         sess.step()
     sess.sync()
     parallel.barrier(group)
@@ -417,6 +434,27 @@ def run_ours(args) -> None:
     work1k = sess.work()
     F.kernel_timing(False)
     ktimes = F.kernel_times(reset=True)
+    sess.sess.close()
+
+    # stage split and per-frame curve: the same frames on a fresh one-stream
+    # session without kernel instrumentation, stepped one at a time, so the
+    # stage events are sequential and sum to the frame (the pipelined value
+    # frames overlap frame f+1's camera + initial sampling with frame f's reuse)
+    os.environ["TOFR_PIPELINE"] = "0"
+    try:
+        sess = new_session()
+    finally:
+        if pipe_env is None:
+            os.environ.pop("TOFR_PIPELINE", None)
+        else:
+            os.environ["TOFR_PIPELINE"] = pipe_env
+    curve, stage_one = [], [0.0] * 6
+    for fr in range(warm + args.steps):
+        sess.step(stats=True)
+        tot, st6 = sess.sess.last_ms()
+        curve.append(round(tot, 4))
+        if fr >= warm:
+            stage_one = [a + b for a, b in zip(stage_one, st6)]
 
     # e2e through the public API: step + image read-back to pinned host memory,
     # on a fresh session over the same frames as the device-timed run (W warm-up
@@ -426,13 +464,13 @@ def run_ours(args) -> None:
     sess.sess.close()
     sess = new_session()
     parallel.barrier(group)
-    e2e_s = sess.run_e2e(args.steps, warm=args.warmup)
+    e2e_s = sess.run_e2e(args.steps, warm=warm)
     e2e_s = parallel.max_over_ranks(e2e_s * 1e3, group) * 1e-3
     h2d, d2h = sess.io_bytes()
 
     # roofline of the dominant kernel: algorithmic bytes per launch / average
     # launch duration (CUDA events on the session stream, timed region above)
-    avg = [x / args.steps for x in stage_tot]
+    avg = [x / args.steps for x in stage_one]
     names = ["init", "temporal", "bin", "spatial", "shade"]
     items = band_px * (cfg.bins if cfg.mode == F.MODE_TRANSIENT or plain else 1)
     # the dominant compute kernel (halo staging, which waits on the exchange at
@@ -456,13 +494,26 @@ def run_ours(args) -> None:
     algo = per_unit * units.get(unit, 0)
     pk = peaks()
     achieved = algo / dur_s / 1e9 if dur_s > 0 else 0.0
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(f"{args.workload}:{dom}")
-        except Exception:
-            traffic = None
+    # ncu evidence of the same kernel (profiles/kernel_profile.json, written by
+    # tools/kernel_profile.py from a --set full capture of one steady-state
+    # frame's launches of this workload): DRAM bytes and FP64 flops per unit of
+    # work, scaled to this run's units per launch
+    prof = kernel_profile(args.workload, dom)
+    upl = units.get(unit, 0)
+    traffic = round(prof["dram_bytes_per_unit"] * upl) if prof else None
+    fp64 = None
+    fp64_peak = r.fp64_peak_gflops() if rank == 0 else 0.0
+    if prof and dur_s > 0 and fp64_peak > 0:
+        fl = prof["fp64_flops_per_unit"] * upl
+        inst = prof["fp64_inst_per_unit"] * upl
+        fp64 = {"bound": "fp64", "kernel": dom, "achieved": fl / dur_s / 1e9, "peak": fp64_peak,
+                "peak_src": "measured (k_fp64_peak: DFMA chains on this device)", "unit": "GFLOP/s",
+                "frac": fl / dur_s / 1e9 / fp64_peak,
+                # --fmad=false (parity): DADD/DMUL issue like a DFMA but count one flop, so the
+                # pipe occupancy is the instruction rate over the DFMA instruction peak
+                "inst_frac": inst / dur_s / 1e9 / (fp64_peak / 2),
+                "flops_per_launch": fl, "flops_per_unit": prof["fp64_flops_per_unit"], "unit_of_work": unit,
+                "units_per_launch": upl, "avg_launch_ms": dur_s * 1e3, "source": prof["source"]}
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
     workv = {k: work1[k] - work0[k] for k in work1} if work1 else {}  # the value frames
     rays = (workv.get("rays_closest", 0) + workv.get("rays_any", 0)) if workv else 0
@@ -486,7 +537,7 @@ def run_ours(args) -> None:
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / frames, "higher_is_better": True, "scaling": "strong",
+            "warmup": warm, "warmup_requested": args.warmup, "ms_per_step": t_max / frames, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "scene": scene_name, "resolution": f"{w}x{h}",
                        "parallelism": (f"rowband{emulated[0]}: the band of rank {emulated[1]} (rows "
@@ -497,7 +548,16 @@ def run_ours(args) -> None:
                                                          if ws > 1 else "single")),
                        "l2": "inputs larger than L2 (reservoir grids 2 x 730 MB)"},
             "mpaths_per_s": (sess.owned_pixels() if emulated else w * h) * cfg.m_init * fps / 1e6,
-            "stage_ms": {n: round(a, 4) for n, a in zip(names + ["total"], avg)},
+            "stage_ms": {**{n: round(a, 4) for n, a in zip(names + ["total"], avg)},
+                         "note": "one-stream pass over the same frames (stages sum to its frame); the "
+                                 "pipelined value frame overlaps camera + init of f+1 with reuse of f"},
+            "frame_ms_curve": curve,
+            "work_per_frame": {k: v / frames for k, v in workv.items()} if workv else None,
+            # units of work of one value frame, per KERNEL_BYTES unit (tools/kernel_profile.py)
+            "units_per_frame": {"pixel": band_px, "item": items,
+                                "job": workv.get("shift_jobs", 0) / frames if workv else 0,
+                                "deposit": workv.get("deposits", 0) / frames if workv else 0,
+                                "merge": workv.get("merges", 0) / frames if workv else 0},
             "shift_stats_one_frame": shift_stats,
             "frame_latency": latency,
             "e2e": {"value": frames / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
@@ -509,6 +569,7 @@ def run_ours(args) -> None:
                          "avg_launch_ms": dur_s * 1e3, "launches": dom_n,
                          "note": "FP64 latency/divergence-bound shift and trace kernels: HBM fraction is small "
                                  "by construction (SURVEY 8d); see rays_per_s and kernel_ms"},
+            "roofline_fp64": fp64,
             "kernel_ms_per_step": kernel_ms,
             "reservoir_pool": pool_info,
             "rays_per_s": rays / t_s if t_s > 0 else None,

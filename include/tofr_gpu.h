@@ -271,6 +271,10 @@ uint64_t tofr_fnv1a64(const void* data, uint64_t n);
  * whose bits differ (0 expected) */
 int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
 
+/* measured FP64 throughput of the context's device (DFMA chains; GFLOP/s with
+ * 2 flops per DFMA): the FP64 roofline's peak */
+int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops);
+
 /* parity probes: rays[i] = {o.xyz, d.xyz, tmin, tmax}; mode 0 = closest hit
  * (Bvh::intersect_min) -> t, tri; mode 1 = occluded(a = o, b = d) -> tri = 0/1 */
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* s, double frame, const double* rays, int32_t n,

@@ -155,6 +155,7 @@ def _declare(lib) -> None:
     lib.tofr_fnv1a64.argtypes = [C.c_char_p, C.c_uint64]
     lib.tofr_fnv1a64.restype = C.c_uint64
     lib.tofr_gpu_selftest_div.argtypes = [vp, C.c_uint64, C.c_uint64, P(C.c_uint64)]
+    lib.tofr_gpu_fp64_peak.argtypes = [vp, P(C.c_double)]
     lib.tofr_gpu_probe_rays.argtypes = [vp, vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
                                         P(C.c_double), P(C.c_int32)]
     lib.tofr_scene_probe_rays_host.argtypes = [vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,

@@ -288,6 +288,12 @@ class Renderer:
                                                  max_depth, _dptr(mean), _dptr(se)))
         return mean, se
 
+    def fp64_peak_gflops(self) -> float:
+        """Measured FP64 DFMA throughput of this device (GFLOP/s): the FP64 roofline peak."""
+        v = C.c_double(0)
+        self._check(self._lib.tofr_gpu_fp64_peak(self.handle, C.byref(v)))
+        return float(v.value)
+
     def probe_rays(self, scene, frame: float, rays: np.ndarray, mode: int):
         s = self._scene(scene)
         rays = np.ascontiguousarray(rays, dtype=np.float64)

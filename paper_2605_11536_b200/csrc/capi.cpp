@@ -1599,6 +1599,14 @@ int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mi
     });
 }
 
+int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops) {
+    return guard(ctx, [&] {
+        if (!ctx || !gflops) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");
+        *gflops = measure_fp64_peak_gflops(ctx->stream);
+        ck(cudaGetLastError(), "fp64 peak");
+    });
+}
+
 int tofr_gpu_probe_rays(tofr_gpu* ctx, const tofr_scene* sc, double frame, const double* rays, int32_t n,
                         int32_t mode, double* out_t, int32_t* out_tri) {
     return guard(ctx, [&] {

@@ -829,8 +829,8 @@ __global__ void k_hist_image(const double* hist, int p0, int p1, int B, double s
 
 // ---------------------------------------------------------------------------
 // trace-only transient deposits (render_transient_plain, pipeline.hpp:531-571;
-// TransientHistogram::deposit, transport.hpp:121-126): nested-loop variant
-// (TOFR_TRACE=legacy); the default is k_trace<PlainSink2> (tofr_trace.cu).
+// TransientHistogram::deposit, transport.hpp:121-126): nested-loop walk
+// (default; TOFR_TRACE=wave: the k_trace<PlainSink2> state machine).
 
 struct PlainSink {
     HistSpec h;
@@ -850,6 +850,96 @@ struct PlainSink {
     }
 };
 
+// Path tree of a plain deposit run (Tracer::trace_tree + emit_nee,
+// transport.hpp:224-328, with build_rec = false and no ellipsoidal strategy,
+// pipeline.hpp:535-555): the same operations as trace_tree / emit_nee in the
+// same order, but only the current vertex is kept (no record is ever built,
+// and without the ellipsoidal MIS no earlier vertex is read), so the walk
+// needs no per-thread vertex history in local memory.
+template <class Sink>
+__device__ void trace_tree_deposit(const FrameView& F, const PathCfg& cfg, int px, int py, const GHit& g, Rng& rng,
+                                   Sink& sink) {
+    if (g.tri < 0) return;
+    V3 d0 = primary_dir(F.cam, px, py);
+    const GTriInfo& ti = F.tri[g.tri];
+    WalkV x;
+    x.p = F.cam.pos + d0 * g.t;
+    x.n = ti.n;
+    x.tri = g.tri;
+    x.mat = ti.mat;
+    x.wi = -d0;
+    x.fw = splat(1);
+    x.pdf = 1;
+    x.len = g.t;
+    const RecSrc none{nullptr, 0, nullptr, 0};
+    for (int d = 1; d + 1 <= cfg.max_depth && d < kMaxVerts - 1; ++d) {
+        const GMat& m = F.mats[x.mat];
+        if (m.kind != MAT_MIRROR) {  // emit_nee at x
+            Cand c;
+            bool ok = true;
+            if (F.light.regime == LIGHT_WIDE) {
+                LightSample ls;
+                ok = light_sample(F.light, x.p, ls);
+                if (ok) {
+                    c.len = x.len + ls.dist;
+                    ok = sink.wants(c.len) && !occluded(F, x.p, F.light.pos);
+                }
+                if (ok) {
+                    V3 f_at = eval_bsdf(m, x.n, x.wi, ls.dir);
+                    double cos_v = fabs(dot(x.n, ls.dir));
+                    c.f = x.fw * f_at * (cos_v) * ls.value;
+                }
+            } else {
+                ok = F.lsub.valid;
+                V3 dvec, wto;
+                if (ok) {
+                    dvec = F.lsub.pos - x.p;
+                    double dist = norm(dvec);
+                    ok = !(dist <= F.eps_ray * 2);
+                    if (ok) {
+                        wto = dvec / dist;
+                        c.len = x.len + dist + F.lsub.chain_len;
+                        ok = sink.wants(c.len) && !occluded(F, x.p, F.lsub.pos);
+                    }
+                }
+                if (ok) {
+                    V3 f_at = eval_bsdf(m, x.n, x.wi, wto);
+                    V3 f_s = eval_bsdf(F.mats[F.lsub.mat], F.lsub.n, -wto, F.lsub.wo_light);
+                    double gg = geom_term(x.p, x.n, F.lsub.pos, F.lsub.n);
+                    c.f = x.fw * f_at * gg * f_s * F.lsub.power;
+                }
+            }
+            if (ok && c.len > 0) {
+                c.pdf = x.pdf;
+                c.u = 0;
+                c.depth = d + 1;
+                if (luminance(c.f) > 0 && finite3(c.f)) sink.emit(c, 1.0, none);
+            }
+        }
+        if (d + 2 > cfg.max_depth) break;
+        double surv = rr_survival(d, cfg.use_rr);
+        if (surv < 1.0 && rng_next(rng) >= surv) break;
+        BsdfSample bs = sample_bsdf(m, x.n, x.wi, rng);
+        if (!bs.valid) break;
+        Hit nh;
+        if (!intersect(F, x.p, bs.wo, nh)) break;
+        const GTriInfo& wt = F.tri[nh.tri];
+        WalkV w;
+        w.p = nh.pos;
+        w.n = wt.n;
+        w.tri = nh.tri;
+        w.mat = wt.mat;
+        w.wi = -bs.wo;
+        double gt = geom_term(x.p, x.n, w.p, w.n);
+        V3 fr_val = m.kind == MAT_MIRROR ? m.albedo : eval_bsdf(m, x.n, x.wi, bs.wo);
+        w.fw = x.fw * fr_val * gt;
+        double cos_w = fabs(dot(w.n, bs.wo));
+        w.pdf = x.pdf * surv * bs.pdf * cos_w / (nh.t * nh.t);
+        w.len = x.len + nh.t;
+        x = w;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     HistSpec h, int m_init, int frame_idx, double* hist,
                                                     double* img, unsigned long long* q) {
@@ -858,8 +948,6 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
     stage_frame(F, smem, off);
     __syncthreads();
     int W = F.cam.w;
-    WalkV v[kMaxVerts];
-    NoEll ell;
     size_t n = size_t(bd.y1 - bd.y0) * W;
     uint32_t n_dep = 0;
     TOFR_FOR_ITEMS(i, n, q) {
@@ -870,8 +958,7 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
         GHit g = gbuf[p];
         for (int s = 0; s < m_init; ++s) {
             Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
-            Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
-            trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+            trace_tree_deposit(F, cfg, px, py, g, rng, sink);
         }
     }
     work_add(cfg.work, WK_DEPOSITS, n_dep);
@@ -986,6 +1073,52 @@ __global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long* ba
             local += __double_as_longlong(got[j]) != __double_as_longlong(ref[j]);
     }
     if (local) atomicAdd(bad, local);
+}
+
+// FP64 issue peak (the FP64 roofline's denominator, measured, not a data-sheet
+// number): 8 independent DFMA chains per thread, enough warps per SM to hide
+// the pipe latency.  flops = 2 per DFMA.
+__global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, double m, double c) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        a0 = __fma_rn(a0, m, c);
+        a1 = __fma_rn(a1, m, c);
+        a2 = __fma_rn(a2, m, c);
+        a3 = __fma_rn(a3, m, c);
+        a4 = __fma_rn(a4, m, c);
+        a5 = __fma_rn(a5, m, c);
+        a6 = __fma_rn(a6, m, c);
+        a7 = __fma_rn(a7, m, c);
+    }
+    double sum = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (sum == 12345.678) out[0] = sum;  // keeps the chains alive
+}
+double measure_fp64_peak_gflops(cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    if (cudaMalloc(&out, 8) != cudaSuccess) return 0;
+    const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, s);
+        k_fp64_peak<<<blocks, threads, 0, s>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double fl = 2.0 * 8.0 * double(iters) * blocks * threads;
+        if (rep > 0 && ms > 0) best = fl / (ms * 1e-3) / 1e9 > best ? fl / (ms * 1e-3) / 1e9 : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return best;
 }
 
 void launch_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s) {
@@ -1278,9 +1411,11 @@ void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const 
                        cudaStream_t s) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
-    // path-tree state machine (no vertex history: plain deposits build no
-    // records); the nested-loop kernel with TOFR_TRACE=legacy
-    if (trace_wave()) {
+    // nested-loop walk without vertex history (trace_tree_deposit): measured
+    // faster than the path-tree state machine for plain deposits, where every
+    // candidate in the histogram range is traced and lanes stay in step
+    // (C4 plain 0.99 vs 1.17 ms per frame); the state machine with TOFR_TRACE=wave
+    if (std::getenv("TOFR_TRACE") && std::strcmp(std::getenv("TOFR_TRACE"), "wave") == 0) {
         launch_trace_plain(F, bd, g, cfg, h, m_init, frame_idx, hist, img, q, s);
         return;
     }

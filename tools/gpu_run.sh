@@ -24,6 +24,17 @@ for s in "$@"; do
       ncu -i $f.ncu-rep --page source --print-source cuda,sass --csv --launch-count 1 > /tmp/src.csv 2>/dev/null
       python tools/ncu_lines.py /tmp/src.csv 30 > ${f/full_/lines_}.txt 2>&1
       rm -f $f.ncu-rep ;;
+    kprof) # kprof:<wl>:<kernel>:<launches per frame>:<warm> -> profiles-ready kernel_profile.json entry
+      W=${d:-25}; L=${c:-1}; f=$O/kprof_${a}_$b; K=$b
+      case $b in k_trace_*) K=k_trace ;; esac   # the library names k_trace's instantiations per sink
+      timeout 1800 ncu --set full --metrics smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum \
+          --clock-control none --import-source on -k regex:"^$K(<|\\(|$)" -s $((W * L)) -c $L -o $f \
+          python bench.py --workload $a --steps 1 --warmup $W --no-cpu-baseline > $f.json 2> $f.err
+      python tools/kernel_profile.py --out $O/kernel_profile.json --wl $a --kernel $b --bench $f.json $f.ncu-rep >> $O/kprof.log 2>&1
+      python tools/ncu_summary.py full $f.ncu-rep > $f.txt 2>&1
+      ncu -i $f.ncu-rep --page source --print-source cuda,sass --csv --launch-count 1 > /tmp/src.csv 2>/dev/null
+      python tools/ncu_lines.py /tmp/src.csv 30 > ${f/kprof_/lines_}.txt 2>&1
+      rm -f $f.ncu-rep; tail -1 $O/kprof.log ;;
     cmd) eval "$a" > $O/cmd_${b:-x}.log 2>&1; tail -5 $O/cmd_${b:-x}.log ;;
   esac
 done
