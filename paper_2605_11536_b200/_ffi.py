@@ -176,7 +176,7 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
     "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_pool", "tofr_gpu_session_row_cost", "tofr_gpu_session_destroy",
     "tofr_gpu_kernel_timing", "tofr_gpu_kernel_launches", "tofr_gpu_kernel_times", "tofr_gpu_kernel_times_reset",
-    "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
+    "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_fp64_peak", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )
 
 
