@@ -92,6 +92,26 @@ WORKLOADS = {
                          m_cap=20, seed=1),
             "C4 (reservoirs): boxes_doppler 1920x1080 transient 1024 bins [7,27), depth 8, render_transient "
             "temporal + 1x3 spatial r10 per bin, row bands with reservoir halo exchange"),
+    # transient ReSTIR at 1080p on one GPU, the paper's transient setting (temporal
+    # reuse only) on the C2 scene and bin range
+    "t1080": ("cornell", 1920, 1080,
+              RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=1,
+                           temporal=True, m_cap=20, max_depth=6, seed=1),
+              "transient 1080p: cornell 1920x1080, 256 bins [8,20), render_transient reservoirs, temporal reuse "
+              "only (the paper's transient setting)"),
+    "t1080b64": ("cornell", 1920, 1080,
+                 RenderConfig(mode=F.MODE_TRANSIENT, bins=64, hist_t0=8.0, hist_bin_width=0.1875, m_init=1,
+                              temporal=True, m_cap=20, max_depth=6, seed=1),
+                 "transient 1080p: cornell 1920x1080, 64 bins [8,20), render_transient reservoirs, temporal reuse "
+                 "only (the paper's transient setting)"),
+    # the paper's gated timing (256x256 NLOS scan, ellipsoidal
+    # initial sampling + temporal + spatial reuse, 4 ms/image on an RTX 3090),
+    # on the bundled wide-light scene with a narrow gate
+    "nlos": ("cornell_wide", 256, 256,
+             RenderConfig(gate=_gate(6.0, 0.01), m_init=1, init=F.INIT_ELLIPSOIDAL, temporal=True, spatial_passes=1,
+                          spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+             "NLOS-style gated: cornell_wide 256x256, gate tau=6.0 dtau=0.01, ellipsoidal initial sampling + "
+             "temporal + 1x3 spatial r10 (paper: 4 ms/image on an RTX 3090)"),
 }
 
 PLAIN = {"c2p", "c4p"}
@@ -240,8 +260,13 @@ def cpu_reference_sample(wl: str, frames: int = 2) -> dict:
     cores = os.cpu_count() or 1
     R.set_threads(cores)
     sd = scenes.bundled(scene_name, w, h)
-    if wl == "c2r":  # 512^2 x 256 bins of 624 B reservoirs needs 84 GB: time 128^2 bands-equivalent
-        sd = scenes.bundled(scene_name, 128, 128)
+    # render_transient's 624 B reservoirs per pixel-bin do not fit host RAM at the
+    # workload's size (512^2 x 256 bins: 84 GB per grid pair): time a 128-pixel-wide
+    # image of the same aspect and scale by the pixel count (labelled in `sample`)
+    scaled = cfg.mode == F.MODE_TRANSIENT and wl not in PLAIN
+    sw, sh = (128, max(1, round(128 * h / w))) if scaled else (w, h)
+    if scaled:
+        sd = scenes.bundled(scene_name, sw, sh)
     rs = R.RefScene(sd)
     c = RenderConfig(**{**cfg.__dict__})
     c.frames = frames
@@ -250,11 +275,11 @@ def cpu_reference_sample(wl: str, frames: int = 2) -> dict:
     t0 = time.perf_counter()
     fn(rs, c)
     dt = time.perf_counter() - t0
-    if wl == "c2r":
-        dt *= (w * h) / (128 * 128)  # extrapolated to the full image (labelled in the sample text)
+    if scaled:
+        dt *= (w * h) / (sw * sh)  # extrapolated to the full image (labelled in the sample text)
     drv = "render_transient_plain" if wl in PLAIN else ("render_transient" if cfg.mode == F.MODE_TRANSIENT
                                                          else "render_gated")
-    what = (f"{drv}(frames={frames}) at 128x128, time scaled x{(w * h) // (128 * 128)} to {w}x{h}" if wl == "c2r"
+    what = (f"{drv}(frames={frames}) at {sw}x{sh}, time scaled x{(w * h) / (sw * sh):.0f} to {w}x{h}" if scaled
             else f"{drv}(frames={frames}) of the full {w}x{h} workload")
     return {"seconds": dt, "frames": frames, "cores": R.threads(), "pixels": w * h, "what": what}
 

@@ -124,6 +124,7 @@ struct tofr_gpu {
     // collectors finalise handles in arbitrary order)
     int live_sessions = 0;
     bool closing = false;
+    const void* l2_owner = nullptr;  // session holding the stream's persisting L2 window
 };
 
 namespace {
@@ -264,6 +265,14 @@ struct tofr_session {
         }
         if (err_host) cudaFreeHost(err_host);
         if (occ_host) cudaFreeHost(occ_host);
+        if (ctx && ctx->l2_owner == this) {  // drop the persisting L2 window over our buffer
+            cudaStreamAttrValue a;
+            std::memset(&a, 0, sizeof(a));
+            cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+            cudaCtxResetPersistingL2Cache();
+            cudaGetLastError();
+            ctx->l2_owner = nullptr;
+        }
         release_buffers();
         if (ctx && --ctx->live_sessions == 0 && ctx->closing) release_ctx(ctx);
     }
@@ -423,6 +432,31 @@ void check_config(const tofr_render_config* c) {
 
 enum SessionKind { KIND_RESTIR = 0, KIND_PLAIN = 1, KIND_BARE = 2 };
 
+// Persisting L2 access-policy window on the context stream over [p, p + bytes),
+// owned by session `owner` (its destructor clears it).
+void set_l2_window(tofr_gpu* ctx, const void* owner, void* p, size_t bytes) {
+    int dev = 0, max_persist = 0, max_win = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist <= 0 || max_win <= 0) return;
+    cudaStreamAttrValue a;
+    std::memset(&a, 0, sizeof(a));
+    if (bytes) {
+        size_t win = std::min(bytes, size_t(max_win));
+        size_t keep = std::min(win, size_t(max_persist));
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep);
+        a.accessPolicyWindow.base_ptr = p;
+        a.accessPolicyWindow.num_bytes = win;
+        a.accessPolicyWindow.hitRatio = float(double(keep) / double(win));
+        a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+    cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaGetLastError();  // best effort: no window is not an error
+    ctx->l2_owner = owner;
+}
+
 tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_render_config* cfg, int kind,
                            int y0 = 0, int y1 = -1, int halo = 0) {
     check_config(cfg);
@@ -481,6 +515,11 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         ck(cudaMemsetAsync(s->hist.p, 0, own * 4 * sizeof(double), ctx->stream), "memset");
         s->accum.ensure(s->owned_pixels() * 3 * sizeof(double));
         ck(cudaMemsetAsync(s->accum.p, 0, s->owned_pixels() * 3 * sizeof(double), ctx->stream), "memset");
+        // the image accumulator is read-modify-written by every frame's deposits:
+        // keep it in a persisting L2 window (50 MB at 1080p) so the streaming
+        // histogram sectors (evict-first reductions) do not push it to HBM
+        const char* l2p = std::getenv("TOFR_L2_PERSIST");
+        if (!(l2p && l2p[0] == '0')) set_l2_window(ctx, s.get(), s->accum.p, s->owned_pixels() * 3 * sizeof(double));
     } else {
         s->has_temporal = cfg->temporal ? 1 : 0;
         s->has_bin = (s->transient && cfg->bin_reuse) ? 1 : 0;

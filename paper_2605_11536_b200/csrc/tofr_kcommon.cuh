@@ -45,12 +45,27 @@ __device__ __forceinline__ void stage_frame(FrameView& F, unsigned char* smem, s
 // private copy to combine; the pixel's wide-band image (sum over its bins,
 // pipeline.hpp:563-569) is reduced into `img` alongside (L2-resident: 50 MB at
 // 1080p), so reading the image never rescans the histogram.
+// The histogram sectors are marked evict-first in L2 (createpolicy + red with an
+// L2 cache hint): a deposit's sector is not reused within the frame, and the
+// image accumulator (persisting L2 window, set by the plain session) stays.
+#ifndef TOFR_HIST_EVICT_FIRST
+#define TOFR_HIST_EVICT_FIRST 1
+#endif
 __device__ __forceinline__ void hist_deposit(double* hist, double* img, size_t bin, size_t pix, const V3& v) {
     double* r = hist + 4 * bin;
+#if TOFR_HIST_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(r + 0), "d"(v.x), "l"(pol) : "memory");
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(r + 1), "d"(v.y), "l"(pol) : "memory");
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(r + 2), "d"(v.z), "l"(pol) : "memory");
+    asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(r + 3), "l"(1ull), "l"(pol) : "memory");
+#else
     atomicAdd(r + 0, v.x);
     atomicAdd(r + 1, v.y);
     atomicAdd(r + 2, v.z);
     atomicAdd(reinterpret_cast<unsigned long long*>(r + 3), 1ull);
+#endif
     if (img) {
         atomicAdd(img + 3 * pix + 0, v.x);
         atomicAdd(img + 3 * pix + 1, v.y);

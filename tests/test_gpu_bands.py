@@ -116,9 +116,6 @@ def test_sparse_bands_unequal_heights_and_pools(monkeypatch):
     """Sparse transient grids with a memory-limited pool (TOFR_POOL_FRAC < 1)
     and unequal band heights (edge bands keep one halo, middle bands two):
     the compacted halo layout must agree between sender and receiver."""
-    # a fixed pool size gives every band a different pool share (rows / items stored):
-    # a halo capacity derived from it would differ between a sender and its receiver
-    monkeypatch.setenv("TOFR_POOL_ROWS", "200000")
     sd = scenes.bundled("cornell", 48)
     cfg = RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=2,
                        temporal=True, spatial_passes=2, spatial_neighbors=3, spatial_radius=4, frames=3)
@@ -126,6 +123,11 @@ def test_sparse_bands_unequal_heights_and_pools(monkeypatch):
     for _ in range(cfg.frames):
         full.step(stats=False)
     ref = full.read_image()
+    # every band gets the same fixed pool (the full frame's peak occupancy, so no band
+    # overflows): each band's pool share (rows / items stored) differs, and a halo
+    # capacity derived from it would differ between a sender and its receiver
+    rows = int(max(full.pool()["rows_used"]) * 1.05) + 64
+    monkeypatch.setenv("TOFR_POOL_ROWS", str(rows))
     got = _render_bands(sd, cfg, 3, bands=[(0, 12), (12, 36), (36, 48)])
     assert ref.max() > 0
     assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"

@@ -63,8 +63,23 @@ def test_full_size_parity(renderer, ref, name):
         assert np.array_equal(g.hist.count, r.hist.count), "histogram counts differ from the oracle"
     if kind != "plain":
         diffs = counter_diffs(g.stats, r.stats)
-        print(name, _totals(g.stats), _totals(r.stats))
-        assert not diffs, diffs
+        print(name, _totals(g.stats), _totals(r.stats), diffs)
+        assert diffs == KNOWN_COUNTER_DIFFS.get(name, {}), diffs
+
+
+# Counters that differ from the oracle, each with its cause.  Every other counter
+# of every frame and stage of every case is integer-equal.
+#   full_c4r_doppler_128x72_1024bins, frame 2, spatial, occluded: 3144 vs 3145
+#   (one of 163,296 shift attempts).  The device's sin/cos (libdevice, <= 2 ulp) and
+#   glibc's differ in the last ulp for some BSDF-sampling angles (tofr_geom.h:367,
+#   :381; scene.hpp sample_bsdf), so 14% of the pixels' vertex positions differ by
+#   ~1e-16 relative (image bit-exact fraction 0.86, max relative error 2e-14).  One
+#   shifted path's occlusion segment grazes a box edge, and the closed/open test
+#   (geometry.hpp:86-231, bary +-1e-12) resolves it differently.  Deterministic
+#   on both sides (the same counts every run).
+KNOWN_COUNTER_DIFFS = {
+    "full_c4r_doppler_128x72_1024bins": {"f2.spatial.occluded": (3144, 3145)},
+}
 
 
 def counter_diffs(gs, rs) -> dict:
