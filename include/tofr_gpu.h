@@ -211,6 +211,22 @@ int tofr_gpu_session_band(tofr_session* ss, int32_t* y0, int32_t* y1, int32_t* r
  * stream and return 0; a non-zero return aborts the step. */
 typedef int (*tofr_halo_exchange_fn)(void* user, int32_t pass);
 int tofr_gpu_session_set_halo_exchange(tofr_session* ss, tofr_halo_exchange_fn fn, void* user);
+/* Native halo transports (no host callback per exchange):
+ *  - NCCL, one process per GPU: every rank calls tofr_gpu_session_halo_nccl
+ *    with the same 128-byte ncclUniqueId (rank 0: tofr_gpu_nccl_unique_id,
+ *    broadcast by the host), its rank and the world size; rank g's band lies
+ *    above rank g+1's.  ncclSend/ncclRecv with g-1 and g+1 run in one group on
+ *    the session stream (libnccl.so.2 is loaded at run time:
+ *    TOFR_ERR_UNSUPPORTED when it is missing).
+ *  - in-process peer copies: tofr_gpu_session_link_halo(upper, lower) joins
+ *    two adjacent band sessions of one process (any devices; NVLink P2P when
+ *    they differ); each band is stepped from its own host thread.
+ * tofr_gpu_session_halo_transport names the active one: "nccl", "peer",
+ * "callback" or "none". */
+int tofr_gpu_nccl_unique_id(uint8_t* id128);
+int tofr_gpu_session_halo_nccl(tofr_session* ss, const uint8_t* id128, int32_t rank, int32_t world);
+int tofr_gpu_session_link_halo(tofr_session* upper, tofr_session* lower);
+int tofr_gpu_session_halo_transport(tofr_session* ss, const char** name);
 int tofr_gpu_session_halo_buffers(tofr_session* ss, void** send_lo, void** recv_lo, uint64_t* bytes_lo,
                                   void** send_hi, void** recv_hi, uint64_t* bytes_hi);
 int tofr_gpu_session_step(tofr_session* ss, tofr_frame_stats* stats);

@@ -139,6 +139,10 @@ def _declare(lib) -> None:
     lib.tofr_gpu_session_band.argtypes = [vp] + [P(C.c_int32)] * 4
     lib.tofr_gpu_session_set_halo_exchange.argtypes = [vp, HALO_FN, vp]
     lib.tofr_gpu_session_halo_buffers.argtypes = [vp, P(vp), P(vp), P(C.c_uint64), P(vp), P(vp), P(C.c_uint64)]
+    lib.tofr_gpu_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.tofr_gpu_session_halo_nccl.argtypes = [vp, C.c_char_p, C.c_int32, C.c_int32]
+    lib.tofr_gpu_session_link_halo.argtypes = [vp, vp]
+    lib.tofr_gpu_session_halo_transport.argtypes = [vp, P(C.c_char_p)]
     lib.tofr_gpu_session_stage_totals.argtypes = [vp, P(C.c_double), P(C.c_int64), P(C.c_uint64), C.c_int32]
     lib.tofr_gpu_session_io_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     lib.tofr_gpu_session_destroy.argtypes = [vp]
@@ -173,7 +177,8 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_create", "tofr_gpu_session_step", "tofr_gpu_session_read_image", "tofr_gpu_session_sync",
     "tofr_gpu_session_last_ms", "tofr_gpu_session_io_bytes", "tofr_gpu_session_stream",
     "tofr_gpu_session_create_band", "tofr_gpu_session_band", "tofr_gpu_session_set_halo_exchange",
-    "tofr_gpu_session_halo_buffers", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
+    "tofr_gpu_session_halo_buffers", "tofr_gpu_nccl_unique_id", "tofr_gpu_session_halo_nccl",
+    "tofr_gpu_session_link_halo", "tofr_gpu_session_halo_transport", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
     "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_pool", "tofr_gpu_session_row_cost", "tofr_gpu_session_destroy",
     "tofr_gpu_kernel_timing", "tofr_gpu_kernel_launches", "tofr_gpu_kernel_times", "tofr_gpu_kernel_times_reset",
     "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_fp64_peak", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",

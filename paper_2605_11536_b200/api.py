@@ -288,6 +288,15 @@ class Renderer:
                                                  max_depth, _dptr(mean), _dptr(se)))
         return mean, se
 
+    def nccl_unique_id(self) -> bytes | None:
+        """A fresh 128-byte ncclUniqueId (None when libnccl.so.2 cannot be loaded)."""
+        buf = C.create_string_buffer(128)
+        rc = self._lib.tofr_gpu_nccl_unique_id(buf)
+        if rc == F.TOFR_ERR_UNSUPPORTED:
+            return None
+        self._check(rc)
+        return buf.raw
+
     def fp64_peak_gflops(self) -> float:
         """Measured FP64 DFMA throughput of this device (GFLOP/s): the FP64 roofline peak."""
         v = C.c_double(0)
@@ -386,6 +395,24 @@ class Session:
             C.byref(n[1])))
         return {"send_lo": int(p[0].value or 0), "recv_lo": int(p[1].value or 0), "bytes_lo": int(n[0].value),
                 "send_hi": int(p[2].value or 0), "recv_hi": int(p[3].value or 0), "bytes_hi": int(n[1].value)}
+
+    def halo_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Native NCCL halo transport (one process per GPU; every rank passes the
+        same 128-byte id from Renderer.nccl_unique_id, broadcast by the host)."""
+        self._r._check(self._r._lib.tofr_gpu_session_halo_nccl(self.handle, bytes(unique_id), int(rank),
+                                                               int(world)))
+
+    def link_halo(self, lower: "Session") -> None:
+        """Native in-process transport: this band's bottom halo <-> the band
+        directly below (peer copies on the session streams; each band is
+        stepped from its own host thread)."""
+        self._r._check(self._r._lib.tofr_gpu_session_link_halo(self.handle, lower.handle))
+
+    def halo_transport(self) -> str:
+        """"nccl", "peer", "callback" or "none"."""
+        n = C.c_char_p()
+        self._r._check(self._r._lib.tofr_gpu_session_halo_transport(self.handle, C.byref(n)))
+        return n.value.decode()
 
     def set_halo_exchange(self, fn) -> None:
         """fn(pass) -> None: move the packed halo rows (see tofr_gpu.h)."""

@@ -27,7 +27,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu", "tofr_trace.cu"]
-HOST_SOURCES = ["host_scene.cpp", "capi.cpp", "ktime.cpp"]
+HOST_SOURCES = ["host_scene.cpp", "capi.cpp", "ktime.cpp", "halo_transport.cpp"]
 HEADERS = [
     "tofr_core.h",
     "tofr_geom.h",
@@ -38,6 +38,7 @@ HEADERS = [
     "ktime.h",
     "tofr_kernels.h",
     "host_scene.h",
+    "halo_transport.h",
 ]
 
 
@@ -98,7 +99,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("native build failed")
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(tmp)] + [str(o) for o in objs]
-         + ["-Xlinker", "-rpath,$ORIGIN"], verbose)
+         + ["-ldl", "-Xlinker", "-rpath,$ORIGIN"], verbose)
     os.replace(tmp, LIB)
     return LIB
 
@@ -131,7 +132,7 @@ def build_variants(variants: dict, verbose: bool = False) -> dict:
     for tag, objs in outs.items():
         lib = vdir / f"libtofr_b200_{tag}.so"
         _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(lib)] + [str(o) for o in objs]
-             + [str(o) for o in host_objs] + ["-Xlinker", "-rpath,$ORIGIN"], verbose)
+             + [str(o) for o in host_objs] + ["-ldl", "-Xlinker", "-rpath,$ORIGIN"], verbose)
         libs[tag] = lib
     return libs
 

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/tofr_gpu.h"
+#include "halo_transport.h"
 #include "host_scene.h"
 #include "ktime.h"
 #include "tofr_kernels.h"
@@ -208,8 +209,10 @@ struct tofr_session {
     bool wave = false;
     DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng, wv_mlist;
     size_t wv_cap = 0;
-    tofr_halo_exchange_fn xfn = nullptr;
+    tofr_halo_exchange_fn xfn = nullptr;  // host callback transport (gloo / tests)
     void* xuser = nullptr;
+    std::unique_ptr<HaloTransport> xport;   // native transport (NCCL or in-process peer copies)
+    std::shared_ptr<PeerEndpoint> peer;
     uint64_t halo_exchanges = 0;
     // per-frame stage events, two frames in flight
     cudaEvent_t ev[2][7] = {};
@@ -728,17 +731,38 @@ void flush_all(tofr_session* s) {
 // Halo exchange of a global-indexed grid around the band: pack the edge rows
 // the neighbours need, let the caller move them (NCCL / P2P, ordered on the
 // session stream), unpack what arrived into the halo rows.
+HaloBufs halo_bufs(const tofr_session* s) {
+    HaloBufs b;
+    b.send_lo = s->send_lo.p;
+    b.recv_lo = s->recv_lo.p;
+    b.bytes_lo = s->send_lo.p ? s->send_lo.n : 0;
+    b.send_hi = s->send_hi.p;
+    b.recv_hi = s->recv_hi.p;
+    b.bytes_hi = s->send_hi.p ? s->send_hi.n : 0;
+    b.device = s->ctx->device;
+    b.stream = s->ctx->stream;
+    return b;
+}
+
 void exchange_halo(tofr_session* s, ResStore g, int pass) {
     if (s->r0 == s->y0 && s->r1 == s->y1) return;
-    if (!s->xfn) throw ScopeError(TOFR_ERR_INVALID, "band session with a halo needs a halo exchange callback");
+    if (!s->xport && !s->xfn)
+        throw ScopeError(TOFR_ERR_INVALID, "band session with a halo needs a halo transport (NCCL, peer link or "
+                                           "exchange callback)");
     cudaStream_t st = s->ctx->stream;
     size_t per_row = size_t(s->W) * s->B;
     size_t lo = size_t(s->y0 - s->r0) * per_row, hi = size_t(s->r1 - s->y1) * per_row;
+    const HaloBufs hb = halo_bufs(s);
+    if (s->xport) s->xport->before_pack(hb);
     launch_halo_pack(g, size_t(s->y0) * per_row, lo, s->send_lo.as<double2>(), halo_cap(s, lo), st);
     launch_halo_pack(g, size_t(s->y1) * per_row - hi, hi, s->send_hi.as<double2>(), halo_cap(s, hi), st);
     ck(cudaGetLastError(), "halo pack");
-    int rc = s->xfn(s->xuser, pass);
-    if (rc != 0) throw ScopeError(TOFR_ERR_CUDA, "halo exchange callback failed");
+    if (s->xport) {
+        s->xport->exchange(hb, pass);
+    } else {
+        int rc = s->xfn(s->xuser, pass);
+        if (rc != 0) throw ScopeError(TOFR_ERR_CUDA, "halo exchange callback failed");
+    }
     launch_halo_unpack(g, size_t(s->r0) * per_row, lo, s->recv_lo.as<double2>(), halo_cap(s, lo), st);
     launch_halo_unpack(g, size_t(s->y1) * per_row, hi, s->recv_hi.as<double2>(), halo_cap(s, hi), st);
     ck(cudaGetLastError(), "halo unpack");
@@ -1397,6 +1421,47 @@ int tofr_gpu_session_set_halo_exchange(tofr_session* ss, tofr_halo_exchange_fn f
     if (!ss) return TOFR_ERR_INVALID;
     ss->xfn = fn;
     ss->xuser = user;
+    return TOFR_OK;
+}
+
+int tofr_gpu_nccl_unique_id(uint8_t* id) {
+    if (!id) return TOFR_ERR_INVALID;
+    if (!nccl_available()) return TOFR_ERR_UNSUPPORTED;
+    try {
+        nccl_unique_id(id);
+    } catch (const std::exception&) {
+        return TOFR_ERR_CUDA;
+    }
+    return TOFR_OK;
+}
+
+int tofr_gpu_session_halo_nccl(tofr_session* ss, const uint8_t* id, int32_t rank, int32_t world) {
+    if (!ss || !id) return TOFR_ERR_INVALID;
+    return guard(ss->ctx, [&] {
+        if (!nccl_available()) throw ScopeError(TOFR_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+        ss->xport = make_nccl_transport(id, rank, world, ss->ctx->device);
+    });
+}
+
+int tofr_gpu_session_link_halo(tofr_session* upper, tofr_session* lower) {
+    if (!upper || !lower || upper == lower) return TOFR_ERR_INVALID;
+    return guard(upper->ctx, [&] {
+        if (upper->y1 != lower->y0 || upper->W != lower->W || upper->B != lower->B)
+            throw ScopeError(TOFR_ERR_INVALID, "link_halo: the bands are not adjacent (upper.y1 != lower.y0)");
+        if ((upper->r1 - upper->y1) != (lower->y0 - lower->r0))
+            throw ScopeError(TOFR_ERR_INVALID, "link_halo: the bands keep different halos");
+        for (tofr_session* s : {upper, lower})
+            if (!s->peer) {
+                s->peer = make_peer_endpoint(halo_bufs(s));
+                s->xport = make_peer_transport(s->peer);
+            }
+        peer_link(upper->peer, lower->peer);
+    });
+}
+
+int tofr_gpu_session_halo_transport(tofr_session* ss, const char** name) {
+    if (!ss || !name) return TOFR_ERR_INVALID;
+    *name = ss->xport ? ss->xport->name() : (ss->xfn ? "callback" : "none");
     return TOFR_OK;
 }
 

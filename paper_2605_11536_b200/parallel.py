@@ -21,6 +21,7 @@ band.  For a moving camera the library also exchanges the final grid's halo
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -251,7 +252,10 @@ class BandSession:
         self.exchanger = None
         if emulate and halo > 0:
             self.sess.set_halo_exchange(lambda pass_: None)
+        elif world > 1 and halo > 0 and self._native_nccl(renderer, group):
+            pass  # library-side ncclSend / ncclRecv on the session stream, no host callback
         elif world > 1 and halo > 0:
+            # host-staged transport (gloo: CPU tests, several ranks sharing one GPU)
             hb = self.sess.halo_buffers()
             dev = torch.device("cuda", torch.cuda.current_device())
             self.exchanger = HaloExchanger(rank, world, group, _wrap(hb["send_lo"], hb["bytes_lo"], dev),
@@ -260,6 +264,24 @@ class BandSession:
                                            _wrap(hb["recv_hi"], hb["bytes_hi"], dev), stream=self.stream)
             self.sess.set_halo_exchange(self.exchanger)
         self._pinned = None
+
+    def _native_nccl(self, renderer, group) -> bool:
+        """NCCL process group: hand the library its own communicator (rank 0's
+        ncclUniqueId broadcast over the group) so every halo exchange is a
+        ncclSend / ncclRecv pair on the session stream.  TOFR_HALO_TRANSPORT=
+        callback keeps the torch.distributed callback instead."""
+        import torch.distributed as dist
+        if dist.get_backend(group) != "nccl" or os.environ.get("TOFR_HALO_TRANSPORT", "native") == "callback":
+            return False
+        box = [renderer.nccl_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        if box[0] is None:  # libnccl not loadable by the library: every rank falls back
+            return False
+        self.sess.halo_nccl(box[0], self.rank, self.world)
+        return True
+
+    def halo_transport(self) -> str:
+        return self.sess.halo_transport()
 
     def owned_pixels(self) -> int:
         return (self.y1 - self.y0) * self.W

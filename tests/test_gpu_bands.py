@@ -49,13 +49,22 @@ CASES = {
 }
 
 
-def _render_bands(sd, cfg, world, bands=None):
+def _render_bands(sd, cfg, world, bands=None, transport="peer"):
+    """transport "peer": the library's native in-process transport (peer copies
+    between the band sessions' streams, no host callback); "callback": device
+    copies issued from the exchange callback (the host-staged path)."""
     import torch
     H = sd.camera.height
     halo = halo_rows(cfg.spatial_radius, cfg.spatial_passes, motion_rows_for(sd, cfg))
     bands = bands or [band_rows(H, world, g) for g in range(world)]
     rs = [Renderer(0) for _ in range(world)]
     ss = [rs[g].session(sd, cfg, band=(*bands[g], halo)) for g in range(world)]
+    if transport == "peer":
+        if halo > 0:
+            for g in range(world - 1):
+                ss[g].link_halo(ss[g + 1])
+            assert all(s.halo_transport() == "peer" for s in ss)
+        return _run_threads(ss, cfg, None)
     dev = torch.device("cuda", 0)
     bufs = []
     for s in ss:
@@ -78,6 +87,11 @@ def _render_bands(sd, cfg, world, bands=None):
 
     for g, s in enumerate(ss):
         s.set_halo_exchange(make_cb(g))
+    return _run_threads(ss, cfg, bar)
+
+
+def _run_threads(ss, cfg, bar):
+    world = len(ss)
     errs = []
 
     def run(g):
@@ -87,7 +101,8 @@ def _render_bands(sd, cfg, world, bands=None):
             ss[g].sync()
         except Exception as e:  # pragma: no cover - reported below
             errs.append(e)
-            bar.abort()
+            if bar is not None:
+                bar.abort()
 
     ts = [threading.Thread(target=run, args=(g,)) for g in range(world)]
     for t in ts:
@@ -100,14 +115,15 @@ def _render_bands(sd, cfg, world, bands=None):
 
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("world", [2, 3])
-def test_bands_equal_full_frame(name, world):
+@pytest.mark.parametrize("transport", ["peer", "callback"])
+def test_bands_equal_full_frame(name, world, transport):
     build, cfg = CASES[name]
     sd = build()
     full = Renderer(0).session(sd, cfg)
     for _ in range(cfg.frames):
         full.step(stats=False)
     ref = full.read_image()
-    got = _render_bands(sd, cfg, world)
+    got = _render_bands(sd, cfg, world, transport=transport)
     assert ref.max() > 0
     assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"
 
@@ -140,3 +156,24 @@ def test_moving_camera_band_without_halo_is_rejected():
     cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0), m_init=1, temporal=True, frames=2)
     with pytest.raises(Exception, match="reprojection halo"):
         Renderer(0).session(sd, cfg, band=(0, 16, 0))
+
+
+def test_nccl_transport_initialises():
+    """The library's own NCCL communicator (libnccl.so.2 loaded at run time)
+    comes up on this device and becomes the band's transport.  A second rank
+    cannot share one GPU with NCCL, so the send/recv pairs themselves run only
+    on multi-GPU nodes (same group calls as the peer path's copies)."""
+    r = Renderer(0)
+    uid = r.nccl_unique_id()
+    if uid is None:
+        pytest.skip("libnccl.so.2 not loadable")
+    assert len(uid) == 128
+    sd = scenes.bundled("cornell", 32)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=1, temporal=True, spatial_passes=1,
+                       spatial_neighbors=3, spatial_radius=4, frames=1)
+    s = r.session(sd, cfg, band=(0, 16, 4))
+    assert s.halo_transport() == "none"
+    s.halo_nccl(uid, 0, 1)
+    assert s.halo_transport() == "nccl"
+    s.step(stats=False)  # world 1: no peer, the exchange is an empty group
+    s.sync()
