@@ -708,6 +708,10 @@ void flush_set(tofr_session* s, int set) {
         for (int k = 0; k < 3; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[8 * set + k]);
     unsigned long long pool_err = 0;
     if (s->sparse) std::memcpy(&pool_err, s->occ_host + 8 * set + 4, 8);
+    if ((s->err_host[set] | pool_err) & kErrHalo)
+        throw ScopeError(TOFR_ERR_OOM,
+                         "compacted halo overflow: more non-empty reservoirs in the halo rows than TOFR_HALO_FRAC "
+                         "of them (raise it on every rank)");
     if ((s->err_host[set] | pool_err) & kErrPool)
         throw ScopeError(TOFR_ERR_OOM,
                          "transient reservoir pool full: more non-empty reservoirs than TOFR_POOL_FRAC of the grid "

@@ -1183,7 +1183,7 @@ __global__ void k_halo_pack_sparse(ResStore grid, size_t item0, size_t n, double
         if (!ne) continue;
         size_t r = r0 + __popc(m & ((1u << lane) - 1));
         if (r >= cap) {
-            atomicOr(grid.err, kErrPool);
+            atomicOr(grid.err, kErrHalo);
             continue;
         }
         __stcg(&h.idx[r], uint32_t(i));

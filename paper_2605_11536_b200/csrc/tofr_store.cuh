@@ -44,6 +44,7 @@ constexpr int kResChunks = 24;
 // row is allocated once.
 constexpr uint32_t kNoSlot = 0xffffffffu;
 constexpr unsigned long long kErrPool = 1ull << 62;
+constexpr unsigned long long kErrHalo = 1ull << 61;  // compacted halo: more non-empty rows than its capacity
 
 struct ResStore {
     double2* base;

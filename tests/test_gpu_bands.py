@@ -144,6 +144,9 @@ def test_sparse_bands_unequal_heights_and_pools(monkeypatch):
     # capacity derived from it would differ between a sender and its receiver
     rows = int(max(full.pool()["rows_used"]) * 1.05) + 64
     monkeypatch.setenv("TOFR_POOL_ROWS", str(rows))
+    # this small frame is densely filled (m_init 2, two spatial passes): a larger
+    # compacted-halo capacity than the default half of the halo rows, still < n
+    monkeypatch.setenv("TOFR_HALO_FRAC", "0.9")
     got = _render_bands(sd, cfg, 3, bands=[(0, 12), (12, 36), (36, 48)])
     assert ref.max() > 0
     assert np.array_equal(got, ref), f"{int((got != ref).sum())} values differ"
