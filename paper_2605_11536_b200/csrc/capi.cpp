@@ -212,6 +212,9 @@ struct tofr_session {
     tofr_halo_exchange_fn xfn = nullptr;  // host callback transport (gloo / tests)
     void* xuser = nullptr;
     std::unique_ptr<HaloTransport> xport;   // native transport (NCCL or in-process peer copies)
+    DevBuf ell_jobs, ell_res, ell_st, ell_ctr, ell_list, ell_count;  // wavefront ellipsoidal sampler
+    EllScratch ell{};
+    bool ell_ready = false;
     std::shared_ptr<PeerEndpoint> peer;
     uint64_t halo_exchanges = 0;
     // per-frame stage events, two frames in flight
@@ -735,6 +738,32 @@ void flush_all(tofr_session* s) {
 // Halo exchange of a global-indexed grid around the band: pack the edge rows
 // the neighbours need, let the caller move them (NCCL / P2P, ordered on the
 // session stream), unpack what arrived into the halo rows.
+// Scratch of the wavefront ellipsoidal sampler (EllScratch, tofr_ellipsoid.cuh)
+// for an ellipsoidal gated initialisation; null: the per-lane sampler
+// (TOFR_ELL=legacy, or not enough memory).
+const EllScratch* ell_scratch(tofr_session* s, const PathCfg& pc, const InitParams& ip) {
+    if (!pc.ellipsoidal || ip.mode != INIT_ELLIPSOIDAL) return nullptr;
+    const char* e = std::getenv("TOFR_ELL");
+    if (e && std::strcmp(e, "legacy") == 0) return nullptr;
+    const int per_pixel = std::max(1, ip.m_init) * std::max(1, s->cfg.max_depth - 2);
+    const size_t slots = s->owned_pixels() * size_t(per_pixel);
+    if (!s->ell_ready || s->ell.per_pixel != per_pixel) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && slots * kEllSlotBytes > fr / 2) return nullptr;
+        s->ell_jobs.ensure(slots * sizeof(EllJob));
+        s->ell_res.ensure(slots * sizeof(EllRes));
+        s->ell_st.ensure(slots);
+        s->ell_ctr.ensure(slots * 8);
+        s->ell_list.ensure(slots * 4);
+        s->ell_count.ensure(16);
+        s->ell = EllScratch{s->ell_jobs.as<EllJob>(), s->ell_res.as<EllRes>(), s->ell_st.as<uint8_t>(),
+                            s->ell_ctr.as<uint64_t>(), s->ell_list.as<uint32_t>(), s->ell_count.as<unsigned int>(),
+                            per_pixel};
+        s->ell_ready = true;
+    }
+    return &s->ell;
+}
+
 HaloBufs halo_bufs(const tofr_session* s) {
     HaloBufs b;
     b.send_lo = s->send_lo.p;
@@ -854,7 +883,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         if (s->transient)
             launch_init_transient(F, bd, g, pc, ip, h, f, cur, q_side, fs);
         else
-            launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs);
+            launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs, ell_scratch(s, pc, ip));
         cudaEventRecord(ev[1], fs);
         if (piped) {  // the main stream continues once this frame's reservoirs exist
             cudaEventRecord(s->ev_init[set], fs);

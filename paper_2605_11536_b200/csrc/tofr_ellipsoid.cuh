@@ -15,6 +15,7 @@
 //   transport.hpp:332-444  emit_ellipsoidal, ell_pdf_at, ell_length_gradient
 #pragma once
 
+#include "tofr_kernels.h"
 #include "tofr_path.cuh"
 
 namespace tofr_b200 {
@@ -120,8 +121,13 @@ __device__ inline bool arc_inside(const ConicArc& arc, const HalfPlane* edges, d
     return true;
 }
 
-// clip_ellipsoid_triangle (ellipsoid.hpp:167-269)
-__device__ bool clip_ellipsoid_triangle(const FrameView& F, const Ellipsoid& e, int tri, ConicArc& arc) {
+// clip_ellipsoid_triangle (ellipsoid.hpp:167-269), split in two: the conic,
+// its cut angles and the kept segments [t0, t1] (clip_geometry), then the
+// segments' arc lengths (arc_lengths: the 32-point Gauss-Legendre integrals,
+// the expensive part).  A kept segment's length is always > 0 (the integrand
+// |d/dth arc| >= min(r1, r2) > 0 and t1 - t0 >= 1e-12), so the reference's
+// `len <= 0` skip never fires and the segment list is fixed by the geometry.
+__device__ bool clip_geometry(const FrameView& F, const Ellipsoid& e, int tri, ConicArc& arc) {
     const GTriIsect& g = tri_geo(F, tri);
     arc.origin = g.v0;
     arc.frame = tangent_frame(F, tri);
@@ -191,13 +197,9 @@ __device__ bool clip_ellipsoid_triangle(const FrameView& F, const Ellipsoid& e, 
         if (t1 - t0 < 1e-12) return;
         double mid = 0.5 * (t0 + t1);
         if (!arc_inside(arc, edges, mid)) return;
-        double len = arc_integrate(arc, t0, t1);
-        if (len <= 0) return;
         arc.t0[arc.nseg] = t0;
         arc.t1[arc.nseg] = t1;
-        arc.len[arc.nseg] = len;
         arc.nseg++;
-        arc.total_len += len;
     };
     if (nc == 0) {
         if (!arc_inside(arc, edges, 0)) return false;
@@ -209,8 +211,21 @@ __device__ bool clip_ellipsoid_triangle(const FrameView& F, const Ellipsoid& e, 
             add_seg(t0, t1);
         }
     }
-    if (arc.nseg == 0 || arc.total_len <= 0) return false;
-    return true;
+    return arc.nseg > 0;
+}
+
+__device__ inline void arc_lengths(ConicArc& arc) {
+    arc.total_len = 0;
+    for (int i = 0; i < arc.nseg; ++i) {
+        arc.len[i] = arc_integrate(arc, arc.t0[i], arc.t1[i]);
+        arc.total_len += arc.len[i];
+    }
+}
+
+__device__ bool clip_ellipsoid_triangle(const FrameView& F, const Ellipsoid& e, int tri, ConicArc& arc) {
+    if (!clip_geometry(F, e, tri, arc)) return false;
+    arc_lengths(arc);
+    return arc.total_len > 0;
 }
 
 // sample_arc (ellipsoid.hpp:273-296)
@@ -245,6 +260,44 @@ struct EllSample {
     int tri;
     double pdf_arc;
 };
+
+// area-weighted BVH descent + triangle pick of sample_connection_vertex
+// (ellipsoid.hpp:310-340): the triangle and p_desc * p_tri
+__device__ bool descend_pick(const FrameView& F, const Ellipsoid& e, Rng& rng, int& tri_out, double& p_dt) {
+    if (!node_overlaps_i(F, e, 0)) return false;
+    double p_desc = 1.0;
+    int ni = 0;
+    while (F.aux[ni].count == 0) {
+        int li = F.aux[ni].left, ri = F.aux[ni].right;
+        double wl = node_overlaps_i(F, e, li) ? F.aux[li].tri_area : 0.0;
+        double wr = node_overlaps_i(F, e, ri) ? F.aux[ri].tri_area : 0.0;
+        double sum = wl + wr;
+        if (sum <= 0) return false;
+        if (rng_next(rng) * sum < wl) {
+            p_desc *= wl / sum;
+            ni = li;
+        } else {
+            p_desc *= wr / sum;
+            ni = ri;
+        }
+    }
+    const GNodeAux& leaf = F.aux[ni];
+    double pick = rng_next(rng) * leaf.tri_area;
+    int tri_id = F.tri_id[leaf.first];
+    double acc = 0;
+    for (int i = 0; i < leaf.count; ++i) {
+        int id = F.tri_id[leaf.first + i];
+        acc += F.tri[id].area;
+        if (pick <= acc || i == leaf.count - 1) {
+            tri_id = id;
+            break;
+        }
+    }
+    double p_tri = F.tri[tri_id].area / leaf.tri_area;
+    tri_out = tri_id;
+    p_dt = p_desc * p_tri;
+    return true;
+}
 
 // sample_connection_vertex (ellipsoid.hpp:310-352)
 __device__ bool sample_connection_vertex(const FrameView& F, const Ellipsoid& e, Rng& rng, EllSample& s) {
@@ -340,8 +393,82 @@ __device__ double ell_pdf_at(const FrameView& F, const PathCfg& cfg, const WalkV
     return pdf_arc * grad / cfg.ell_width;
 }
 
+// ---------------------------------------------------------------------------
+// Wavefront ellipsoidal sampling (three launches instead of one per-lane
+// sample_connection_vertex):
+//   plan   (k_ell_plan)   the path trees' walks; every ellipsoidal step runs its
+//                         BVH descent + triangle pick (the ellipsoid RNG draws)
+//                         and the conic clip GEOMETRY, draws the arc target and
+//                         records a job; no candidates, no NEE rays.
+//   arcs   (k_ell_arcs)   one warp per job: the segment lengths and the <= 60
+//                         bisection steps of sample_arc, each 32-point
+//                         Gauss-Legendre integral with one node per lane and
+//                         the terms summed in the reference's order.
+//   replay (k_init_gated) the RIS initialisation with the jobs' vertices in
+//                         place of sample_connection_vertex (the ellipsoid RNG
+//                         counter restored from the plan).
+// Every value is computed by the same operations as the per-lane sampler, so
+// the vertices and pdfs are bit-identical to it (and to the reference's).
+
+struct DirectSampler {
+    __device__ bool sample(const FrameView& F, const Ellipsoid& e, Rng& rng, EllSample& q) {
+        return sample_connection_vertex(F, e, rng, q);
+    }
+};
+
+struct PlanSampler {
+    EllScratch es;
+    size_t slot0;
+    int k;
+    __device__ bool sample(const FrameView& F, const Ellipsoid& e, Rng& rng, EllSample&) {
+        size_t slot = slot0 + size_t(k++);
+        int tri = -1;
+        double p_dt = 0;
+        ConicArc arc;
+        bool ok = descend_pick(F, e, rng, tri, p_dt) && clip_geometry(F, e, tri, arc);
+        if (ok) {
+            EllJob& j = es.jobs[slot];
+            j.center = arc.center;
+            j.ax1 = arc.ax1;
+            j.ax2 = arc.ax2;
+            j.r1 = arc.r1;
+            j.r2 = arc.r2;
+            for (int i = 0; i < arc.nseg; ++i) {
+                j.t0[i] = arc.t0[i];
+                j.t1[i] = arc.t1[i];
+            }
+            j.nseg = arc.nseg;
+            j.tri = tri;
+            j.p_dt = p_dt;
+            j.u = rng_next(rng);
+            es.list[atomicAdd(es.count, 1u)] = uint32_t(slot);
+        }
+        es.st[slot] = ok ? 1 : 0;
+        es.ctr[slot] = rng.ctr;
+        return false;  // the plan emits nothing
+    }
+};
+
+struct ReplaySampler {
+    EllScratch es;
+    size_t slot0;
+    int k;
+    __device__ bool sample(const FrameView&, const Ellipsoid&, Rng& rng, EllSample& q) {
+        size_t slot = slot0 + size_t(k++);
+        rng.ctr = es.ctr[slot];
+        if (!es.st[slot]) return false;
+        EllRes r = es.res[slot];
+        q.pos = r.pos;
+        q.tri = es.jobs[slot].tri;
+        q.pdf_arc = r.pdf_arc;
+        return true;
+    }
+};
+
 // emit_ellipsoidal (transport.hpp:332-415) as a walk hook.
-struct EllStep {
+template <class Sampler>
+struct EllStepT {
+    Sampler smp;
     __device__ double pdf_at(const FrameView& F, const PathCfg& cfg, const WalkV& at, const V3& qpos,
                              int qtri, double total_len) {
         return ell_pdf_at(F, cfg, at, qpos, qtri, total_len);
@@ -365,7 +492,7 @@ struct EllStep {
         Ellipsoid e;
         if (!ellipsoid_from_constraint(x.p, lpos, l_rem, e)) return;
         EllSample q;
-        if (!sample_connection_vertex(F, e, rng, q)) return;  // consumes the ellipsoid lane
+        if (!smp.sample(F, e, rng, q)) return;  // consumes the ellipsoid lane
         const GTriInfo& qt = F.tri[q.tri];
         const GMat& qm = F.mats[qt.mat];
         if (qm.kind == MAT_MIRROR) return;
@@ -420,6 +547,18 @@ struct EllStep {
         sink.emit(c, mis_m, rs);
     }
 };
+using EllStep = EllStepT<DirectSampler>;
+
+// one warp: 32-point Gauss-Legendre integral of |d arc / d th| over [a, b],
+// node i on lane i, s += w_i f_i in i order (arc_integrate's operations)
+__device__ inline double arc_integrate_warp(const ConicArc& arc, double a, double b, double glx, double glw) {
+    double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+    double term = glw * arc_speed(arc, mid + half * glx);
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += __shfl_sync(0xffffffffu, term, i);
+    return s * half;
+}
 
 #endif  // __CUDACC__
 

@@ -202,7 +202,7 @@ __device__ void init_pixel(const FrameView& F, const PathCfg& cfg, const InitPar
 
 __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     InitParams ip, int frame_idx, ResStore cur,
-                                                    unsigned long long* q) {
+                                                    unsigned long long* q, EllScratch es) {
     extern __shared__ __align__(16) unsigned char smem[];
     size_t off = 0;
     stage_frame(F, smem, off);
@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F
         int px = p % W, py = p / W;
         Res r;
         GHit g = gbuf[p];
-        if (cfg.ellipsoidal) {
+        if (cfg.ellipsoidal && es.jobs) {  // replay of the planned + bisected ellipsoidal vertices
+            EllStepT<ReplaySampler> ell{ReplaySampler{es, i * size_t(es.per_pixel), 0}};
+            init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
+        } else if (cfg.ellipsoidal) {
             EllStep ell;
             init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
         } else {
@@ -223,6 +226,104 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F
             init_pixel(F, cfg, ip, g, px, py, frame_idx, r, v, ell);
         }
         res_store_result(cur, size_t(p), r);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// wavefront ellipsoidal sampling (tofr_ellipsoid.cuh): plan and arcs launches
+
+// a sink that wants no candidate: emit_nee culls every NEE before its ray
+struct NullSink {
+    __device__ bool wants(double) const { return false; }
+    __device__ void emit(const Cand&, double, const RecSrc&) {}
+};
+
+// the path trees of run_ris (pipeline.hpp:114-128) with the ellipsoidal step
+// recording jobs: same walk and ellipsoid RNG draws as the replay
+__global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_ell_plan(FrameView F, Band bd, const GHit* gbuf,
+                                                                  PathCfg cfg, int m_init, int frame_idx,
+                                                                  EllScratch es, unsigned long long* q) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    size_t off = 0;
+    stage_frame(F, smem, off);
+    __syncthreads();
+    int W = F.cam.w;
+    WalkV v[kMaxVerts];
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    TOFR_FOR_ITEMS(i, n, q) {
+        int p = bd.y0 * W + int(i);
+        int px = p % W, py = p / W;
+        uint64_t pix = uint64_t(py) * W + px;
+        GHit g = gbuf[p];
+        NullSink sink;
+        EllStepT<PlanSampler> ell{PlanSampler{es, i * size_t(es.per_pixel), 0}};
+        for (int s = 0; s < m_init; ++s) {
+            Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
+            Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
+            trace_tree(F, cfg, px, py, g, rng, erng, sink, v, ell);
+        }
+    }
+}
+
+// one warp per job: arc_lengths + sample_arc (ellipsoid.hpp:167-296) with
+// warp-wide Gauss-Legendre integrals; lane 0 writes the vertex and its pdf
+__global__ void __launch_bounds__(256) k_ell_arcs(FrameView F, EllScratch es, unsigned long long* q) {
+    const int lane = threadIdx.x & 31;
+    const double glx = c_gl_x[lane], glw = c_gl_w[lane];
+    const unsigned n = *es.count;
+    for (;;) {
+        unsigned long long jn = 0;
+        if (lane == 0) jn = atomicAdd(q, 1ull);
+        jn = __shfl_sync(0xffffffffu, jn, 0);
+        if (jn >= n) break;
+        const uint32_t slot = es.list[jn];
+        const EllJob& J = es.jobs[slot];
+        ConicArc arc;
+        const GTriIsect& tg = tri_geo(F, J.tri);
+        arc.origin = tg.v0;
+        arc.frame = tangent_frame(F, J.tri);
+        arc.center = J.center;
+        arc.ax1 = J.ax1;
+        arc.ax2 = J.ax2;
+        arc.r1 = J.r1;
+        arc.r2 = J.r2;
+        arc.nseg = J.nseg;
+        arc.total_len = 0;
+        for (int i = 0; i < arc.nseg; ++i) {  // arc_lengths
+            arc.t0[i] = J.t0[i];
+            arc.t1[i] = J.t1[i];
+            arc.len[i] = arc_integrate_warp(arc, arc.t0[i], arc.t1[i], glx, glw);
+            arc.total_len += arc.len[i];
+        }
+        // sample_arc (ellipsoid.hpp:273-296) with the planned draw
+        double target = J.u * arc.total_len;
+        int si = arc.nseg - 1;
+        for (int i = 0; i < arc.nseg; ++i) {
+            if (target <= arc.len[i] || i == arc.nseg - 1) {
+                si = i;
+                break;
+            }
+            target -= arc.len[i];
+        }
+        double sl = arc.len[si];
+        target = target < 0.0 ? 0.0 : (target > sl ? sl : target);
+        double lo = arc.t0[si], hi = arc.t1[si];
+        for (int it = 0; it < 60; ++it) {
+            double mid = 0.5 * (lo + hi);
+            double l = arc_integrate_warp(arc, arc.t0[si], mid, glx, glw);
+            if (l < target)
+                lo = mid;
+            else
+                hi = mid;
+            if ((hi - lo) * arc_speed(arc, 0.5 * (lo + hi)) < 1e-6 * dmax(arc.total_len, 1e-30)) break;
+        }
+        if (lane == 0) {
+            double pdf_len = 1.0 / arc.total_len;
+            EllRes r;
+            r.pos = arc.origin + to_world(arc.frame, arc_point2(arc, 0.5 * (lo + hi)));
+            r.pdf_arc = J.p_dt * pdf_len;
+            es.res[slot] = r;
+        }
     }
 }
 
@@ -1268,7 +1369,8 @@ void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s)
     kernel<<<persistent_grid(reinterpret_cast<const void*>(kernel), 128, smem, n), 128, smem, s>>>
 
 void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s) {
+                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s,
+                       const EllScratch* es) {
     size_t n = band_pixels(bd, F.cam.w);
     if (!n) return;
     if (ip.mode == INIT_DIRECT && !cfg.ellipsoidal && trace_wave()) {
@@ -1276,9 +1378,24 @@ void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const 
         return;
     }
     size_t sm = frame_smem_bytes(F);
+    EllScratch none{};
+    const bool wave_ell = cfg.ellipsoidal && ip.mode == INIT_ELLIPSOIDAL && es && es->jobs;
+    if (wave_ell) {
+        cudaMemsetAsync(es->count, 0, sizeof(unsigned int), s);
+        {
+            KScope ks("k_ell_plan", s);
+            TOFR_PERSISTENT(k_ell_plan, n, sm)(F, bd, g, cfg, ip.m_init, frame_idx, *es, q);
+        }
+        {
+            cudaMemsetAsync(q, 0, sizeof(unsigned long long), s);
+            KScope ks("k_ell_arcs", s);
+            k_ell_arcs<<<persistent_grid(reinterpret_cast<const void*>(k_ell_arcs), 256, 0, n * 32), 256, 0, s>>>(
+                F, *es, q);
+        }
+    }
     {
         KScope ks("k_init_gated", s);
-        TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q);
+        TOFR_PERSISTENT(k_init_gated, n, sm)(F, bd, g, cfg, ip, frame_idx, cur, q, wave_ell ? *es : none);
     }
 }
 

@@ -14,6 +14,33 @@ constexpr size_t kSmemStageLimit = 20 * 1024;
 
 enum : int { INIT_DIRECT = 0, INIT_ELLIPSOIDAL = 1, INIT_SHRINK = 2 };
 
+// Wavefront ellipsoidal sampling scratch (tofr_ellipsoid.cuh: plan -> arcs ->
+// replay).  Per band pixel `per_pixel` slots, slot k = the pixel's k-th
+// connection-vertex sampler call.
+struct EllJob {
+    V2 center, ax1, ax2;
+    double r1, r2;
+    double t0[6], t1[6];
+    double u;     // the arc draw (sample_arc's rng_next)
+    double p_dt;  // p_desc * p_tri
+    int nseg, tri;
+};
+struct EllRes {
+    V3 pos;
+    double pdf_arc;
+};
+struct EllScratch {
+    EllJob* jobs;
+    EllRes* res;
+    uint8_t* st;      // 1: job recorded (the clip kept a segment), 0: the sampler failed
+    uint64_t* ctr;    // ellipsoid RNG counter after the sampler call
+    uint32_t* list;   // slots with a job
+    unsigned int* count;
+    int per_pixel;
+};
+// bytes of scratch per slot (EllScratch)
+constexpr size_t kEllSlotBytes = sizeof(EllJob) + sizeof(EllRes) + 1 + 8 + 4;
+
 struct InitParams {
     int mode;
     int m_init;
@@ -152,7 +179,7 @@ void launch_gbuffer(const FrameView& F, const Band& bd, GHit* g, cudaStream_t s)
 // The path kernels below are persistent with dynamic work distribution; `q`
 // is one device u64 of the caller's (zeroed by the launcher, stream-ordered).
 void launch_init_gated(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
-                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s);
+                       const InitParams& ip, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s, const EllScratch* es = nullptr);
 void launch_init_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg,
                            const InitParams& ip, const HistSpec& h, int frame_idx, ResStore cur,
                            unsigned long long* q, cudaStream_t s);

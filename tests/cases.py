@@ -135,6 +135,12 @@ FULL_CASES = {
                                                       temporal=True, spatial_passes=1, spatial_neighbors=3,
                                                       spatial_radius=10, m_cap=20, frames=3, seed=1),
                                          "transient"),
+    # the paper's gated timing configuration: ellipsoidal initial
+    # sampling + temporal + spatial reuse at 256^2 with a narrow gate (bench `nlos`)
+    "nlos_cornell_wide_256": (lambda: scenes.bundled("cornell_wide", 256, 256),
+                              RenderConfig(gate=gate(6.0, 0.01), m_init=1, init=F.INIT_ELLIPSOIDAL, temporal=True,
+                                           spatial_passes=1, spatial_neighbors=3, spatial_radius=10, m_cap=20,
+                                           max_depth=6, frames=4, seed=1), "gated"),
     "full_c5_cornell_wide_256_25frames": (lambda: scenes.bundled("cornell_wide", 256, 256),
                                           RenderConfig(gate=gate(6.0, 0.0173), gate_step=0.01, m_init=1,
                                                        temporal=True, spatial_passes=1, spatial_neighbors=3,

@@ -111,10 +111,12 @@ print(json.dumps(stats))
 
 
 @pytest.mark.parametrize("name", ["full_c3_boxes_doppler_1080p", "full_c1_cornell_256", "mirror_replay",
-                                  "transient_full", "doppler_scene_reuse"])
+                                  "transient_full", "doppler_scene_reuse", "ellipsoidal_init",
+                                  "ellipsoidal_collimated", "nlos_cornell_wide_256"])
 def test_wavefront_bit_identical_to_per_item_kernels(tmp_path, name):
     outs = []
-    for tag, extra in (("wave", {}), ("legacy", {"TOFR_REUSE": "legacy", "TOFR_TRACE": "legacy"})):
+    for tag, extra in (("wave", {}), ("legacy", {"TOFR_REUSE": "legacy", "TOFR_TRACE": "legacy",
+                                                 "TOFR_ELL": "legacy"})):
         env = {**os.environ, **extra}
         f = tmp_path / f"{tag}.npy"
         p = subprocess.run([sys.executable, "-c", _CHILD, str(ROOT), name, str(f)], capture_output=True, text=True,
