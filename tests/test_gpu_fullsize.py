@@ -77,8 +77,16 @@ def test_full_size_parity(renderer, ref, name):
 #   shifted path's occlusion segment grazes a box edge, and the closed/open test
 #   (geometry.hpp:86-231, bary +-1e-12) resolves it differently.  Deterministic
 #   on both sides (the same counts every run).
+#   nlos_cornell_wide_256, frame 3, spatial, occluded: 1695 vs 1696 (one of 657,114
+#   attempts).  Same mechanism through the ellipsoidal sampler's transcendentals
+#   (atan2 / acos of the conic cut angles, sin / cos of its Gauss-Legendre nodes,
+#   ellipsoid.hpp:167-296): 61% of the pixels differ in the last bits (max relative
+#   error 1.5e-12), and one shifted segment's grazing occlusion test flips.  The
+#   wavefront sampler is bit-identical to the per-lane one (test below), so the
+#   difference is libm, not the restructuring.
 KNOWN_COUNTER_DIFFS = {
     "full_c4r_doppler_128x72_1024bins": {"f2.spatial.occluded": (3144, 3145)},
+    "nlos_cornell_wide_256": {"f3.spatial.occluded": (1695, 1696)},
 }
 
 
