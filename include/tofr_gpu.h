@@ -287,6 +287,12 @@ uint64_t tofr_fnv1a64(const void* data, uint64_t n);
  * whose bits differ (0 expected) */
 int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
 
+/* diagnostic (a -DTOFR_SOLVE_PROFILE=1 build only, else TOFR_ERR_UNSUPPORTED):
+ * per solved shift job {cycles from refill to finish, trial rounds | Newton
+ * iterations << 32 | re-projection rays << 40, SM clock at finish}; copies up
+ * to cap records (3 u64 each) and resets the recorder */
+int tofr_gpu_debug_solve_profile(uint64_t* out, uint64_t cap, uint64_t* n);
+
 /* measured FP64 throughput of the context's device (DFMA chains; GFLOP/s with
  * 2 flops per DFMA): the FP64 roofline's peak */
 int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops);

@@ -1736,6 +1736,14 @@ int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mi
     });
 }
 
+int tofr_gpu_debug_solve_profile(uint64_t* out, uint64_t cap, uint64_t* n) {
+    if (!n) return TOFR_ERR_INVALID;
+    size_t m = 0;
+    bool ok = debug_solve_profile(reinterpret_cast<unsigned long long*>(out), size_t(cap), &m);
+    *n = m;
+    return ok ? TOFR_OK : TOFR_ERR_UNSUPPORTED;
+}
+
 int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops) {
     return guard(ctx, [&] {
         if (!ctx || !gflops) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");

@@ -219,6 +219,7 @@ void launch_halo_unpack(ResStore grid, size_t item0, size_t n_items, const doubl
 void launch_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s);
 // measured FP64 DFMA throughput of this device (GFLOP/s, 2 flops per DFMA)
 double measure_fp64_peak_gflops(cudaStream_t s);
+bool debug_solve_profile(unsigned long long* out, size_t cap, size_t* n);
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
                        cudaStream_t s);
 

@@ -732,6 +732,19 @@ __global__ void __launch_bounds__(128)
 
 // SP: the grids may be sparse (transient); !SP instantiations (gated grids)
 // see slot == nullptr at compile time and drop the slot-map branches.
+// Diagnostic build (-DTOFR_SOLVE_PROFILE=1, a tools variant): per solved job,
+// {cycles from its refill to its finish, trial rounds it took part in, Newton
+// iterations, re-projection rays, SM cycle at finish} for the latency-floor
+// analysis of DESIGN 8 (tofr_gpu_debug_solve_profile).
+#ifndef TOFR_SOLVE_PROFILE
+#define TOFR_SOLVE_PROFILE 0
+#endif
+#if TOFR_SOLVE_PROFILE
+constexpr unsigned kSolveProfCap = 1u << 22;
+__device__ unsigned long long g_solve_prof[kSolveProfCap][3];
+__device__ unsigned int g_solve_prof_n;
+#endif
+
 template <bool VEL, bool SP>
 __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     k_shift_solve(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
@@ -771,6 +784,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     V2 step{0, 0};
     int iter = 0, bt = 0;
     bool pdl_fired = false;
+#if TOFR_SOLVE_PROFILE
+    long long prof_t0 = 0;
+    unsigned prof_rounds = 0, prof_rays0 = 0;
+#endif
 
     for (;;) {
         // ---- refill: idle lanes take the next jobs (one atomic per warp), but only
@@ -850,6 +867,11 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             bt = 0;
                             init = true;
                             active = true;
+#if TOFR_SOLVE_PROFILE
+                            prof_t0 = clock64();
+                            prof_rounds = 0;
+                            prof_rays0 = n_rays;
+#endif
                         }
                     }
                 }
@@ -954,6 +976,9 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         }
         unsigned em = __ballot_sync(0xffffffffu, (active && !parked) || helper);
         if (!((active && !parked) || helper)) continue;
+#if TOFR_SOLVE_PROFILE
+        if (active) ++prof_rounds;
+#endif
         __syncwarp(em);
         const Frame2 Jt = F.tframe[ttri];
         const Frame2 Js = F.tframe[stri];
@@ -1021,6 +1046,18 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
             scale *= 0.5;
         }
         if (fin) {
+#if TOFR_SOLVE_PROFILE
+            {
+                unsigned k = atomicAdd(&g_solve_prof_n, 1u);
+                if (k < kSolveProfCap) {
+                    long long now = clock64();
+                    g_solve_prof[k][0] = (unsigned long long)(now - prof_t0);
+                    g_solve_prof[k][1] = (unsigned long long)prof_rounds | ((unsigned long long)iter << 32) |
+                                         ((unsigned long long)(n_rays - prof_rays0) << 40);
+                    g_solve_prof[k][2] = (unsigned long long)now;
+                }
+            }
+#endif
             if (cfg.row_cost)  // the job's destination row: Newton iterations + setup and finish
                 atomicAdd(&cfg.row_cost[job_get(q, job).dpy], (unsigned long long)(iter) + 4ull);
             if (count) SCTR(SC_ITERATIONS, iter);
@@ -1631,6 +1668,28 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
         lc.numAttrs = 1;
         cudaLaunchKernelEx(&lc, finish, F0, F1, g0, g1, st0, st1, q, cfg, ctr, fq);
     }
+}
+
+// solve profile of a TOFR_SOLVE_PROFILE build: copies min(n, cap) records
+// (3 u64 each) and resets; returns false when the build has no profiler
+bool debug_solve_profile(unsigned long long* out, size_t cap, size_t* n) {
+#if TOFR_SOLVE_PROFILE
+    unsigned cnt = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&cnt, g_solve_prof_n, sizeof(cnt));
+    size_t m = cnt < kSolveProfCap ? cnt : kSolveProfCap;
+    if (m > cap) m = cap;
+    if (out && m) cudaMemcpyFromSymbol(out, g_solve_prof, m * 3 * sizeof(unsigned long long));
+    *n = m;
+    unsigned zero = 0;
+    cudaMemcpyToSymbol(g_solve_prof_n, &zero, sizeof(zero));
+    return true;
+#else
+    (void)out;
+    (void)cap;
+    *n = 0;
+    return false;
+#endif
 }
 
 void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
