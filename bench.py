@@ -112,6 +112,13 @@ WORKLOADS = {
                           spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
              "NLOS-style gated: cornell_wide 256x256, gate tau=6.0 dtau=0.01, ellipsoidal initial sampling + "
              "temporal + 1x3 spatial r10 (paper: 4 ms/image on an RTX 3090)"),
+    # BVH stress: cornell_wide's box + a 102,410-triangle displaced torus (64,875
+    # nodes, traversed from global memory), C3' gate and reuse
+    "mesh": ("mesh", 1920, 1080,
+             RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
+                          spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+             "mesh: cornell_wide box + 102,410-triangle torus (BVH in global memory) 1920x1080 gated tau=6.0 "
+             "dtau=0.0173, m_init 1, temporal + 1x3 spatial r10"),
 }
 
 PLAIN = {"c2p", "c4p"}

@@ -169,8 +169,7 @@ def reference_render(scene: RefScene, frame: float, gate: GateSpec, spp: int, se
     return mean, se
 
 
-def dump_bvh(scene: RefScene, frame: float = 0.0):
-    cap = 1 << 14
+def dump_bvh(scene: RefScene, frame: float = 0.0, cap: int = 1 << 14):
     nodes = np.zeros((cap, 11))
     parent = np.zeros(cap, dtype=np.int32)
     order = np.zeros(cap, dtype=np.int32)

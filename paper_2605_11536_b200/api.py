@@ -185,10 +185,11 @@ class Scene:
         return {"width": w.value, "height": h.value, "n_tris": nt.value, "n_nodes": nn.value, "diag": diag.value}
 
     def dump_bvh(self, frame: float = 0.0):
-        cap = 1 << 20
-        nodes = np.zeros((cap // 64, 11))
-        parent = np.zeros(cap // 64, dtype=np.int32)
-        order = np.zeros(cap // 64, dtype=np.int32)
+        info = self.info()
+        cap = max(16384, 2 * info["n_tris"] + 2)  # a binary tree over n leaves' triangles: < 2n nodes
+        nodes = np.zeros((cap, 11))
+        parent = np.zeros(cap, dtype=np.int32)
+        order = np.zeros(cap, dtype=np.int32)
         nn, nt = C.c_int32(), C.c_int32()
         diag = C.c_double()
         err = C.create_string_buffer(512)

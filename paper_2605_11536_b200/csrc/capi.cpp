@@ -167,6 +167,7 @@ struct FrameSlot {
     PackedFrame pk;
     FrameView view;
     DevBuf gbuf;  // rows [r0, r1)
+    bool cached = false;  // static scene: blob holds the (frame-invariant) snapshot
 };
 
 struct tofr_session {
@@ -178,6 +179,7 @@ struct tofr_session {
     // row band: compute rows [y0, y1), store rows [r0, r1)
     int y0 = 0, y1 = 0, r0 = 0, r1 = 0;
     bool cam_moves = false;
+    bool static_frames = false;  // frame-invariant snapshot: built and uploaded once per slot
     FrameSlot slot[2];
     DevBuf res[3];
     int cur = 0, prev = 1, spare = 2;
@@ -399,8 +401,26 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width, const
     return p;
 }
 
+// Static scenes (no animated object, no camera track): build_frame
+// (scene.hpp:479-548) returns the same snapshot for every frame -- same
+// world-space triangles, same SAH tree, same camera and beam -- so each slot
+// builds and uploads it once (a 10^5-triangle mesh costs ~0.1 s of host SAH
+// build per frame otherwise, the reference's per-frame rebuild, scene.hpp:503).
+bool static_scene(const HScene& sc) {
+    for (const HObject& o : sc.objects)
+        if (o.track.animated()) return false;
+    return sc.camera.track.size() <= 1;
+}
+
 void upload_frame(tofr_session* s, int which, double frame, int frame_id, cudaStream_t st) {
     FrameSlot& sl = s->slot[which];
+    sl.gbuf.ensure(size_t(s->r1 - s->r0) * s->W * sizeof(GHit));
+    if (sl.cached) {
+        sl.pk.view.frame_id = frame_id;
+        sl.view = rebase_view(sl.pk, static_cast<const unsigned char*>(sl.blob.p));
+        s->last_h2d = 0;
+        return;
+    }
     HFrame hf = build_frame(s->scene, frame);
     if (hf.max_depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
     sl.pk = pack_frame(s->scene, hf, frame_id);
@@ -412,8 +432,8 @@ void upload_frame(tofr_session* s, int which, double frame, int frame_id, cudaSt
     sl.blob.ensure(nb);
     ck(cudaMemcpyAsync(sl.blob.p, sl.staging.p, nb, cudaMemcpyHostToDevice, st), "frame upload");
     sl.view = rebase_view(sl.pk, static_cast<const unsigned char*>(sl.blob.p));
-    sl.gbuf.ensure(size_t(s->r1 - s->r0) * s->W * sizeof(GHit));
     s->last_h2d = nb;
+    sl.cached = s->static_frames;
 }
 
 void check_config(const tofr_render_config* c) {
@@ -483,6 +503,8 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     if ((y0 - s->r0) > (y1 - y0) || (s->r1 - y1) > (y1 - y0))
         throw ScopeError(TOFR_ERR_INVALID, "row band thinner than its halo (use fewer ranks)");
     s->cam_moves = !sc->s.camera.track.empty();
+    const char* sf = std::getenv("TOFR_STATIC_FRAMES");
+    s->static_frames = static_scene(sc->s) && !(sf && sf[0] == '0');
     if (kind == KIND_RESTIR && cfg && cfg->temporal && s->cam_moves && halo == 0 && (y0 > 0 || y1 < s->H))
         throw ScopeError(TOFR_ERR_INVALID,
                          "row band of a moving camera with temporal reuse needs a reprojection halo (halo > 0)");

@@ -336,8 +336,119 @@ BUNDLED = {"cornell": cornell, "cornell_wide": cornell_wide, "boxes_doppler": bo
 
 
 def bundled(name: str, width: int | None = None, height: int | None = None) -> SceneDef:
+    if name == "mesh":  # the BVH stress scene (not a bundled .scn)
+        return mesh_scene(width or 256, height)
     d = BUNDLED[name]()
     if width:
         d.camera.width = width
         d.camera.height = height or width
     return d
+
+
+# ---------------------------------------------------------------------------
+# BVH stress scene: the cornell_wide box with a finely
+# tessellated, displaced torus loaded through the OBJ path (scene_io.hpp:102-132)
+
+
+def torus_mesh(nu: int = 320, nv: int = 160, R: float = 0.45, r: float = 0.18, bumps: float = 0.04,
+               center=(0.0, -0.35, 0.0)):
+    """Displaced torus: (vertices, faces) with 2 * nu * nv triangles and no
+    degenerate ones.  Vertices are rounded through 17 significant digits, so
+    the OBJ text (write_torus_obj) and the inline triangles (mesh_scene) hold
+    the same doubles."""
+    verts = []
+    cx, cy, cz = center
+    for i in range(nu):
+        u = 2 * math.pi * i / nu
+        for j in range(nv):
+            v = 2 * math.pi * j / nv
+            rr = r * (1.0 + bumps / r * math.sin(7 * u) * math.sin(5 * v))
+            x = (R + rr * math.cos(v)) * math.cos(u)
+            z = (R + rr * math.cos(v)) * math.sin(u)
+            y = rr * math.sin(v)
+            verts.append(tuple(float(f"{c:.17g}") for c in (x + cx, y * 0.8 + cy, z + cz)))
+    faces = []
+    for i in range(nu):
+        for j in range(nv):
+            a = i * nv + j
+            b = ((i + 1) % nu) * nv + j
+            c = ((i + 1) % nu) * nv + (j + 1) % nv
+            d = i * nv + (j + 1) % nv
+            faces += [(a, b, c), (a, c, d)]
+    return verts, faces
+
+
+def write_torus_obj(path, nu: int = 320, nv: int = 160) -> int:
+    """The torus as an OBJ triangle list ("v" / "f" records, scene_io.hpp:102-132)."""
+    verts, faces = torus_mesh(nu, nv)
+    lines = [f"v {x:.17g} {y:.17g} {z:.17g}" for x, y, z in verts]
+    lines += [f"f {a + 1} {b + 1} {c + 1}" for a, b, c in faces]
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    return len(faces)
+
+
+def mesh_scene(width: int = 256, height: int | None = None, nu: int = 320, nv: int = 160) -> SceneDef:
+    """cornell_wide's box, light and camera plus the torus (glossy) with its
+    triangles inline: the same scene as mesh_scene_file's .scn + OBJ."""
+    d = cornell_wide()
+    d.objects = d.objects[:3]  # box, left, right (no tall box)
+    metal = 3
+    verts, faces = torus_mesh(nu, nv)
+    t = ObjectDef("torus")
+    for a, b, c in faces:
+        t.tri(verts[a], verts[b], verts[c], metal)
+    d.objects.append(t)
+    d.camera.width = width
+    d.camera.height = height or width
+    return d
+
+
+def mesh_scene_file(directory, width: int = 256, height: int = 256, nu: int = 320, nv: int = 160) -> str:
+    """Writes torus.obj + mesh_box.scn into `directory` (cornell_wide's box,
+    wide light and camera; 2 * nu * nv torus triangles: 102,400 by default)
+    and returns the .scn path (load with Scene.create / the oracle's RefScene)."""
+    from pathlib import Path
+    d = Path(directory)
+    d.mkdir(parents=True, exist_ok=True)
+    write_torus_obj(d / "torus.obj", nu, nv)
+    scn = f"""camera {{
+  position 0 0 3
+  forward 0 0 -1
+  up 0 1 0
+  fov_deg 36.87
+  resolution {width} {height}
+}}
+material white {{ kind diffuse albedo 0.73 0.73 0.73 }}
+material red   {{ kind diffuse albedo 0.63 0.065 0.05 }}
+material green {{ kind diffuse albedo 0.14 0.45 0.091 }}
+material metal {{ kind glossy albedo 0.8 0.8 0.8 roughness 0.3 }}
+light {{
+  regime wide
+  position 0 0.9 0
+  direction 0 -1 0
+  cone_deg 160
+  intensity 8 8 8
+}}
+object box {{
+  material white
+  quad -1 -1 -1   1 -1 -1   1 -1 1   -1 -1 1
+  quad -1 1 -1   -1 1 1   1 1 1   1 1 -1
+  quad -1 -1 -1   -1 1 -1   1 1 -1   1 -1 -1
+}}
+object left {{
+  material red
+  quad -1 -1 -1   -1 -1 1   -1 1 1   -1 1 -1
+}}
+object right {{
+  material green
+  quad 1 -1 -1   1 1 -1   1 1 1   1 -1 1
+}}
+object torus {{
+  material metal
+  obj torus.obj
+}}
+"""
+    p = d / "mesh_box.scn"
+    p.write_text(scn)
+    return str(p)

@@ -38,6 +38,30 @@ def test_converged_error_matches_oracle(renderer, ref):
     assert abs(mg.relmse - mr.relmse) <= 1e-6 * mr.relmse
 
 
+def test_transient_converged_error_matches_oracle(renderer, ref):
+    """Parity level 3 for the transient output (pipeline.hpp:396-528, :588-607):
+    the relMSE / MAPE of the ReSTIR histogram (temporal reuse, bins as pixels)
+    against a high-sample plain-deposit histogram (render_transient_plain, an
+    unbiased per-bin estimate) equal the CPU oracle's own errors against its
+    own plain reference, to 1e-6 relative."""
+    sd = scenes.bundled("cornell", 32)
+    base = dict(mode=F.MODE_TRANSIENT, bins=16, hist_t0=8.0, hist_bin_width=0.75, max_depth=6)
+    restir = RenderConfig(**base, m_init=2, temporal=True, m_cap=20, frames=4, seed=3)
+    plain = RenderConfig(**base, m_init=64, frames=2, seed=17)
+    rs = ref.RefScene(sd)
+    g_ref, r_ref = renderer.render_transient_plain(sd, plain), ref.render_transient_plain(rs, plain)
+    g, r = renderer.render_transient(sd, restir), ref.render_transient(rs, restir)
+    mg = Hn.compute_metrics(g.hist.rgb, g_ref.hist.rgb)
+    mr = Hn.compute_metrics(r.hist.rgb, r_ref.hist.rgb)
+    print("gpu", mg, "cpu", mr)
+    assert r_ref.hist.rgb.max() > 0 and mr.relmse > 0
+    assert abs(mg.mape - mr.mape) <= 1e-6 * mr.mape
+    assert abs(mg.relmse - mr.relmse) <= 1e-6 * mr.relmse
+    # and the images (sum over bins) the same way
+    mgi, mri = Hn.compute_metrics(g.image, g_ref.image), Hn.compute_metrics(r.image, r_ref.image)
+    assert abs(mgi.relmse - mri.relmse) <= 1e-6 * mri.relmse
+
+
 def test_render_equal_time_reps(renderer):
     sd = scenes.bundled("cornell", 24)
     cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=2, spatial_passes=1,

@@ -135,3 +135,18 @@ def test_plain_deposits_are_deterministic():
     assert np.array_equal(a.hist.rgb, b.hist.rgb)
     assert np.array_equal(a.hist.count, b.hist.count)
     assert np.array_equal(a.image, b.image)
+
+
+@pytest.mark.parametrize("name", ["cornell", "mesh"])
+def test_static_scene_snapshot_cache_is_bit_identical(name, monkeypatch):
+    """Static scenes upload their frame snapshot once per slot (the host SAH
+    build of a 10^5-triangle mesh would run every frame otherwise): the frames
+    equal those of per-frame rebuilds (TOFR_STATIC_FRAMES=0)."""
+    sd = scenes.mesh_scene(32) if name == "mesh" else scenes.bundled("cornell", 40)
+    cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0 if name == "mesh" else 10.0, 0.3, 1.0), m_init=1,
+                       temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=4, frames=4)
+    got = Renderer(0).render_gated(sd, cfg)
+    monkeypatch.setenv("TOFR_STATIC_FRAMES", "0")
+    ref = Renderer(0).render_gated(sd, cfg)
+    assert ref.image.max() > 0
+    assert np.array_equal(got.image, ref.image)
