@@ -688,10 +688,12 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         if (lo) {
             s->send_lo.ensure(lo);
             s->recv_lo.ensure(lo);
+            ck(cudaMemsetAsync(s->recv_lo.p, 0, lo, ctx->stream), "memset");  // empty until received
         }
         if (hi) {
             s->send_hi.ensure(hi);
             s->recv_hi.ensure(hi);
+            ck(cudaMemsetAsync(s->recv_hi.p, 0, hi, ctx->stream), "memset");
         }
     }
     return s.release();
@@ -1494,6 +1496,9 @@ int tofr_gpu_session_halo_nccl(tofr_session* ss, const uint8_t* id, int32_t rank
     if (!ss || !id) return TOFR_ERR_INVALID;
     return guard(ss->ctx, [&] {
         if (!nccl_available()) throw ScopeError(TOFR_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+        // rank g's band lies above rank g+1's: a halo side needs a neighbour rank
+        if ((ss->r0 < ss->y0 && rank == 0) || (ss->r1 > ss->y1 && rank == world - 1))
+            throw ScopeError(TOFR_ERR_INVALID, "halo_nccl: the band keeps a halo on a side without a neighbour rank");
         ss->xport = make_nccl_transport(id, rank, world, ss->ctx->device);
     });
 }

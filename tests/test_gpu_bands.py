@@ -174,9 +174,13 @@ def test_nccl_transport_initialises():
     sd = scenes.bundled("cornell", 32)
     cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 10.0, 0.3, 1.0), m_init=1, temporal=True, spatial_passes=1,
                        spatial_neighbors=3, spatial_radius=4, frames=1)
-    s = r.session(sd, cfg, band=(0, 16, 4))
-    assert s.halo_transport() == "none"
+    band = r.session(sd, cfg, band=(0, 16, 4))
+    assert band.halo_transport() == "none"
+    with pytest.raises(Exception, match="without a neighbour rank"):
+        band.halo_nccl(uid, 0, 1)  # its lower halo would have no sender
+    s = r.session(sd, cfg)  # world 1: the whole frame, no halo
     s.halo_nccl(uid, 0, 1)
     assert s.halo_transport() == "nccl"
-    s.step(stats=False)  # world 1: no peer, the exchange is an empty group
+    s.step(stats=False)
     s.sync()
+    assert s.read_image().max() > 0
