@@ -135,7 +135,7 @@ def test_traversal_bitexact_large_mesh(renderer, ref):
     rs = ref.RefScene(sd)
     t, tri = renderer.probe_rays(sd, 0.0, rays, 0)
     rt, rtri = ref.probe_rays(rs, 0.0, rays, 0)
-    assert (tri >= 0).mean() > 0.9
+    assert (tri >= 0).mean() > 0.5 and (tri >= 10).mean() > 0.02  # ids >= 10: the torus
     assert np.array_equal(tri, rtri)
     assert np.array_equal(t, rt)
     seg = _random_rays(20000, rng, box=1.0, segments=True)
