@@ -547,6 +547,7 @@ def run_ours(args) -> None:
                 "flops_per_launch": fl, "flops_per_unit": prof["fp64_flops_per_unit"], "unit_of_work": unit,
                 "units_per_launch": upl, "avg_launch_ms": dur_s * 1e3, "source": prof["source"]}
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
+    kernel_launches = {k: round(v[1] / args.steps, 2) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
     workv = {k: work1[k] - work0[k] for k in work1} if work1 else {}  # the value frames
     rays = (workv.get("rays_closest", 0) + workv.get("rays_any", 0)) if workv else 0
     t_s = t_max * 1e-3
@@ -603,6 +604,7 @@ def run_ours(args) -> None:
                                  "by construction (SURVEY 8d); see rays_per_s and kernel_ms"},
             "roofline_fp64": fp64,
             "kernel_ms_per_step": kernel_ms,
+            "kernel_launches_per_step": kernel_launches,
             "reservoir_pool": pool_info,
             "rays_per_s": rays / t_s if t_s > 0 else None,
             "shift_jobs_per_s": workv.get("shift_jobs", 0) / t_s if (t_s > 0 and workv) else None,
