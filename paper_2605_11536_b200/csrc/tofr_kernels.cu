@@ -932,6 +932,9 @@ __global__ void k_hist_image(const double* hist, int p0, int p1, int B, double s
 // trace-only transient deposits (render_transient_plain, pipeline.hpp:531-571;
 // TransientHistogram::deposit, transport.hpp:121-126): nested-loop walk
 // (default; TOFR_TRACE=wave: the k_trace<PlainSink2> state machine).
+#ifndef TOFR_PLAIN_HISTORY
+#define TOFR_PLAIN_HISTORY 0
+#endif
 
 struct PlainSink {
     HistSpec h;
@@ -1051,6 +1054,9 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
     int W = F.cam.w;
     size_t n = size_t(bd.y1 - bd.y0) * W;
     uint32_t n_dep = 0;
+#if TOFR_PLAIN_HISTORY
+    WalkV vh[kMaxVerts];
+#endif
     TOFR_FOR_ITEMS(i, n, q) {
         int p = bd.y0 * W + int(i);
         int px = p % W, py = p / W;
@@ -1059,7 +1065,13 @@ __global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const 
         GHit g = gbuf[p];
         for (int s = 0; s < m_init; ++s) {
             Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
+#if TOFR_PLAIN_HISTORY  // A/B variant: the generic walk with its vertex history
+            Rng erng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 2);
+            NoEll ell;
+            trace_tree(F, cfg, px, py, g, rng, erng, sink, vh, ell);
+#else
             trace_tree_deposit(F, cfg, px, py, g, rng, sink);
+#endif
         }
     }
     work_add(cfg.work, WK_DEPOSITS, n_dep);
