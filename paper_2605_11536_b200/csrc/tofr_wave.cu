@@ -55,6 +55,13 @@
 #ifndef TOFR_HELP_IDLE
 #define TOFR_HELP_IDLE 0
 #endif
+// 1: a batch with fewer jobs than 32 per warp of the grid is spread over all
+// warps (at most ceil(jobs / warps) busy lanes per warp), so every busy lane
+// has idle lanes of its own warp to run its halving ladder from the first
+// round (without it the first warps take 32 jobs each and the rest exit)
+#ifndef TOFR_SHARE
+#define TOFR_SHARE 1
+#endif
 
 namespace tofr_b200 {
 
@@ -789,6 +796,10 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
     unsigned prof_rounds = 0, prof_rays0 = 0;
 #endif
 
+    // small batches: busy lanes per warp if the jobs are spread over every warp
+    const uint32_t n_warps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t share = j1 > j0 ? (j1 - j0 + n_warps - 1) / n_warps : 1u;
+    const bool spread = TOFR_SHARE && share < 32;
     for (;;) {
         // ---- refill: idle lanes take the next jobs (one atomic per warp), but only
         // once at least TOFR_REFILL lanes are idle (or none is busy), so the
@@ -797,6 +808,11 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned im = __ballot_sync(0xffffffffu, idle);
         unsigned bm = __ballot_sync(0xffffffffu, active);
         bool need = idle && (__popc(im) >= TOFR_REFILL || bm == 0);
+        if (spread) {  // at most `share` busy lanes; the others stay free to help
+            unsigned nm0 = __ballot_sync(0xffffffffu, need);
+            int room = int(share) - __popc(bm);
+            need = need && room > 0 && __popc(nm0 & ((1u << lane) - 1)) < room;
+        }
         unsigned m = __ballot_sync(0xffffffffu, need);
         if (m) {
             int leader = __ffs(m) - 1;
@@ -898,7 +914,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int owner = lane, hk = 0, K = 0;
         unsigned group = 1u << lane;
         {
-            const bool free_lane = TOFR_HELP_IDLE ? !active : exhausted;
+            const bool free_lane = (TOFR_HELP_IDLE || spread) ? !active : exhausted;
             unsigned idle = __ballot_sync(0xffffffffu, free_lane);
             unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked);
             if (idle && cand) {
