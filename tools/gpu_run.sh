@@ -20,7 +20,6 @@ for s in "$@"; do
         python bench.py --workload $a --steps 2 --warmup 25 --no-cpu-baseline > $O/ncu_full_$a.log 2>&1
       f=$O/full_${a}_$(echo $b|tr -dc a-z_)
       python tools/ncu_summary.py full $f.ncu-rep > $f.txt 2>&1
-      python tools/traffic_json.py --out $O/traffic.json $f.ncu-rep >> $O/traffic.log 2>&1
       ncu -i $f.ncu-rep --page source --print-source cuda,sass --csv --launch-count 1 > /tmp/src.csv 2>/dev/null
       python tools/ncu_lines.py /tmp/src.csv 30 > ${f/full_/lines_}.txt 2>&1
       rm -f $f.ncu-rep ;;
