@@ -1044,7 +1044,10 @@ __device__ void trace_tree_deposit(const FrameView& F, const PathCfg& cfg, int p
     }
 }
 
-__global__ void __launch_bounds__(128) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
+#ifndef TOFR_PLAIN_MINB
+#define TOFR_PLAIN_MINB 4
+#endif
+__global__ void __launch_bounds__(128, TOFR_PLAIN_MINB) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     HistSpec h, int m_init, int frame_idx, double* hist,
                                                     double* img, unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];

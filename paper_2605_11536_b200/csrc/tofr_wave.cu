@@ -62,6 +62,14 @@
 #ifndef TOFR_SHARE
 #define TOFR_SHARE 1
 #endif
+// >0: a lane whose solve has rejected TOFR_ESCALATE halvings in a row (or
+// passed two Newton iterations) is "slow": its warp stops refilling until its
+// slow lanes finish, and the lanes that free up run their halving ladders
+// (the tail-phase helpers) -- the long serial chains that end every shift
+// batch get helpers before the queue drains
+#ifndef TOFR_ESCALATE
+#define TOFR_ESCALATE 0
+#endif
 
 namespace tofr_b200 {
 
@@ -808,6 +816,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         unsigned im = __ballot_sync(0xffffffffu, idle);
         unsigned bm = __ballot_sync(0xffffffffu, active);
         bool need = idle && (__popc(im) >= TOFR_REFILL || bm == 0);
+#if TOFR_ESCALATE
+        const unsigned slow_m = __ballot_sync(0xffffffffu, active && !init && (bt >= TOFR_ESCALATE || iter >= 2));
+        if (slow_m) need = false;  // keep the freed lanes as helpers of the slow chains
+#else
+        const unsigned slow_m = 0;
+#endif
         if (spread) {  // at most `share` busy lanes; the others stay free to help
             unsigned nm0 = __ballot_sync(0xffffffffu, need);
             int room = int(share) - __popc(bm);
@@ -914,9 +928,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
         int owner = lane, hk = 0, K = 0;
         unsigned group = 1u << lane;
         {
-            const bool free_lane = (TOFR_HELP_IDLE || spread) ? !active : exhausted;
+            const bool free_lane = (TOFR_HELP_IDLE || spread || slow_m) ? !active : exhausted;
             unsigned idle = __ballot_sync(0xffffffffu, free_lane);
-            unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked);
+            // helpers go to the slow chains first while the queue still has work
+            const bool drained = __any_sync(0xffffffffu, exhausted);
+            unsigned cand = __ballot_sync(0xffffffffu, active && !init && !parked &&
+                                                           (drained || !slow_m || ((slow_m >> lane) & 1u)));
             if (idle && cand) {
                 // idle lanes are dealt out in rank order, H to each busy lane
                 tail = true;
@@ -1428,7 +1445,14 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
     }
 }
 
-__global__ void k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int frame_idx, ResStore cur,
+// merge kernels: chains of dependent gathers (merge list -> source pixel ->
+// slot map -> pool row -> chunks), latency-bound; TOFR_APPLY_MINB resident
+// 256-thread CTAs per SM trade registers for loads in flight
+#ifndef TOFR_APPLY_MINB
+#define TOFR_APPLY_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TOFR_APPLY_MINB)
+    k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int frame_idx, ResStore cur,
                                  ResStore prev, WaveScratch ws) {
     int B = cg.transient ? cg.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B;
@@ -1562,7 +1586,7 @@ __global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid g
     }
 }
 
-__global__ void k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass, int j,
+__global__ void __launch_bounds__(256, TOFR_APPLY_MINB) k_spatial_apply(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass, int j,
                                 int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
