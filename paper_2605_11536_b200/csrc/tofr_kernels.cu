@@ -1045,7 +1045,7 @@ __device__ void trace_tree_deposit(const FrameView& F, const PathCfg& cfg, int p
 }
 
 #ifndef TOFR_PLAIN_MINB
-#define TOFR_PLAIN_MINB 4
+#define TOFR_PLAIN_MINB 5
 #endif
 __global__ void __launch_bounds__(128, TOFR_PLAIN_MINB) k_hist_plain(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg,
                                                     HistSpec h, int m_init, int frame_idx, double* hist,

@@ -1449,7 +1449,7 @@ __global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView
 // slot map -> pool row -> chunks), latency-bound; TOFR_APPLY_MINB resident
 // 256-thread CTAs per SM trade registers for loads in flight
 #ifndef TOFR_APPLY_MINB
-#define TOFR_APPLY_MINB 1
+#define TOFR_APPLY_MINB 5
 #endif
 __global__ void __launch_bounds__(256, TOFR_APPLY_MINB)
     k_temporal_apply(Band bd, int W, GateGrid cg, PathCfg cfg, int frame_idx, ResStore cur,
