@@ -211,6 +211,8 @@ struct tofr_session {
     bool wave = false;
     DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng, wv_mlist;
     size_t wv_cap = 0;
+    DevBuf row_jobs;          // per-row shift-job bounds of a stage (adaptive row batches)
+    size_t batches_seen = 0;  // most row batches one stage took
     tofr_halo_exchange_fn xfn = nullptr;  // host callback transport (gloo / tests)
     void* xuser = nullptr;
     std::unique_ptr<HaloTransport> xport;   // native transport (NCCL or in-process peer copies)
@@ -294,7 +296,7 @@ struct tofr_session {
         res_rows.release();
         for (DevBuf* b : {&wv_done, &wv_fin_ctr, &wv_nbr, &row_cost, &read_stage[0], &read_stage[1], &image, &accum, &hist, &ctr, &send_lo, &send_hi, &recv_lo, &recv_hi, &wo_cls,
                           &wo_counts, &wo_perm, &sp_mapped, &sp_ok, &sp_rng, &sp_list, &sp_count, &wv_jobs, &wv_out,
-                          &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist})
+                          &wv_ctl, &wv_map_a, &wv_map_b, &wv_tsrc, &wv_rng, &wv_mlist, &row_jobs})
             b->release();
     }
 };
@@ -331,6 +333,50 @@ int wave_batches(const tofr_session* s, size_t per) {
     size_t rows_fit = s->wv_cap / std::max<size_t>(1, per * per_row);
     if (rows_fit == 0) throw ScopeError(TOFR_ERR_OOM, "reuse shift queue smaller than one image row (raise TOFR_WAVE_CAP)");
     return int((rows + rows_fit - 1) / rows_fit);
+}
+// Row cuts of a wavefront stage.  One batch when the worst case fits the queue;
+// otherwise, for transient grids (TOFR_ADAPTIVE_BATCHES=0: uniform batches), the
+// band is cut from per-row upper bounds of the stage's jobs counted on the
+// device (k_count_temporal / k_count_spatial: exact forward jobs, at most one
+// inverse job per item that can have one), so a grid that is 40% full runs in
+// about 40% of the worst-case batches.  One host sync per stage: transient
+// frames are 10-300 ms.
+template <class Count>
+std::vector<int> stage_cuts(tofr_session* s, const Band& bd, size_t per, cudaStream_t st, Count&& count) {
+    const int nb = wave_batches(s, per);
+    std::vector<int> cuts{bd.y0};
+    const char* ad = std::getenv("TOFR_ADAPTIVE_BATCHES");
+    if (nb > 1 && s->transient && !(ad && ad[0] == '0')) {
+        const int rows = bd.y1 - bd.y0;
+        s->row_jobs.ensure(size_t(rows) * 8);
+        std::vector<unsigned long long> h(static_cast<size_t>(rows), 0ull);
+        count(s->row_jobs.as<unsigned long long>());
+        ck(cudaMemcpyAsync(h.data(), s->row_jobs.p, size_t(rows) * 8, cudaMemcpyDeviceToHost, st), "row jobs");
+        ck(cudaStreamSynchronize(st), "row jobs");
+        unsigned long long acc = 0;
+        for (int r = 0; r < rows; ++r) {
+            if (acc + h[r] > s->wv_cap && acc > 0) {
+                cuts.push_back(bd.y0 + r);
+                acc = 0;
+            }
+            acc += h[r];  // <= wv_cap: a row's worst case fits (wave_batches)
+        }
+    } else {
+        const int step = (bd.y1 - bd.y0 + nb - 1) / nb;  // <= rows_fit of wave_batches
+        for (int y = bd.y0 + step; y < bd.y1; y += step) cuts.push_back(y);
+    }
+    cuts.push_back(bd.y1);
+    s->batches_seen = std::max<size_t>(s->batches_seen, cuts.size() - 1);
+    return cuts;
+}
+template <class Fn>
+void for_row_cuts(const Band& bd, const std::vector<int>& cuts, Fn&& fn) {
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+        Band sb = bd;
+        sb.y0 = cuts[k];
+        sb.y1 = cuts[k + 1];
+        fn(sb);
+    }
 }
 template <class Fn>
 void for_row_batches(const Band& bd, int nb, Fn&& fn) {
@@ -918,11 +964,16 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
-            if (s->wave)
-                for_row_batches(bd, wave_batches(s, 2), [&](const Band& sb) {
-                    launch_temporal_wave(F, sb, g, s->slot[psl].view, gp, pc, cg, pg, f, cur,
-                                         store_of(s, s->res[s->prev]), wv, ctr + 0 * SC_COUNT, q, stream);
+            if (s->wave) {
+                ResStore prev_st = store_of(s, s->res[s->prev]);
+                auto cuts = stage_cuts(s, bd, 2, stream, [&](unsigned long long* rows) {
+                    launch_count_temporal(F, bd, g, s->slot[psl].view, cg, cur, prev_st, wv, rows, stream);
                 });
+                for_row_cuts(bd, cuts, [&](const Band& sb) {
+                    launch_temporal_wave(F, sb, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, prev_st, wv,
+                                         ctr + 0 * SC_COUNT, q, stream);
+                });
+            }
             else
                 launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
                                 wo, ctr + 0 * SC_COUNT, q, stream);
@@ -954,12 +1005,15 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                 scr.count = s->sp_count.as<uint32_t>();
                 scp = &scr;
             }
-            if (s->wave && sp.neighbors > 0 && sp.radius > 0)
-                for_row_batches(bd, wave_batches(s, wave_jobs_per_item(sp.neighbors)), [&](const Band& sb) {
+            if (s->wave && sp.neighbors > 0 && sp.radius > 0) {
+                auto cuts = stage_cuts(s, bd, wave_jobs_per_item(sp.neighbors), stream, [&](unsigned long long* rows) {
+                    launch_count_spatial(F, bd, pc, cg, sp, pass, f, cur, rows, stream);
+                });
+                for_row_cuts(bd, cuts, [&](const Band& sb) {
                     launch_spatial_wave(F, sb, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wv,
                                         ctr + 1 * SC_COUNT, q, stream);
                 });
-            else
+            } else
                 launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
                                ctr + 1 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);

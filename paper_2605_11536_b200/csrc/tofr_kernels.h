@@ -145,6 +145,13 @@ struct WaveScratch {
 // jobs per item a stage can enqueue (capacity planning)
 inline size_t wave_jobs_per_item(int neighbors) { return size_t(neighbors > 1 ? neighbors + 1 : 2); }
 
+// per-row upper bounds of a stage's shift jobs (adaptive row batches)
+void launch_count_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp,
+                           const GateGrid& cg, ResStore cur, ResStore prev, const WaveScratch& ws,
+                           unsigned long long* rows, cudaStream_t s);
+void launch_count_spatial(const FrameView& F, const Band& bd, const PathCfg& cfg, const GateGrid& gg,
+                          const SpatialParams& sp, int pass, int frame_idx, ResStore src, unsigned long long* rows,
+                          cudaStream_t s);
 void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                           const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx, ResStore cur,
                           ResStore prev, const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q,

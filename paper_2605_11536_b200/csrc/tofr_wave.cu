@@ -1732,6 +1732,96 @@ bool debug_solve_profile(unsigned long long* out, size_t cap, size_t* n) {
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Adaptive row batches (transient grids): an upper bound of the shift jobs each
+// image row of a stage will queue, so the host cuts the band into as few row
+// batches as the queue holds (the worst-case sizing, jobs-per-item x items,
+// assumes every reservoir non-empty: 8 batches for 1080p x 64 bins where the
+// grids are ~40% full).  Counts are summed per warp for each row.
+
+__device__ __forceinline__ void row_count_add(unsigned long long* rows, int row, unsigned v) {
+    const unsigned grp = __match_any_sync(0xffffffffu, row);
+    const unsigned sum = __reduce_add_sync(grp, v);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1 && sum) atomicAdd(&rows[row], (unsigned long long)sum);
+}
+
+// temporal (k_temporal_prep): forward job if the reprojected source is
+// non-empty, inverse job if the destination is, both only when the source has M > 0
+__global__ void k_count_temporal(Band bd, int W, GateGrid cg, ResStore cur, ResStore prev, const uint64_t* tsrc,
+                                 unsigned long long* rows) {
+    int B = cg.transient ? cg.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t n_round = (n + 31) / 32 * 32;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += size_t(gridDim.x) * blockDim.x) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        unsigned jobs = 0;
+        if (live) {
+            uint64_t src_pix = tsrc[size_t(p) - size_t(bd.y0) * W];
+            if (src_pix != ~uint64_t(0)) {
+                double2 s0 = ld2(prev, 0, size_t(src_pix) * B + b);
+                if (s0.y > 0) jobs = unsigned(s0.x > 0) + unsigned(ld2(cur, 0, it).x > 0);
+            }
+        }
+        row_count_add(rows, p / W - bd.y0, jobs);
+    }
+}
+
+// spatial pass (k_spatial_prep_fwd / _inv): the forward jobs of every non-empty
+// neighbour, plus at most one inverse job per item at a time (an inverse batch
+// replaces the previous one), only when the item or a neighbour is non-empty
+__global__ void k_count_spatial(Band bd, int W, int H, GateGrid gate, PathCfg cfg, SpatialParams sp, int pass,
+                                int frame_idx, ResStore src_grid, unsigned long long* rows) {
+    int B = gate.transient ? gate.h.bins : 1;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t n_round = (n + 31) / 32 * 32;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += size_t(gridDim.x) * blockDim.x) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int p = int(it / B), b = int(it % B);
+        int px = p % W, py = p / W;
+        unsigned fwd = 0;
+        bool self = false;
+        if (live) {
+            uint64_t rk = spatial_rot_key(uint64_t(p), pass, cfg.seed, frame_idx);
+            for (int j = 0; j < sp.neighbors; ++j) {
+                int nx, ny;
+                size_t si;
+                if (spatial_neighbor(bd, W, H, B, px, py, b, sp, rk, j, src_grid, nx, ny, si) &&
+                    ld2(src_grid, 0, si).x > 0)
+                    ++fwd;
+            }
+            self = ld2(src_grid, 0, it).x > 0;
+        }
+        row_count_add(rows, p / W - bd.y0, fwd + unsigned(self || fwd > 0));
+    }
+}
+
+void launch_count_temporal(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp,
+                           const GateGrid& cg, ResStore cur, ResStore prev, const WaveScratch& ws,
+                           unsigned long long* rows, cudaStream_t s) {
+    size_t npx = size_t(bd.y1 - bd.y0) * Fc.cam.w, n = npx * (cg.transient ? cg.h.bins : 1);
+    if (!n) return;
+    cudaMemsetAsync(rows, 0, size_t(bd.y1 - bd.y0) * sizeof(unsigned long long), s);
+    {
+        KScope ks("k_temporal_reproject", s);
+        k_temporal_reproject<<<grid_n(npx, 256), 256, 0, s>>>(Fc, bd, gc, Fp, ws);
+    }
+    KScope ks("k_count_temporal", s);
+    k_count_temporal<<<grid_n(n, 256), 256, 0, s>>>(bd, Fc.cam.w, cg, cur, prev, ws.tsrc, rows);
+}
+
+void launch_count_spatial(const FrameView& F, const Band& bd, const PathCfg& cfg, const GateGrid& gg,
+                          const SpatialParams& sp, int pass, int frame_idx, ResStore src, unsigned long long* rows,
+                          cudaStream_t s) {
+    size_t n = size_t(bd.y1 - bd.y0) * F.cam.w * (gg.transient ? gg.h.bins : 1);
+    if (!n) return;
+    cudaMemsetAsync(rows, 0, size_t(bd.y1 - bd.y0) * sizeof(unsigned long long), s);
+    KScope ks("k_count_spatial", s);
+    k_count_spatial<<<grid_n(n, 256), 256, 0, s>>>(bd, F.cam.w, F.cam.h, gg, cfg, sp, pass, frame_idx, src, rows);
+}
+
 void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, const FrameView& Fp, const GHit* gp,
                           const PathCfg& cfg, const GateGrid& cg, const GateGrid& pg, int frame_idx, ResStore cur,
                           ResStore prev, const WaveScratch& ws, unsigned long long* ctr, unsigned long long* q,

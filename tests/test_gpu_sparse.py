@@ -129,12 +129,20 @@ def test_gated_row_batches_equal_one_batch():
                    {k: v for k, v in b[stage].items() if k != "seconds"}
 
 
-def test_transient_row_batches_equal_one_batch():
+@pytest.mark.parametrize("adaptive", ["1", "0"])
+def test_transient_row_batches_equal_one_batch(adaptive):
+    """Row batches cut from the device-counted per-row job bounds (adaptive,
+    the default for transient grids) or uniformly from the worst case: the
+    same bits as one batch, and the queue never overflows."""
     scene, cfg = CASES["temporal_spatial"]
     cfg = RenderConfig(**{**cfg.__dict__, "frames": 5})
     one = _render(scene, cfg, TOFR_SPARSE="1")
-    many = _render(scene, cfg, TOFR_SPARSE="1", TOFR_WAVE_CAP="20000")
+    many = _render(scene, cfg, TOFR_SPARSE="1", TOFR_WAVE_CAP="20000", TOFR_ADAPTIVE_BATCHES=adaptive)
     assert np.array_equal(many.hist.rgb, one.hist.rgb)
+    for a, b in zip(many.stats, one.stats):
+        for stage in ("temporal", "spatial"):
+            assert {k: v for k, v in a[stage].items() if k != "seconds"} == \
+                   {k: v for k, v in b[stage].items() if k != "seconds"}
 
 
 def test_queue_smaller_than_a_row_raises():
