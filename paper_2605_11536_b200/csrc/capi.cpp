@@ -335,18 +335,20 @@ int wave_batches(const tofr_session* s, size_t per) {
     return int((rows + rows_fit - 1) / rows_fit);
 }
 // Row cuts of a wavefront stage.  One batch when the worst case fits the queue;
-// otherwise, for transient grids (TOFR_ADAPTIVE_BATCHES=0: uniform batches), the
-// band is cut from per-row upper bounds of the stage's jobs counted on the
-// device (k_count_temporal / k_count_spatial: exact forward jobs, at most one
-// inverse job per item that can have one), so a grid that is 40% full runs in
-// about 40% of the worst-case batches.  One host sync per stage: transient
-// frames are 10-300 ms.
+// otherwise uniform row batches sized for the worst case, or -- opt-in,
+// TOFR_ADAPTIVE_BATCHES=1, transient grids -- cuts from per-row upper bounds of
+// the stage's jobs counted on the device (k_count_temporal / k_count_spatial:
+// exact forward jobs, at most one inverse job per item that can have one; one
+// host sync per stage).  Measured: 8 -> 2 batches at 1080p x 64 bins, 119 -> 17
+// solve launches per C4 band frame, but the transient stages are throughput-
+// bound, so the saved tails (solve 6.85 -> 6.76 ms) do not pay for the count
+// pass (0.8-3.2 ms): 21.5 -> 20.9 frames/s, C4 band 3.80 -> 3.82 (r02s).
 template <class Count>
 std::vector<int> stage_cuts(tofr_session* s, const Band& bd, size_t per, cudaStream_t st, Count&& count) {
     const int nb = wave_batches(s, per);
     std::vector<int> cuts{bd.y0};
     const char* ad = std::getenv("TOFR_ADAPTIVE_BATCHES");
-    if (nb > 1 && s->transient && !(ad && ad[0] == '0')) {
+    if (nb > 1 && s->transient && ad && ad[0] == '1') {
         const int rows = bd.y1 - bd.y0;
         s->row_jobs.ensure(size_t(rows) * 8);
         std::vector<unsigned long long> h(static_cast<size_t>(rows), 0ull);
