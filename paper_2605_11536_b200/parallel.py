@@ -271,8 +271,9 @@ class BandSession:
         ncclSend / ncclRecv pair on the session stream.  TOFR_HALO_TRANSPORT=
         callback keeps the torch.distributed callback instead."""
         import torch.distributed as dist
-        if dist.get_backend(group) != "nccl" or os.environ.get("TOFR_HALO_TRANSPORT", "native") == "callback":
-            return False
+        mode = os.environ.get("TOFR_HALO_TRANSPORT", "native")
+        if mode == "callback" or (dist.get_backend(group) != "nccl" and mode != "nccl"):
+            return False  # TOFR_HALO_TRANSPORT=nccl: the library's NCCL even on a gloo group
         box = [renderer.nccl_unique_id() if self.rank == 0 else None]
         dist.broadcast_object_list(box, src=0, group=group)
         if box[0] is None:  # libnccl not loadable by the library: every rank falls back
