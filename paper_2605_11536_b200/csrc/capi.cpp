@@ -188,6 +188,7 @@ struct tofr_session {
     bool sparse = false;
     size_t pool_rows = 0;
     int pool_planes = kResChunks;  // chunk planes of a sparse grid (header included)
+    bool compact_rows = false;     // sparse rows without the k = 2 prefix cache (ResStore::compact)
     // solve / finish overlap (ShiftQueue::done, ShiftOverlap; opt-in TOFR_OVERLAP=1)
     DevBuf wv_done, wv_fin_ctr, wv_nbr;
     uint32_t ov_epoch = 0;
@@ -303,8 +304,15 @@ struct tofr_session {
 
 namespace {
 
+template <class T>
+const T* rows_base_c(const DevBuf& b, int row0, size_t per_row) {
+    return b.as<T>() - ptrdiff_t(size_t(row0) * per_row);
+}
+
 // Global-indexed views of band-local buffers (see Band in tofr_kernels.h).
-ResStore store_of(const tofr_session* s, const DevBuf& b) {
+// `frame_slot`: the frame slot whose G-buffer and camera the grid's records
+// belong to (compact pool rows rebuild their prefix cache from them).
+ResStore store_of(const tofr_session* s, const DevBuf& b, int frame_slot = -1) {
     size_t items = s->items_stored();
     ptrdiff_t off = ptrdiff_t(size_t(s->r0) * s->W * s->B);
     if (!s->sparse) return ResStore{b.as<double2>() - off, items};
@@ -316,6 +324,13 @@ ResStore store_of(const tofr_session* s, const DevBuf& b) {
     st.rows = s->res_rows.as<unsigned int>() + k;
     st.err = reinterpret_cast<unsigned long long*>(s->res_rows.as<unsigned char>() + 16);
     st.planes = s->pool_planes;
+    if (s->compact_rows) {
+        if (frame_slot < 0) throw ScopeError(TOFR_ERR_INVALID, "compact reservoir rows need their frame");
+        st.compact = 1;
+        st.gbuf = rows_base_c<GHit>(s->slot[frame_slot].gbuf, s->r0, s->W);
+        st.cam = s->slot[frame_slot].view.cam;
+        st.bins = s->B;
+    }
     return st;
 }
 
@@ -617,7 +632,12 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 for (const HMaterial& m : sc->s.materials)
                     if (!m.reconnectable()) lanes = true;
                 s->pool_planes = lanes ? kResChunks : 20;
-                const size_t row_bytes = size_t(s->pool_planes - 1) * 16;
+                // ... and without replay lanes every record reconnects at k = 2, so its
+                // prefix cache (chunks 5-9) is rebuilt from the G-buffer: 224 B rows
+                // (TOFR_COMPACT_ROWS=0: 304 B)
+                const char* cr = std::getenv("TOFR_COMPACT_ROWS");
+                s->compact_rows = !lanes && !(cr && cr[0] == '0');
+                const size_t row_bytes = size_t(s->pool_planes - 1 - (s->compact_rows ? 5 : 0)) * 16;
                 size_t rows = items;
                 size_t fr = 0, tot = 0;
                 if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
@@ -631,7 +651,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 if (const char* pr = std::getenv("TOFR_POOL_ROWS")) rows = size_t(std::strtoull(pr, nullptr, 10));
                 if (rows > 0xfffffff0ull) rows = 0xfffffff0ull;
                 s->pool_rows = rows;
-                rb = items * 16 + size_t(s->pool_planes - 1) * (rows + 2) * 16;
+                rb = items * 16 + row_bytes * (rows + 2);
                 for (int k = 0; k < 3; ++k)
                     if (k < 2 || s->has_bin || s->has_spatial) {
                         s->res_slot[k].ensure(items * sizeof(uint32_t));
@@ -951,7 +971,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         // gates fall back to plain RIS (pipeline.hpp:110, :130)
         InitParams ip{vel ? int(INIT_DIRECT) : c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
         reset_store(s, s->cur, fs);
-        ResStore cur = store_of(s, s->res[s->cur]);
+        ResStore cur = store_of(s, s->res[s->cur], sl);
         if (s->transient)
             launch_init_transient(F, bd, g, pc, ip, h, f, cur, q_side, fs);
         else
@@ -967,7 +987,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};
             const GHit* gp = rows_base<GHit>(s->slot[psl].gbuf, s->r0, s->W);
             if (s->wave) {
-                ResStore prev_st = store_of(s, s->res[s->prev]);
+                ResStore prev_st = store_of(s, s->res[s->prev], psl);
                 auto cuts = stage_cuts(s, bd, 2, stream, [&](unsigned long long* rows) {
                     launch_count_temporal(F, bd, g, s->slot[psl].view, cg, cur, prev_st, wv, rows, stream);
                 });
@@ -977,16 +997,16 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                 });
             }
             else
-                launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev]),
+                launch_temporal(F, bd, g, s->slot[psl].view, gp, pc, cg, pg, f, cur, store_of(s, s->res[s->prev], psl),
                                 wo, ctr + 0 * SC_COUNT, q, stream);
         }
         cudaEventRecord(ev[2], stream);
         if (piped) cudaEventRecord(s->ev_temporal[set], stream);
         if (s->transient && c.bin_reuse) {
             reset_store(s, s->spare, stream);
-            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare]), ctr + 2 * SC_COUNT, q, stream);
+            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare], sl), ctr + 2 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
-            cur = store_of(s, s->res[s->cur]);
+            cur = store_of(s, s->res[s->cur], sl);
         }
         cudaEventRecord(ev[3], stream);
         SpatialParams sp{c.spatial_neighbors, c.spatial_radius};
@@ -1012,14 +1032,14 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                     launch_count_spatial(F, bd, pc, cg, sp, pass, f, cur, rows, stream);
                 });
                 for_row_cuts(bd, cuts, [&](const Band& sb) {
-                    launch_spatial_wave(F, sb, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wv,
+                    launch_spatial_wave(F, sb, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare], sl), wv,
                                         ctr + 1 * SC_COUNT, q, stream);
                 });
             } else
-                launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare]), wo, scp,
+                launch_spatial(F, bd, g, pc, cg, sp, pass, f, cur, store_of(s, s->res[s->spare], sl), wo, scp,
                                ctr + 1 * SC_COUNT, q, stream);
             std::swap(s->cur, s->spare);
-            cur = store_of(s, s->res[s->cur]);
+            cur = store_of(s, s->res[s->cur], sl);
         }
         cudaEventRecord(ev[4], stream);
         if (s->transient)

@@ -57,6 +57,17 @@ struct ResStore {
     // and velocity chunks (20-23) when no record can have them (no
     // non-reconnectable material, length gates): 20
     int planes = kResChunks;
+    // Compact pool rows (sparse, no replay lanes): every record then has its
+    // reconnection vertex at k = 2, so its identity-prefix cache -- chunks 5-9
+    // (prefix pdf / length / throughput, p1, wi1) -- is a function of its own
+    // pixel's primary hit in the grid's frame (the G-buffer hit and camera:
+    // pdf 1, length t, throughput 1, p1 = cam + d0 t, wi1 = -d0, exactly the
+    // values the trace and the shift write).  Those planes are not stored
+    // (304 -> 224 B per row, SURVEY 8d's record size); readers rebuild them.
+    int compact = 0;
+    const GHit* gbuf = nullptr;  // the grid's frame: G-buffer (global pixel index) and camera
+    GCam cam{};
+    int bins = 1;
 };
 
 #if defined(__CUDACC__)
@@ -83,12 +94,37 @@ __device__ __forceinline__ size_t res_row_w(const ResStore& s, size_t i) {
 }
 __device__ __forceinline__ double2* res_planes(const ResStore& s) { return s.slot ? s.pool : s.base; }
 
-// chunk c >= 1 at a known row
+// chunk c >= 1 at a known row (compact rows: chunks 5-9 are not stored -- they
+// read as zero, writes are dropped -- and chunks >= 10 sit 5 planes lower)
+__device__ __forceinline__ bool res_derived_chunk(const ResStore& s, int c) { return s.compact && c >= 5 && c <= 9; }
+__device__ __forceinline__ int res_plane(const ResStore& s, int c) { return (s.compact && c >= 10) ? c - 5 : c; }
 __device__ __forceinline__ double2 ld2r(const ResStore& s, int c, size_t row) {
-    return __ldcg(&res_planes(s)[size_t(c) * s.stride + row]);
+    if (res_derived_chunk(s, c)) return make_double2(0.0, 0.0);
+    return __ldcg(&res_planes(s)[size_t(res_plane(s, c)) * s.stride + row]);
 }
 __device__ __forceinline__ void st2r(const ResStore& s, int c, size_t row, double2 v) {
-    __stcg(&res_planes(s)[size_t(c) * s.stride + row], v);
+    if (res_derived_chunk(s, c)) return;
+    __stcg(&res_planes(s)[size_t(res_plane(s, c)) * s.stride + row], v);
+}
+
+// identity-prefix cache of the record of item i, rebuilt for a compact row
+// (see ResStore::compact): prefix pdf, length, throughput, p1, wi1
+struct PrefixCache {
+    double pdf, len;
+    V3 fw, p1, wi1;
+};
+__device__ __forceinline__ PrefixCache res_prefix_derived(const ResStore& s, size_t i) {
+    const size_t p = i / size_t(s.bins);
+    const int px = int(p % size_t(s.cam.w)), py = int(p / size_t(s.cam.w));
+    const GHit g = s.gbuf[p];
+    const V3 d0 = primary_dir(s.cam, px, py);
+    PrefixCache c;
+    c.pdf = 1;
+    c.len = g.t;
+    c.fw = splat(1);
+    c.p1 = s.cam.pos + d0 * g.t;
+    c.wi1 = -d0;
+    return c;
 }
 
 __device__ __forceinline__ double2 ld2(const ResStore& s, int c, size_t i) {
@@ -221,6 +257,14 @@ __device__ inline void res_load_rec(const ResStore& s, size_t i, Sample& y, bool
         memcpy(&mi, &c.y, 8);
         q.m2 = mi.x;
         q.obj2 = mi.y;
+    }
+    if (s.compact) {
+        const PrefixCache pc = res_prefix_derived(s, i);
+        q.prefix_pdf = pc.pdf;
+        q.prefix_len = pc.len;
+        q.prefix_fw = pc.fw;
+        q.p1 = pc.p1;
+        q.wi1 = pc.wi1;
     }
     if (vel) {
         c = ld2r(s, 22, row);

@@ -319,15 +319,24 @@ __device__ __forceinline__ V3 rec_suffix_f(const ResStore& s, size_t i, int& m2)
 __device__ __forceinline__ Prefix stored_prefix_at(const FrameView& F, const ResStore& s, size_t i, int tri1,
                                                    bool vel) {
     Prefix pre;
-    double2 c5 = ld2(s, 5, i), c6 = ld2(s, 6, i), c7 = ld2(s, 7, i), c8 = ld2(s, 8, i), c9 = ld2(s, 9, i),
-            c10 = ld2(s, 10, i);
     pre.ok = 1;
-    pre.pdf = c5.x;
-    pre.len = c5.y;
-    pre.fw = V3{c6.x, c6.y, c7.x};
-    pre.p1 = V3{c7.y, c8.x, c8.y};
+    if (s.compact) {
+        const PrefixCache pc = res_prefix_derived(s, i);
+        pre.pdf = pc.pdf;
+        pre.len = pc.len;
+        pre.fw = pc.fw;
+        pre.p1 = pc.p1;
+        pre.wi1 = pc.wi1;
+    } else {
+        double2 c5 = ld2(s, 5, i), c6 = ld2(s, 6, i), c7 = ld2(s, 7, i), c8 = ld2(s, 8, i), c9 = ld2(s, 9, i),
+                c10 = ld2(s, 10, i);
+        pre.pdf = c5.x;
+        pre.len = c5.y;
+        pre.fw = V3{c6.x, c6.y, c7.x};
+        pre.p1 = V3{c7.y, c8.x, c8.y};
+        pre.wi1 = V3{c9.x, c9.y, c10.x};
+    }
     pre.n1 = F.tri[tri1].n;
-    pre.wi1 = V3{c9.x, c9.y, c10.x};
     pre.tri1 = tri1;
     pre.m1 = F.tri[tri1].mat;
     pre.u = vel ? ld2(s, 22, i).y : 0.0;
@@ -1192,7 +1201,7 @@ __global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
             out_fail(q, k);
             continue;
         }
-        double rec_prefix_pdf = ld2(st, 5, jb.item).x;
+        double rec_prefix_pdf = st.compact ? res_prefix_derived(st, jb.item).pdf : ld2(st, 5, jb.item).x;
         double jac = (rec_prefix_pdf / pre.pdf) * j_newton;
         if (!isfinite(jac) || jac < cfg.jac_min || jac > cfg.jac_max) {
             if (count) ctr.v[SC_JAC_CLAMPED]++;

@@ -151,3 +151,19 @@ def test_queue_smaller_than_a_row_raises():
     scene, cfg = CASES["temporal_spatial"]
     with pytest.raises(TofrError, match="smaller than one image row"):
         _render(scene, cfg, TOFR_WAVE_CAP="10")
+
+
+@pytest.mark.parametrize("name", ["temporal_spatial", "bin_reuse", "animated"])
+def test_compact_rows_equal_full_rows(name):
+    """Compact pool rows (224 B: the k = 2 prefix cache rebuilt from the
+    G-buffer, ResStore::compact) against full 304 B rows (TOFR_COMPACT_ROWS=0):
+    bit-identical histograms and shift counters."""
+    scene, cfg = CASES[name]
+    a = _render(scene, cfg, TOFR_SPARSE="1")
+    b = _render(scene, cfg, TOFR_SPARSE="1", TOFR_COMPACT_ROWS="0")
+    assert b.hist.rgb.max() > 0
+    assert np.array_equal(a.hist.rgb, b.hist.rgb)
+    for x, y in zip(a.stats, b.stats):
+        for stage in ("temporal", "spatial", "bin"):
+            assert {k: v for k, v in x[stage].items() if k != "seconds"} == \
+                   {k: v for k, v in y[stage].items() if k != "seconds"}
