@@ -458,6 +458,10 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width, const
     p.m_cap = c.m_cap;
     p.seed = c.seed;
     p.replay = 0;
+    {
+        const char* wc = std::getenv("TOFR_WALK_CUTOFF");
+        p.walk_cutoff = (wc && wc[0] == '0') ? 0 : 1;
+    }
     p.work = nullptr;
     for (const HMaterial& m : sc.materials)
         if (!m.reconnectable()) p.replay = 1;

@@ -100,6 +100,7 @@ struct RisSink {
     double phat;
     Sample* win;
     __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ double walk_max() const { return center + width; }
     __device__ void emit(const Cand& c, double mis, const RecSrc& rs) {
         double p = luminance(c.f) * gate_w(center, width, c.len);
         if (p <= 0 || !(c.pdf > 0)) return;
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_init_gated(FrameView F
 
 // a sink that wants no candidate: emit_nee culls every NEE before its ray
 struct NullSink {
+    double reach;  // the replay's walk cutoff (the same walk, the same sampler calls)
     __device__ bool wants(double) const { return false; }
+    __device__ double walk_max() const { return reach; }
     __device__ void emit(const Cand&, double, const RecSrc&) {}
 };
 
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(128, TOFR_REUSE_MINB) k_ell_plan(FrameView F, 
         int px = p % W, py = p / W;
         uint64_t pix = uint64_t(py) * W + px;
         GHit g = gbuf[p];
-        NullSink sink;
+        NullSink sink{cfg.ell_center + cfg.ell_width};
         EllStepT<PlanSampler> ell{PlanSampler{es, i * size_t(es.per_pixel), 0}};
         for (int s = 0; s < m_init; ++s) {
             Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), pix, uint64_t(s), 0);
@@ -340,6 +343,7 @@ struct BinSink {
         int b = bin_of(h, len);
         return b >= 0 && gate_w(bin_center(h, b), h.bw, len) > 0;
     }
+    __device__ double walk_max() const { return h.t0 + (h.bins + 1) * h.bw; }
     __device__ void emit(const Cand& c, double mis, const RecSrc& rs) {
         int b = bin_of(h, c.len);
         if (b < 0 || !(c.pdf > 0)) return;
@@ -944,6 +948,7 @@ struct PlainSink {
     size_t base, pix;
     uint32_t* n_dep;
     __device__ bool wants(double len) const { return bin_of(h, len) >= 0; }
+    __device__ double walk_max() const { return h.t0 + (h.bins + 1) * h.bw; }
     __device__ void emit(const Cand& c, double mis, const RecSrc&) {
         if (!(c.pdf > 0)) return;
         V3 val = c.f * (mis / c.pdf / m_init);
@@ -1021,6 +1026,7 @@ __device__ void trace_tree_deposit(const FrameView& F, const PathCfg& cfg, int p
             }
         }
         if (d + 2 > cfg.max_depth) break;
+        if (cfg.walk_cutoff && x.len > sink.walk_max()) break;  // no later candidate can be wanted
         double surv = rr_survival(d, cfg.use_rr);
         if (surv < 1.0 && rng_next(rng) >= surv) break;
         BsdfSample bs = sample_bsdf(m, x.n, x.wi, rng);
@@ -1087,6 +1093,7 @@ struct RefSink {
     double center, width;
     V3 est;
     __device__ bool wants(double len) const { return gate_w(center, width, len) > 0; }
+    __device__ double walk_max() const { return center + width; }
     __device__ void emit(const Cand& c, double mis, const RecSrc&) {
         double w = gate_w(center, width, c.len);
         if (w > 0 && c.pdf > 0) est = est + c.f * (mis * w / c.pdf);

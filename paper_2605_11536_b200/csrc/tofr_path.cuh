@@ -103,6 +103,9 @@ struct PathCfg {
     uint64_t seed;
     int gate_vel;  // velocity (Doppler) gate: the gated quantity is u, gate centre/width in u units
     int replay;  // the scene has non-reconnectable materials: records with k > 2 exist
+    // end a path tree once its length passes the sink's reach (no later
+    // candidate can be wanted; same candidates, fewer rays; TOFR_WALK_CUTOFF=0: off)
+    int walk_cutoff;
     unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
     // per-image-row shift cost (Newton iterations + 4 per job whose
     // destination lies in the row; null = off): the load-balancing probe of
@@ -376,6 +379,9 @@ __device__ void trace_tree(const FrameView& F, const PathCfg& cfg, int px, int p
             if (cfg.ellipsoidal) ell.step(F, cfg, v, d, ell_rng, rng.key, sink);
         }
         if (d + 2 > cfg.max_depth) break;
+        // walk cutoff: lengths only grow along the walk, so past the sink's reach
+        // no later candidate (NEE, ellipsoidal or extension) can be wanted
+        if (cfg.walk_cutoff && v[d].len > sink.walk_max()) break;
         v[d].lane = uint32_t(rng.ctr);
         double surv = rr_survival(d, cfg.use_rr);
         if (surv < 1.0 && rng_next(rng) >= surv) break;

@@ -41,6 +41,7 @@
 #define TOFR_TRACE_MINB 4
 #endif
 
+
 namespace tofr_b200 {
 
 // ---------------------------------------------------------------------------
@@ -73,6 +74,10 @@ struct GatedSink {
     __device__ void tree_begin() {}
     __device__ void tree_end() {}
     __device__ bool wants(double len, double u) const { return gate_w(center, width, VEL ? u : len) > 0; }
+    // lengths only grow along a walk: beyond this no candidate of the tree can
+    // be in the gate (a full width of margin over center + width / 2); velocity
+    // gates are not monotone
+    __device__ double walk_max() const { return VEL ? kInf : center + width; }
     __device__ void emit(const FrameView& F, const Cand& c, double mis, const RecSrc& rs) {
         double p = luminance(c.f) * gate_w(center, width, VEL ? c.u : c.len);
         if (p <= 0 || !(c.pdf > 0)) return;
@@ -121,6 +126,7 @@ struct BinsSink {
         int b = bin_of(h, len);
         return b >= 0 && gate_w(bin_center(h, b), h.bw, len) > 0;
     }
+    __device__ double walk_max() const { return h.t0 + (h.bins + 1) * h.bw; }
     __device__ void emit(const FrameView& F, const Cand& c, double mis, const RecSrc& rs) {
         int b = bin_of(h, c.len);
         if (b < 0 || !(c.pdf > 0)) return;
@@ -175,6 +181,7 @@ struct PlainSink2 {
         hist_deposit(hist, img, base + b, pix, val);
         ++deposits;
     }
+    __device__ double walk_max() const { return h.t0 + (h.bins + 1) * h.bw; }
     __device__ void end() {}
     __device__ void flush(unsigned long long* work) { work_add(work, WK_DEPOSITS, deposits); }
 };
@@ -203,6 +210,7 @@ struct RefSink2 {
         double w = gate_w(center, width, c.len);
         if (w > 0 && c.pdf > 0) est = est + c.f * (mis * w / c.pdf);
     }
+    __device__ double walk_max() const { return center + width; }
     __device__ void end() {
         V3 m = sum / double(spp);
         V3 var = sum2 / double(spp) - m * m;
@@ -384,6 +392,15 @@ __global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
                     }
                     d = 1;
                     state = ST_NEE;
+                    continue;
+                }
+                // walk cutoff: path lengths only grow (every segment adds a
+                // non-negative length), so once x.len passes the sink's reach no
+                // NEE or later candidate of this tree can be wanted -- the tree
+                // ends here with the same candidates (the next tree has its own
+                // RNG stream)
+                if (cfg.walk_cutoff && x.len > sk.walk_max()) {
+                    d = cfg.max_depth + 2;
                     continue;
                 }
                 const GMat& mx = Fs.mats[x.mat];

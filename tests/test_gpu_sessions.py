@@ -150,3 +150,36 @@ def test_static_scene_snapshot_cache_is_bit_identical(name, monkeypatch):
     ref = Renderer(0).render_gated(sd, cfg)
     assert ref.image.max() > 0
     assert np.array_equal(got.image, ref.image)
+
+
+@pytest.mark.parametrize("kind", ["gated", "transient", "plain", "ellipsoidal", "reference"])
+def test_walk_cutoff_is_bit_identical(kind, monkeypatch):
+    """Path trees end once their length passes the sink's reach (lengths only
+    grow along a walk, so no later candidate could be wanted; the next tree has
+    its own RNG stream): every output equals the full walks' (TOFR_WALK_CUTOFF=0)."""
+    r = Renderer(0)
+    sd = scenes.bundled("boxes_doppler" if kind in ("gated", "plain") else "cornell_wide", 40)
+    if kind == "gated":
+        cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.2, 1.0), m_init=2, temporal=True, spatial_passes=1,
+                           spatial_neighbors=3, spatial_radius=5, frames=3)
+        run = lambda: (r.render_gated(sd, cfg).image,)  # noqa: E731
+    elif kind == "transient":
+        cfg = _transient_cfg(hist_t0=3.0, hist_bin_width=0.25, temporal=True, spatial_passes=1,
+                             spatial_neighbors=2, spatial_radius=3, frames=3)
+        run = lambda: (r.render_transient(sd, cfg).hist.rgb,)  # noqa: E731
+    elif kind == "plain":
+        cfg = _transient_cfg(bins=100, hist_t0=7.0, hist_bin_width=0.05, m_init=4, max_depth=8, frames=2)
+        run = lambda: (lambda o: (o.hist.rgb, o.hist.count))(r.render_transient_plain(sd, cfg))  # noqa: E731
+    elif kind == "ellipsoidal":
+        cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 6.0, 0.1, 1.0), m_init=2, init=F.INIT_ELLIPSOIDAL,
+                           temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=4, frames=2)
+        run = lambda: (r.render_gated(sd, cfg).image,)  # noqa: E731
+    else:
+        gate = GateSpec(F.GATE_LENGTH, 6.0, 0.3, 1.0)
+        run = lambda: r.reference_render(sd, 0.0, gate, 16, 3, 6)  # noqa: E731
+    got = run()
+    monkeypatch.setenv("TOFR_WALK_CUTOFF", "0")
+    full = run()
+    assert full[0].max() > 0
+    for a, b in zip(got, full):
+        assert np.array_equal(a, b)
