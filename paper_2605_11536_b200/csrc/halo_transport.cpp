@@ -78,15 +78,19 @@ struct NcclHaloTransport : HaloTransport {
     void exchange(const HaloBufs& b, int) override {
         const NcclApi& n = nccl();
         nccl_ok(n.GroupStart(), "group start");
+        // the group is always closed, also when an enqueue fails
+        ncclResult_t r = ncclSuccess;
         if (rank > 0 && b.bytes_lo) {
-            nccl_ok(n.Send(b.send_lo, b.bytes_lo, ncclUint8, rank - 1, comm, b.stream), "send");
-            nccl_ok(n.Recv(b.recv_lo, b.bytes_lo, ncclUint8, rank - 1, comm, b.stream), "recv");
+            if (r == ncclSuccess) r = n.Send(b.send_lo, b.bytes_lo, ncclUint8, rank - 1, comm, b.stream);
+            if (r == ncclSuccess) r = n.Recv(b.recv_lo, b.bytes_lo, ncclUint8, rank - 1, comm, b.stream);
         }
         if (rank < world - 1 && b.bytes_hi) {
-            nccl_ok(n.Send(b.send_hi, b.bytes_hi, ncclUint8, rank + 1, comm, b.stream), "send");
-            nccl_ok(n.Recv(b.recv_hi, b.bytes_hi, ncclUint8, rank + 1, comm, b.stream), "recv");
+            if (r == ncclSuccess) r = n.Send(b.send_hi, b.bytes_hi, ncclUint8, rank + 1, comm, b.stream);
+            if (r == ncclSuccess) r = n.Recv(b.recv_hi, b.bytes_hi, ncclUint8, rank + 1, comm, b.stream);
         }
-        nccl_ok(n.GroupEnd(), "group end");
+        ncclResult_t e = n.GroupEnd();
+        nccl_ok(r, "send/recv");
+        nccl_ok(e, "group end");
     }
     const char* name() const override { return "nccl"; }
 };
