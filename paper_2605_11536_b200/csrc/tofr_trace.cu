@@ -157,104 +157,6 @@ struct BinsSink {
     __device__ void flush(unsigned long long*) {}
 };
 
-// RIS into per-(pixel, bin) reservoirs with the running sums in registers: a
-// pixel's bins belong to its lane alone and start empty every frame, so each
-// touched bin's w_sum and the winner's p-hat live in a small per-lane table
-// instead of a read-modify-write of chunk 0 per candidate (a dependent HBM
-// round trip on the lane's critical path).  At the pixel's end every touched
-// bin gets its final header (W = w_sum / p-hat, M = 1: ris_finalize, the same
-// division); untouched bins keep the (0, 1) the band was filled with.  A pixel
-// that touches more than kBinCache bins keeps the extra ones in HBM (w_sum in
-// chunk 0, finished at its end the same way).
-constexpr int kBinCache = 8;
-struct BinsSinkC {
-    ResStore st;
-    HistSpec h;
-    double inv;
-    Rng pick;
-    size_t base;
-    int nb;
-    int bin[kBinCache];
-    double wsum[kBinCache], ph[kBinCache];
-    int spill;  // bins kept in HBM (beyond the table)
-    __device__ void begin(const PathCfg& cfg, uint64_t fk, uint64_t pix, size_t p, int) {
-        pick = rng_make(cfg.seed, fk, pix, 0, 9);
-        base = p * size_t(h.bins);
-        nb = 0;
-        spill = 0;
-    }
-    __device__ void tree_begin() {}
-    __device__ void tree_end() {}
-    __device__ bool wants(double len, double) const {
-        int b = bin_of(h, len);
-        return b >= 0 && gate_w(bin_center(h, b), h.bw, len) > 0;
-    }
-    __device__ double walk_max() const { return h.t0 + (h.bins + 1) * h.bw; }
-    __device__ void emit(const FrameView& F, const Cand& c, double mis, const RecSrc& rs) {
-        int b = bin_of(h, c.len);
-        if (b < 0 || !(c.pdf > 0)) return;
-        double p = luminance(c.f) * gate_w(bin_center(h, b), h.bw, c.len);
-        if (p <= 0) return;
-        double w = mis * inv * p / c.pdf;
-        if (!isfinite(w) || w < 0) return;
-        if (w <= 0) return;
-        int e = -1;
-#pragma unroll
-        for (int k = 0; k < kBinCache; ++k)
-            if (k < nb && bin[k] == b) e = k;
-        double w_sum;
-        const size_t i = base + b;
-        if (e < 0 && nb < kBinCache) {
-            e = nb++;
-            bin[e] = b;
-            wsum[e] = 0;
-            ph[e] = 0;
-        }
-        if (e >= 0) {
-            w_sum = wsum[e] + w;
-            wsum[e] = w_sum;
-        } else {  // table full: this bin's running sum in HBM (chunk 0, zero-filled with M = 1)
-            double2 c0 = ld2(st, 0, i);
-            w_sum = c0.x + w;
-            st2(st, 0, i, w_sum, c0.y);
-            spill = 1;
-        }
-        if (rng_next(pick) * w_sum < w) {
-            Res r;
-            r.W = w_sum;
-            r.M = 1;
-            r.has = 1;
-            r.phat = p;
-            r.y.f = c.f;
-            r.y.len = c.len;
-            r.y.u = c.u;
-            r.y.depth = c.depth;
-            build_record<false>(F, rs, r.y.rec);
-            res_store(st, i, r);
-            if (e >= 0) ph[e] = p;
-        }
-    }
-    __device__ void end() {
-        for (int k = 0; k < nb; ++k) {
-            double Wv = (wsum[k] > 0 && ph[k] > 0) ? wsum[k] / ph[k] : 0;
-            st2(st, 0, base + bin[k], Wv, 1.0);
-        }
-        if (spill)  // bins beyond the table: ris_finalize from HBM
-            for (int b = 0; b < h.bins; ++b) {
-                bool cached = false;
-                for (int k = 0; k < nb; ++k) cached |= bin[k] == b;
-                if (cached) continue;
-                const size_t i = base + b;
-                double2 c0 = ld2(st, 0, i);
-                if (c0.x > 0) {
-                    double phat = ld2(st, 1, i).x;
-                    st2(st, 0, i, phat > 0 ? c0.x / phat : 0, 1.0);
-                }
-            }
-    }
-    __device__ void flush(unsigned long long*) {}
-};
-
 // TransientHistogram::deposit of every candidate (f * mis / pdf / m_init,
 // pipeline.hpp:547-556, transport.hpp:121-126) -- see hist_deposit
 struct PlainSink2 {
@@ -623,36 +525,11 @@ void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const
         run(GatedSink<false>{}, std::false_type{});
 }
 
-// chunk 0 of every (pixel, bin) of the band -> (0, 1): an empty reservoir with
-// M = 1, what ris_finalize leaves for a bin without candidates
-__global__ void k_fill_empty(ResStore st, size_t i0, size_t i1) {
-    for (size_t i = i0 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < i1; i += size_t(gridDim.x) * blockDim.x)
-        st2(st, 0, i, 0.0, 1.0);
-}
-
-#ifndef TOFR_BIN_CACHE
-#define TOFR_BIN_CACHE 1
-#endif
-
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,
                             const HistSpec& h, int frame_idx, ResStore cur, unsigned long long* q, cudaStream_t s) {
     size_t n = size_t(bd.y1 - bd.y0) * F.cam.w * h.bins;
     if (!n) return;
     size_t i0 = size_t(bd.y0) * F.cam.w * h.bins;
-    if (TOFR_BIN_CACHE) {
-        size_t blocks = (n + 255) / 256;
-        if (blocks > 148 * 32) blocks = 148 * 32;
-        {
-            KScope ks("k_fill_empty", s);
-            k_fill_empty<<<int(blocks), 256, 0, s>>>(cur, i0, i0 + n);
-        }
-        BinsSinkC sk;
-        sk.st = cur;
-        sk.h = h;
-        sk.inv = 1.0 / m_init;
-        launch_trace("k_trace_bins", F, bd, g, cfg, m_init, uint64_t(frame_idx), sk, q, s);
-        return;
-    }
     cudaMemsetAsync(cur.base + i0, 0, n * sizeof(double2), s);  // chunk 0 plane of the band
     BinsSink sk;
     sk.st = cur;
