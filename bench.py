@@ -128,6 +128,11 @@ WORKLOADS = {
                           spatial_radius=10, m_cap=20, max_depth=6, seed=1),
              "mesh: cornell_wide box + 102,410-triangle torus (BVH in global memory) 1920x1080 gated tau=6.0 "
              "dtau=0.0173, m_init 1, temporal + 1x3 spatial r10"),
+    "mesh_anim": ("mesh_anim", 1920, 1080,
+                  RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1,
+                               spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
+                  "mesh (animated): the 102,410-triangle torus turning and drifting -- a new BVH every frame, "
+                  "built on the device -- 1920x1080 gated tau=6.0 dtau=0.0173, temporal + 1x3 spatial r10"),
 }
 
 PLAIN = {"c2p", "c4p"}

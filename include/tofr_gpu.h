@@ -287,6 +287,13 @@ uint64_t tofr_fnv1a64(const void* data, uint64_t n);
  * whose bits differ (0 expected) */
 int tofr_gpu_selftest_div(tofr_gpu* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
 
+/* tofr_scene_dump_bvh of the tree built on the device (bvh_build.cu) for the
+ * frame's world-space triangles: the same layout, for node-for-node parity
+ * checks against the host builder (wide-light scenes) */
+int tofr_gpu_dump_bvh_device(tofr_gpu* ctx, const tofr_scene* s, double frame, int32_t cap_nodes, double* nodes,
+                             int32_t* node_parent, int32_t* n_nodes, int32_t cap_tris, int32_t* tri_order,
+                             int32_t* n_tris, double* diag);
+
 /* diagnostic (a -DTOFR_SOLVE_PROFILE=1 build only, else TOFR_ERR_UNSUPPORTED):
  * per solved shift job {cycles from refill to finish, trial rounds | Newton
  * iterations << 32 | re-projection rays << 40, SM clock at finish}; copies up

@@ -289,6 +289,21 @@ class Renderer:
                                                  max_depth, _dptr(mean), _dptr(se)))
         return mean, se
 
+    def dump_bvh_device(self, scene, frame: float = 0.0):
+        """Scene.dump_bvh of the tree built on the device (bvh_build.cu)."""
+        s = self._scene(scene)
+        cap = max(16384, 2 * s.info()["n_tris"] + 2)
+        nodes = np.zeros((cap, 11))
+        parent = np.zeros(cap, dtype=np.int32)
+        order = np.zeros(cap, dtype=np.int32)
+        nn, nt = C.c_int32(), C.c_int32()
+        diag = C.c_double()
+        self._check(self._lib.tofr_gpu_dump_bvh_device(self.handle, s.handle, frame, cap, _dptr(nodes),
+                                                       parent.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nn),
+                                                       cap, order.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                       C.byref(nt), C.byref(diag)))
+        return nodes[:nn.value].copy(), parent[:nn.value].copy(), order[:nt.value].copy(), diag.value
+
     def nccl_unique_id(self) -> bytes | None:
         """A fresh 128-byte ncclUniqueId (None when libnccl.so.2 cannot be loaded)."""
         buf = C.create_string_buffer(128)

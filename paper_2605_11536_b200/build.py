@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu", "tofr_trace.cu"]
+DEVICE_SOURCES = ["tofr_kernels.cu", "tofr_wave.cu", "tofr_trace.cu", "bvh_build.cu"]
 HOST_SOURCES = ["host_scene.cpp", "capi.cpp", "ktime.cpp", "halo_transport.cpp"]
 HEADERS = [
     "tofr_core.h",
@@ -39,6 +39,7 @@ HEADERS = [
     "tofr_kernels.h",
     "host_scene.h",
     "halo_transport.h",
+    "bvh_build.h",
 ]
 
 

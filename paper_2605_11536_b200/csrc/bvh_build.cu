@@ -1,0 +1,496 @@
+// bvh_build.cu -- the binned SAH BVH of a frame built on the device,
+// node-for-node the host builder's (SahBuilder, host_scene.cpp), which is the
+// reference's Bvh::build_node (geometry.hpp:234-317): 8 bins on the widest
+// centroid axis, <= 4 triangles per leaf, stable partition, the same
+// fall-backs, node boxes, tri_area sums and depth-first (pre-order) numbering.
+//
+// Level-synchronous: one CTA per node of the current level computes its box,
+// centroid box and binned split (min / max reductions: exact in any order),
+// its tri_area (a sequential sum by one thread: the reference's order), and
+// stably partitions its range of the triangle order (block-wide scans); the
+// children form the next level.  After the last level the nodes are
+// renumbered in the reference's depth-first order (subtree sizes bottom-up,
+// pre-order indices top-down) and packed into the frame snapshot layout
+// (pack_frame: threaded hit / miss links, leaf-order triangles, per-triangle
+// info and tangent frames) in place, in the slot's device blob.
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bvh_build.h"
+#include "ktime.h"
+
+namespace tofr_b200 {
+
+namespace {
+
+struct BNode {  // a node in build (creation) order
+    V3 lo, hi;
+    double tri_area;
+    int left, right, first, count, parent, pad;
+};
+
+struct BTri {  // == HTri (host_scene.h): v0, v1, v2, n, material, object, area
+    V3 v0, v1, v2, n;
+    int material, object;
+    double area;
+};
+
+constexpr int kBinsDev = 8;
+constexpr int kBuildThreads = 256;
+
+__device__ __forceinline__ double centroid_axis(const BTri& t, int a) {
+    return (comp(t.v0, a) + comp(t.v1, a) + comp(t.v2, a)) / 3.0;
+}
+__device__ __forceinline__ double box_area(const V3& lo, const V3& hi) {  // Box::area
+    V3 e = hi - lo;
+    if (e.x < 0) return 0;
+    return 2.0 * (e.x * e.y + e.y * e.z + e.z * e.x);
+}
+
+// block-wide min / max of one double (every thread gets the result)
+__device__ double block_min(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = sh[0];
+    for (int i = 1; i < int(blockDim.x >> 5); ++i) r = dmin(r, sh[i]);
+    return r;
+}
+__device__ double block_max(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = sh[0];
+    for (int i = 1; i < int(blockDim.x >> 5); ++i) r = dmax(r, sh[i]);
+    return r;
+}
+__device__ int block_sum(int v, int* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    int r = 0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) r += sh[i];
+    return r;
+}
+// exclusive block scan of a 0/1 flag; returns the prefix, *total the block sum
+__device__ int block_scan(int f, int* sh, int* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    const int in_warp = __popc(m & ((1u << l) - 1));
+    __syncthreads();
+    if (l == 0) sh[w] = __popc(m);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+        if (i < w) before += sh[i];
+        all += sh[i];
+    }
+    *total = all;
+    return before + in_warp;
+}
+
+// one level: CTA b builds node tasks[b]
+__global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, int* order, int* tmp, BNode* nodes,
+                                                             const int* tasks, int n_tasks, int* next, int* n_next,
+                                                             int* n_nodes) {
+    if (int(blockIdx.x) >= n_tasks) return;
+    __shared__ double shd[kBuildThreads / 32];
+    __shared__ int shi[kBuildThreads / 32];
+    __shared__ int s_split, s_axis;
+    __shared__ double s_lo, s_width;
+    const int id = tasks[blockIdx.x];
+    const int first = nodes[id].first, count = nodes[id].count;
+    // box and centroid box
+    V3 lo{kInf, kInf, kInf}, hi{-kInf, -kInf, -kInf}, clo = lo, chi = hi;
+    for (int i = first + threadIdx.x; i < first + count; i += blockDim.x) {
+        const BTri& t = tris[order[i]];
+        lo = vmin(vmin(vmin(lo, t.v0), t.v1), t.v2);
+        hi = vmax(vmax(vmax(hi, t.v0), t.v1), t.v2);
+        V3 c = (t.v0 + t.v1 + t.v2) / 3.0;
+        clo = vmin(clo, c);
+        chi = vmax(chi, c);
+    }
+    lo = V3{block_min(lo.x, shd), block_min(lo.y, shd), block_min(lo.z, shd)};
+    hi = V3{block_max(hi.x, shd), block_max(hi.y, shd), block_max(hi.z, shd)};
+    clo = V3{block_min(clo.x, shd), block_min(clo.y, shd), block_min(clo.z, shd)};
+    chi = V3{block_max(chi.x, shd), block_max(chi.y, shd), block_max(chi.z, shd)};
+    if (threadIdx.x == 0) {
+        double area = 0;  // the reference's order: area += t.area over the range
+        for (int i = first; i < first + count; ++i) area += tris[order[i]].area;
+        BNode& nd = nodes[id];
+        nd.lo = lo;
+        nd.hi = hi;
+        nd.tri_area = area;
+        nd.left = nd.right = -1;
+    }
+    if (count <= 4) return;  // leaf
+    if (threadIdx.x == 0) {
+        V3 ext = chi - clo;
+        int axis = ext.x > ext.y ? (ext.x > ext.z ? 0 : 2) : (ext.y > ext.z ? 1 : 2);
+        s_axis = axis;
+        s_lo = comp(clo, axis);
+        s_width = comp(ext, axis);
+    }
+    __syncthreads();
+    const int axis = s_axis;
+    const double blo = s_lo, width = s_width;
+    int mid = first + count / 2;
+    if (!(width < 1e-12)) {
+        auto bin_of = [&](const BTri& t) {
+            double c = (centroid_axis(t, axis) - blo) / width;
+            int b = int(c * kBinsDev);
+            return b < kBinsDev - 1 ? b : kBinsDev - 1;
+        };
+        int bc[kBinsDev];
+        V3 bl[kBinsDev], bh[kBinsDev];
+#pragma unroll
+        for (int k = 0; k < kBinsDev; ++k) {
+            bc[k] = 0;
+            bl[k] = V3{kInf, kInf, kInf};
+            bh[k] = V3{-kInf, -kInf, -kInf};
+        }
+        for (int i = first + threadIdx.x; i < first + count; i += blockDim.x) {
+            const BTri& t = tris[order[i]];
+            int b = bin_of(t);
+#pragma unroll
+            for (int k = 0; k < kBinsDev; ++k)
+                if (k == b) {
+                    bc[k]++;
+                    bl[k] = vmin(vmin(vmin(bl[k], t.v0), t.v1), t.v2);
+                    bh[k] = vmax(vmax(vmax(bh[k], t.v0), t.v1), t.v2);
+                }
+        }
+        __shared__ int s_bc[kBinsDev];
+        __shared__ double s_bl[kBinsDev][3], s_bh[kBinsDev][3];
+#pragma unroll 1
+        for (int k = 0; k < kBinsDev; ++k) {
+            int c = block_sum(bc[k], shi);
+            double l0 = block_min(bl[k].x, shd), l1 = block_min(bl[k].y, shd), l2 = block_min(bl[k].z, shd);
+            double h0 = block_max(bh[k].x, shd), h1 = block_max(bh[k].y, shd), h2 = block_max(bh[k].z, shd);
+            if (threadIdx.x == 0) {
+                s_bc[k] = c;
+                s_bl[k][0] = l0;
+                s_bl[k][1] = l1;
+                s_bl[k][2] = l2;
+                s_bh[k][0] = h0;
+                s_bh[k][1] = h1;
+                s_bh[k][2] = h2;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {  // SAH over the 7 bin boundaries (SahBuilder)
+            double best_cost = kInf;
+            int best = -1;
+            for (int sp = 1; sp < kBinsDev; ++sp) {
+                V3 llo{kInf, kInf, kInf}, lhi{-kInf, -kInf, -kInf}, rlo = llo, rhi = lhi;
+                int lc = 0, rc = 0;
+                for (int i = 0; i < sp; ++i) {
+                    if (s_bc[i]) {
+                        llo = vmin(llo, V3{s_bl[i][0], s_bl[i][1], s_bl[i][2]});
+                        lhi = vmax(lhi, V3{s_bh[i][0], s_bh[i][1], s_bh[i][2]});
+                    }
+                    lc += s_bc[i];
+                }
+                for (int i = sp; i < kBinsDev; ++i) {
+                    if (s_bc[i]) {
+                        rlo = vmin(rlo, V3{s_bl[i][0], s_bl[i][1], s_bl[i][2]});
+                        rhi = vmax(rhi, V3{s_bh[i][0], s_bh[i][1], s_bh[i][2]});
+                    }
+                    rc += s_bc[i];
+                }
+                if (lc == 0 || rc == 0) continue;
+                double cost = box_area(llo, lhi) * lc + box_area(rlo, rhi) * rc;
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = sp;
+                }
+            }
+            s_split = best;
+        }
+        __syncthreads();
+        const int split = s_split;
+        if (split >= 0) {
+            // stable partition of [first, first + count) by bin < split
+            int n_left = 0;
+            for (int base = first; base < first + count; base += blockDim.x) {
+                int i = base + threadIdx.x;
+                int f = (i < first + count) ? int(bin_of(tris[order[i]]) < split) : 0;
+                n_left += block_sum(f, shi);
+            }
+            int lpos = first, rpos = first + n_left;
+            for (int base = first; base < first + count; base += blockDim.x) {
+                int i = base + threadIdx.x;
+                bool live = i < first + count;
+                int id_i = live ? order[i] : 0;
+                int f = live ? int(bin_of(tris[id_i]) < split) : 0;
+                int tot_l = 0, tot_r = 0;
+                int pl = block_scan(f, shi, &tot_l);
+                int pr = block_scan(live && !f ? 1 : 0, shi, &tot_r);
+                if (live) tmp[f ? lpos + pl : rpos + pr] = id_i;
+                lpos += tot_l;
+                rpos += tot_r;
+            }
+            __syncthreads();
+            for (int i = first + threadIdx.x; i < first + count; i += blockDim.x) order[i] = tmp[i];
+            mid = first + n_left;
+            if (mid == first || mid == first + count) mid = first + count / 2;
+        }
+    }
+    if (threadIdx.x == 0) {
+        int c = atomicAdd(n_nodes, 2);
+        BNode l{}, r{};
+        l.first = first;
+        l.count = mid - first;
+        l.parent = id;
+        r.first = mid;
+        r.count = first + count - mid;
+        r.parent = id;
+        nodes[c] = l;
+        nodes[c + 1] = r;
+        nodes[id].left = c;
+        nodes[id].right = c + 1;
+        int t = atomicAdd(n_next, 2);
+        next[t] = c;
+        next[t + 1] = c + 1;
+    }
+}
+
+// subtree sizes, bottom-up over one level's nodes
+__global__ void k_bvh_sizes(const BNode* nodes, const int* level, int n, int* size) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int id = level[k];
+    const BNode& nd = nodes[id];
+    size[id] = nd.left < 0 ? 1 : 1 + size[nd.left] + size[nd.right];
+}
+// pre-order indices and escape links, top-down over one level's nodes
+// (pack_frame: esc[right] = left, esc[left] = esc[parent])
+__global__ void k_bvh_preorder(const BNode* nodes, const int* level, int n, const int* size, int* pre, int* esc) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int id = level[k];
+    const BNode& nd = nodes[id];
+    if (nd.left < 0) return;
+    pre[nd.left] = pre[id] + 1;
+    pre[nd.right] = pre[id] + 1 + size[nd.left];
+    esc[nd.right] = pre[nd.left];
+    esc[nd.left] = esc[id];
+}
+// node arrays of the snapshot (GNode, GNodeAux) at pre-order positions, and the
+// leaf of every triangle
+__global__ void k_bvh_pack_nodes(const BNode* nodes, int nn, const int* pre, const int* esc, const int* order,
+                                 GNode* gn, GNodeAux* ga, GTriInfo* info) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= nn) return;
+    const BNode& h = nodes[id];
+    const int p = pre[id];
+    const bool leaf = h.left < 0;
+    GNode g;
+    g.lo[0] = h.lo.x;
+    g.lo[1] = h.lo.y;
+    g.lo[2] = h.lo.z;
+    g.hi[0] = h.hi.x;
+    g.hi[1] = h.hi.y;
+    g.hi[2] = h.hi.z;
+    g.first = leaf ? h.first : 0;
+    g.count = leaf ? h.count : 0;
+    g.miss_next = esc[id];
+    g.hit_next = leaf ? esc[id] : pre[h.right];
+    gn[p] = g;
+    GNodeAux a;
+    a.tri_area = h.tri_area;
+    a.left = leaf ? -1 : pre[h.left];
+    a.right = leaf ? -1 : pre[h.right];
+    a.parent = h.parent < 0 ? -1 : pre[h.parent];
+    a.first = g.first;
+    a.count = g.count;
+    a.pad = 0;
+    ga[p] = a;
+    if (leaf)
+        for (int i = h.first; i < h.first + h.count; ++i) {
+            info[order[i]].leaf = p;
+            info[order[i]].leaf_slot = i;
+        }
+}
+// per-triangle arrays: leaf-order intersection records, ids, info, tangent frames
+__global__ void k_bvh_pack_tris(const BTri* tris, const int* order, int nt, GTriIsect* isect, int* tri_id,
+                                GTriInfo* info, Frame2* tframe) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nt) return;
+    const BTri& o = tris[order[j]];
+    isect[j].v0 = o.v0;
+    isect[j].e1 = o.v1 - o.v0;
+    isect[j].e2 = o.v2 - o.v0;
+    tri_id[j] = order[j];
+    const BTri& t = tris[j];  // info and frames by original triangle id
+    GTriInfo& in = info[j];
+    in.n = t.n;
+    in.mat = t.material;
+    in.obj = t.object;
+    in.area = t.area;
+    in.pad2 = 0;
+    tframe[j] = tangent_frame_of(t.n, t.v1 - t.v0, t.v2 - t.v0);
+}
+__global__ void k_iota(int* a, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = i;
+}
+
+void ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error(std::string("device bvh ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+
+}  // namespace
+
+DeviceBvh::~DeviceBvh() { release(); }
+void DeviceBvh::release() {
+    for (void** p : {&tris, &order, &tmp, &nodes, &bfs, &size, &pre, &esc, &ctr, &host_ctr}) {
+        if (*p) {
+            if (p == &host_ctr)
+                cudaFreeHost(*p);
+            else
+                cudaFree(*p);
+            *p = nullptr;
+        }
+    }
+    cap = 0;
+}
+void DeviceBvh::ensure(int nt) {
+    if (nt <= cap) return;
+    release();
+    const size_t n = size_t(nt), nn = 2 * n;
+    ok(cudaMalloc(&tris, n * sizeof(BTri)), "alloc");
+    ok(cudaMalloc(&order, n * sizeof(int)), "alloc");
+    ok(cudaMalloc(&tmp, n * sizeof(int)), "alloc");
+    ok(cudaMalloc(&nodes, nn * sizeof(BNode)), "alloc");
+    ok(cudaMalloc(&bfs, nn * sizeof(int)), "alloc");
+    ok(cudaMalloc(&size, nn * sizeof(int)), "alloc");
+    ok(cudaMalloc(&pre, nn * sizeof(int)), "alloc");
+    ok(cudaMalloc(&esc, nn * sizeof(int)), "alloc");
+    ok(cudaMalloc(&ctr, 16), "alloc");
+    ok(cudaMallocHost(&host_ctr, 16), "alloc");
+    cap = nt;
+}
+
+int DeviceBvh::build(const void* host_tris, int n_tris, cudaStream_t s) {
+    const int nt = n_tris;
+    static_assert(sizeof(BTri) == 112, "BTri mirrors HTri");
+    ensure(nt);
+    this->nt = nt;
+    ok(cudaMemcpyAsync(tris, host_tris, size_t(nt) * sizeof(BTri), cudaMemcpyHostToDevice, s), "upload");
+    {
+        KScope ks("k_iota", s);
+        k_iota<<<(nt + 255) / 256, 256, 0, s>>>(static_cast<int*>(order), nt);
+    }
+    BNode root{};
+    root.first = 0;
+    root.count = nt;
+    root.parent = -1;
+    ok(cudaMemcpyAsync(nodes, &root, sizeof(BNode), cudaMemcpyHostToDevice, s), "root");
+    int* bfs_i = static_cast<int*>(bfs);
+    int* ctr_i = static_cast<int*>(ctr);  // [0] nodes made, [1] next level's tasks
+    int* hc = static_cast<int*>(host_ctr);
+    int zero_one[2] = {1, 0};
+    ok(cudaMemcpyAsync(ctr_i, zero_one, 8, cudaMemcpyHostToDevice, s), "ctr");
+    ok(cudaMemcpyAsync(bfs_i, &zero_one[1], 4, cudaMemcpyHostToDevice, s), "bfs");  // level 0 = node 0
+    level_off.assign(1, 0);
+    level_n.assign(1, 1);
+    for (int L = 0; level_n.back() > 0; ++L) {
+        if (L > 62) throw std::runtime_error("bvh deeper than supported");
+        const int off = level_off.back(), n = level_n.back();
+        ok(cudaMemsetAsync(ctr_i + 1, 0, 4, s), "ctr");
+        {
+            KScope ks("k_bvh_level", s);
+            k_bvh_level<<<n, kBuildThreads, 0, s>>>(static_cast<const BTri*>(tris), static_cast<int*>(order),
+                                                     static_cast<int*>(tmp), static_cast<BNode*>(nodes), bfs_i + off,
+                                                     n, bfs_i + off + n, ctr_i + 1, ctr_i);
+        }
+        ok(cudaMemcpyAsync(hc, ctr_i, 8, cudaMemcpyDeviceToHost, s), "ctr");
+        ok(cudaStreamSynchronize(s), "level");
+        level_off.push_back(off + n);
+        level_n.push_back(hc[1]);
+    }
+    n_nodes = hc[0];
+    depth = int(level_n.size()) - 1;
+    ok(cudaGetLastError(), "levels");
+    // the reference's depth-first numbering: subtree sizes, then pre-order
+    const BNode* nd = static_cast<const BNode*>(nodes);
+    for (int L = depth - 1; L >= 0; --L) {
+        int n = level_n[L];
+        KScope ks("k_bvh_sizes", s);
+        k_bvh_sizes<<<(n + 255) / 256, 256, 0, s>>>(nd, bfs_i + level_off[L], n, static_cast<int*>(size));
+    }
+    int root_pre_esc[2] = {0, -1};
+    ok(cudaMemcpyAsync(pre, &root_pre_esc[0], 4, cudaMemcpyHostToDevice, s), "pre");
+    ok(cudaMemcpyAsync(esc, &root_pre_esc[1], 4, cudaMemcpyHostToDevice, s), "esc");
+    for (int L = 0; L < depth; ++L) {
+        int n = level_n[L];
+        KScope ks("k_bvh_preorder", s);
+        k_bvh_preorder<<<(n + 255) / 256, 256, 0, s>>>(nd, bfs_i + level_off[L], n, static_cast<int*>(size),
+                                                        static_cast<int*>(pre), static_cast<int*>(esc));
+    }
+    ok(cudaGetLastError(), "pre-order");
+    return n_nodes;
+}
+
+void DeviceBvh::pack(unsigned char* blob, const PackedFrame& shell, cudaStream_t s) {
+    const int nt = shell.view.n_tris;
+    const BNode* nd = static_cast<const BNode*>(nodes);
+    GTriInfo* info = reinterpret_cast<GTriInfo*>(blob + shell.off_tri);
+    {
+        KScope ks("k_bvh_pack_tris", s);
+        k_bvh_pack_tris<<<(nt + 255) / 256, 256, 0, s>>>(
+            static_cast<const BTri*>(tris), static_cast<const int*>(order), nt,
+            reinterpret_cast<GTriIsect*>(blob + shell.off_isect), reinterpret_cast<int*>(blob + shell.off_tri_id),
+            info, reinterpret_cast<Frame2*>(blob + shell.off_tframe));
+    }
+    {
+        KScope ks("k_bvh_pack_nodes", s);
+        k_bvh_pack_nodes<<<(n_nodes + 255) / 256, 256, 0, s>>>(
+            nd, n_nodes, static_cast<const int*>(pre), static_cast<const int*>(esc), static_cast<const int*>(order),
+            reinterpret_cast<GNode*>(blob + shell.off_nodes), reinterpret_cast<GNodeAux*>(blob + shell.off_aux), info);
+    }
+    ok(cudaGetLastError(), "pack");
+}
+
+void DeviceBvh::dump(double* nodes_out, int32_t* parent_out, int32_t* order_out, cudaStream_t s) {
+    // the host builder's dump layout (tofr_scene_dump_bvh): per node lo, hi,
+    // tri_area, left, right, first, count in pre-order, the parents, tri_order
+    std::vector<BNode> h(static_cast<size_t>(n_nodes));
+    std::vector<int> pre_h(static_cast<size_t>(n_nodes));
+    ok(cudaMemcpyAsync(h.data(), nodes, h.size() * sizeof(BNode), cudaMemcpyDeviceToHost, s), "dump");
+    ok(cudaMemcpyAsync(pre_h.data(), pre, pre_h.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "dump");
+    ok(cudaMemcpyAsync(order_out, order, size_t(nt) * sizeof(int), cudaMemcpyDeviceToHost, s), "dump");
+    ok(cudaStreamSynchronize(s), "dump");
+    for (size_t id = 0; id < h.size(); ++id) {
+        const BNode& b = h[id];
+        double* o = nodes_out + 11 * size_t(pre_h[id]);
+        const bool leaf = b.left < 0;
+        o[0] = b.lo.x;
+        o[1] = b.lo.y;
+        o[2] = b.lo.z;
+        o[3] = b.hi.x;
+        o[4] = b.hi.y;
+        o[5] = b.hi.z;
+        o[6] = b.tri_area;
+        o[7] = leaf ? -1 : pre_h[size_t(b.left)];
+        o[8] = leaf ? -1 : pre_h[size_t(b.right)];
+        o[9] = leaf ? b.first : 0;
+        o[10] = leaf ? b.count : 0;
+        parent_out[pre_h[id]] = b.parent < 0 ? -1 : pre_h[size_t(b.parent)];
+    }
+}
+
+}  // namespace tofr_b200

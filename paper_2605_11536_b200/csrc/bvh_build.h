@@ -1,0 +1,32 @@
+// bvh_build.h -- the frame's SAH BVH built on the device (bvh_build.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "host_scene.h"
+#include "tofr_geom.h"
+
+namespace tofr_b200 {
+
+// Per-session scratch of the device build.  build() uploads the frame's
+// world-space triangles (HTri layout) and builds the tree (one host sync per
+// level); pack() writes the snapshot's tree and triangle arrays into a device
+// blob laid out by pack_frame_shell(..., n_nodes, ...).
+struct DeviceBvh {
+    void *tris = nullptr, *order = nullptr, *tmp = nullptr, *nodes = nullptr, *bfs = nullptr, *size = nullptr,
+         *pre = nullptr, *esc = nullptr, *ctr = nullptr, *host_ctr = nullptr;
+    int cap = 0, nt = 0, n_nodes = 0, depth = 0;
+    std::vector<int> level_off, level_n;
+    ~DeviceBvh();
+    void release();
+    void ensure(int nt);
+    int build(const void* host_tris, int nt, cudaStream_t s);  // -> node count
+    void pack(unsigned char* blob, const PackedFrame& shell, cudaStream_t s);
+    // the host builder's dump layout (tofr_scene_dump_bvh), for parity checks
+    void dump(double* nodes_out, int32_t* parent_out, int32_t* order_out, cudaStream_t s);
+};
+
+}  // namespace tofr_b200

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/tofr_gpu.h"
+#include "bvh_build.h"
 #include "halo_transport.h"
 #include "host_scene.h"
 #include "ktime.h"
@@ -180,6 +181,9 @@ struct tofr_session {
     int y0 = 0, y1 = 0, r0 = 0, r1 = 0;
     bool cam_moves = false;
     bool static_frames = false;  // frame-invariant snapshot: built and uploaded once per slot
+    // the frame's BVH built on the device (large animated meshes; wide light)
+    bool device_bvh = false;
+    std::unique_ptr<DeviceBvh> dbvh;
     FrameSlot slot[2];
     DevBuf res[3];
     int cur = 0, prev = 1, spare = 2;
@@ -488,6 +492,28 @@ void upload_frame(tofr_session* s, int which, double frame, int frame_id, cudaSt
         s->last_h2d = 0;
         return;
     }
+    if (s->device_bvh) {  // the tree built on the device (bvh_build.cu), packed in place
+        HFrame hf = build_frame(s->scene, frame, false);
+        if (!s->dbvh) s->dbvh = std::make_unique<DeviceBvh>();
+        const int nt = int(hf.tris.size());
+        sl.staging.ensure(size_t(nt) * sizeof(HTri));
+        std::memcpy(sl.staging.p, hf.tris.data(), size_t(nt) * sizeof(HTri));
+        const int nn = s->dbvh->build(sl.staging.p, nt, st);
+        if (s->dbvh->depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
+        sl.pk = pack_frame_shell(s->scene, hf, nn, frame_id);
+        sl.blob.ensure(sl.pk.blob.size());
+        // the shell's host part: materials and velocity fields
+        unsigned char* dst = static_cast<unsigned char*>(sl.blob.p);
+        const size_t small = sl.pk.off_tframe - sl.pk.off_mats;
+        ck(cudaMemcpyAsync(dst + sl.pk.off_mats, sl.pk.blob.data() + sl.pk.off_mats, small, cudaMemcpyHostToDevice, st),
+           "frame upload");
+        s->dbvh->pack(dst, sl.pk, st);
+        ck(cudaStreamSynchronize(st), "frame upload");  // the staging buffer is reused by the next frame
+        sl.view = rebase_view(sl.pk, dst);
+        s->last_h2d = size_t(nt) * sizeof(HTri) + small;
+        sl.cached = s->static_frames;
+        return;
+    }
     HFrame hf = build_frame(s->scene, frame);
     if (hf.max_depth > 60) throw ScopeError(TOFR_ERR_SCENE, "bvh deeper than supported");
     sl.pk = pack_frame(s->scene, hf, frame_id);
@@ -572,6 +598,19 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
     s->cam_moves = !sc->s.camera.track.empty();
     const char* sf = std::getenv("TOFR_STATIC_FRAMES");
     s->static_frames = static_scene(sc->s) && !(sf && sf[0] == '0');
+    {
+        // TOFR_DEVICE_BVH=1: always (wide-light scenes), 0: never; default: when a
+        // non-static frame has >= 4096 triangles (the host SAH build then costs
+        // more than the device build's per-level syncs)
+        size_t ntri = 0;
+        for (const HObject& o : sc->s.objects) ntri += o.local.size();
+        const char* db = std::getenv("TOFR_DEVICE_BVH");
+        const bool wide = sc->s.light.regime == LIGHT_WIDE;
+        if (db && db[0] == '1')
+            s->device_bvh = wide;
+        else if (!(db && db[0] == '0'))
+            s->device_bvh = wide && !s->static_frames && ntri >= 4096;
+    }
     if (kind == KIND_RESTIR && cfg && cfg->temporal && s->cam_moves && halo == 0 && (y0 > 0 || y1 < s->H))
         throw ScopeError(TOFR_ERR_INVALID,
                          "row band of a moving camera with temporal reuse needs a reprojection halo (halo > 0)");
@@ -1452,6 +1491,22 @@ int tofr_scene_dump_bvh(const tofr_scene* s, double frame, int32_t cap_nodes, do
         }
         if (tri_order && int(f.tri_order.size()) <= cap_tris)
             for (size_t i = 0; i < f.tri_order.size(); ++i) tri_order[i] = f.tri_order[i];
+    });
+}
+
+int tofr_gpu_dump_bvh_device(tofr_gpu* ctx, const tofr_scene* s, double frame, int32_t cap_nodes, double* nodes,
+                             int32_t* node_parent, int32_t* n_nodes, int32_t cap_tris, int32_t* tri_order,
+                             int32_t* n_tris, double* diag) {
+    return guard(ctx, [&] {
+        if (!ctx || !s) throw ScopeError(TOFR_ERR_INVALID, "null handle");
+        HFrame f = build_frame(s->s, frame, false);
+        DeviceBvh db;
+        int nn = db.build(f.tris.data(), int(f.tris.size()), ctx->stream);
+        if (n_nodes) *n_nodes = nn;
+        if (n_tris) *n_tris = int32_t(f.tris.size());
+        if (diag) *diag = f.diag;
+        if (nodes && node_parent && tri_order && nn <= cap_nodes && int(f.tris.size()) <= cap_tris)
+            db.dump(nodes, node_parent, tri_order, ctx->stream);
     });
 }
 

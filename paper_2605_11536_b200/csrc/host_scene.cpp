@@ -551,7 +551,7 @@ std::vector<GMat> device_materials(const HScene& s) {
     return out;
 }
 
-HFrame build_frame(const HScene& def, double frame) {
+HFrame build_frame(const HScene& def, double frame, bool build_bvh) {
     HFrame f;
     f.frame = frame;
     for (size_t i = 0; i < def.objects.size(); ++i) {
@@ -593,18 +593,30 @@ HFrame build_frame(const HScene& def, double frame) {
     if (f.tris.empty()) throw std::runtime_error("bvh: empty mesh");
     for (const HTri& t : f.tris)
         if (t.area <= 1e-12) throw std::runtime_error("bvh: degenerate triangle");
-    f.tri_order.resize(f.tris.size());
-    for (size_t i = 0; i < f.tris.size(); ++i) f.tri_order[i] = int(i);
-    f.nodes.reserve(f.tris.size() * 2);
-    SahBuilder b{f.tris, f.tri_order, f.nodes};
-    b.build(0, int(f.tris.size()), -1);
-    f.diag = norm(f.nodes[0].hi - f.nodes[0].lo);
+    if (build_bvh) {
+        f.tri_order.resize(f.tris.size());
+        for (size_t i = 0; i < f.tris.size(); ++i) f.tri_order[i] = int(i);
+        f.nodes.reserve(f.tris.size() * 2);
+        SahBuilder b{f.tris, f.tri_order, f.nodes};
+        b.build(0, int(f.tris.size()), -1);
+        f.diag = norm(f.nodes[0].hi - f.nodes[0].lo);
+        f.leaf_of.assign(f.tris.size(), -1);
+        for (size_t n = 0; n < f.nodes.size(); ++n)
+            if (f.nodes[n].count > 0)
+                for (int i = 0; i < f.nodes[n].count; ++i) f.leaf_of[f.tri_order[f.nodes[n].first + i]] = int(n);
+        f.max_depth = tree_depth(f.nodes, 0);
+    } else {
+        // the tree is built on the device (bvh_build.cu); its root box is the
+        // box of every vertex (min / max: the same bounds in any order)
+        Box box;
+        for (const HTri& t : f.tris) {
+            box.grow(t.v0);
+            box.grow(t.v1);
+            box.grow(t.v2);
+        }
+        f.diag = norm(box.hi - box.lo);
+    }
     f.eps_ray = 1e-4 * f.diag;
-    f.leaf_of.assign(f.tris.size(), -1);
-    for (size_t n = 0; n < f.nodes.size(); ++n)
-        if (f.nodes[n].count > 0)
-            for (int i = 0; i < f.nodes[n].count; ++i) f.leaf_of[f.tri_order[f.nodes[n].first + i]] = int(n);
-    f.max_depth = tree_depth(f.nodes, 0);
 
     // camera frame (scene.hpp:375-384)
     HCamPose pose = def.camera.pose_at(frame);
@@ -636,6 +648,7 @@ HFrame build_frame(const HScene& def, double frame) {
     std::memset(&f.lsub, 0, sizeof(f.lsub));
     f.lsub.tri = f.lsub.obj = f.lsub.mat = -1;
     if (def.light.regime == LIGHT_COLLIMATED) {
+        if (!build_bvh) throw std::runtime_error("device BVH build: the collimated beam trace needs the host tree");
         // trace the beam through mirrors to its first non-delta hit
         PackedFrame pk = pack_frame(def, f, 0);
         FrameView v = rebase_view(pk, pk.blob.data());
@@ -761,6 +774,50 @@ PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id) {
     std::memcpy(p.blob.data() + p.off_mats, mats.data(), mats.size() * sizeof(GMat));
     if (!f.obj_vel.empty()) std::memcpy(p.blob.data() + p.off_vel, f.obj_vel.data(), f.obj_vel.size() * sizeof(GVel));
 
+    FrameView& v = p.view;
+    std::memset(&v, 0, sizeof(v));
+    v.n_nodes = nn;
+    v.n_tris = nt;
+    v.n_mats = int(mats.size());
+    v.geo_motion = f.geo_motion;
+    v.cam = f.cam;
+    v.light = f.light;
+    v.lsub = f.lsub;
+    v.eps_ray = f.eps_ray;
+    v.diag = f.diag;
+    v.frame_id = frame_id;
+    v.n_obj = int(f.obj_vel.size());
+    v.cam_vel = f.cam_vel;
+    return p;
+}
+
+PackedFrame pack_frame_shell(const HScene& s, const HFrame& f, int nn, int frame_id) {
+    // the layout of pack_frame for nn nodes; only the materials and velocity
+    // fields are filled (the device writes the tree and triangle arrays)
+    PackedFrame p;
+    const int nt = int(f.tris.size());
+    std::vector<GMat> mats = device_materials(s);
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t off = 0;
+    p.off_nodes = off;
+    off = align(off + nn * sizeof(GNode));
+    p.off_aux = off;
+    off = align(off + nn * sizeof(GNodeAux));
+    p.off_isect = off;
+    off = align(off + nt * sizeof(GTriIsect));
+    p.off_tri_id = off;
+    off = align(off + nt * sizeof(int));
+    p.off_tri = off;
+    off = align(off + nt * sizeof(GTriInfo));
+    p.off_mats = off;
+    off = align(off + mats.size() * sizeof(GMat));
+    p.off_vel = off;
+    off = align(off + f.obj_vel.size() * sizeof(GVel));
+    p.off_tframe = off;
+    off = align(off + nt * sizeof(Frame2));
+    p.blob.assign(off, 0);
+    std::memcpy(p.blob.data() + p.off_mats, mats.data(), mats.size() * sizeof(GMat));
+    if (!f.obj_vel.empty()) std::memcpy(p.blob.data() + p.off_vel, f.obj_vel.data(), f.obj_vel.size() * sizeof(GVel));
     FrameView& v = p.view;
     std::memset(&v, 0, sizeof(v));
     v.n_nodes = nn;

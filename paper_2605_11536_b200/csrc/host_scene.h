@@ -129,7 +129,10 @@ struct HFrame {
 
 // Builds the snapshot for `frame` (scene.hpp:479-548).  Throws
 // std::runtime_error("bvh: empty mesh" / "bvh: degenerate triangle").
-HFrame build_frame(const HScene& s, double frame);
+HFrame build_frame(const HScene& s, double frame, bool build_bvh = true);
+// pack_frame's layout for an nn-node tree built elsewhere (the device): the
+// blob holds the materials and velocity fields only; the rest is written in place
+PackedFrame pack_frame_shell(const HScene& s, const HFrame& f, int nn, int frame_id);
 
 // Device layout of a frame; `view` pointers are relative to blob start.
 PackedFrame pack_frame(const HScene& s, const HFrame& f, int frame_id);

@@ -336,8 +336,8 @@ BUNDLED = {"cornell": cornell, "cornell_wide": cornell_wide, "boxes_doppler": bo
 
 
 def bundled(name: str, width: int | None = None, height: int | None = None) -> SceneDef:
-    if name == "mesh":  # the BVH stress scene (not a bundled .scn)
-        return mesh_scene(width or 256, height)
+    if name in ("mesh", "mesh_anim"):  # the BVH stress scene (not a bundled .scn)
+        return mesh_scene(width or 256, height, animated=name == "mesh_anim")
     d = BUNDLED[name]()
     if width:
         d.camera.width = width
@@ -388,9 +388,12 @@ def write_torus_obj(path, nu: int = 320, nv: int = 160) -> int:
     return len(faces)
 
 
-def mesh_scene(width: int = 256, height: int | None = None, nu: int = 320, nv: int = 160) -> SceneDef:
+def mesh_scene(width: int = 256, height: int | None = None, nu: int = 320, nv: int = 160,
+               animated: bool = False) -> SceneDef:
     """cornell_wide's box, light and camera plus the torus (glossy) with its
-    triangles inline: the same scene as mesh_scene_file's .scn + OBJ."""
+    triangles inline: the same scene as mesh_scene_file's .scn + OBJ.
+    animated: the torus turns about y (30 degrees over 20 frames) and drifts
+    along x, so every frame needs a new BVH (the device build's case)."""
     d = cornell_wide()
     d.objects = d.objects[:3]  # box, left, right (no tall box)
     metal = 3
@@ -398,6 +401,10 @@ def mesh_scene(width: int = 256, height: int | None = None, nu: int = 320, nv: i
     t = ObjectDef("torus")
     for a, b, c in faces:
         t.tri(verts[a], verts[b], verts[c], metal)
+    if animated:
+        half = math.radians(30.0) / 2
+        t.track = [PoseKey(0.0, (1.0, 0.0, 0.0, 0.0), (0.0, 0.0, 0.0)),
+                   PoseKey(20.0, (math.cos(half), 0.0, math.sin(half), 0.0), (0.1, 0.0, 0.0))]
     d.objects.append(t)
     d.camera.width = width
     d.camera.height = height or width

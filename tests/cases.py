@@ -117,6 +117,11 @@ CASES["mesh_torus_reuse"] = (lambda: scenes.mesh_scene(48),
                              RenderConfig(gate=gate(6.0, 0.2), m_init=1, temporal=True, spatial_passes=1,
                                           spatial_neighbors=3, spatial_radius=6, frames=2), "gated")
 
+# the same mesh moving (a new BVH every frame: built on the device by default)
+CASES["mesh_anim_reuse"] = (lambda: scenes.mesh_scene(40, animated=True),
+                            RenderConfig(gate=gate(6.0, 0.2), m_init=1, temporal=True, spatial_passes=1,
+                                         spatial_neighbors=3, spatial_radius=6, frames=3, frame0=4), "gated")
+
 REFERENCE_CASES = {
     "ref_cornell_wide": (lambda: scenes.bundled("cornell_wide", 32), 0.0, gate(6.0, 0.5), 16, 3, 6),
     "ref_cornell": (lambda: scenes.bundled("cornell", 32), 0.0, gate(10.0, 0.5), 16, 5, 6),
