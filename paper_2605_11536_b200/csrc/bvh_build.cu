@@ -123,9 +123,19 @@ __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, i
     hi = V3{block_max(hi.x, shd), block_max(hi.y, shd), block_max(hi.z, shd)};
     clo = V3{block_min(clo.x, shd), block_min(clo.y, shd), block_min(clo.z, shd)};
     chi = V3{block_max(chi.x, shd), block_max(chi.y, shd), block_max(chi.z, shd)};
+    // tri_area: the reference's sequential sum (area += t.area over the range, in
+    // order) by one thread, its operands gathered into shared memory by the block
+    __shared__ double s_area[1024];
+    double area = 0;
+    for (int base = first; base < first + count; base += 1024) {
+        const int m = min(1024, first + count - base);
+        __syncthreads();
+        for (int k = threadIdx.x; k < m; k += blockDim.x) s_area[k] = tris[order[base + k]].area;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int k = 0; k < m; ++k) area += s_area[k];
+    }
     if (threadIdx.x == 0) {
-        double area = 0;  // the reference's order: area += t.area over the range
-        for (int i = first; i < first + count; ++i) area += tris[order[i]].area;
         BNode& nd = nodes[id];
         nd.lo = lo;
         nd.hi = hi;
