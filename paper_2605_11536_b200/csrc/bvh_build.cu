@@ -98,6 +98,31 @@ __device__ int block_scan(int f, int* sh, int* total) {
     return before + in_warp;
 }
 
+constexpr int kSmallNode = 64;  // nodes this small are built by one thread
+
+// children of node id (ranges [first, mid), [mid, first + count)); they join
+// the next level's big list (next[0..]) or small list (next[kSmallList..])
+__device__ void make_children(BNode* nodes, int id, int first, int count, int mid, int* next, int* n_next,
+                              int* n_nodes) {
+    int c = atomicAdd(n_nodes, 2);
+    BNode l{}, r{};
+    l.first = first;
+    l.count = mid - first;
+    l.parent = id;
+    r.first = mid;
+    r.count = first + count - mid;
+    r.parent = id;
+    nodes[c] = l;
+    nodes[c + 1] = r;
+    nodes[id].left = c;
+    nodes[id].right = c + 1;
+    for (int k = 0; k < 2; ++k) {
+        const bool small = (k ? r.count : l.count) <= kSmallNode;
+        int t = atomicAdd(&n_next[small ? 1 : 0], 1);
+        next[small ? n_next[2] + t : t] = c + k;  // n_next[2]: the small list's offset
+    }
+}
+
 // one level: CTA b builds node tasks[b]
 __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, int* order, int* tmp, BNode* nodes,
                                                              const int* tasks, int n_tasks, int* next, int* n_next,
@@ -255,23 +280,97 @@ __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, i
             if (mid == first || mid == first + count) mid = first + count / 2;
         }
     }
-    if (threadIdx.x == 0) {
-        int c = atomicAdd(n_nodes, 2);
-        BNode l{}, r{};
-        l.first = first;
-        l.count = mid - first;
-        l.parent = id;
-        r.first = mid;
-        r.count = first + count - mid;
-        r.parent = id;
-        nodes[c] = l;
-        nodes[c + 1] = r;
-        nodes[id].left = c;
-        nodes[id].right = c + 1;
-        int t = atomicAdd(n_next, 2);
-        next[t] = c;
-        next[t + 1] = c + 1;
+    if (threadIdx.x == 0) make_children(nodes, id, first, count, mid, next, n_next, n_nodes);
+}
+
+// one thread per node of <= kSmallNode triangles: the host builder's loops as
+// they are (sequential, no barriers), children stay small
+__global__ void k_bvh_level_small(const BTri* tris, int* order, int* tmp, BNode* nodes, const int* tasks,
+                                  int n_tasks, int* next, int* n_next, int* n_nodes) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_tasks) return;
+    const int id = tasks[k];
+    const int first = nodes[id].first, count = nodes[id].count;
+    V3 lo{kInf, kInf, kInf}, hi{-kInf, -kInf, -kInf}, clo = lo, chi = hi;
+    double area = 0;
+    for (int i = first; i < first + count; ++i) {
+        const BTri& t = tris[order[i]];
+        lo = vmin(vmin(vmin(lo, t.v0), t.v1), t.v2);
+        hi = vmax(vmax(vmax(hi, t.v0), t.v1), t.v2);
+        V3 c = (t.v0 + t.v1 + t.v2) / 3.0;
+        clo = vmin(clo, c);
+        chi = vmax(chi, c);
+        area += t.area;
     }
+    BNode& nd = nodes[id];
+    nd.lo = lo;
+    nd.hi = hi;
+    nd.tri_area = area;
+    nd.left = nd.right = -1;
+    if (count <= 4) return;
+    V3 ext = chi - clo;
+    const int axis = ext.x > ext.y ? (ext.x > ext.z ? 0 : 2) : (ext.y > ext.z ? 1 : 2);
+    const double blo = comp(clo, axis), width = comp(ext, axis);
+    int mid = first + count / 2;
+    if (!(width < 1e-12)) {
+        auto bin_of = [&](const BTri& t) {
+            double c = (centroid_axis(t, axis) - blo) / width;
+            int b = int(c * kBinsDev);
+            return b < kBinsDev - 1 ? b : kBinsDev - 1;
+        };
+        int bc[kBinsDev];
+        V3 bl[kBinsDev], bh[kBinsDev];
+        for (int b = 0; b < kBinsDev; ++b) {
+            bc[b] = 0;
+            bl[b] = V3{kInf, kInf, kInf};
+            bh[b] = V3{-kInf, -kInf, -kInf};
+        }
+        for (int i = first; i < first + count; ++i) {
+            const BTri& t = tris[order[i]];
+            int b = bin_of(t);
+            bc[b]++;
+            bl[b] = vmin(vmin(vmin(bl[b], t.v0), t.v1), t.v2);
+            bh[b] = vmax(vmax(vmax(bh[b], t.v0), t.v1), t.v2);
+        }
+        double best_cost = kInf;
+        int best = -1;
+        for (int sp = 1; sp < kBinsDev; ++sp) {
+            V3 llo{kInf, kInf, kInf}, lhi{-kInf, -kInf, -kInf}, rlo = llo, rhi = lhi;
+            int lc = 0, rc = 0;
+            for (int i = 0; i < sp; ++i) {
+                if (bc[i]) {
+                    llo = vmin(llo, bl[i]);
+                    lhi = vmax(lhi, bh[i]);
+                }
+                lc += bc[i];
+            }
+            for (int i = sp; i < kBinsDev; ++i) {
+                if (bc[i]) {
+                    rlo = vmin(rlo, bl[i]);
+                    rhi = vmax(rhi, bh[i]);
+                }
+                rc += bc[i];
+            }
+            if (lc == 0 || rc == 0) continue;
+            double cost = box_area(llo, lhi) * lc + box_area(rlo, rhi) * rc;
+            if (cost < best_cost) {
+                best_cost = cost;
+                best = sp;
+            }
+        }
+        if (best >= 0) {  // std::stable_partition by bin < best
+            int nl = 0;
+            for (int i = first; i < first + count; ++i)
+                if (bin_of(tris[order[i]]) < best) tmp[first + nl++] = order[i];
+            int nr = nl;
+            for (int i = first; i < first + count; ++i)
+                if (!(bin_of(tris[order[i]]) < best)) tmp[first + nr++] = order[i];
+            for (int i = first; i < first + count; ++i) order[i] = tmp[i];
+            mid = first + nl;
+            if (mid == first || mid == first + count) mid = first + count / 2;
+        }
+    }
+    make_children(nodes, id, first, count, mid, next, n_next, n_nodes);
 }
 
 // subtree sizes, bottom-up over one level's nodes
@@ -366,7 +465,7 @@ void ok(cudaError_t e, const char* what) {
 
 DeviceBvh::~DeviceBvh() { release(); }
 void DeviceBvh::release() {
-    for (void** p : {&tris, &order, &tmp, &nodes, &bfs, &size, &pre, &esc, &ctr, &host_ctr}) {
+    for (void** p : {&tris, &order, &tmp, &nodes, &bfs, &next_lists, &size, &pre, &esc, &ctr, &host_ctr}) {
         if (*p) {
             if (p == &host_ctr)
                 cudaFreeHost(*p);
@@ -386,6 +485,7 @@ void DeviceBvh::ensure(int nt) {
     ok(cudaMalloc(&tmp, n * sizeof(int)), "alloc");
     ok(cudaMalloc(&nodes, nn * sizeof(BNode)), "alloc");
     ok(cudaMalloc(&bfs, nn * sizeof(int)), "alloc");
+    ok(cudaMalloc(&next_lists, 2 * nn * sizeof(int)), "alloc");
     ok(cudaMalloc(&size, nn * sizeof(int)), "alloc");
     ok(cudaMalloc(&pre, nn * sizeof(int)), "alloc");
     ok(cudaMalloc(&esc, nn * sizeof(int)), "alloc");
@@ -410,27 +510,46 @@ int DeviceBvh::build(const void* host_tris, int n_tris, cudaStream_t s) {
     root.parent = -1;
     ok(cudaMemcpyAsync(nodes, &root, sizeof(BNode), cudaMemcpyHostToDevice, s), "root");
     int* bfs_i = static_cast<int*>(bfs);
-    int* ctr_i = static_cast<int*>(ctr);  // [0] nodes made, [1] next level's tasks
+    int* nxt = static_cast<int*>(next_lists);
+    // [0] nodes made, [1] next level's big tasks, [2] its small tasks, [3] the
+    // small list's offset in `nxt`
+    int* ctr_i = static_cast<int*>(ctr);
     int* hc = static_cast<int*>(host_ctr);
-    int zero_one[2] = {1, 0};
-    ok(cudaMemcpyAsync(ctr_i, zero_one, 8, cudaMemcpyHostToDevice, s), "ctr");
-    ok(cudaMemcpyAsync(bfs_i, &zero_one[1], 4, cudaMemcpyHostToDevice, s), "bfs");  // level 0 = node 0
+    const int root_small = nt <= kSmallNode ? 1 : 0;
+    int init[4] = {1, 0, 0, 0};
+    ok(cudaMemcpyAsync(ctr_i, init, 16, cudaMemcpyHostToDevice, s), "ctr");
+    ok(cudaMemcpyAsync(bfs_i, &init[3], 4, cudaMemcpyHostToDevice, s), "bfs");  // level 0 = node 0
     level_off.assign(1, 0);
     level_n.assign(1, 1);
+    level_nb.assign(1, 1 - root_small);
     for (int L = 0; level_n.back() > 0; ++L) {
         if (L > 62) throw std::runtime_error("bvh deeper than supported");
-        const int off = level_off.back(), n = level_n.back();
-        ok(cudaMemsetAsync(ctr_i + 1, 0, 4, s), "ctr");
-        {
+        const int off = level_off.back(), n = level_n.back(), nb = level_nb.back(), ns = n - nb;
+        int c[3] = {0, 0, 2 * n};  // children of n nodes: <= 2n per list
+        ok(cudaMemcpyAsync(ctr_i + 1, c, 12, cudaMemcpyHostToDevice, s), "ctr");
+        if (nb) {
             KScope ks("k_bvh_level", s);
-            k_bvh_level<<<n, kBuildThreads, 0, s>>>(static_cast<const BTri*>(tris), static_cast<int*>(order),
-                                                     static_cast<int*>(tmp), static_cast<BNode*>(nodes), bfs_i + off,
-                                                     n, bfs_i + off + n, ctr_i + 1, ctr_i);
+            k_bvh_level<<<nb, kBuildThreads, 0, s>>>(static_cast<const BTri*>(tris), static_cast<int*>(order),
+                                                      static_cast<int*>(tmp), static_cast<BNode*>(nodes), bfs_i + off,
+                                                      nb, nxt, ctr_i + 1, ctr_i);
         }
-        ok(cudaMemcpyAsync(hc, ctr_i, 8, cudaMemcpyDeviceToHost, s), "ctr");
+        if (ns) {
+            KScope ks("k_bvh_level_small", s);
+            k_bvh_level_small<<<(ns + 127) / 128, 128, 0, s>>>(static_cast<const BTri*>(tris), static_cast<int*>(order),
+                                                                static_cast<int*>(tmp), static_cast<BNode*>(nodes),
+                                                                bfs_i + off + nb, ns, nxt, ctr_i + 1, ctr_i);
+        }
+        ok(cudaMemcpyAsync(hc, ctr_i, 12, cudaMemcpyDeviceToHost, s), "ctr");
         ok(cudaStreamSynchronize(s), "level");
+        const int nb2 = hc[1], ns2 = hc[2];
+        // the next level: [big tasks | small tasks], contiguous after this one
+        if (nb2) ok(cudaMemcpyAsync(bfs_i + off + n, nxt, size_t(nb2) * 4, cudaMemcpyDeviceToDevice, s), "level");
+        if (ns2)
+            ok(cudaMemcpyAsync(bfs_i + off + n + nb2, nxt + 2 * n, size_t(ns2) * 4, cudaMemcpyDeviceToDevice, s),
+               "level");
         level_off.push_back(off + n);
-        level_n.push_back(hc[1]);
+        level_n.push_back(nb2 + ns2);
+        level_nb.push_back(nb2);
     }
     n_nodes = hc[0];
     depth = int(level_n.size()) - 1;

@@ -16,10 +16,10 @@ namespace tofr_b200 {
 // level); pack() writes the snapshot's tree and triangle arrays into a device
 // blob laid out by pack_frame_shell(..., n_nodes, ...).
 struct DeviceBvh {
-    void *tris = nullptr, *order = nullptr, *tmp = nullptr, *nodes = nullptr, *bfs = nullptr, *size = nullptr,
-         *pre = nullptr, *esc = nullptr, *ctr = nullptr, *host_ctr = nullptr;
+    void *tris = nullptr, *order = nullptr, *tmp = nullptr, *nodes = nullptr, *bfs = nullptr, *next_lists = nullptr,
+         *size = nullptr, *pre = nullptr, *esc = nullptr, *ctr = nullptr, *host_ctr = nullptr;
     int cap = 0, nt = 0, n_nodes = 0, depth = 0;
-    std::vector<int> level_off, level_n;
+    std::vector<int> level_off, level_n, level_nb;  // per level: first task, tasks, big tasks
     ~DeviceBvh();
     void release();
     void ensure(int nt);
