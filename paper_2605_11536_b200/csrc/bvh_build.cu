@@ -81,6 +81,51 @@ __device__ int block_sum(int v, int* sh) {
     for (int i = 0; i < int(blockDim.x >> 5); ++i) r += sh[i];
     return r;
 }
+// block-wide min (k < nmin) / max (k >= nmin) of N doubles per thread, written to
+// out[N] in shared memory: one shuffle tree per value, one barrier pair
+template <int N>
+__device__ void block_minmax(double (&v)[N], int nmin, double (*wsh)[N], double* out) {
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        for (int o = 16; o > 0; o >>= 1) {
+            double w = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = k < nmin ? dmin(v[k], w) : dmax(v[k], w);
+        }
+    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int k = 0; k < N; ++k) wsh[wid][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < N) {
+        const int k = threadIdx.x;
+        double r = wsh[0][k];
+        for (int i = 1; i < int(blockDim.x >> 5); ++i) r = k < nmin ? dmin(r, wsh[i][k]) : dmax(r, wsh[i][k]);
+        out[k] = r;
+    }
+    __syncthreads();
+}
+
+// exclusive block scan of a small count per thread; *total = the block sum
+__device__ int block_scan_count(int c, int* sh, int* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += t;
+    }
+    __syncthreads();
+    if (l == 31) sh[w] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+        if (i < w) before += sh[i];
+        all += sh[i];
+    }
+    *total = all;
+    return before + incl - c;
+}
+
 // exclusive block scan of a 0/1 flag; returns the prefix, *total the block sum
 __device__ int block_scan(int f, int* sh, int* total) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -144,10 +189,15 @@ __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, i
         clo = vmin(clo, c);
         chi = vmax(chi, c);
     }
-    lo = V3{block_min(lo.x, shd), block_min(lo.y, shd), block_min(lo.z, shd)};
-    hi = V3{block_max(hi.x, shd), block_max(hi.y, shd), block_max(hi.z, shd)};
-    clo = V3{block_min(clo.x, shd), block_min(clo.y, shd), block_min(clo.z, shd)};
-    chi = V3{block_max(chi.x, shd), block_max(chi.y, shd), block_max(chi.z, shd)};
+    {
+        __shared__ double wsh12[kBuildThreads / 32][12], out12[12];
+        double v[12] = {lo.x, lo.y, lo.z, clo.x, clo.y, clo.z, hi.x, hi.y, hi.z, chi.x, chi.y, chi.z};
+        block_minmax<12>(v, 6, wsh12, out12);
+        lo = V3{out12[0], out12[1], out12[2]};
+        clo = V3{out12[3], out12[4], out12[5]};
+        hi = V3{out12[6], out12[7], out12[8]};
+        chi = V3{out12[9], out12[10], out12[11]};
+    }
     // tri_area: the reference's sequential sum (area += t.area over the range, in
     // order) by one thread, its operands gathered into shared memory by the block
     __shared__ double s_area[1024];
@@ -206,22 +256,39 @@ __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, i
         }
         __shared__ int s_bc[kBinsDev];
         __shared__ double s_bl[kBinsDev][3], s_bh[kBinsDev][3];
-#pragma unroll 1
-        for (int k = 0; k < kBinsDev; ++k) {
-            int c = block_sum(bc[k], shi);
-            double l0 = block_min(bl[k].x, shd), l1 = block_min(bl[k].y, shd), l2 = block_min(bl[k].z, shd);
-            double h0 = block_max(bh[k].x, shd), h1 = block_max(bh[k].y, shd), h2 = block_max(bh[k].z, shd);
-            if (threadIdx.x == 0) {
-                s_bc[k] = c;
-                s_bl[k][0] = l0;
-                s_bl[k][1] = l1;
-                s_bl[k][2] = l2;
-                s_bh[k][0] = h0;
-                s_bh[k][1] = h1;
-                s_bh[k][2] = h2;
+        {  // all bins at once: 24 minima, 24 maxima; counts by warp sums
+            __shared__ double wsh48[kBuildThreads / 32][48], out48[48];
+            double v[48];
+#pragma unroll
+            for (int k = 0; k < kBinsDev; ++k) {
+                v[3 * k + 0] = bl[k].x;
+                v[3 * k + 1] = bl[k].y;
+                v[3 * k + 2] = bl[k].z;
+                v[24 + 3 * k + 0] = bh[k].x;
+                v[24 + 3 * k + 1] = bh[k].y;
+                v[24 + 3 * k + 2] = bh[k].z;
             }
+            block_minmax<48>(v, 24, wsh48, out48);
+            __shared__ int wc[kBuildThreads / 32][kBinsDev];
+#pragma unroll
+            for (int k = 0; k < kBinsDev; ++k)
+                for (int o = 16; o > 0; o >>= 1) bc[k] += __shfl_xor_sync(0xffffffffu, bc[k], o);
+            if ((threadIdx.x & 31) == 0)
+#pragma unroll
+                for (int k = 0; k < kBinsDev; ++k) wc[threadIdx.x >> 5][k] = bc[k];
+            __syncthreads();
+            if (threadIdx.x < kBinsDev) {
+                const int k = threadIdx.x;
+                int c = 0;
+                for (int i = 0; i < int(blockDim.x >> 5); ++i) c += wc[i][k];
+                s_bc[k] = c;
+                for (int a = 0; a < 3; ++a) {
+                    s_bl[k][a] = out48[3 * k + a];
+                    s_bh[k][a] = out48[24 + 3 * k + a];
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (threadIdx.x == 0) {  // SAH over the 7 bin boundaries (SahBuilder)
             double best_cost = kInf;
             int best = -1;
@@ -254,25 +321,46 @@ __global__ void __launch_bounds__(kBuildThreads) k_bvh_level(const BTri* tris, i
         __syncthreads();
         const int split = s_split;
         if (split >= 0) {
-            // stable partition of [first, first + count) by bin < split
+            // stable partition of [first, first + count) by bin < split: chunks of
+            // 4 consecutive elements per thread, one count scan per chunk
+            constexpr int kPer = 4;
+            const int chunk = kPer * int(blockDim.x);
             int n_left = 0;
-            for (int base = first; base < first + count; base += blockDim.x) {
-                int i = base + threadIdx.x;
-                int f = (i < first + count) ? int(bin_of(tris[order[i]]) < split) : 0;
-                n_left += block_sum(f, shi);
+            for (int base = first; base < first + count; base += chunk) {
+                int c = 0;
+                for (int e = 0; e < kPer; ++e) {
+                    int i = base + kPer * int(threadIdx.x) + e;
+                    if (i < first + count) c += int(bin_of(tris[order[i]]) < split);
+                }
+                n_left += block_sum(c, shi);
             }
             int lpos = first, rpos = first + n_left;
-            for (int base = first; base < first + count; base += blockDim.x) {
-                int i = base + threadIdx.x;
-                bool live = i < first + count;
-                int id_i = live ? order[i] : 0;
-                int f = live ? int(bin_of(tris[id_i]) < split) : 0;
-                int tot_l = 0, tot_r = 0;
-                int pl = block_scan(f, shi, &tot_l);
-                int pr = block_scan(live && !f ? 1 : 0, shi, &tot_r);
-                if (live) tmp[f ? lpos + pl : rpos + pr] = id_i;
+            for (int base = first; base < first + count; base += chunk) {
+                int ids[kPer], fl[kPer], c = 0, live_n = 0;
+                for (int e = 0; e < kPer; ++e) {
+                    int i = base + kPer * int(threadIdx.x) + e;
+                    bool live = i < first + count;
+                    ids[e] = live ? order[i] : -1;
+                    fl[e] = live ? int(bin_of(tris[ids[e]]) < split) : 0;
+                    c += fl[e];
+                    live_n += live ? 1 : 0;
+                }
+                int tot_l = 0;
+                const int pl = block_scan_count(c, shi, &tot_l);
+                // elements before this thread's in the chunk, minus the left ones among them
+                const int before = min(kPer * int(threadIdx.x), max(0, first + count - base));
+                int l = pl, r = before - pl;
+                for (int e = 0; e < kPer; ++e) {
+                    if (ids[e] < 0) continue;
+                    if (fl[e])
+                        tmp[lpos + l++] = ids[e];
+                    else
+                        tmp[rpos + r++] = ids[e];
+                }
+                const int chunk_n = min(chunk, first + count - base);
                 lpos += tot_l;
-                rpos += tot_r;
+                rpos += chunk_n - tot_l;
+                (void)live_n;
             }
             __syncthreads();
             for (int i = first + threadIdx.x; i < first + count; i += blockDim.x) order[i] = tmp[i];
