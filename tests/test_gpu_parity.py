@@ -163,6 +163,36 @@ def test_device_bvh_matches_host(renderer, scene_name, frames):
         assert a[3] == b[3]
 
 
+def test_device_bvh_wide_levels_degenerate(renderer):
+    """Wide (multi-CTA) levels of the device build on awkward inputs: 9000
+    copies of one triangle (a wide node with no centroid extent: halved, no
+    split), a random triangle soup (unbalanced SAH splits across chunk
+    boundaries) and a thin sliver stack -- node-for-node the host build."""
+    from paper_2605_11536_b200 import scenes
+    from paper_2605_11536_b200.api import Scene
+    from paper_2605_11536_b200.scenes import ObjectDef
+    rng = np.random.default_rng(11)
+    sd = scenes.cornell_wide()
+    dup, soup, sliver = ObjectDef("dup"), ObjectDef("soup"), ObjectDef("sliver")
+    for _ in range(9000):
+        dup.tri((0.1, 0.1, 0.1), (0.2, 0.1, 0.1), (0.1, 0.2, 0.15), 0)
+    for _ in range(7000):
+        c = rng.uniform(-0.9, 0.9, 3) * np.array([1.0, 0.05, 1.0])
+        d = rng.normal(0, 0.02, (2, 3))
+        soup.tri(tuple(c), tuple(c + d[0]), tuple(c + d[1]), 1)
+    for i in range(5000):
+        z = -0.5 + 1e-9 * i
+        sliver.tri((-0.3, -0.3, z), (0.3, -0.3, z), (0.0, 0.3, z + 1e-13), 2)
+    sd.objects += [dup, soup, sliver]
+    sd.camera.width = sd.camera.height = 16
+    a = renderer.dump_bvh_device(sd, 0.0)
+    b = Scene.create(sd).dump_bvh(0.0)
+    assert len(a[0]) == len(b[0]) and len(a[2]) == len(b[2])
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    assert a[3] == b[3]
+
+
 def test_device_bvh_render_bit_identical(monkeypatch):
     """Frames rendered with the device-built BVH equal those of the host build
     (animated 10^5-triangle mesh: a new tree every frame)."""

@@ -47,6 +47,9 @@ elif case == "ellipsoidal":
     out = r.render_gated(scenes.bundled("cornell_wide", 12), RenderConfig(gate=g(6.0, 0.1), m_init=1,
                          init=F.INIT_ELLIPSOIDAL, temporal=True, spatial_passes=1, spatial_neighbors=2,
                          spatial_radius=2, frames=2))
+elif case == "bvh":  # the device BVH build: wide (multi-CTA), per-CTA and per-warp levels, side stream
+    r.dump_bvh_device(scenes.bundled("mesh_anim", 16), 7.5)
+    out = None
 elif case == "reference":
     r.reference_render(scenes.bundled("cornell", 12), 0.0, g(10.0, 0.5), 4, 3, 6)
     out = None
@@ -62,6 +65,7 @@ CASES = {
     "plain": {},
     "ellipsoidal": {},
     "reference": {},
+    "bvh": {},
     "gated_overlap": {"TOFR_OVERLAP": "1"},
 }
 TOOLS = ["memcheck", "racecheck", "synccheck"]
