@@ -68,6 +68,10 @@ struct ResStore {
     const GHit* gbuf = nullptr;  // the grid's frame: G-buffer (global pixel index) and camera
     GCam cam{};
     int bins = 1;
+    // a record pinned by res_pin: its pool row, looked up once (the slot map
+    // is read with ld.global.cg, a volatile asm the compiler cannot merge, so
+    // every chunk access would otherwise re-read it before its own load)
+    size_t pin_item = ~size_t(0), pin_row = 0;
 };
 
 #if defined(__CUDACC__)
@@ -75,6 +79,7 @@ struct ResStore {
 // pool row of item i for reading chunks >= 1 (the zero row when it has none)
 __device__ __forceinline__ size_t res_row(const ResStore& s, size_t i) {
     if (s.slot == nullptr) return i;
+    if (i == s.pin_item) return s.pin_row;
     uint32_t r = __ldcg(&s.slot[i]);
     return r == kNoSlot ? s.stride - 1 : size_t(r);
 }
@@ -93,6 +98,14 @@ __device__ __forceinline__ size_t res_row_w(const ResStore& s, size_t i) {
     return r;
 }
 __device__ __forceinline__ double2* res_planes(const ResStore& s) { return s.slot ? s.pool : s.base; }
+// a copy of s with item i's row looked up once, for a kernel that reads (never
+// writes) several chunks of that record
+__device__ __forceinline__ ResStore res_pin(const ResStore& s, size_t i) {
+    ResStore v = s;
+    v.pin_row = res_row(s, i);
+    v.pin_item = i;
+    return v;
+}
 
 // chunk c >= 1 at a known row (compact rows: chunks 5-9 are not stored -- they
 // read as zero, writes are dropped -- and chunks >= 10 sit 5 planes lower)

@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(128)
         uint32_t k = j0 + uint32_t(i);
         Job jb = job_get(q, k);
         int dsel = (jb.meta & JOB_DST1) ? 1 : 0;
-        const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+        const ResStore st = res_pin((jb.meta & JOB_REC1) ? st1 : st0, jb.item);
         Meta mt = ld_meta(st, jb.item);
         bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
         bool identity = same_frame && jb.spx == jb.dpx && jb.spy == jb.dpy;
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     Job jb = job_get(q, job);
                     dsel = (jb.meta & JOB_DST1) ? 1 : 0;
                     const FrameView& F = sF[dsel];
-                    const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+                    const ResStore st = res_pin((jb.meta & JOB_REC1) ? st1 : st0, jb.item);
                     count = (jb.meta & JOB_COUNT) != 0;
                     if (count) SCTR(SC_ATTEMPTS, 1);
                     Meta mt = ld_meta(st, jb.item);
@@ -1172,7 +1172,7 @@ __global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
         Job jb = job_get(q, k);
         int dsel = (jb.meta & JOB_DST1) ? 1 : 0;
         const FrameView& F = sF[dsel];
-        const ResStore& st = (jb.meta & JOB_REC1) ? st1 : st0;
+        const ResStore st = res_pin((jb.meta & JOB_REC1) ? st1 : st0, jb.item);
         bool count = (jb.meta & JOB_COUNT) != 0;
         Meta mt = ld_meta(st, jb.item);
         bool same_frame = ((jb.meta & JOB_SRC1) != 0) == (dsel != 0);
