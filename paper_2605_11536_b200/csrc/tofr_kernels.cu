@@ -872,9 +872,10 @@ __device__ __forceinline__ V3 shade_item(const ResStore& s, size_t i, double c, 
     int has;
     res_load_hdr(s, i, W, M, has);
     if (!has || W <= 0) return splat(0);
-    double2 c1 = ld2(s, 1, i), c2 = ld2(s, 2, i), c3 = ld2(s, 3, i);
+    const size_t row = res_row(s, i);
+    double2 c1 = ld2r(s, 1, row), c2 = ld2r(s, 2, row), c3 = ld2r(s, 3, row);
     V3 f{c2.x, c2.y, c3.x};
-    double gv = gate_vel ? ld2(s, 22, i).x : c1.y;
+    double gv = gate_vel ? ld2r(s, 22, row).x : c1.y;
     return f * (W * gate_w(c, w, gv));
 }
 

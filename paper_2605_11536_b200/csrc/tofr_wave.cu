@@ -1312,11 +1312,10 @@ __global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
 // ---------------------------------------------------------------------------
 // merge-side helpers
 
-// chunks [from, 24) of record i -> record j, without the replay lanes (20-21)
-// unless the record has lanes
-__device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const ResStore& dst, size_t j, int from,
-                                            int n_lanes, bool vel) {
-    const size_t ri = res_row(src, i), rj = res_row_w(dst, j);
+// chunks [from, 24) of the record at row ri -> row rj, without the replay
+// lanes (20-21) unless the record has lanes
+__device__ __forceinline__ void copy_chunks_r(const ResStore& src, size_t ri, const ResStore& dst, size_t rj,
+                                              int from, int n_lanes, bool vel) {
     for (int c = from; c < (vel ? kResChunks : 22); ++c) {
         if ((c == 20 || c == 21) && n_lanes <= 0) continue;
         st2r(dst, c, rj, ld2r(src, c, ri));
@@ -1324,24 +1323,27 @@ __device__ __forceinline__ void copy_chunks(const ResStore& src, size_t i, const
 }
 
 // Selected mapped record (job k) -> reservoir `it` with the merge's W, M, p-hat.
+// (Rows looked up once: every slot-map read is a separate volatile load.)
 __device__ __forceinline__ void put_mapped(const ResStore& o, uint32_t k, const ResStore& dst, size_t it, double W,
                                            double M, double phat, bool vel) {
     st2(dst, 0, it, W, M);
-    st2(dst, 1, it, phat, ld2(o, 1, k).y);
-    double2 c4 = ld2(o, 4, k);
+    const size_t ro = res_row(o, k), rj = res_row_w(dst, it);
+    st2r(dst, 1, rj, make_double2(phat, ld2r(o, 1, ro).y));
+    double2 c4 = ld2r(o, 4, ro);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    copy_chunks(o, k, dst, it, 2, mt.nl, vel);
+    copy_chunks_r(o, ro, dst, rj, 2, mt.nl, vel);
 }
 
 // Reservoir copy src[it] -> dst[it] with a new W, M (sample and p-hat kept).
 __device__ __forceinline__ void copy_res(const ResStore& src, const ResStore& dst, size_t it, double W, double M,
                                          bool vel) {
     st2(dst, 0, it, W, M);
-    double2 c4 = ld2(src, 4, it);
+    const size_t ri = res_row(src, it), rj = res_row_w(dst, it);
+    double2 c4 = ld2r(src, 4, ri);
     Meta mt;
     memcpy(&mt, &c4, 16);
-    copy_chunks(src, it, dst, it, 1, mt.nl, vel);
+    copy_chunks_r(src, ri, dst, rj, 1, mt.nl, vel);
 }
 
 // header (W, M, has, p-hat) of a reservoir
