@@ -984,6 +984,9 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         wv.q.jobs = s->wv_jobs.as<double2>();
         wv.q.cap = s->wv_cap;
         wv.q.out = ResStore{s->wv_out.as<double2>(), s->wv_cap};
+        // mapped records land in compact grids only: their prefix-cache chunks
+        // (5-9) would be dropped by put_mapped, so the job outputs skip them too
+        wv.q.out.compact = s->compact_rows ? 1 : 0;
         wv.q.ctl = s->wv_ctl.as<uint32_t>();
         wv.map_a = s->wv_map_a.as<uint32_t>();
         wv.map_b = s->wv_map_b.as<uint32_t>();
