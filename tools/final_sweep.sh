@@ -5,7 +5,7 @@
 TAG=${1:-final}; O=gpurun_out/$TAG; mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -q --timeout 1800 > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
-bash tools/gpu_run.sh $TAG kprof:c2r:k_shift_finish:4:25 kprof:t1080b64:k_shift_finish:8:25 kprof:c3w:k_trace_gated:1:25 kprof:c4r:k_spatial_apply:102:25 kprof:mesh_anim:k_bvh_level:17:25 > /dev/null 2>&1
+bash tools/gpu_run.sh $TAG kprof:c3:k_shift_solve:4:25 kprof:c2r:k_shift_finish:4:25 kprof:t1080b64:k_shift_finish:8:25 kprof:t1080b64:k_shift_solve:8:25 kprof:t1080b64:k_temporal_apply:8:25 > /dev/null 2>&1
 python - <<PY
 import json
 p='profiles/kernel_profile.json'; d=json.load(open(p)); n=json.load(open('$O/kernel_profile.json'))
