@@ -167,3 +167,35 @@ def test_compact_rows_equal_full_rows(name):
         for stage in ("temporal", "spatial", "bin"):
             assert {k: v for k, v in x[stage].items() if k != "seconds"} == \
                    {k: v for k, v in y[stage].items() if k != "seconds"}
+
+
+def test_transient_1080p_bench_config_invariants():
+    """The bench's transient workload at its full size (t1080b64: cornell
+    1920x1080 x 64 bins, temporal reuse; the oracle cannot hold its 133 M
+    reservoirs): compact rows against full rows and many row batches against
+    the default batches give the same histogram bits and counters, and every
+    frame's shift counters are self-consistent (success <= newton_ok <= solves
+    <= attempts)."""
+    import bench
+    scene_name, w, h, cfg, _ = bench.WORKLOADS["t1080b64"]
+    cfg = RenderConfig(**{**cfg.__dict__, "frames": 4})
+    sd = scenes.bundled(scene_name, w, h)
+
+    def run(**env):
+        with _env(**env):
+            out = Renderer(0).render_transient(sd, cfg)
+        return out.hist.rgb, out.stats
+
+    a, sa = run()
+    assert a.shape[:2] == (h, w) and a.max() > 0
+    for fs in sa:
+        t = fs["temporal"]
+        assert t["success"] <= t["newton_ok"] <= t["solves"] <= t["attempts"]
+    for env in ({"TOFR_COMPACT_ROWS": "0"}, {"TOFR_WAVE_CAP": "4000000"}):
+        b, sb = run(**env)
+        assert np.array_equal(a, b), env
+        del b
+        for x, y in zip(sa, sb):
+            for stage in ("temporal", "spatial", "bin"):
+                assert {k: v for k, v in x[stage].items() if k != "seconds"} == \
+                       {k: v for k, v in y[stage].items() if k != "seconds"}, env
