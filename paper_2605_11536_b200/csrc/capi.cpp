@@ -1705,7 +1705,8 @@ int tofr_gpu_session_read_image_async(tofr_session* ss, double* pinned_image, in
                               scale, rows_base<double>(stage, ss->y0, size_t(ss->W) * 3), st);
             ck(cudaGetLastError(), "hist image");
         } else {
-            ck(cudaMemcpyAsync(stage.p, ss->image.p, bytes, cudaMemcpyDeviceToDevice, st), "d2d");
+            launch_copy_f64(ss->image.as<double>(), bytes / 8, stage.as<double>(), st);
+            ck(cudaGetLastError(), "image copy");
         }
         ck(cudaEventRecord(ss->staged_ev[slot], st), "event");
         ck(cudaStreamWaitEvent(ss->copy_stream, ss->staged_ev[slot], 0), "wait");

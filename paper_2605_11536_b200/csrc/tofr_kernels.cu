@@ -1577,6 +1577,22 @@ void launch_scale3(const double* a, size_t n_pixels, double scale, double* out, 
     k_scale3<<<grid_for(n_pixels * 3, 256), 256, 0, s>>>(a, n_pixels * 3, scale, out);
 }
 
+// device-to-device copy of an image on the SMs (the copy engine's D2D path
+// measured several times slower, on the frame's critical path)
+__global__ void k_copy_f64(const double* a, size_t n, double* out) {
+    const size_t n2 = n / 2;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    double2* o2 = reinterpret_cast<double2*>(out);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n2; i += size_t(gridDim.x) * blockDim.x)
+        __stcs(&o2[i], __ldcs(&a2[i]));
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) out[n - 1] = a[n - 1];
+}
+void launch_copy_f64(const double* a, size_t n, double* out, cudaStream_t s) {
+    if (!n) return;
+    KScope ks("k_copy_f64", s);
+    k_copy_f64<<<grid_for(n / 2 + 1, 256), 256, 0, s>>>(a, n, out);
+}
+
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
                       double width, int spp, uint64_t frame_key, double* mean, double* se, unsigned long long* q,
                       cudaStream_t s) {

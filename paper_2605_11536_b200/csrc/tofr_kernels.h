@@ -208,6 +208,7 @@ void launch_shade_transient(ResStore cur, const Band& bd, int W, const HistSpec&
 void launch_hist_plain(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
                        int m_init, int frame_idx, double* hist, double* img, unsigned long long* q,
                        cudaStream_t s);
+void launch_copy_f64(const double* a, size_t n, double* out, cudaStream_t s);  // 16 B aligned
 void launch_scale3(const double* a, size_t n_pixels, double scale, double* out, cudaStream_t s);
 void launch_reference(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
                       double width, int spp, uint64_t frame_key, double* mean, double* se, unsigned long long* q,
