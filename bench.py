@@ -66,6 +66,14 @@ WORKLOADS = {
             RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, temporal=True, spatial_passes=1, spatial_neighbors=3,
                          spatial_radius=10, m_cap=20, max_depth=6, seed=1),
             "C3': cornell_wide 1920x1080 gated tau=6.0 dtau=0.0173, m_init 1, temporal + 1x3 spatial r10"),
+    # the paper's shrink initialisation (wide-gate RIS, shrink_map to the fine
+    # gate) on C3' (per-item init kernel, k_init_gated)
+    "c3w_shrink": ("cornell_wide", 1920, 1080,
+                   RenderConfig(gate=_gate(6.0, 0.0173), m_init=1, init=F.INIT_SHRINK, shrink_k=10.0, shrink_r=1.0,
+                                temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=10, m_cap=20,
+                                max_depth=6, seed=1),
+                   "C3' with shrink initialisation (K 10, R 1): cornell_wide 1920x1080 gated tau=6.0 dtau=0.0173, "
+                   "temporal + 1x3 spatial r10"),
     "c5": ("cornell_wide", 1920, 1080,
            RenderConfig(gate=_gate(6.0, 0.0173), gate_step=0.01, m_init=1, temporal=True, spatial_passes=1,
                         spatial_neighbors=3, spatial_radius=10, m_cap=20, max_depth=6, seed=1),
@@ -82,6 +90,13 @@ WORKLOADS = {
             RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=1,
                          temporal=True, m_cap=20, max_depth=6, seed=1),
             "C2(ii): cornell 512x512 transient 256 bins [8,20), render_transient reservoirs, temporal reuse"),
+    # C2(ii) with the optional +-1 bin reuse stage (pipeline.hpp:273-299; per-item
+    # kernel k_binreuse)
+    "c2r_bin": ("cornell", 512, 512,
+                RenderConfig(mode=F.MODE_TRANSIENT, bins=256, hist_t0=8.0, hist_bin_width=0.046875, m_init=1,
+                             temporal=True, bin_reuse=True, m_cap=20, max_depth=6, seed=1),
+                "C2(ii) + bin reuse: cornell 512x512 transient 256 bins [8,20), render_transient reservoirs, "
+                "temporal reuse then +-1 bin reuse"),
     "c4p": ("boxes_doppler", 1920, 1080,
             RenderConfig(mode=F.MODE_TRANSIENT, bins=1024, hist_t0=7.0, hist_bin_width=0.01953125, m_init=1,
                          max_depth=8, seed=1),
@@ -167,6 +182,8 @@ KERNEL_BYTES = {
     "k_spatial_prep_fwd": ("item", 16),
     "k_spatial_prep_inv": ("item", 16 + 16),
     "k_spatial_apply": ("merge", 3 * R_BYTES),
+    # per-item +-1 bin reuse: the three headers (own, b-1, b+1) + the output record
+    "k_binreuse": ("item", 3 * 16 + R_BYTES),
     "k_shade_gated": ("pixel", 24 + 12 + 24),
     "k_shade_transient": ("item", 16 + 24),
     "k_gbuffer": ("pixel", GHIT_BYTES),

@@ -720,9 +720,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             const char* rv = std::getenv("TOFR_REUSE");
             size_t own_items = s->owned_pixels() * s->B;
             size_t nj = size_t(std::max(0, cfg->spatial_neighbors));
-            s->wave = (s->has_temporal || s->has_spatial) && !(rv && std::strcmp(rv, "legacy") == 0);
+            s->wave = (s->has_temporal || s->has_spatial || s->has_bin) && !(rv && std::strcmp(rv, "legacy") == 0);
             if (s->wave) {
                 size_t per = wave_jobs_per_item(s->has_spatial ? cfg->spatial_neighbors : 0);
+                if (s->has_bin) per = std::max<size_t>(per, 3);  // bin reuse: 2 forward + 1 inverse
                 size_t cap = per * own_items;
                 // 64 M jobs (38 GB) when a quarter of the free memory holds them, else 32 M;
                 // larger stages run in row batches (wave_batches)
@@ -740,7 +741,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_jobs.ensure(cap * kJobChunks * 16);
                 s->wv_out.ensure(cap * kResChunks * 16);
                 s->wv_ctl.ensure(16);
-                s->wv_map_a.ensure(std::max<size_t>(1, nj) * own_items * sizeof(uint32_t));
+                s->wv_map_a.ensure(std::max<size_t>(s->has_bin ? 2 : 1, nj) * own_items * sizeof(uint32_t));
                 s->wv_map_b.ensure(own_items * sizeof(uint32_t));
                 s->wv_tsrc.ensure(own_items * sizeof(uint64_t));
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
@@ -1050,7 +1051,15 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         if (piped) cudaEventRecord(s->ev_temporal[set], stream);
         if (s->transient && c.bin_reuse) {
             reset_store(s, s->spare, stream);
-            launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare], sl), ctr + 2 * SC_COUNT, q, stream);
+            if (s->wave) {  // per pixel: no halo; 2 forward + 1 inverse job per item
+                for_row_batches(bd, wave_batches(s, 3), [&](const Band& sb) {
+                    launch_binreuse_wave(F, sb, g, pc, cg, f, cur, store_of(s, s->res[s->spare], sl), wv,
+                                         ctr + 2 * SC_COUNT, q, stream);
+                });
+            } else {
+                launch_binreuse(F, bd, g, pc, h, f, cur, store_of(s, s->res[s->spare], sl), ctr + 2 * SC_COUNT, q,
+                                stream);
+            }
             std::swap(s->cur, s->spare);
             cur = store_of(s, s->res[s->cur], sl);
         }

@@ -198,6 +198,11 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
                     const SpatialParams& sp, int pass, int frame_idx, ResStore src, ResStore dst,
                     const WorkOrder& wo, const SpatialScratch* sc, unsigned long long* ctr, unsigned long long* q,
                     cudaStream_t s);
+// bin reuse on the wavefront shift engine (tofr_wave.cu); src / dst: the stage's
+// input and output grids
+void launch_binreuse_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                          int frame_idx, ResStore src, ResStore dst, const WaveScratch& ws, unsigned long long* ctr,
+                          unsigned long long* q, cudaStream_t s);
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
                      int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, unsigned long long* q,
                      cudaStream_t s);

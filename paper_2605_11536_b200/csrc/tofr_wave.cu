@@ -1638,6 +1638,139 @@ __global__ void __launch_bounds__(256, TOFR_APPLY_MINB) k_spatial_apply(FrameVie
 }
 
 // ---------------------------------------------------------------------------
+// bin reuse (stage::bin_reuse, pipeline.hpp:273-299): every pixel-bin merges
+// bins b - 1 and b + 1 of its own pixel, in that order, on the spatial pass's
+// scheme -- the forward shifts of both neighbours in one batch, then per
+// neighbour j the inverse shift of the current output, the shifts, the merge.
+// A shift between bins keeps the pixel (stored prefix) and moves the path
+// length by the bin pitch (the Newton target's gate delta).
+
+// neighbour j (0: b - 1, 1: b + 1) of item p * B + b; false when outside the
+// bins or empty of confidence (bin_reuse skips src.M <= 0)
+__device__ __forceinline__ bool bin_neighbor(int B, size_t p, int b, int j, const ResStore& src, int& nb,
+                                             size_t& si) {
+    nb = j == 0 ? b - 1 : b + 1;
+    if (nb < 0 || nb >= B) return false;
+    si = p * size_t(B) + size_t(nb);
+    return ld2(src, 0, si).y > 0;
+}
+
+__global__ void k_bin_prep_fwd(Band bd, int W, GateGrid gate, ResStore src_grid, WaveScratch ws) {
+    const int B = gate.h.bins;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        size_t p = it / B;
+        int b = int(it % B);
+        int px = int(p % W), py = int(p / W);
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        for (int j = 0; j < 2; ++j) {
+            int nb = 0;
+            size_t si = 0;
+            // a forward shift attempt per non-empty neighbour bin (counted)
+            bool want = live && bin_neighbor(B, p, b, j, src_grid, nb, si) && ld2(src_grid, 0, si).x > 0;
+            uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
+            if (k != kNoJob) {
+                double sc, sw;
+                gate_of(gate, nb, sc, sw);
+                job_put(ws.q, k, si, JOB_FULL | JOB_COUNT, px, py, px, py, sc, dc, dw);
+            }
+            if (live) ws.map_a[size_t(j) * n + i] = k;
+        }
+    }
+}
+
+__global__ void k_bin_prep_inv(Band bd, int W, PathCfg cfg, GateGrid gate, int j, ResStore src_grid,
+                               ResStore dst_grid, WaveScratch ws) {
+    const int B = gate.h.bins;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
+    const ResStore& out_grid = j == 0 ? src_grid : dst_grid;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        size_t p = it / B;
+        int b = int(it % B);
+        int px = int(p % W), py = int(p / W);
+        int nb = 0;
+        size_t si = 0;
+        bool want = false, merge = false;
+        if (live) {
+            if (!bin_neighbor(B, p, b, j, src_grid, nb, si)) {
+                if (j == 0) {  // the output starts as the stage input
+                    double2 c0 = ld2(src_grid, 0, it);
+                    if (c0.x > 0)
+                        copy_res(src_grid, dst_grid, it, c0.x, c0.y, false);
+                    else
+                        res_store_w(dst_grid, it, 0.0, c0.y);
+                    ws.rng_ctr[i] = 0;
+                }
+            } else {
+                double2 o0 = ld2(out_grid, 0, it), s0 = ld2(src_grid, 0, si);
+                want = o0.x > 0;
+                merge = want || s0.x > 0;
+                if (!merge) {  // both empty: the merge only adds the confidences (no RNG draw)
+                    res_store_w(dst_grid, it, 0.0, dmin(o0.y + s0.y, cfg.m_cap));
+                    if (j == 0) ws.rng_ctr[i] = 0;
+                }
+            }
+        }
+        uint32_t k = block_append_jobs(ws, uint32_t(want), merge, uint32_t(i), bd.err, cfg.work, sh);
+        if (k != kNoJob) {
+            double dc, dw, sc, sw;
+            gate_of(gate, b, dc, dw);
+            gate_of(gate, nb, sc, sw);
+            job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, px, py, dc, sc, dw);
+            ws.map_b[i] = k;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, TOFR_APPLY_MINB)
+    k_bin_apply(Band bd, int W, PathCfg cfg, GateGrid gate, int j, int frame_idx, ResStore src_grid,
+                ResStore dst_grid, WaveScratch ws) {
+    const int B = gate.h.bins;
+    size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
+    uint32_t cnt = ws.q.ctl[3];
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < cnt; l += gridDim.x * blockDim.x) {
+        size_t i = ws.mlist[l], it = base + i;
+        size_t p = it / B;
+        int b = int(it % B);
+        int nb = 0;
+        size_t si = 0;
+        bin_neighbor(B, p, b, j, src_grid, nb, si);
+        Res out, src;
+        res_head_phat(j == 0 ? src_grid : dst_grid, it, out);
+        res_head_phat(src_grid, si, src);
+        double dc, dw;
+        gate_of(gate, b, dc, dw);
+        MergeShift ms{0, 1.0, 0.0};
+        Sample mapped;
+        double mgv = 0;
+        uint32_t kf = src.has ? ws.map_a[size_t(j) * n + i] : kNoJob;
+        fwd_output(ws.q, kf, 0, ms, mapped, mgv);
+        ms.phat_src_of_dst = inv_output(ws.q, out.has ? ws.map_b[i] : kNoJob);
+        Rng rng = rng_make(cfg.seed, uint64_t(frame_idx), uint64_t(p), uint64_t(b), 12);
+        if (j > 0) rng.ctr = ws.rng_ctr[i];
+        int which = gris_merge(out, src, ms, mapped, mgv, dc, dw, cfg.m_cap, rng);
+        if (which == 2)
+            put_mapped(ws.q.out, kf, dst_grid, it, out.W, out.M, out.phat, false);
+        else if (which == 1 && j == 0)
+            copy_res(src_grid, dst_grid, it, out.W, out.M, false);
+        else  // kept in place (j > 0) or empty
+            res_store_w(dst_grid, it, out.W, out.M);
+        if (j == 0) ws.rng_ctr[i] = rng.ctr;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // queue control and launchers
 
 // op 0: empty queue; op 1: mark the end (the next batch starts after it);
@@ -1897,6 +2030,41 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
         {
             KScope ks("k_spatial_apply", s);
             k_spatial_apply<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+        }
+    }
+}
+
+void launch_binreuse_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
+                          int frame_idx, ResStore src, ResStore dst, const WaveScratch& ws, unsigned long long* ctr,
+                          unsigned long long* q, cudaStream_t s) {
+    const int W = F.cam.w;
+    size_t n = size_t(bd.y1 - bd.y0) * W * gg.h.bins;
+    if (!n) return;
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    }
+    {
+        KScope ks("k_bin_prep_fwd", s);
+        k_bin_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(bd, W, gg, src, ws);
+    }
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 3);
+    }
+    for (int j = 0; j < 2; ++j) {
+        if (j > 0) {
+            KScope ks("k_queue_ctl", s);
+            k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 2);
+        }
+        {
+            KScope ks("k_bin_prep_inv", s);
+            k_bin_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(bd, W, cfg, gg, j, src, dst, ws);
+        }
+        run_shifts(F, F, g, g, src, dst, ws.q, ws.ov, cfg, ctr, q, s);
+        {
+            KScope ks("k_bin_apply", s);
+            k_bin_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, W, cfg, gg, j, frame_idx, src, dst, ws);
         }
     }
 }

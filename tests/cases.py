@@ -86,6 +86,15 @@ CASES = {
                        RenderConfig(mode=F.MODE_TRANSIENT, bins=16, hist_t0=5.0, hist_bin_width=0.25, m_init=2,
                                     temporal=True, bin_reuse=True, spatial_passes=1, spatial_neighbors=2,
                                     spatial_radius=3, frames=2), "transient"),
+    # bin reuse after temporal reuse, no spatial pass (the wavefront bin stage
+    # alone), and on moving geometry
+    "transient_bin_reuse": (lambda: scenes.bundled("cornell", 24),
+                            RenderConfig(mode=F.MODE_TRANSIENT, bins=32, hist_t0=8.0, hist_bin_width=0.375,
+                                         m_init=2, temporal=True, bin_reuse=True, frames=3), "transient"),
+    "transient_bin_reuse_animated": (lambda: scenes.bundled("boxes_doppler", 20),
+                                     RenderConfig(mode=F.MODE_TRANSIENT, bins=24, hist_t0=7.0, hist_bin_width=0.5,
+                                                  m_init=2, temporal=True, bin_reuse=True, max_depth=8, frames=3),
+                                     "transient"),
     "transient_b1_equals_gated": (lambda: scenes.bundled("cornell", 24),
                                   RenderConfig(mode=F.MODE_TRANSIENT, bins=1, hist_t0=10.0 - 0.25,
                                                hist_bin_width=0.5, m_init=4, spatial_passes=1,
