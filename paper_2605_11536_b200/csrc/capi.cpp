@@ -215,6 +215,10 @@ struct tofr_session {
     // wavefront reuse (tofr_wave.cu; TOFR_REUSE=legacy selects the per-item kernels)
     bool wave = false;
     DevBuf wv_jobs, wv_out, wv_ctl, wv_map_a, wv_map_b, wv_tsrc, wv_rng, wv_mlist;
+    // shrink initialiser on the wavefront engine: the rough (wide-gate) grid and
+    // the pick stream's counter per pixel between the RIS runs and the merge
+    bool shrink_wave = false;
+    DevBuf shrink_rough, shrink_pick;
     size_t wv_cap = 0;
     DevBuf row_jobs;          // per-row shift-job bounds of a stage (adaptive row batches)
     size_t batches_seen = 0;  // most row batches one stage took
@@ -466,6 +470,7 @@ PathCfg path_cfg(const tofr_render_config& c, double center, double width, const
         const char* wc = std::getenv("TOFR_WALK_CUTOFF");
         p.walk_cutoff = (wc && wc[0] == '0') ? 0 : 1;
     }
+    p.shrink_k = c.shrink_k;
     p.work = nullptr;
     for (const HMaterial& m : sc.materials)
         if (!m.reconnectable()) p.replay = 1;
@@ -720,7 +725,12 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             const char* rv = std::getenv("TOFR_REUSE");
             size_t own_items = s->owned_pixels() * s->B;
             size_t nj = size_t(std::max(0, cfg->spatial_neighbors));
-            s->wave = (s->has_temporal || s->has_spatial || s->has_bin) && !(rv && std::strcmp(rv, "legacy") == 0);
+            const char* tv = std::getenv("TOFR_TRACE");
+            const bool shrink = !s->transient && cfg->init_mode == TOFR_INIT_SHRINK &&
+                                cfg->gate_kind == TOFR_GATE_LENGTH && !(tv && std::strcmp(tv, "legacy") == 0);
+            s->wave = (s->has_temporal || s->has_spatial || s->has_bin || shrink) &&
+                      !(rv && std::strcmp(rv, "legacy") == 0);
+            s->shrink_wave = shrink && s->wave && !s->sparse;
             if (s->wave) {
                 size_t per = wave_jobs_per_item(s->has_spatial ? cfg->spatial_neighbors : 0);
                 if (s->has_bin) per = std::max<size_t>(per, 3);  // bin reuse: 2 forward + 1 inverse
@@ -747,6 +757,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 s->wv_rng.ensure(own_items * sizeof(uint64_t));
                 s->wv_mlist.ensure(own_items * sizeof(uint32_t));
                 s->wv_nbr.ensure(std::max<size_t>(1, nj) * s->owned_pixels() * sizeof(uint32_t));
+                if (s->shrink_wave) {
+                    s->shrink_rough.ensure(rb);
+                    s->shrink_pick.ensure(s->owned_pixels() * sizeof(uint64_t));
+                }
                 // opt-in (TOFR_OVERLAP=1): measured 2-7% slower -- the finish warps
                 // take issue slots from the tail's serial Newton chains
                 const char* ovs = std::getenv("TOFR_OVERLAP");
@@ -1019,16 +1033,43 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         InitParams ip{vel ? int(INIT_DIRECT) : c.init_mode, c.m_init, center, width, c.shrink_k, c.shrink_r};
         reset_store(s, s->cur, fs);
         ResStore cur = store_of(s, s->res[s->cur], sl);
-        if (s->transient)
+        // shrink initialiser (pipeline.hpp:137-183) on the wavefront engine: the
+        // rough and fine RIS runs here, the shrink_map shifts and the merge on
+        // the main stream below (they use the stage shift queue)
+        int shrink_fine = -1;
+        ResStore rough{};
+        if (s->transient) {
             launch_init_transient(F, bd, g, pc, ip, h, f, cur, q_side, fs);
-        else
+        } else if (s->shrink_wave && ip.mode == INIT_SHRINK) {
+            int m_rough = int(std::llround(ip.shrink_r * ip.m_init));
+            m_rough = std::min(std::max(m_rough, 0), ip.m_init);
+            const int m_fine = ip.m_init - m_rough;
+            uint64_t* pick = s->shrink_pick.as<uint64_t>();
+            if (m_rough == 0 || !(ip.shrink_k >= 1)) {  // no rough candidates / K < 1: the fine RIS alone
+                if (m_rough == 0)
+                    launch_trace_gated_ris(F, bd, g, pc, ip.m_init, center, width, f, cur, nullptr, nullptr, q_side, fs);
+                else  // shrink_map refuses K < 1: every rough winner fails to map
+                    launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs, nullptr);
+            } else {
+                rough = ResStore{s->shrink_rough.as<double2>() - ptrdiff_t(size_t(s->r0) * s->W), s->items_stored()};
+                launch_trace_gated_ris(F, bd, g, pc, m_rough, center, width * ip.shrink_k, f, rough, nullptr, pick,
+                                       q_side, fs);
+                if (m_fine > 0)
+                    launch_trace_gated_ris(F, bd, g, pc, m_fine, center, width, f, cur, pick, pick, q_side, fs);
+                shrink_fine = m_fine;
+            }
+        } else {
             launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs, ell_scratch(s, pc, ip));
+        }
         cudaEventRecord(ev[1], fs);
         if (piped) {  // the main stream continues once this frame's reservoirs exist
             cudaEventRecord(s->ev_init[set], fs);
             cudaStreamWaitEvent(stream, s->ev_init[set], 0);
             ck(cudaMemsetAsync(ctr, 0, (3 * SC_COUNT + 1) * sizeof(unsigned long long), stream), "memset");
         }
+        if (shrink_fine >= 0)
+            launch_shrink_wave(F, bd, g, pc, center, width, shrink_fine, f, rough, cur, s->shrink_pick.as<uint64_t>(),
+                               wv, ctr + 0 * SC_COUNT, q, stream);
         GateGrid cg{s->transient ? 1 : 0, center, width, h};
         if (c.temporal && f > 0) {
             GateGrid pg{s->transient ? 1 : 0, s->prev_center, s->prev_width, h};

@@ -107,6 +107,11 @@ enum : uint32_t {
     JOB_DST1 = 4u,    // destination domain is frame 1
     JOB_FULL = 8u,    // output the mapped record (else only p-hat of the source gate)
     JOB_COUNT = 16u,  // accumulate the shift counters (forward shifts)
+    // shrink_map (shiftmap.hpp:789-876) instead of shift_sample: same pixel and
+    // frame, Newton target L0 + (len - L0) / K (JOB_FULL: forward) or * K
+    // (inverse) with L0 = the job's dc, Jacobian * 1/K or * K after the clamp,
+    // inverse p-hat on the K-times wider gate
+    JOB_SHRINK = 32u,
 };
 constexpr uint32_t kNoJob = 0xffffffffu;
 
@@ -203,6 +208,16 @@ void launch_spatial(const FrameView& F, const Band& bd, const GHit* g, const Pat
 void launch_binreuse_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const GateGrid& gg,
                           int frame_idx, ResStore src, ResStore dst, const WaveScratch& ws, unsigned long long* ctr,
                           unsigned long long* q, cudaStream_t s);
+// shrink initialiser on the wavefront engine: the two RIS runs (k_trace, the
+// pick stream's counter carried in pick_in / pick_out), then the shrink_map
+// jobs and the per-pixel merge into `fine` (tofr_wave.cu)
+void launch_trace_gated_ris(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int trees,
+                            double center, double width, int frame_idx, ResStore cur, const uint64_t* pick_in,
+                            uint64_t* pick_out, unsigned long long* q, cudaStream_t s);
+void launch_shrink_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
+                        double width, int m_fine, int frame_idx, ResStore rough, ResStore fine,
+                        const uint64_t* pick_ctr, const WaveScratch& ws, unsigned long long* ctr,
+                        unsigned long long* q, cudaStream_t s);
 void launch_binreuse(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, const HistSpec& h,
                      int frame_idx, ResStore src, ResStore dst, unsigned long long* ctr, unsigned long long* q,
                      cudaStream_t s);

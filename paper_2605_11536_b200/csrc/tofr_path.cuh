@@ -106,6 +106,7 @@ struct PathCfg {
     // end a path tree once its length passes the sink's reach (no later
     // candidate can be wanted; same candidates, fewer rays; TOFR_WALK_CUTOFF=0: off)
     int walk_cutoff;
+    double shrink_k;           // shrink initialiser's gate widening K (JOB_SHRINK jobs)
     unsigned long long* work;  // device work counters [WK_COUNT] (may be null)
     // per-image-row shift cost (Newton iterations + 4 per job whose
     // destination lies in the row; null = off): the load-balancing probe of

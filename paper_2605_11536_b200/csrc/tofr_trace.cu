@@ -64,11 +64,18 @@ struct GatedSink {
     int has;
     Rng pick;
     size_t item;
+    // the pick stream's counter carried between RIS runs of one pixel (the
+    // shrink initialiser's rough then fine runs share the stream): read at
+    // begin, written at end, indexed by item - pbase (null: a fresh stream)
+    const uint64_t* pick_in = nullptr;
+    uint64_t* pick_out = nullptr;
+    size_t pbase = 0;
     __device__ void begin(const PathCfg& cfg, uint64_t fk, uint64_t pix, size_t p, int) {
         w_sum = 0;
         phat = 0;
         has = 0;
         pick = rng_make(cfg.seed, fk, pix, 0, 9);
+        if (pick_in) pick.ctr = pick_in[p - pbase];
         item = p;
     }
     __device__ void tree_begin() {}
@@ -104,6 +111,7 @@ struct GatedSink {
     __device__ void end() {
         double W = (has && phat > 0) ? w_sum / phat : 0;
         res_store_w(dense(cur), item, W, 1.0);
+        if (pick_out) pick_out[item - pbase] = pick.ctr;
     }
     __device__ void flush(unsigned long long*) {}
 };
@@ -523,6 +531,20 @@ void launch_trace_gated(const FrameView& F, const Band& bd, const GHit* g, const
         run(GatedSink<true>{}, std::true_type{});
     else
         run(GatedSink<false>{}, std::false_type{});
+}
+
+void launch_trace_gated_ris(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int trees,
+                            double center, double width, int frame_idx, ResStore cur, const uint64_t* pick_in,
+                            uint64_t* pick_out, unsigned long long* q, cudaStream_t s) {
+    GatedSink<false> sk{};
+    sk.cur = cur;
+    sk.center = center;
+    sk.width = width;
+    sk.inv = 1.0 / trees;
+    sk.pick_in = pick_in;
+    sk.pick_out = pick_out;
+    sk.pbase = size_t(bd.y0) * F.cam.w;
+    launch_trace<GatedSink<false>, false>("k_trace_gated", F, bd, g, cfg, trees, uint64_t(frame_idx), sk, q, s);
 }
 
 void launch_trace_transient(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, int m_init,

@@ -876,7 +876,8 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                     } else {
                         spos = rec_p(st, jb.item);
                         stri = mt.ptri;
-                        if (!cfg.newton) {
+                        const bool shrink = (jb.meta & JOB_SHRINK) != 0;
+                        if (!cfg.newton && !shrink) {  // shrink_map always solves
                             sol_put(q, job, spos, stri, 1.0, 3);
                         } else {
                             p1 = pre.p1;
@@ -885,8 +886,16 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                             double src_total = VEL ? ld2(st, 22, jb.item).x : ld2(st, 1, jb.item).y;
                             double prefix_part = VEL ? pre.u : pre.len;
                             double suffix_part = VEL ? suf.u : suf.len;
-                            double gate_delta = jb.dc - jb.sc;
-                            double target_local = src_total + gate_delta - prefix_part - suffix_part;
+                            double target_local;
+                            if (shrink) {  // shrink_map: contract (expand) about the gate centre L0
+                                const double L0 = jb.dc, K = cfg.shrink_k;
+                                const double target_total =
+                                    (jb.meta & JOB_FULL) ? (src_total - L0) / K + L0 : (src_total - L0) * K + L0;
+                                target_local = target_total - prefix_part - suffix_part;
+                            } else {
+                                double gate_delta = jb.dc - jb.sc;
+                                target_local = src_total + gate_delta - prefix_part - suffix_part;
+                            }
                             if (VEL) {
                                 vobj1 = F.tri[pre.tri1].obj;
                                 vobj2 = suf.vobj;
@@ -1208,6 +1217,8 @@ __global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
             out_fail(q, k);
             continue;
         }
+        const bool shrink = (jb.meta & JOB_SHRINK) != 0;
+        if (shrink) jac = jac * ((jb.meta & JOB_FULL) ? 1.0 / cfg.shrink_k : cfg.shrink_k);
         // rebuild_sample
         V3 d1 = ppos - pre.p1;
         double l1 = norm(d1);
@@ -1258,7 +1269,8 @@ __global__ void __launch_bounds__(128, TOFR_FINISH_MINB)
         double gv = gate_value(VEL, len, u_total);
         if (count && gate_w(jb.dc, jb.dw, gv) > 0 && luminance(f) > 0) ctr.v[SC_SUCCESS]++;
         if (!(jb.meta & JOB_FULL)) {  // inverse shift: p-hat of the source gate times |J|
-            st2(q.out, 0, k, luminance(f) * gate_w(jb.dc, jb.dw, gv) * jac, 1.0);
+            const double sw = shrink ? jb.dw * cfg.shrink_k : jb.dw;  // shrink: the wide gate
+            st2(q.out, 0, k, luminance(f) * gate_w(jb.dc, sw, gv) * jac, 1.0);
             continue;
         }
         // mapped record (rebuild_sample's record update, stored as res_store would)
@@ -1771,6 +1783,85 @@ __global__ void __launch_bounds__(256, TOFR_APPLY_MINB)
 }
 
 // ---------------------------------------------------------------------------
+// shrink initialiser (initial_sampling's shrink branch, pipeline.hpp:137-183):
+// the rough (wide-gate) and fine RIS reservoirs come from two k_trace runs that
+// share the pixel's pick stream; here the rough winner's forward shrink_map and
+// the fine winner's inverse one run as shift jobs, then one merge per pixel.
+
+__global__ void k_shrink_prep(Band bd, int W, double center, double width, int m_fine, ResStore rough,
+                              ResStore fine, WaveScratch ws, unsigned long long* work) {
+    size_t base = size_t(bd.y0) * W, n = size_t(bd.y1 - bd.y0) * W;
+    size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    __shared__ uint32_t sh[33];
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+        bool live = i < n;
+        size_t it = base + (live ? i : 0);
+        int px = int(it % W), py = int(it / W);
+        const bool fwd = live && ld2(rough, 0, it).x > 0;
+        const bool inv = fwd && m_fine > 0 && ld2(fine, 0, it).x > 0;
+        uint32_t k = block_append_jobs(ws, uint32_t(fwd) + uint32_t(inv), false, uint32_t(i), bd.err, work, sh);
+        if (k != kNoJob) {
+            job_put(ws.q, k, it, JOB_FULL | JOB_SHRINK, px, py, px, py, center, center, width);
+            ws.map_a[i] = k;
+            if (inv) {
+                job_put(ws.q, k + 1, it, JOB_SHRINK | JOB_REC1, px, py, px, py, center, center, width);
+                ws.map_b[i] = k + 1;
+            }
+        }
+    }
+}
+
+__global__ void k_shrink_merge(Band bd, int W, PathCfg cfg, double center, double width, int m_fine, int frame_idx,
+                               ResStore rough, ResStore fine, WaveScratch ws, const uint64_t* pick_ctr) {
+    size_t base = size_t(bd.y0) * W, n = size_t(bd.y1 - bd.y0) * W;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        size_t it = base + i;
+        Res r, out;
+        res_head_phat(rough, it, r);
+        if (!r.has) {  // rough empty: the fine reservoir (M = 1) is the result
+            if (m_fine == 0) res_store_w(fine, it, 0.0, 1.0);
+            continue;
+        }
+        Rng pick = rng_make(cfg.seed, uint64_t(frame_idx), uint64_t(it), 0, 9);
+        pick.ctr = pick_ctr[i];
+        MergeShift ms{0, 1.0, 0.0};
+        Sample mapped;
+        double mgv = 0;
+        const uint32_t kf = ws.map_a[i];
+        fwd_output(ws.q, kf, 0, ms, mapped, mgv);
+        if (m_fine == 0) {  // every tree on the wide gate: one candidate, the mapped winner
+            double w_sum = 0, ph = 0;
+            int has = 0;
+            if (ms.valid) {
+                double pyv = luminance(mapped.f) * gate_w(center, width, mgv);
+                double w = pyv * r.W * ms.jac;
+                if (isfinite(w) && w > 0) {
+                    w_sum += w;
+                    if (rng_next(pick) * w_sum < w) {
+                        has = 1;
+                        ph = pyv;
+                    }
+                }
+            }
+            const double Wv = (has && ph > 0) ? w_sum / ph : 0;
+            if (has)
+                put_mapped(ws.q.out, kf, fine, it, Wv, 1.0, ph, false);
+            else
+                res_store_w(fine, it, Wv, 1.0);
+            continue;
+        }
+        res_head_phat(fine, it, out);
+        ms.phat_src_of_dst = inv_output(ws.q, out.has ? ws.map_b[i] : kNoJob);
+        int which = gris_merge(out, r, ms, mapped, mgv, center, width, cfg.m_cap, pick);
+        if (which == 2)  // the rough winner, contracted onto the fine gate
+            put_mapped(ws.q.out, kf, fine, it, out.W, out.M, out.phat, false);
+        else  // the fine winner kept in place, or empty
+            res_store_w(fine, it, out.W, out.M);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // queue control and launchers
 
 // op 0: empty queue; op 1: mark the end (the next batch starts after it);
@@ -2066,6 +2157,29 @@ void launch_binreuse_wave(const FrameView& F, const Band& bd, const GHit* g, con
             KScope ks("k_bin_apply", s);
             k_bin_apply<<<grid_n(n, 256), 256, 0, s>>>(bd, W, cfg, gg, j, frame_idx, src, dst, ws);
         }
+    }
+}
+
+void launch_shrink_wave(const FrameView& F, const Band& bd, const GHit* g, const PathCfg& cfg, double center,
+                        double width, int m_fine, int frame_idx, ResStore rough, ResStore fine,
+                        const uint64_t* pick_ctr, const WaveScratch& ws, unsigned long long* ctr,
+                        unsigned long long* q, cudaStream_t s) {
+    const int W = F.cam.w;
+    size_t n = size_t(bd.y1 - bd.y0) * W;
+    if (!n) return;
+    {
+        KScope ks("k_queue_ctl", s);
+        k_queue_ctl<<<1, 1, 0, s>>>(ws.q.ctl, 0);
+    }
+    {
+        KScope ks("k_shrink_prep", s);
+        k_shrink_prep<<<grid_n(n, 256), 256, 0, s>>>(bd, W, center, width, m_fine, rough, fine, ws, nullptr);
+    }
+    run_shifts(F, F, g, g, rough, fine, ws.q, ws.ov, cfg, ctr, q, s);
+    {
+        KScope ks("k_shrink_merge", s);
+        k_shrink_merge<<<grid_n(n, 256), 256, 0, s>>>(bd, W, cfg, center, width, m_fine, frame_idx, rough, fine, ws,
+                                                       pick_ctr);
     }
 }
 

@@ -72,6 +72,17 @@ CASES = {
     "shrink_r05": (lambda: scenes.bundled("cornell_wide", 32),
                    RenderConfig(gate=gate(6.0, 0.05), m_init=4, init=F.INIT_SHRINK, shrink_k=10, shrink_r=0.5),
                    "gated"),
+    # shrink initialiser under temporal + spatial reuse, on moving boxes, and
+    # with every tree on the fine gate (R = 0: the plain RIS)
+    "shrink_r05_reuse": (lambda: scenes.bundled("boxes_doppler", 28),
+                         RenderConfig(gate=gate(10.0, 0.3), m_init=3, init=F.INIT_SHRINK, shrink_k=4, shrink_r=0.5,
+                                      temporal=True, spatial_passes=1, spatial_neighbors=3, spatial_radius=4,
+                                      frames=3),
+                         "gated"),
+    "shrink_r0": (lambda: scenes.bundled("cornell_wide", 24),
+                  RenderConfig(gate=gate(6.0, 0.05), m_init=2, init=F.INIT_SHRINK, shrink_k=10, shrink_r=0.0,
+                               temporal=True, frames=2),
+                  "gated"),
     # transient
     "plain_cornell": (lambda: scenes.bundled("cornell", 32),
                       RenderConfig(mode=F.MODE_TRANSIENT, bins=64, hist_t0=8.0, hist_bin_width=0.1875, m_init=2,

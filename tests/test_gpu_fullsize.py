@@ -120,6 +120,7 @@ print(json.dumps(stats))
 
 @pytest.mark.parametrize("name", ["full_c3_boxes_doppler_1080p", "full_c1_cornell_256", "mirror_replay",
                                   "transient_full", "transient_bin_reuse", "transient_bin_reuse_animated",
+                                  "shrink_r1", "shrink_r05", "shrink_r05_reuse",
                                   "doppler_scene_reuse", "ellipsoidal_init",
                                   "ellipsoidal_collimated", "nlos_cornell_wide_256"])
 def test_wavefront_bit_identical_to_per_item_kernels(tmp_path, name):
