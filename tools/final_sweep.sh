@@ -13,7 +13,7 @@ for k,v in n.items(): v['source'] += ' [$TAG]'; d[k]=v
 json.dump(d, open(p,'w'), indent=1, sort_keys=True); json.dump(d, open('$O/kernel_profile_merged.json','w'), indent=1, sort_keys=True)
 PY
 timeout 900 python bench.py --steps 20 --warmup 25 > $O/bench_c3.json 2> $O/bench_c3.err
-for wl in c3d c3w c1 c2p c2r c4p t1080b64 t1080 nlos nlos_scan mesh mesh_anim; do
+for wl in c3d c3w c3w_shrink c1 c2p c2r c2r_bin c4p t1080b64 t1080 nlos nlos_scan mesh mesh_anim; do
   timeout 900 python bench.py --workload $wl --steps 20 --warmup 25 --no-cpu-baseline > $O/bench_$wl.json 2> $O/bench_$wl.err
 done
 timeout 900 python bench.py --workload c5 --steps 120 --warmup 25 --no-cpu-baseline > $O/bench_c5.json 2> $O/bench_c5.err
