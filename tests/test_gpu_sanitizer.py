@@ -84,6 +84,10 @@ def test_sanitizer_clean(tmp_path, tool, name):
     p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1200)
     log = p.stdout + p.stderr
     (tmp_path / "sanitizer.log").write_text(log)
+    if "child ok" not in log and "compute-sanitizer is closed" in log:
+        # some GPU pools disable the tool (runs under it left GPUs needing a
+        # reset); the recorded clean runs are profiles/r02/pytest_bands_sanitizer.log
+        pytest.skip(log.strip().splitlines()[0][:200])
     assert "child ok" in log, log[-3000:]
     assert p.returncode == 0, log[-3000:]
     clean = "ERROR SUMMARY: 0 errors" in log or "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" in log
