@@ -300,6 +300,13 @@ int tofr_gpu_dump_bvh_device(tofr_gpu* ctx, const tofr_scene* s, double frame, i
  * to cap records (3 u64 each) and resets the recorder */
 int tofr_gpu_debug_solve_profile(uint64_t* out, uint64_t cap, uint64_t* n);
 
+/* bounds-check self-test: one thread asks a 4-item grid for the pool row of
+ * item 5.  A checked build (-DTOFR_CHECK=1) traps (returns TOFR_ERR_CUDA and
+ * leaves the context unusable: call it in a throw-away process); the product
+ * build, which does no checks and touches no memory there, returns TOFR_OK
+ * with *checked = 0.  *checked = 1 when the library was built with checks. */
+int tofr_gpu_debug_check_selftest(tofr_gpu* ctx, int32_t* checked);
+
 /* measured FP64 throughput of the context's device (DFMA chains; GFLOP/s with
  * 2 flops per DFMA): the FP64 roofline's peak */
 int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops);

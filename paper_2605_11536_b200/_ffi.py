@@ -163,6 +163,7 @@ def _declare(lib) -> None:
     lib.tofr_gpu_dump_bvh_device.argtypes = [vp, vp, C.c_double, C.c_int32, P(C.c_double), P(C.c_int32),
                                              P(C.c_int32), C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_double)]
     lib.tofr_gpu_debug_solve_profile.argtypes = [P(C.c_uint64), C.c_uint64, P(C.c_uint64)]
+    lib.tofr_gpu_debug_check_selftest.argtypes = [vp, P(C.c_int32)]
     lib.tofr_gpu_probe_rays.argtypes = [vp, vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
                                         P(C.c_double), P(C.c_int32)]
     lib.tofr_scene_probe_rays_host.argtypes = [vp, C.c_double, P(C.c_double), C.c_int32, C.c_int32,
@@ -184,7 +185,7 @@ EXPORTED_SYMBOLS = (
     "tofr_gpu_session_link_halo", "tofr_gpu_session_halo_transport", "tofr_gpu_session_stage_totals", "tofr_gpu_session_create_plain",
     "tofr_gpu_session_read_histogram", "tofr_gpu_session_read_image_async", "tofr_gpu_session_wait_read", "tofr_gpu_session_work", "tofr_gpu_session_pool", "tofr_gpu_session_row_cost", "tofr_gpu_session_destroy",
     "tofr_gpu_kernel_timing", "tofr_gpu_kernel_launches", "tofr_gpu_kernel_times", "tofr_gpu_kernel_times_reset",
-    "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_fp64_peak", "tofr_gpu_dump_bvh_device", "tofr_gpu_debug_solve_profile", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
+    "tofr_fnv1a64", "tofr_gpu_selftest_div", "tofr_gpu_fp64_peak", "tofr_gpu_dump_bvh_device", "tofr_gpu_debug_solve_profile", "tofr_gpu_debug_check_selftest", "tofr_gpu_probe_rays", "tofr_scene_probe_rays_host", "tofr_scene_dump_bvh",
 )
 
 

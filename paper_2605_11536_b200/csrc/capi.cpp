@@ -323,9 +323,16 @@ const T* rows_base_c(const DevBuf& b, int row0, size_t per_row) {
 ResStore store_of(const tofr_session* s, const DevBuf& b, int frame_slot = -1) {
     size_t items = s->items_stored();
     ptrdiff_t off = ptrdiff_t(size_t(s->r0) * s->W * s->B);
-    if (!s->sparse) return ResStore{b.as<double2>() - off, items};
+    if (!s->sparse) {
+        ResStore st{b.as<double2>() - off, items};
+        st.ilo = size_t(off);
+        st.ihi = size_t(off) + items;
+        return st;
+    }
     int k = int(&b - &s->res[0]);
     ResStore st{b.as<double2>() - off, s->pool_rows + 2};
+    st.ilo = size_t(off);
+    st.ihi = size_t(off) + items;
     st.slot = s->res_slot[k].as<uint32_t>() - off;
     // chunk planes 1..23 follow the header plane; plane c at pool + c * stride
     st.pool = b.as<double2>() + items - ptrdiff_t(st.stride);
@@ -999,6 +1006,7 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         wv.q.jobs = s->wv_jobs.as<double2>();
         wv.q.cap = s->wv_cap;
         wv.q.out = ResStore{s->wv_out.as<double2>(), s->wv_cap};
+        wv.q.out.ihi = s->wv_cap;
         // mapped records land in compact grids only: their prefix-cache chunks
         // (5-9) would be dropped by put_mapped, so the job outputs skip them too
         wv.q.out.compact = s->compact_rows ? 1 : 0;
@@ -1052,6 +1060,8 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
                     launch_init_gated(F, bd, g, pc, ip, f, cur, q_side, fs, nullptr);
             } else {
                 rough = ResStore{s->shrink_rough.as<double2>() - ptrdiff_t(size_t(s->r0) * s->W), s->items_stored()};
+                rough.ilo = size_t(s->r0) * s->W;
+                rough.ihi = rough.ilo + s->items_stored();
                 launch_trace_gated_ris(F, bd, g, pc, m_rough, center, width * ip.shrink_k, f, rough, nullptr, pick,
                                        q_side, fs);
                 if (m_fine > 0)
@@ -1958,6 +1968,19 @@ int tofr_gpu_debug_solve_profile(uint64_t* out, uint64_t cap, uint64_t* n) {
     bool ok = debug_solve_profile(reinterpret_cast<unsigned long long*>(out), size_t(cap), &m);
     *n = m;
     return ok ? TOFR_OK : TOFR_ERR_UNSUPPORTED;
+}
+
+int tofr_gpu_debug_check_selftest(tofr_gpu* ctx, int32_t* checked) {
+    return guard(ctx, [&] {
+        if (!ctx || !checked) throw ScopeError(TOFR_ERR_INVALID, "bad arguments");
+        DevBuf out;
+        out.ensure(sizeof(unsigned long long));
+        *checked = launch_check_selftest(out.as<unsigned long long>(), ctx->stream);
+        ck(cudaStreamSynchronize(ctx->stream), "check selftest");
+        unsigned long long v = 0;
+        ck(cudaMemcpy(&v, out.p, sizeof(v), cudaMemcpyDeviceToHost), "check selftest");
+        if (v != 5) throw ScopeError(TOFR_ERR_CUDA, "check selftest: unexpected row");
+    });
 }
 
 int tofr_gpu_fp64_peak(tofr_gpu* ctx, double* gflops) {

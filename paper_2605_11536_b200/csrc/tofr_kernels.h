@@ -248,6 +248,8 @@ void launch_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad, cud
 // measured FP64 DFMA throughput of this device (GFLOP/s, 2 flops per DFMA)
 double measure_fp64_peak_gflops(cudaStream_t s);
 bool debug_solve_profile(unsigned long long* out, size_t cap, size_t* n);
+// bounds-check self-test (tofr_gpu_debug_check_selftest); returns TOFR_CHECK
+int launch_check_selftest(unsigned long long* out, cudaStream_t s);
 void launch_probe_rays(const FrameView& F, const double* rays, int n, int mode, double* out_t, int* out_tri,
                        cudaStream_t s);
 

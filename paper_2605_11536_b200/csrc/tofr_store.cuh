@@ -20,6 +20,8 @@
 //                              15: n2.x, n2.y
 #pragma once
 
+#include <cstdio>
+
 #include "tofr_path.cuh"
 
 namespace tofr_b200 {
@@ -72,19 +74,43 @@ struct ResStore {
     // is read with ld.global.cg, a volatile asm the compiler cannot merge, so
     // every chunk access would otherwise re-read it before its own load)
     size_t pin_item = ~size_t(0), pin_row = 0;
+    // global item range the grid holds (checked only in a -DTOFR_CHECK=1 build)
+    size_t ilo = 0, ihi = ~size_t(0);
 };
 
 #if defined(__CUDACC__)
 
+// Checked build (-DTOFR_CHECK=1, the `check` library variant): every grid,
+// pool-row and job-queue index is bounds-checked on the device; a failed check
+// prints its site and traps (the launch fails, the host call returns an error).
+#ifndef TOFR_CHECK
+#define TOFR_CHECK 0
+#endif
+#if TOFR_CHECK
+#define TOFR_CHK(cond)                                                                        \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("TOFR_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   int(blockIdx.x), int(threadIdx.x));                                       \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define TOFR_CHK(cond) ((void)0)
+#endif
+
 // pool row of item i for reading chunks >= 1 (the zero row when it has none)
 __device__ __forceinline__ size_t res_row(const ResStore& s, size_t i) {
+    TOFR_CHK(i >= s.ilo && i < s.ihi);
     if (s.slot == nullptr) return i;
     if (i == s.pin_item) return s.pin_row;
     uint32_t r = __ldcg(&s.slot[i]);
+    TOFR_CHK(r == kNoSlot || size_t(r) < s.stride - 2);
     return r == kNoSlot ? s.stride - 1 : size_t(r);
 }
 // pool row of item i for writing chunks >= 1 (allocated on first use)
 __device__ __forceinline__ size_t res_row_w(const ResStore& s, size_t i) {
+    TOFR_CHK(i >= s.ilo && i < s.ihi);
     if (s.slot == nullptr) return i;
     uint32_t r = __ldcg(&s.slot[i]);
     if (r == kNoSlot) {
@@ -111,11 +137,18 @@ __device__ __forceinline__ ResStore res_pin(const ResStore& s, size_t i) {
 // read as zero, writes are dropped -- and chunks >= 10 sit 5 planes lower)
 __device__ __forceinline__ bool res_derived_chunk(const ResStore& s, int c) { return s.compact && c >= 5 && c <= 9; }
 __device__ __forceinline__ int res_plane(const ResStore& s, int c) { return (s.compact && c >= 10) ? c - 5 : c; }
+__device__ __forceinline__ void res_chk_row(const ResStore& s, int c, size_t row) {
+    TOFR_CHK(c >= 0 && res_plane(s, c) < (s.slot ? s.planes - (s.compact ? 5 : 0) : kResChunks));
+    TOFR_CHK(s.slot ? row < s.stride : (row >= s.ilo && row < s.ihi));
+    (void)s, (void)c, (void)row;
+}
 __device__ __forceinline__ double2 ld2r(const ResStore& s, int c, size_t row) {
+    res_chk_row(s, c, row);
     if (res_derived_chunk(s, c)) return make_double2(0.0, 0.0);
     return __ldcg(&res_planes(s)[size_t(res_plane(s, c)) * s.stride + row]);
 }
 __device__ __forceinline__ void st2r(const ResStore& s, int c, size_t row, double2 v) {
+    res_chk_row(s, c, row);
     if (res_derived_chunk(s, c)) return;
     __stcg(&res_planes(s)[size_t(res_plane(s, c)) * s.stride + row], v);
 }
@@ -141,10 +174,12 @@ __device__ __forceinline__ PrefixCache res_prefix_derived(const ResStore& s, siz
 }
 
 __device__ __forceinline__ double2 ld2(const ResStore& s, int c, size_t i) {
+    TOFR_CHK(i >= s.ilo && i < s.ihi);
     if (c == 0) return __ldcg(&s.base[i]);
     return ld2r(s, c, res_row(s, i));
 }
 __device__ __forceinline__ void st2(const ResStore& s, int c, size_t i, double a, double b) {
+    TOFR_CHK(i >= s.ilo && i < s.ihi);
     if (c == 0)
         __stcg(&s.base[i], make_double2(a, b));
     else

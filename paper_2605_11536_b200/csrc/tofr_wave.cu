@@ -86,9 +86,11 @@ struct Job {
 };
 
 __device__ __forceinline__ double2 jld(const ShiftQueue& q, int c, uint32_t k) {
+    TOFR_CHK(c >= 0 && c < kJobChunks && size_t(k) < q.cap);
     return __ldcg(&q.jobs[size_t(c) * q.cap + k]);
 }
 __device__ __forceinline__ void jst(const ShiftQueue& q, int c, uint32_t k, double2 v) {
+    TOFR_CHK(c >= 0 && c < kJobChunks && size_t(k) < q.cap);
     __stcg(&q.jobs[size_t(c) * q.cap + k], v);
 }
 
@@ -1943,6 +1945,20 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
         lc.numAttrs = 1;
         cudaLaunchKernelEx(&lc, finish, F0, F1, g0, g1, st0, st1, q, cfg, ctr, fq);
     }
+}
+
+// an out-of-range item of a 4-item dense grid: traps in a TOFR_CHECK build
+// (res_row of a dense grid touches no memory, so the product build just
+// returns the index)
+__global__ void k_check_selftest(ResStore st, unsigned long long* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = res_row(st, 5);
+}
+int launch_check_selftest(unsigned long long* out, cudaStream_t s) {
+    ResStore st{nullptr, 4};
+    st.ilo = 0;
+    st.ihi = 4;
+    k_check_selftest<<<1, 32, 0, s>>>(st, out);
+    return TOFR_CHECK;
 }
 
 // solve profile of a TOFR_SOLVE_PROFILE build: copies min(n, cap) records

@@ -55,6 +55,8 @@ elif case == "reference":
     out = None
 if out is not None:
     assert out.image.max() > 0
+    import hashlib
+    print("image sha1", hashlib.sha1(out.image.tobytes()).hexdigest())
 print("child ok")
 """
 
