@@ -296,7 +296,7 @@ int tofr_gpu_dump_bvh_device(tofr_gpu* ctx, const tofr_scene* s, double frame, i
 
 /* diagnostic (a -DTOFR_SOLVE_PROFILE=1 build only, else TOFR_ERR_UNSUPPORTED):
  * per solved shift job {cycles from refill to finish, trial rounds | Newton
- * iterations << 32 | re-projection rays << 40, SM clock at finish}; copies up
+ * iterations << 32 | re-projection rays << 40, global timer (ns) at finish}; copies up
  * to cap records (3 u64 each) and resets the recorder */
 int tofr_gpu_debug_solve_profile(uint64_t* out, uint64_t cap, uint64_t* n);
 

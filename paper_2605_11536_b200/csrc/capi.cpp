@@ -184,9 +184,12 @@ struct tofr_session {
     // the frame's BVH built on the device (large animated meshes; wide light)
     bool device_bvh = false;
     std::unique_ptr<DeviceBvh> dbvh;
-    FrameSlot slot[2];
-    DevBuf res[3];
+    FrameSlot slot[3];
+    DevBuf res[4];
     int cur = 0, prev = 1, spare = 2;
+    // three-deep frame pipeline (gated sessions, see `side`): a fourth grid
+    // (index xg, -1 = none) and a third frame slot (nslots)
+    int xg = -1, nslots = 2;
     // sparse transient grids (tofr_store.cuh): slot map per grid, pool rows
     // handed out per grid ([3] u32), pool rows per grid (+2 reserved rows)
     bool sparse = false;
@@ -237,7 +240,11 @@ struct tofr_session {
     // done -- concurrently with frame f-1's spatial pass and shading on the
     // main stream.  They touch only the buffers frame f-1 no longer reads after
     // its temporal stage: the frame slot / G-buffer of frame f-2 and the grid
-    // that held frame f-2's final reservoirs.
+    // that held frame f-2's final reservoirs.  Gated sessions keep one frame
+    // more (a fourth grid, a third slot): frame f's side work then waits for
+    // frame f-2's temporal stage only, so it can also fill the SMs frame f-1's
+    // temporal shift batch leaves idle while its slowest Newton chains finish
+    // (TOFR_PIPE_DEPTH=2: the two-frame pipeline).
     cudaStream_t side = nullptr;
     cudaEvent_t ev_temporal[2] = {}, ev_init[2] = {};
     bool pending[2] = {false, false};
@@ -725,6 +732,19 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
         ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
         if (s->res[2].p) ck(cudaMemsetAsync(s->res[2].p, 0, rb, ctx->stream), "memset");
+        // only for frames staged in shared memory: a snapshot traversed from
+        // L2 (the 10^5-triangle mesh) measured 6% slower with a third frame's
+        // copy competing for the cache (profiles/r02/ab_pipe.txt)
+        size_t n_tris = 0;
+        for (const HObject& o : s->scene.objects) n_tris += o.local.size();
+        const bool staged = n_tris * (2 * sizeof(GNode) + sizeof(GTriIsect)) <= kSmemStageLimit;
+        const char* pdepth = std::getenv("TOFR_PIPE_DEPTH");
+        if (s->side && !s->transient && staged && !(pdepth && pdepth[0] == '2')) {
+            s->res[3].ensure(rb);
+            ck(cudaMemsetAsync(s->res[3].p, 0, rb, ctx->stream), "memset");
+            s->xg = 3;
+            s->nslots = 3;
+        }
         {
             // wavefront reuse: job queue of (N + 1) jobs per item for the spatial
             // pass (2 for temporal), bounded for the transient grids, whose
@@ -967,9 +987,15 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
     int f = s->f;
     int set = f & 1;
     flush_set(s, set);  // frame f-2: frees its event set and its staging buffer
-    int sl = f & 1, psl = sl ^ 1;
-    if (s->side && !s->plain && f > 0)  // frame f-1 no longer reads frame f-2's slot and grid
-        cudaStreamWaitEvent(s->side, s->ev_temporal[set ^ 1], 0);
+    int sl = f % s->nslots, psl = (f + s->nslots - 1) % s->nslots;
+    if (s->side && !s->plain) {
+        if (s->nslots == 3) {
+            if (f > 1)  // frame f-1 no longer reads frame f-3's slot and grid after frame f-2's temporal stage
+                cudaStreamWaitEvent(s->side, s->ev_temporal[set], 0);
+        } else if (f > 0) {  // frame f-1 no longer reads frame f-2's slot and grid
+            cudaStreamWaitEvent(s->side, s->ev_temporal[set ^ 1], 0);
+        }
+    }
     upload_frame(s, sl, c.frame0 + f, f, (s->side && !s->plain) ? s->side : stream);
     const FrameView& F = s->slot[sl].view;
     GHit* g_local = s->slot[sl].gbuf.as<GHit>();
@@ -1158,7 +1184,14 @@ void session_step(tofr_session* s, tofr_frame_stats* st) {
         // frame's temporal stage the neighbours' final reservoirs too
         if (prev_halo && c.temporal) exchange_halo(s, cur, -1);
         cudaEventRecord(ev[5], stream);
-        std::swap(s->cur, s->prev);  // bufs.flip()
+        if (s->xg >= 0) {  // bufs.flip() with a fourth grid: the next init writes frame f-2's final grid
+            const int fin = s->cur;
+            s->cur = s->xg;
+            s->xg = s->prev;
+            s->prev = fin;
+        } else {
+            std::swap(s->cur, s->prev);  // bufs.flip()
+        }
     }
     ck(cudaMemcpyAsync(&s->err_host[set], ctr + 3 * SC_COUNT, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        stream),

@@ -40,6 +40,9 @@
 #ifndef TOFR_TRACE_MINB
 #define TOFR_TRACE_MINB 4
 #endif
+#ifndef TOFR_TRACE_BLOCK
+#define TOFR_TRACE_BLOCK 128
+#endif
 
 
 namespace tofr_b200 {
@@ -239,7 +242,7 @@ struct RefSink2 {
 enum : int { ST_IDLE = 0, ST_NEE = 1, ST_EXT = 2, ST_SHADOW = 3, ST_EXTEND = 4 };
 
 template <class Sink, bool VEL>
-__global__ void __launch_bounds__(128, TOFR_TRACE_MINB)
+__global__ void __launch_bounds__(TOFR_TRACE_BLOCK, TOFR_TRACE_MINB * 128 / TOFR_TRACE_BLOCK)
     k_trace(FrameView F, Band bd, const GHit* gbuf, PathCfg cfg, int trees, uint64_t frame_key, Sink proto,
             unsigned long long* q) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -512,7 +515,8 @@ static void launch_trace(const char* kname, const FrameView& F, const Band& bd, 
     const void* kf = reinterpret_cast<const void*>(k_trace<Sink, VEL>);
     {
         KScope ks(kname, s);
-        k_trace<Sink, VEL><<<persistent_grid(kf, 128, sm, n), 128, sm, s>>>(F, bd, g, cfg, trees, frame_key, sk, q);
+        k_trace<Sink, VEL><<<persistent_grid(kf, TOFR_TRACE_BLOCK, sm, n), TOFR_TRACE_BLOCK, sm, s>>>(F, bd, g, cfg,
+                                                                                               trees, frame_key, sk, q);
     }
 }
 

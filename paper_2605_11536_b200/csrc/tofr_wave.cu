@@ -40,6 +40,10 @@
 #ifndef TOFR_FINISH_MINB
 #define TOFR_FINISH_MINB TOFR_WAVE_MINB
 #endif
+// threads per CTA of the persistent solve (TOFR_WAVE_MINB CTAs of 128 per SM)
+#ifndef TOFR_SOLVE_BLOCK
+#define TOFR_SOLVE_BLOCK 128
+#endif
 // idle lanes a warp of k_shift_solve collects before it refills them
 #ifndef TOFR_REFILL
 #define TOFR_REFILL 12
@@ -760,7 +764,7 @@ __global__ void __launch_bounds__(128)
 // see slot == nullptr at compile time and drop the slot-map branches.
 // Diagnostic build (-DTOFR_SOLVE_PROFILE=1, a tools variant): per solved job,
 // {cycles from its refill to its finish, trial rounds it took part in, Newton
-// iterations, re-projection rays, SM cycle at finish} for the latency-floor
+// iterations, re-projection rays, global timer (ns) at finish} for the latency-floor
 // analysis of DESIGN 8 (tofr_gpu_debug_solve_profile).
 #ifndef TOFR_SOLVE_PROFILE
 #define TOFR_SOLVE_PROFILE 0
@@ -772,7 +776,7 @@ __device__ unsigned int g_solve_prof_n;
 #endif
 
 template <bool VEL, bool SP>
-__global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
+__global__ void __launch_bounds__(TOFR_SOLVE_BLOCK, TOFR_WAVE_MINB * 128 / TOFR_SOLVE_BLOCK)
     k_shift_solve(FrameView F0, FrameView F1, const GHit* g0, const GHit* g1, ResStore st0, ResStore st1,
                   ShiftQueue q, PathCfg cfg, unsigned long long* ctr_out, unsigned long long* wq) {
     if (!SP) st0.slot = st1.slot = nullptr;
@@ -1104,10 +1108,12 @@ __global__ void __launch_bounds__(128, TOFR_WAVE_MINB)
                 unsigned k = atomicAdd(&g_solve_prof_n, 1u);
                 if (k < kSolveProfCap) {
                     long long now = clock64();
+                    unsigned long long gt;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
                     g_solve_prof[k][0] = (unsigned long long)(now - prof_t0);
                     g_solve_prof[k][1] = (unsigned long long)prof_rounds | ((unsigned long long)iter << 32) |
                                          ((unsigned long long)(n_rays - prof_rays0) << 40);
-                    g_solve_prof[k][2] = (unsigned long long)now;
+                    g_solve_prof[k][2] = gt;
                 }
             }
 #endif
@@ -1927,7 +1933,8 @@ static void run_shifts(const FrameView& F0, const FrameView& F1, const GHit* g0,
     if (overlap) cudaMemsetAsync(fq, 0, sizeof(unsigned long long), s);
     {
         KScope ks("k_shift_solve", s);
-        solve<<<persistent_grid(reinterpret_cast<const void*>(solve), 128, sm, cap_jobs), 128, sm, s>>>(
+        solve<<<persistent_grid(reinterpret_cast<const void*>(solve), TOFR_SOLVE_BLOCK, sm, cap_jobs), TOFR_SOLVE_BLOCK,
+                sm, s>>>(
             F0, F1, g0, g1, st0, st1, q, cfg, ctr, wq);
     }
     if (!overlap) cudaMemsetAsync(fq, 0, sizeof(unsigned long long), s);

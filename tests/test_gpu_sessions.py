@@ -102,19 +102,24 @@ def test_spatial_radius_zero_is_a_no_op(mode, variant):
     assert np.array_equal(zero.image, off.image)
 
 
-@pytest.mark.parametrize("name", ["gated", "transient"])
+@pytest.mark.parametrize("name", ["gated", "gated_depth2", "gated_temporal_only", "transient"])
 def test_pipelined_frames_equal_serial(name, monkeypatch):
     """Pipelined sessions (the default) run the camera and initial sampling of
-    frame f on a side stream while frame f-1 finishes: the frames must equal
-    those of one stream (TOFR_PIPELINE=0)."""
+    frame f on a side stream while frame f-1 (gated: also frame f-2, a fourth
+    grid and a third frame slot; TOFR_PIPE_DEPTH=2: two frames) finishes: the
+    frames must equal those of one stream (TOFR_PIPELINE=0).  Seven frames take
+    the gated ring of grids and slots around twice."""
     sd = scenes.bundled("boxes_doppler", 40)
-    if name == "gated":
-        cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True,
-                           spatial_passes=1, spatial_neighbors=3, spatial_radius=5, frames=4)
+    if name == "gated_depth2":
+        monkeypatch.setenv("TOFR_PIPE_DEPTH", "2")
+    if name.startswith("gated"):
+        sp = dict(spatial_passes=0) if name == "gated_temporal_only" else \
+            dict(spatial_passes=1, spatial_neighbors=3, spatial_radius=5)
+        cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True, frames=7, **sp)
     else:
         cfg = _transient_cfg(hist_t0=7.0, hist_bin_width=0.5, temporal=True, spatial_passes=1,
                              spatial_neighbors=3, spatial_radius=4, frames=4)
-    render = Renderer(0).render_gated if name == "gated" else Renderer(0).render_transient
+    render = Renderer(0).render_gated if name.startswith("gated") else Renderer(0).render_transient
     got = render(sd, cfg)
     monkeypatch.setenv("TOFR_PIPELINE", "0")
     ref = render(sd, cfg)

@@ -68,6 +68,16 @@ for k in (0, 1, 2, 3, 4, 5):
     if m.any():
         print(f"  iter {k}: {m.sum():7d} jobs, mean {cyc[m].mean() / mhz:7.1f} us, max {cyc[m].max() / mhz:7.1f} us, "
               f"mean rounds {rounds[m].mean():5.1f}, mean rays {rays[m].mean():5.1f}")
+# timeline: the frame's solve launches, split at gaps of > 15 us between job
+# finishes (each launch is followed by its finish and merge kernels); per
+# launch the time by which 50 / 90 / 99 / 100% of its jobs had finished
+t = np.sort(a[:, 2].astype(np.float64)) / 1e3
+cut = np.flatnonzero(np.diff(t) > 15.0) + 1
+print("  launch timeline (us from the launch's first finish): jobs, t50, t90, t99, t100")
+for seg in np.split(t, cut):
+    s = seg - seg[0]
+    print(f"   {len(seg):8d} {np.percentile(s, 50):8.1f} {np.percentile(s, 90):8.1f} {np.percentile(s, 99):8.1f} "
+          f"{s[-1]:8.1f}")
 r_us = cyc / np.maximum(rounds, 1) / mhz
 print(f"  us per trial round: p50 {np.percentile(r_us, 50):.2f} p90 {np.percentile(r_us, 90):.2f} "
       f"p99 {np.percentile(r_us, 99):.2f}")
