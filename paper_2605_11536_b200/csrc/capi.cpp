@@ -833,6 +833,10 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             ck(cudaMemsetAsync(s->accum.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
             ck(cudaMemsetAsync(s->image.p, 0, npix * 3 * sizeof(double), ctx->stream), "memset");
         }
+        // read-back staging (tofr_gpu_session_read_image_async) allocated with the
+        // session: a cudaMalloc at the first read-backs of a frame loop would
+        // synchronise the device in the middle of it
+        for (auto& rs : s->read_stage) rs.ensure(s->owned_pixels() * 24);
         size_t per_row_items = size_t(s->W) * s->B;
         size_t lo = halo_bytes(size_t(s->y0 - s->r0) * per_row_items, halo_cap(s.get(), size_t(s->y0 - s->r0) * per_row_items),
                                s->sparse);
