@@ -282,6 +282,55 @@ __device__ __forceinline__ uint32_t block_append_jobs(const WaveScratch& ws, uin
     return k;
 }
 
+// The multi-item form: a thread appends `njobs` consecutive job slots and
+// `nmerge` consecutive merge-list slots (its items' entries, in its item
+// order).  Returns the first job slot (kNoJob if none or the queue is full:
+// overflow bit raised) and the first merge-list slot in *mfirst.
+__device__ __forceinline__ uint32_t block_append_jobs_n(const WaveScratch& ws, uint32_t njobs, uint32_t nmerge,
+                                                        uint32_t* mfirst, unsigned long long* err,
+                                                        unsigned long long* work, uint32_t* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t incl = njobs, minc = nmerge;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        uint32_t vm = __shfl_up_sync(0xffffffffu, minc, o);
+        if (lane >= o) {
+            incl += v;
+            minc += vm;
+        }
+    }
+    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31), mtot = __shfl_sync(0xffffffffu, minc, 31);
+    if (lane == 0) {
+        sh[warp] = wtot;
+        sh[nw + warp] = mtot;
+        if (work && mtot) atomicAdd(&work[WK_MERGES], (unsigned long long)mtot);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tj = 0, tm = 0;
+        for (int w = 0; w < nw; ++w) {
+            uint32_t cj = sh[w], cm = sh[nw + w];
+            sh[w] = tj;
+            sh[nw + w] = tm;
+            tj += cj;
+            tm += cm;
+        }
+        sh[2 * nw] = tj ? atomicAdd(&ws.q.ctl[1], tj) : 0u;
+        sh[2 * nw + 1] = tm ? atomicAdd(&ws.q.ctl[3], tm) : 0u;
+    }
+    __syncthreads();
+    const uint32_t k = sh[2 * nw] + sh[warp] + (incl - njobs);
+    *mfirst = sh[2 * nw + 1] + sh[nw + warp] + (minc - nmerge);
+    __syncthreads();  // `sh` is reused by the next call
+    if (!njobs) return kNoJob;
+    if (size_t(k) + njobs > ws.q.cap) {
+        atomicAdd(err, 1ull << 32);
+        return kNoJob;
+    }
+    return k;
+}
+
 __device__ __forceinline__ void block_mlist_append(const WaveScratch& ws, bool want, uint32_t item,
                                                    unsigned long long* work, uint32_t* sh) {
     uint32_t k = block_append(&ws.q.ctl[3], want, sh);
@@ -1424,54 +1473,84 @@ __global__ void k_temporal_reproject(FrameView Fc, Band bd, const GHit* gc, Fram
     }
 }
 
-__global__ void k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg,
-                                PathCfg cfg, ResStore cur, ResStore prev, WaveScratch ws) {
+// TOFR_PREP_ITEMS items per thread and block append: every item's loads
+// (reprojected source pixel, both headers) are issued before the append's
+// barriers, so a thread keeps several dependent-load chains in flight and the
+// block waits at its barriers once per TOFR_PREP_ITEMS x 256 items
+#ifndef TOFR_PREP_ITEMS
+#define TOFR_PREP_ITEMS 4
+#endif
+__global__ void __launch_bounds__(256, 4)
+    k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg, PathCfg cfg,
+                    ResStore cur, ResStore prev, WaveScratch ws) {
+    constexpr int KP = TOFR_PREP_ITEMS;
     int W = Fc.cam.w, B = cg.transient ? cg.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    const size_t tile = size_t(blockDim.x) * KP;
+    const size_t n_round = (n + tile - 1) / tile * tile;  // block-uniform trip count
     __shared__ uint32_t sh[33];
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
-        bool live = i < n;
-        size_t it = base + (live ? i : 0);
-        int p = int(it / B), b = int(it % B);
-        int px = p % W, py = p / W;
-        bool fwd = false, inv = false, merge = false;
-        size_t src_i = 0;
-        int qx = 0, qy = 0;
-        if (live) {
-            uint64_t src_pix = ws.tsrc[size_t(p) - size_t(bd.y0) * W];
-            if (src_pix != ~uint64_t(0)) {
-                qx = int(src_pix % W);
-                qy = int(src_pix / W);
-                src_i = size_t(src_pix) * B + b;
-                double2 s0 = ld2(prev, 0, src_i);
-                if (s0.y > 0) {
-                    double2 c0 = ld2(cur, 0, it);
-                    fwd = s0.x > 0;
-                    inv = c0.x > 0;
-                    merge = fwd || inv;
-                    // both empty: the merge only adds the confidences (no RNG draw)
-                    if (!merge) res_store_w(cur, it, 0.0, dmin(c0.y + s0.y, cfg.m_cap));
-                }
+    for (size_t t0 = blockIdx.x * tile; t0 < n_round; t0 += size_t(gridDim.x) * tile) {
+        // item k of this thread: t0 + k * blockDim.x + threadIdx.x (coalesced per k)
+        uint64_t sp[KP];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            sp[k] = ~uint64_t(0);
+            if (i < n) sp[k] = ws.tsrc[size_t((base + i) / B) - size_t(bd.y0) * W];
+        }
+        double2 s0[KP], c0[KP];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            s0[k] = make_double2(0.0, 0.0);
+            c0[k] = make_double2(0.0, 0.0);
+            if (sp[k] != ~uint64_t(0)) {
+                const size_t it = base + i;
+                s0[k] = ld2(prev, 0, size_t(sp[k]) * B + it % B);
+                c0[k] = ld2(cur, 0, it);
             }
         }
-        double dc, dw, sc, sw;
-        gate_of(cg, b, dc, dw);
-        gate_of(pg, b, sc, sw);
-        // the item's jobs (forward, then inverse) and its merge-list entry in one
-        // block-wide append
-        const uint32_t k0 = block_append_jobs(ws, uint32_t(fwd) + uint32_t(inv), merge, uint32_t(i), bd.err,
-                                              cfg.work, sh);
-        const uint32_t kf = (fwd && k0 != kNoJob) ? k0 : kNoJob;
-        const uint32_t ki = (inv && k0 != kNoJob) ? k0 + uint32_t(fwd) : kNoJob;
-        if (kf != kNoJob) {
-            job_put(ws.q, kf, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
-            ws.map_a[i] = kf;
+        uint32_t fm = 0, im = 0, mm = 0;  // per-item bits: forward job, inverse job, merge
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            if (sp[k] == ~uint64_t(0) || !(s0[k].y > 0)) continue;
+            const bool fwd = s0[k].x > 0, inv = c0[k].x > 0;
+            if (fwd) fm |= 1u << k;
+            if (inv) im |= 1u << k;
+            if (fwd || inv) {
+                mm |= 1u << k;
+            } else {  // both empty: the merge only adds the confidences (no RNG draw)
+                const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+                res_store_w(cur, base + i, 0.0, dmin(c0[k].y + s0[k].y, cfg.m_cap));
+            }
         }
-        if (ki != kNoJob) {
-            job_put(ws.q, ki, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
-            ws.map_b[i] = ki;
+        // the items' jobs (forward, then inverse, in item order) and merge-list
+        // entries in one block-wide append
+        uint32_t mfirst = 0;
+        uint32_t kj = block_append_jobs_n(ws, uint32_t(__popc(fm) + __popc(im)), uint32_t(__popc(mm)), &mfirst,
+                                          bd.err, cfg.work, sh);
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            if ((mm >> k) & 1u) ws.mlist[mfirst++] = uint32_t(i);
+            const bool fwd = (fm >> k) & 1u, inv = (im >> k) & 1u;
+            if (!(fwd || inv) || kj == kNoJob) continue;
+            const size_t it = base + i;
+            const int p = int(it / B), b = int(it % B);
+            const int px = p % W, py = p / W;
+            const int qx = int(sp[k] % W), qy = int(sp[k] / W);
+            const size_t src_i = size_t(sp[k]) * B + b;
+            double dc, dw, sc, sw;
+            gate_of(cg, b, dc, dw);
+            gate_of(pg, b, sc, sw);
+            if (fwd) {
+                job_put(ws.q, kj, src_i, JOB_REC1 | JOB_SRC1 | JOB_FULL | JOB_COUNT, qx, qy, px, py, sc, dc, dw);
+                ws.map_a[i] = kj++;
+            }
+            if (inv) {
+                job_put(ws.q, kj, it, JOB_DST1, px, py, qx, qy, dc, sc, sw);
+                ws.map_b[i] = kj++;
+            }
         }
     }
 }
@@ -2097,7 +2176,8 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
     }
     {
         KScope ks("k_temporal_prep", s);
-        k_temporal_prep<<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
+        k_temporal_prep<<<grid_n((n + TOFR_PREP_ITEMS - 1) / TOFR_PREP_ITEMS, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg,
+                                                                                             cfg, cur, prev, ws);
     }
     run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, ws.ov, cfg, ctr, q, s);
     {
