@@ -1477,13 +1477,17 @@ __global__ void k_temporal_reproject(FrameView Fc, Band bd, const GHit* gc, Fram
 // (reprojected source pixel, both headers) are issued before the append's
 // barriers, so a thread keeps several dependent-load chains in flight and the
 // block waits at its barriers once per TOFR_PREP_ITEMS x 256 items
+// (stages of at least kPrepItemsMin items: the transient grids; smaller
+// stages -- gated frames -- keep one item per thread, measured faster there:
+// their grids need every thread the machine holds, profiles/r02/ab_prep_items.txt)
 #ifndef TOFR_PREP_ITEMS
 #define TOFR_PREP_ITEMS 4
 #endif
-__global__ void __launch_bounds__(256, 4)
+constexpr size_t kPrepItemsMin = size_t(1) << 22;
+template <int KP>
+__global__ void __launch_bounds__(256, KP > 1 ? 4 : 1)
     k_temporal_prep(FrameView Fc, Band bd, const GHit* gc, FrameView Fp, GateGrid cg, GateGrid pg, PathCfg cfg,
                     ResStore cur, ResStore prev, WaveScratch ws) {
-    constexpr int KP = TOFR_PREP_ITEMS;
     int W = Fc.cam.w, B = cg.transient ? cg.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
     const size_t tile = size_t(blockDim.x) * KP;
@@ -1619,79 +1623,136 @@ __global__ void k_spatial_offsets(Band bd, int W, PathCfg cfg, SpatialParams sp,
     }
 }
 
-__global__ void k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
-                                   int frame_idx, ResStore src_grid, WaveScratch ws) {
+// The spatial prep kernels take TOFR_PREP_ITEMS items per thread per block
+// append, like k_temporal_prep: the neighbour lookups and header gathers of
+// all of them are in flight before the append's barriers.
+template <int KP>
+__global__ void __launch_bounds__(256, KP > 1 ? 4 : 1)
+    k_spatial_prep_fwd(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass, int frame_idx,
+                       ResStore src_grid, WaveScratch ws) {
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    const size_t npx = size_t(bd.y1 - bd.y0) * W;
+    const size_t tile = size_t(blockDim.x) * KP;
+    const size_t n_round = (n + tile - 1) / tile * tile;  // block-uniform trip count
     __shared__ uint32_t sh[33];
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
-        bool live = i < n;
-        size_t it = base + (live ? i : 0);
-        int p = int(it / B), b = int(it % B);
-        int px = p % W, py = p / W;
-        double dc, dw;
-        gate_of(gate, b, dc, dw);
-        const size_t npx = size_t(bd.y1 - bd.y0) * W, lp = size_t(p) - size_t(bd.y0) * W;
+    for (size_t t0 = blockIdx.x * tile; t0 < n_round; t0 += size_t(gridDim.x) * tile) {
         for (int j = 0; j < sp.neighbors; ++j) {
-            int nx = 0, ny = 0;
-            size_t si = 0;
+            int nx[KP], ny[KP];
+            size_t si[KP];
+            uint32_t wm = 0;
             // every non-empty neighbour is a forward shift attempt (counted even
             // when its record has no reconnection vertex, as the reference does)
-            bool want = live &&
-                        spatial_neighbor_at(bd, W, H, B, px, py, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx, ny, si) &&
-                        ld2(src_grid, 0, si).x > 0;
-            uint32_t k = block_queue_append(ws.q, want, bd.err, sh);
-            if (k != kNoJob) job_put(ws.q, k, si, JOB_FULL | JOB_COUNT, nx, ny, px, py, dc, dc, dw);
-            if (live) ws.map_a[size_t(j) * n + i] = k;
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+                nx[k] = ny[k] = 0;
+                si[k] = 0;
+                if (i < n) {
+                    const size_t it = base + i;
+                    const int p = int(it / B), b = int(it % B);
+                    const size_t lp = size_t(p) - size_t(bd.y0) * W;
+                    if (spatial_neighbor_at(bd, W, H, B, p % W, p / W, b, ws.nbr[size_t(j) * npx + lp], src_grid,
+                                            nx[k], ny[k], si[k]) &&
+                        ld2(src_grid, 0, si[k]).x > 0)
+                        wm |= 1u << k;
+                }
+            }
+            uint32_t mfirst = 0;
+            uint32_t kj = block_append_jobs_n(ws, uint32_t(__popc(wm)), 0u, &mfirst, bd.err, nullptr, sh);
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+                if (i >= n) continue;
+                uint32_t slot = kNoJob;
+                if (((wm >> k) & 1u) && kj != kNoJob) {
+                    const size_t it = base + i;
+                    const int p = int(it / B), b = int(it % B);
+                    double dc, dw;
+                    gate_of(gate, b, dc, dw);
+                    slot = kj++;
+                    job_put(ws.q, slot, si[k], JOB_FULL | JOB_COUNT, nx[k], ny[k], p % W, p / W, dc, dc, dw);
+                }
+                ws.map_a[size_t(j) * n + i] = slot;
+            }
         }
     }
 }
 
-__global__ void k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass,
-                                   int j, int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
+template <int KP>
+__global__ void __launch_bounds__(256, KP > 1 ? 4 : 1)
+    k_spatial_prep_inv(FrameView F, Band bd, PathCfg cfg, GateGrid gate, SpatialParams sp, int pass, int j,
+                       int frame_idx, ResStore src_grid, ResStore dst_grid, WaveScratch ws) {
     int W = F.cam.w, H = F.cam.h, B = gate.transient ? gate.h.bins : 1;
     size_t base = size_t(bd.y0) * W * B, n = size_t(bd.y1 - bd.y0) * W * B;
-    size_t stride = size_t(gridDim.x) * blockDim.x;
-    size_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;  // block-uniform trip count
+    const size_t npx = size_t(bd.y1 - bd.y0) * W;
+    const size_t tile = size_t(blockDim.x) * KP;
+    const size_t n_round = (n + tile - 1) / tile * tile;  // block-uniform trip count
     __shared__ uint32_t sh[33];
     const ResStore& out_grid = j == 0 ? src_grid : dst_grid;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
-        bool live = i < n;
-        size_t it = base + (live ? i : 0);
-        int p = int(it / B), b = int(it % B);
-        int px = p % W, py = p / W;
-        double dc, dw;
-        gate_of(gate, b, dc, dw);
-        int nx = 0, ny = 0;
-        size_t si = 0;
-        bool want = false, merge = false;
-        if (live) {
-            const size_t npx = size_t(bd.y1 - bd.y0) * W, lp = size_t(p) - size_t(bd.y0) * W;
-            if (!spatial_neighbor_at(bd, W, H, B, px, py, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx, ny, si)) {
-                if (j == 0) {  // the output starts as the pass input
-                    double2 c0 = ld2(src_grid, 0, it);
-                    if (c0.x > 0)
-                        copy_res(src_grid, dst_grid, it, c0.x, c0.y, cfg.gate_vel);
-                    else
-                        res_store_w(dst_grid, it, 0.0, c0.y);
-                    if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
-                }
-            } else {
-                double2 o0 = ld2(out_grid, 0, it), s0 = ld2(src_grid, 0, si);
-                want = o0.x > 0;
-                merge = want || s0.x > 0;
-                if (!merge) {  // both empty: the merge only adds the confidences (no RNG draw)
-                    res_store_w(dst_grid, it, 0.0, dmin(o0.y + s0.y, cfg.m_cap));
-                    if (j == 0 && j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
-                }
+    for (size_t t0 = blockIdx.x * tile; t0 < n_round; t0 += size_t(gridDim.x) * tile) {
+        int nx[KP], ny[KP];
+        size_t si[KP];
+        double2 o0[KP], s0[KP];
+        uint32_t nb = 0;  // items whose neighbour j exists
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            nx[k] = ny[k] = 0;
+            si[k] = 0;
+            o0[k] = s0[k] = make_double2(0.0, 0.0);
+            if (i >= n) continue;
+            const size_t it = base + i;
+            const int p = int(it / B), b = int(it % B);
+            const size_t lp = size_t(p) - size_t(bd.y0) * W;
+            if (spatial_neighbor_at(bd, W, H, B, p % W, p / W, b, ws.nbr[size_t(j) * npx + lp], src_grid, nx[k],
+                                    ny[k], si[k])) {
+                nb |= 1u << k;
+                o0[k] = ld2(out_grid, 0, it);
+                s0[k] = ld2(src_grid, 0, si[k]);
+            } else if (j == 0) {
+                o0[k] = ld2(src_grid, 0, it);  // the pass input's header (copied below)
             }
         }
-        uint32_t k = block_append_jobs(ws, uint32_t(want), merge, uint32_t(i), bd.err, cfg.work, sh);
-        if (k != kNoJob) {
-            job_put(ws.q, k, it, j == 0 ? 0u : JOB_REC1, px, py, nx, ny, dc, dc, dw);
-            ws.map_b[i] = k;
+        uint32_t wm = 0, mm = 0;  // inverse job, merge
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            if (i >= n) continue;
+            const size_t it = base + i;
+            if (!((nb >> k) & 1u)) {
+                if (j == 0) {  // the output starts as the pass input
+                    if (o0[k].x > 0)
+                        copy_res(src_grid, dst_grid, it, o0[k].x, o0[k].y, cfg.gate_vel);
+                    else
+                        res_store_w(dst_grid, it, 0.0, o0[k].y);
+                    if (j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
+                }
+                continue;
+            }
+            const bool want = o0[k].x > 0, merge = want || s0[k].x > 0;
+            if (want) wm |= 1u << k;
+            if (merge) {
+                mm |= 1u << k;
+            } else {  // both empty: the merge only adds the confidences (no RNG draw)
+                res_store_w(dst_grid, it, 0.0, dmin(o0[k].y + s0[k].y, cfg.m_cap));
+                if (j == 0 && j + 1 < sp.neighbors) ws.rng_ctr[i] = 0;
+            }
+        }
+        uint32_t mfirst = 0;
+        uint32_t kj = block_append_jobs_n(ws, uint32_t(__popc(wm)), uint32_t(__popc(mm)), &mfirst, bd.err, cfg.work,
+                                          sh);
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const size_t i = t0 + size_t(k) * blockDim.x + threadIdx.x;
+            if ((mm >> k) & 1u) ws.mlist[mfirst++] = uint32_t(i);
+            if (!((wm >> k) & 1u) || kj == kNoJob) continue;
+            const size_t it = base + i;
+            const int p = int(it / B), b = int(it % B);
+            double dc, dw;
+            gate_of(gate, b, dc, dw);
+            job_put(ws.q, kj, it, j == 0 ? 0u : JOB_REC1, p % W, p / W, nx[k], ny[k], dc, dc, dw);
+            ws.map_b[i] = kj++;
         }
     }
 }
@@ -2176,8 +2237,11 @@ void launch_temporal_wave(const FrameView& Fc, const Band& bd, const GHit* gc, c
     }
     {
         KScope ks("k_temporal_prep", s);
-        k_temporal_prep<<<grid_n((n + TOFR_PREP_ITEMS - 1) / TOFR_PREP_ITEMS, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg,
-                                                                                             cfg, cur, prev, ws);
+        if (n >= kPrepItemsMin)
+            k_temporal_prep<TOFR_PREP_ITEMS><<<grid_n((n + TOFR_PREP_ITEMS - 1) / TOFR_PREP_ITEMS, 256), 256, 0, s>>>(
+                Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
+        else
+            k_temporal_prep<1><<<grid_n(n, 256), 256, 0, s>>>(Fc, bd, gc, Fp, cg, pg, cfg, cur, prev, ws);
     }
     run_shifts(Fc, Fp, gc, gp, cur, prev, ws.q, ws.ov, cfg, ctr, q, s);
     {
@@ -2205,7 +2269,11 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
     }
     {
         KScope ks("k_spatial_prep_fwd", s);
-        k_spatial_prep_fwd<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
+        if (n >= kPrepItemsMin)
+            k_spatial_prep_fwd<TOFR_PREP_ITEMS><<<grid_n((n + TOFR_PREP_ITEMS - 1) / TOFR_PREP_ITEMS, 256), 256, 0, s>>>(
+                F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
+        else
+            k_spatial_prep_fwd<1><<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, frame_idx, src, ws);
     }
     {
         KScope ks("k_queue_ctl", s);
@@ -2218,7 +2286,11 @@ void launch_spatial_wave(const FrameView& F, const Band& bd, const GHit* g, cons
         }
         {
             KScope ks("k_spatial_prep_inv", s);
-            k_spatial_prep_inv<<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+            if (n >= kPrepItemsMin)
+                k_spatial_prep_inv<TOFR_PREP_ITEMS><<<grid_n((n + TOFR_PREP_ITEMS - 1) / TOFR_PREP_ITEMS, 256), 256, 0,
+                                                      s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
+            else
+                k_spatial_prep_inv<1><<<grid_n(n, 256), 256, 0, s>>>(F, bd, cfg, gg, sp, pass, j, frame_idx, src, dst, ws);
         }
         run_shifts(F, F, g, g, src, dst, ws.q, ws.ov, cfg, ctr, q, s);
         {
