@@ -207,7 +207,7 @@ struct tofr_session {
     // the block per frame set [2][8 u32]
     unsigned int* occ_host = nullptr;
     size_t occ_seen = 0;               // largest of them over the frames flushed so far
-    DevBuf res_slot[3], res_rows;
+    DevBuf res_slot[4], res_rows;
     DevBuf image, accum, hist;  // owned rows only (plain sessions: accum = wide-band image accumulator)
     DevBuf ctr;                             // [3 stages][SC_COUNT] u64 + band error flag + work counter
     DevBuf send_lo, send_hi, recv_lo, recv_hi;
@@ -679,6 +679,15 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         s->has_spatial = cfg->spatial_passes > 0 ? 1 : 0;
         size_t items = s->items_stored();
         size_t rb = items * kResChunks * 16;
+        // three-frame buffers (see `side`): only for frames staged in shared
+        // memory -- a snapshot traversed from L2 (the 10^5-triangle mesh)
+        // measured 6% slower with a third frame's copy competing for the cache
+        // (profiles/r02/ab_pipe.txt); transient grids: below
+        size_t n_tris = 0;
+        for (const HObject& o : s->scene.objects) n_tris += o.local.size();
+        const bool staged = n_tris * (2 * sizeof(GNode) + sizeof(GTriIsect)) <= kSmemStageLimit;
+        const char* pdepth = std::getenv("TOFR_PIPE_DEPTH");
+        bool deep = s->side && staged && !(pdepth && pdepth[0] == '2');
         {
             // transient grids are mostly empty reservoirs: header plane + a pool
             // of sample rows (TOFR_SPARSE=0: dense).  Pool rows per grid: one per
@@ -686,6 +695,9 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
             // fits (TOFR_POOL_FRAC: that fraction of the items instead).
             const char* sp = std::getenv("TOFR_SPARSE");
             s->sparse = s->transient && !(sp && sp[0] == '0');
+            // three-frame buffers for sparse grids only where the fourth grid takes
+            // the place of the spare one a temporal-only session does not use
+            deep = deep && (!s->transient || (s->sparse && !s->has_bin && !s->has_spatial));
             if (s->sparse) {
                 // records of scenes without non-reconnectable materials never carry
                 // replay lanes (k = 2), and transient gates are length gates: the
@@ -703,10 +715,17 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 size_t rows = items;
                 size_t fr = 0, tot = 0;
                 if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-                    size_t ngrid = (s->has_bin || s->has_spatial) ? 3 : 2;
-                    size_t fit = size_t(double(fr) * 0.55) / ngrid;
-                    fit = fit > items * 20 ? (fit - items * 20) / row_bytes : 0;
-                    rows = std::min(rows, std::max<size_t>(fit, 1024));
+                    auto fit_rows = [&](size_t ngrid) {
+                        size_t fit = size_t(double(fr) * 0.55) / ngrid;
+                        fit = fit > items * 20 ? (fit - items * 20) / row_bytes : 0;
+                        return std::min(rows, std::max<size_t>(fit, 1024));
+                    };
+                    const size_t ngrid = (s->has_bin || s->has_spatial) ? 3 : 2;
+                    // the fourth grid only while the pools still hold half the grid
+                    // (1080p x 256 bins: 187 M rows per pool with two, 109 M with three
+                    // -- 94 M in use by frame 45 -- so it keeps two frames)
+                    if (deep && fit_rows(ngrid + 1) < items / 2) deep = false;
+                    rows = fit_rows(deep ? ngrid + 1 : ngrid);
                 }
                 if (const char* pf = std::getenv("TOFR_POOL_FRAC")) rows = size_t(double(items) * std::atof(pf)) + 1;
                 if (rows > items) rows = items;
@@ -714,8 +733,8 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
                 if (rows > 0xfffffff0ull) rows = 0xfffffff0ull;
                 s->pool_rows = rows;
                 rb = items * 16 + row_bytes * (rows + 2);
-                for (int k = 0; k < 3; ++k)
-                    if (k < 2 || s->has_bin || s->has_spatial) {
+                for (int k = 0; k < 4; ++k)
+                    if (k < 2 || ((s->has_bin || s->has_spatial) && k == 2) || (deep && k == 3)) {
                         s->res_slot[k].ensure(items * sizeof(uint32_t));
                         ck(cudaMemsetAsync(s->res_slot[k].p, 0xff, items * sizeof(uint32_t), ctx->stream), "memset");
                     }
@@ -732,14 +751,7 @@ tofr_session* make_session(tofr_gpu* ctx, const tofr_scene* sc, const tofr_rende
         ck(cudaMemsetAsync(s->res[0].p, 0, rb, ctx->stream), "memset");
         ck(cudaMemsetAsync(s->res[1].p, 0, rb, ctx->stream), "memset");
         if (s->res[2].p) ck(cudaMemsetAsync(s->res[2].p, 0, rb, ctx->stream), "memset");
-        // only for frames staged in shared memory: a snapshot traversed from
-        // L2 (the 10^5-triangle mesh) measured 6% slower with a third frame's
-        // copy competing for the cache (profiles/r02/ab_pipe.txt)
-        size_t n_tris = 0;
-        for (const HObject& o : s->scene.objects) n_tris += o.local.size();
-        const bool staged = n_tris * (2 * sizeof(GNode) + sizeof(GTriIsect)) <= kSmemStageLimit;
-        const char* pdepth = std::getenv("TOFR_PIPE_DEPTH");
-        if (s->side && !s->transient && staged && !(pdepth && pdepth[0] == '2')) {
+        if (deep) {
             s->res[3].ensure(rb);
             ck(cudaMemsetAsync(s->res[3].p, 0, rb, ctx->stream), "memset");
             s->xg = 3;
@@ -889,7 +901,7 @@ void flush_set(tofr_session* s, int set) {
     }
     s->tot_frames++;
     if (s->sparse)
-        for (int k = 0; k < 3; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[8 * set + k]);
+        for (int k = 0; k < 4; ++k) s->occ_seen = std::max<size_t>(s->occ_seen, s->occ_host[8 * set + k]);
     unsigned long long pool_err = 0;
     if (s->sparse) std::memcpy(&pool_err, s->occ_host + 8 * set + 4, 8);
     if ((s->err_host[set] | pool_err) & kErrHalo)

@@ -102,7 +102,8 @@ def test_spatial_radius_zero_is_a_no_op(mode, variant):
     assert np.array_equal(zero.image, off.image)
 
 
-@pytest.mark.parametrize("name", ["gated", "gated_depth2", "gated_temporal_only", "transient"])
+@pytest.mark.parametrize("name", ["gated", "gated_depth2", "gated_temporal_only", "transient",
+                                  "transient_temporal_only"])
 def test_pipelined_frames_equal_serial(name, monkeypatch):
     """Pipelined sessions (the default) run the camera and initial sampling of
     frame f on a side stream while frame f-1 (gated: also frame f-2, a fourth
@@ -116,9 +117,11 @@ def test_pipelined_frames_equal_serial(name, monkeypatch):
         sp = dict(spatial_passes=0) if name == "gated_temporal_only" else \
             dict(spatial_passes=1, spatial_neighbors=3, spatial_radius=5)
         cfg = RenderConfig(gate=GateSpec(F.GATE_LENGTH, 12.0, 0.3, 1.0), m_init=1, temporal=True, frames=7, **sp)
-    else:
+    elif name == "transient":
         cfg = _transient_cfg(hist_t0=7.0, hist_bin_width=0.5, temporal=True, spatial_passes=1,
                              spatial_neighbors=3, spatial_radius=4, frames=4)
+    else:  # sparse grids with three-frame buffers (a fourth grid, a third slot)
+        cfg = _transient_cfg(hist_t0=7.0, hist_bin_width=0.5, temporal=True, frames=7)
     render = Renderer(0).render_gated if name.startswith("gated") else Renderer(0).render_transient
     got = render(sd, cfg)
     monkeypatch.setenv("TOFR_PIPELINE", "0")
